@@ -1,0 +1,166 @@
+/* fsg.h -- C ABI of the B200-native FishGym IB-LBM hot path.
+ *
+ * This is the drop-in boundary.  The reference (FishGym,
+ * /root/reference/proj/include/fishsim) exposes the path as a header-only
+ * C++ API with no FFI; each entry point below replaces one reference call,
+ * cited as file:line.  A C++ wrapper with the reference's class shapes
+ * (CoupledSession, LatticeGrid, FrameFollower ...) sits on top of this ABI in
+ * include/fishgym_b200/session.hpp; Python binds it with ctypes
+ * (paper_2206_01683_b200/_abi.py).
+ *
+ * Conventions (identical to the reference):
+ *   cell index    c = x + nx*(y + ny*z)                    lattice.hpp:83-87
+ *   distributions f[i*n + c], i in D3Q19 order             lattice.hpp:17-38, :89-90
+ *   vector fields AoS, v[3*c + k]                          lattice.hpp:129-154
+ *   lattice units; marker state in SI world coordinates    session.hpp:113-126
+ * All host pointers are plain C arrays owned by the caller.  Every call
+ * returns FSG_OK (0) or an error code; fsg_last_error() gives a
+ * thread-local message.  Invalid configuration -> FSG_EINPUT (the
+ * reference throws InputError); runtime instability is NOT an error, it is
+ * reported in fsg_status (solver.hpp:13-20, backend.hpp:37-40).
+ * One session = one device + one CUDA stream; a session is not thread-safe
+ * (SPEC.md:113); independent sessions may run concurrently.
+ */
+#ifndef FSG_H
+#define FSG_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define FSG_ABI_VERSION 1
+
+enum { FSG_OK = 0, FSG_EINPUT = 1, FSG_ECUDA = 2, FSG_ESTATE = 3 };
+
+/* lattice.hpp:53-56 */
+enum { FSG_BOUNDARY_PERIODIC = 0, FSG_BOUNDARY_OPEN = 1 };
+/* kernel.hpp:15-20 */
+enum { FSG_KERNEL_PESKIN4 = 0, FSG_KERNEL_ROMA3 = 1 };
+/* coupling.hpp:73-76 */
+enum { FSG_WALL_SLIP = 0, FSG_WALL_NOSLIP = 1 };
+/* frame.hpp:55 */
+enum { FSG_FRAME_NONE = 0, FSG_FRAME_TRANSLATION = 1, FSG_FRAME_TRANSLATION_YAW = 2, FSG_FRAME_FULL = 3 };
+/* storage/arithmetic of the distribution set:
+ *   FP32 : fp32 storage of f - w_i, fp32 deviation arithmetic (throughput mode, 152 B/cell)
+ *   FP64 : fp64 storage and the reference's fp64 operation order, no FMA
+ *          contraction (parity mode: bit-identical to the reference)            */
+enum { FSG_PRECISION_FP32 = 0, FSG_PRECISION_FP64 = 1 };
+
+/* SessionConfig (session.hpp:12-24) + UnitMap (units.hpp:18-23) +
+ * LatticeGrid ctor arguments (lattice.hpp:63-74). */
+typedef struct {
+  int dims[3];        /* cells per axis, each >= 8 (lattice.hpp:66-67)          */
+  double dx;          /* m per cell                                             */
+  double dt;          /* s per lattice step                                     */
+  double rho;         /* kg/m^3 mapped to lattice density 1                     */
+  double nu;          /* m^2/s ; tau = 3 nu dt/dx^2 + 1/2 must lie in (0.5,1.5]  */
+  int boundary;       /* FSG_BOUNDARY_*  (CoupledSession uses OPEN)             */
+  int kernel;         /* FSG_KERNEL_*                                           */
+  int wall;           /* FSG_WALL_*                                             */
+  int frame_mode;     /* FSG_FRAME_*                                            */
+  int precision;      /* FSG_PRECISION_*                                        */
+  int device;         /* CUDA device ordinal                                    */
+  int max_markers;    /* marker capacity (all bodies), 0 -> 65536               */
+  /* z-slab decomposition; a single-GPU session uses
+   * z_offset = 0 and nz_global = dims[2].  dims[2] is the LOCAL slab depth. */
+  int z_offset;
+  int nz_global;
+} fsg_config;
+
+/* StepStatus (solver.hpp:13-20) + StepOutcome (backend.hpp:37-40). */
+typedef struct {
+  int finite;                 /* every cell had finite rho + |u|^2             */
+  double min_f;               /* min post-collision population                 */
+  int n_nonpositive_rho;      /* FluidMacro::n_nonpositive_rho (solver.hpp:42) */
+  int out_of_bounds_markers;  /* session.hpp:130-134                           */
+  int stable;                 /* finite && min_f > -1e-3 && nonpos == 0        */
+} fsg_status;
+
+/* FrameState (frame.hpp:13-20), world frame; q = (w, x, y, z). */
+typedef struct {
+  double p[3], pd[3], pdd[3], q[4], omega[3], alpha[3];
+} fsg_frame_state;
+
+typedef struct fsg_session fsg_session;
+
+const char* fsg_last_error(void);
+int fsg_abi_version(void);
+/* Default config = SessionConfig defaults (session.hpp:12-24). */
+void fsg_config_default(fsg_config* cfg);
+/* UnitMap::tau (units.hpp:25). */
+double fsg_tau(double dx, double dt, double nu);
+
+/* CoupledSession(cfg) (session.hpp:31-40): validates units (units.hpp:56-68),
+ * dims >= 8, allocates the A/B distribution pair in HBM at rest. */
+int fsg_create(const fsg_config* cfg, fsg_session** out);
+int fsg_destroy(fsg_session* s);
+/* the session's CUDA stream (cudaStream_t), for event timing / interop */
+void* fsg_stream(fsg_session* s);
+
+/* ---- LatticeGrid (lattice.hpp:60-126) ---------------------------------- */
+int fsg_reset_rest(fsg_session* s);                                   /* :98-104  */
+int fsg_initialize(fsg_session* s, const double* rho, const double* u); /* :107-116 */
+int fsg_set_f(fsg_session* s, const double* f);   /* front() assignment, f[19*n]     */
+int fsg_get_f(fsg_session* s, double* f);         /* front() readback (post-stream)  */
+
+/* ---- lbm::solver (solver.hpp) ------------------------------------------ */
+/* BodyForceField used by fsg_collide_and_stream / fsg_macroscopic; NULL clears. */
+int fsg_set_force(fsg_session* s, const double* F);
+int fsg_collide_and_stream(fsg_session* s, fsg_status* st);            /* :103-178 */
+int fsg_macroscopic(fsg_session* s, double* rho, double* u, int* n_nonpositive); /* :25-51 */
+int fsg_total_mass(fsg_session* s, double* mass);                       /* :181-187 */
+int fsg_total_momentum(fsg_session* s, double* p3);                     /* :189-200 */
+
+/* ---- frame (frame.hpp) ---------------------------------------------------- */
+int fsg_set_frame(fsg_session* s, const fsg_frame_state* fs);
+int fsg_get_frame(fsg_session* s, fsg_frame_state* fs);
+/* frame::recenter (frame.hpp:132-154): shifts the lattice by an integer cell
+ * offset and advances the frame origin by R*shift*dx. */
+int fsg_recenter(fsg_session* s, const int shift[3]);
+
+/* ---- coupled step (session.hpp:87-198, fluid half :94-166) -------------- */
+/* Marker state for this step, world frame SI (what robot::update_samples
+ * produces, sampling.hpp:307-322): n_bodies bodies, body b owns markers
+ * [body_offsets[b], body_offsets[b+1]).  points/velocities/normals are [3*m],
+ * areas [m].  Host pointers; copied to HBM. */
+int fsg_set_markers(fsg_session* s, int n_bodies, const int64_t* body_offsets,
+                    const double* points, const double* velocities, const double* normals,
+                    const double* areas);
+/* Same, but the four arrays are DEVICE pointers already resident in HBM. */
+int fsg_set_markers_device(fsg_session* s, int n_bodies, const int64_t* body_offsets,
+                           const double* d_points, const double* d_velocities,
+                           const double* d_normals, const double* d_areas);
+/* One coupled fluid step: bare moments, marker interpolation + direct
+ * forcing, ordered spreading, virtual force, collide+stream+open BC.
+ * Synchronous: returns the StepStatus. */
+int fsg_step(fsg_session* s, fsg_status* st);
+/* Enqueue the step on the session stream without waiting (status available
+ * through fsg_last_status after a later sync). */
+int fsg_step_async(fsg_session* s);
+int fsg_last_status(fsg_session* s, fsg_status* st);
+/* Per-marker world force on the FLUID (N) and validity of the last step
+ * (session.hpp:124-125, :130); CouplingStats per body (coupling.hpp:88-93):
+ * stats[7*b] = {force_on_fluid[3], force_on_body[3], power_on_body}. */
+int fsg_get_marker_forces(fsg_session* s, double* force_world, int* valid, double* stats);
+/* Bare macroscopic fields of the last step (CoupledSession::macro(), session.hpp:95-96). */
+int fsg_get_macro(fsg_session* s, double* rho, double* u);
+/* BodyForceField of the last step, IB + virtual force, AoS (session.hpp:148-163). */
+int fsg_get_force(fsg_session* s, double* F);
+/* Integer stencil sets of the last step, per marker: lo[3], hi[3] (kernel.hpp:36-40). */
+int fsg_get_stencils(fsg_session* s, int* lo_hi);
+
+/* ---- z-slab halo exchange ------------------------------
+ * In a slab session the 5 populations that cross each z face are packed into
+ * a caller-visible device buffer after each step and the neighbour's planes
+ * are unpacked from it before the next step.  Sizes in bytes. */
+size_t fsg_halo_bytes(fsg_session* s);
+int fsg_halo_pack(fsg_session* s, void* d_send_lo, void* d_send_hi);
+int fsg_halo_unpack(fsg_session* s, const void* d_recv_lo, const void* d_recv_hi);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FSG_H */

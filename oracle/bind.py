@@ -1,0 +1,243 @@
+"""ctypes bindings for the oracle -- TEST INFRASTRUCTURE ONLY.
+
+Two CPU libraries live here:
+
+* ``liboracle.so``       -- the plain-C fp64 restatement (fsg_oracle.c);
+* ``_ref/libfishref.so`` -- the reference's own headers compiled unmodified
+                            (ref_driver.cpp), present when /root/reference was
+                            available at build time (built here, shipped to
+                            the GPU box as a prebuilt .so).
+
+Only tests/, __graft_entry__.smoke() and bench.py's CPU-baseline leg import
+this module.  The product package (paper_2206_01683_b200) never does.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ORACLE_SO = os.path.join(HERE, "liboracle.so")
+REF_SO = os.path.join(HERE, "_ref", "libfishref.so")
+
+_dp = C.POINTER(C.c_double)
+_ip = C.POINTER(C.c_int)
+_i64p = C.POINTER(C.c_int64)
+
+
+def build() -> None:
+    """Build liboracle.so (and _ref when /root/reference exists)."""
+    subprocess.run(["make", "-s", "-C", HERE], check=True)
+
+
+def dptr(a: np.ndarray | None):
+    if a is None:
+        return None
+    assert a.dtype == np.float64 and a.flags.c_contiguous
+    return a.ctypes.data_as(_dp)
+
+
+def iptr(a: np.ndarray | None):
+    if a is None:
+        return None
+    assert a.dtype == np.int32 and a.flags.c_contiguous
+    return a.ctypes.data_as(_ip)
+
+
+def i64ptr(a: np.ndarray):
+    assert a.dtype == np.int64 and a.flags.c_contiguous
+    return a.ctypes.data_as(_i64p)
+
+
+def d3(v) -> np.ndarray:
+    return np.ascontiguousarray(np.asarray(v, dtype=np.float64).reshape(-1))
+
+
+def dims_arr(dims) -> np.ndarray:
+    return np.ascontiguousarray(np.asarray(dims, dtype=np.int32))
+
+
+# --------------------------------------------------------------------------
+class FrameState(C.Structure):
+    """orc_frame_state (frame.hpp:13-20): world-frame p, pd, pdd, q(w,x,y,z), omega, alpha."""
+
+    _fields_ = [("p", C.c_double * 3), ("pd", C.c_double * 3), ("pdd", C.c_double * 3),
+                ("q", C.c_double * 4), ("omega", C.c_double * 3), ("alpha", C.c_double * 3)]
+
+    @classmethod
+    def make(cls, p=(0, 0, 0), pd=(0, 0, 0), pdd=(0, 0, 0), q=(1, 0, 0, 0), omega=(0, 0, 0),
+             alpha=(0, 0, 0)):
+        fs = cls()
+        for name, v in (("p", p), ("pd", pd), ("pdd", pdd), ("q", q), ("omega", omega),
+                        ("alpha", alpha)):
+            arr = getattr(fs, name)
+            for k, x in enumerate(v):
+                arr[k] = float(x)
+        return fs
+
+    def as_arrays(self):
+        return {k: np.array(list(getattr(self, k))) for k in ("p", "pd", "pdd", "q", "omega", "alpha")}
+
+
+class FrameConsts(C.Structure):
+    _fields_ = [("R", C.c_double * 9), ("a0", C.c_double * 3), ("omega_f", C.c_double * 3),
+                ("alpha_f", C.c_double * 3)]
+
+
+_oracle = None
+_ref = None
+
+
+def oracle() -> C.CDLL:
+    global _oracle
+    if _oracle is None:
+        if not os.path.exists(ORACLE_SO):
+            build()
+        lib = C.CDLL(ORACLE_SO)
+        sig = {
+            "orc_tau": (C.c_double, [C.c_double, C.c_double, C.c_double]),
+            "orc_equilibrium_dir": (C.c_double, [C.c_int, C.c_double, _dp]),
+            "orc_initialize": (None, [_ip, _dp, _dp, _dp]),
+            "orc_macroscopic": (C.c_int, [_ip, _dp, _dp, _dp, _dp]),
+            "orc_apply_open_boundary": (None, [_ip, _dp]),
+            "orc_collide_and_stream": (None, [_ip, C.c_int, C.c_double, _dp, _dp, _dp, _ip, _dp]),
+            "orc_total_mass": (C.c_double, [_ip, _dp]),
+            "orc_total_momentum": (None, [_ip, _dp, _dp]),
+            "orc_phi": (C.c_double, [C.c_int, C.c_double]),
+            "orc_range": (None, [C.c_int, C.c_double, _ip, _ip]),
+            "orc_marker_in_bounds": (C.c_int, [C.c_int, _ip, _dp]),
+            "orc_interpolate": (None, [C.c_int, _ip, _dp, _dp, _dp]),
+            "orc_spread": (None, [C.c_int, _ip, _dp, _dp, _dp]),
+            "orc_direct_forcing": (None, [_dp, _dp, _dp, C.c_double, C.c_double, C.c_double,
+                                          C.c_double, C.c_int, _dp]),
+            "orc_frame_consts_of": (None, [C.POINTER(FrameState), C.POINTER(FrameConsts)]),
+            "orc_virtual_force": (None, [C.POINTER(FrameConsts), _dp, _dp, _dp]),
+            "orc_recenter": (None, [_ip, C.c_double, _dp, _dp, _ip, C.POINTER(FrameState)]),
+            "orc_session_create": (C.c_void_p, [_ip, C.c_double, C.c_double, C.c_double, C.c_double,
+                                                C.c_int, C.c_int, C.c_int, C.c_int]),
+            "orc_session_destroy": (None, [C.c_void_p]),
+            "orc_session_f": (_dp, [C.c_void_p]),
+            "orc_session_force": (_dp, [C.c_void_p]),
+            "orc_session_rho": (_dp, [C.c_void_p]),
+            "orc_session_u": (_dp, [C.c_void_p]),
+            "orc_session_set_frame": (None, [C.c_void_p, C.POINTER(FrameState)]),
+            "orc_session_get_frame": (None, [C.c_void_p, C.POINTER(FrameState)]),
+            "orc_session_step": (C.c_int, [C.c_void_p, C.c_int, _i64p, _dp, _dp, _dp, _dp, _dp,
+                                           _ip, _dp, _ip, _dp]),
+            "orc_session_recenter": (None, [C.c_void_p, _ip]),
+        }
+        for name, (res, args) in sig.items():
+            fn = getattr(lib, name)
+            fn.restype = res
+            fn.argtypes = args
+        _oracle = lib
+    return _oracle
+
+
+def have_ref() -> bool:
+    return os.path.exists(REF_SO)
+
+
+def ref() -> C.CDLL:
+    global _ref
+    if _ref is None:
+        lib = C.CDLL(REF_SO)
+        vp = C.c_void_p
+        sig = {
+            "ref_last_error": (C.c_char_p, []),
+            "ref_units_tau": (C.c_double, [C.c_double] * 4),
+            "ref_units_validate": (C.c_int, [C.c_double] * 4),
+            "ref_rng_uniform": (None, [C.c_uint64, C.c_int64, _dp]),
+            "ref_rng_normal": (None, [C.c_uint64, C.c_int64, _dp]),
+            "ref_session_create": (vp, [C.c_int, C.c_int, C.c_int, C.c_double, C.c_double,
+                                        C.c_double, C.c_double, C.c_int, C.c_int, C.c_int, C.c_int]),
+            "ref_session_destroy": (None, [vp]),
+            "ref_n_cells": (C.c_int64, [vp]),
+            "ref_reset_rest": (None, [vp]),
+            "ref_set_f": (None, [vp, _dp]),
+            "ref_get_f": (None, [vp, _dp]),
+            "ref_initialize": (None, [vp, _dp, _dp]),
+            "ref_set_force": (None, [vp, _dp]),
+            "ref_get_force": (None, [vp, _dp]),
+            "ref_collide_and_stream": (None, [vp, _ip, _dp]),
+            "ref_apply_open_boundary": (None, [vp]),
+            "ref_macroscopic": (C.c_int, [vp, _dp, _dp]),
+            "ref_total_mass": (C.c_double, [vp]),
+            "ref_total_momentum": (None, [vp, _dp]),
+            "ref_kinetic_energy": (C.c_double, [vp]),
+            "ref_set_frame": (None, [vp, _dp, _dp, _dp, _dp, _dp, _dp]),
+            "ref_get_frame_p": (None, [vp, _dp]),
+            "ref_frame_rotation": (None, [vp, _dp]),
+            "ref_recenter": (None, [vp, _ip]),
+            "ref_session_step": (C.c_int, [vp, C.c_int, _i64p, _dp, _dp, _dp, _dp, _dp, _ip, _dp,
+                                           _ip, _dp]),
+            "ref_get_macro": (None, [vp, _dp, _dp]),
+            "ref_session_marker_xlat": (None, [vp, C.c_int64, _dp, _dp]),
+            "ref_phi": (C.c_double, [C.c_int, C.c_double]),
+            "ref_range": (None, [C.c_int, C.c_double, _ip, _ip]),
+            "ref_marker_in_bounds": (C.c_int, [C.c_int, _ip, _dp]),
+            "ref_interpolate": (None, [C.c_int, _ip, _dp, C.c_int, _dp, _dp]),
+            "ref_spread": (None, [C.c_int, _ip, C.c_int, _dp, _dp, _dp]),
+            "ref_direct_forcing": (None, [_dp, _dp, _dp, C.c_double, C.c_double, C.c_double,
+                                          C.c_double, C.c_int, _dp]),
+            "ref_virtual_force": (None, [_dp, _dp, _dp, _dp, _dp, _dp, _dp]),
+            "ref_follower_create": (vp, [C.c_int, C.c_double]),
+            "ref_follower_destroy": (None, [vp]),
+            "ref_follower_reset": (None, [vp, _dp, C.c_double]),
+            "ref_follower_step": (None, [vp, _dp, _dp, C.c_double]),
+            "ref_follower_state": (None, [vp, _dp]),
+            "ref_quat_exp": (None, [_dp, _dp]),
+        }
+        for name, (res, args) in sig.items():
+            fn = getattr(lib, name)
+            fn.restype = res
+            fn.argtypes = args
+        _ref = lib
+    return _ref
+
+
+# --------------------------------------------------------------------------
+# Reference Rng (core/rng.hpp:14-84), restated in numpy for seeding inputs.
+_M64 = (1 << 64) - 1
+
+
+class Rng:
+    """xoshiro256** with splitmix64 seeding (rng.hpp:14-84), bit-identical to the reference."""
+
+    def __init__(self, seed: int = 0):
+        self.s = [0, 0, 0, 0]
+        x = seed & _M64
+        for k in range(4):
+            x = (x + 0x9E3779B97F4A7C15) & _M64
+            z = x
+            z = ((z ^ (z >> 30)) * 0xBF58476D1CE4E5B9) & _M64
+            z = ((z ^ (z >> 27)) * 0x94D049BB133111EB) & _M64
+            self.s[k] = z ^ (z >> 31)
+
+    @staticmethod
+    def _rotl(x, k):
+        return ((x << k) | (x >> (64 - k))) & _M64
+
+    def next_u64(self) -> int:
+        s = self.s
+        result = (self._rotl((s[1] * 5) & _M64, 7) * 9) & _M64
+        t = (s[1] << 17) & _M64
+        s[2] ^= s[0]
+        s[3] ^= s[1]
+        s[1] ^= s[2]
+        s[0] ^= s[3]
+        s[2] ^= t
+        s[3] = self._rotl(s[3], 45)
+        return result
+
+    def uniform(self, lo: float | None = None, hi: float | None = None) -> float:
+        u = (self.next_u64() >> 11) * (2.0 ** -53)
+        if lo is None:
+            return u
+        return lo + (hi - lo) * u
+
+    def uniforms(self, n: int) -> np.ndarray:
+        return np.array([self.uniform() for _ in range(n)], dtype=np.float64)

@@ -1,0 +1,102 @@
+/* fsg_oracle.h -- TEST INFRASTRUCTURE ONLY.
+ *
+ * Plain-C, fp64 restatement of the reference's IB-LBM hot path
+ * (FishGym, /root/reference/proj/include/fishsim, see each function's
+ * file:line).  It is the CHECKER for the CUDA product path: only tests/,
+ * __graft_entry__.smoke() and bench.py's cpu_baseline leg may load it.
+ *
+ * Parity pinning: every function here is compared bit-for-bit against the
+ * reference's own headers compiled unmodified into oracle/_ref/libfishref.so
+ * (tests/test_oracle.py), and the golden fixtures in tests/golden/ were
+ * produced by that same _ref build (tests/golden/make_golden.py).
+ *
+ * Layout conventions (lattice.hpp:83-90): cell = x + nx*(y + ny*z);
+ * distributions direction-major f[i*n + cell]; vector fields AoS [3*cell+k].
+ */
+#ifndef FSG_ORACLE_H
+#define FSG_ORACLE_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* lattice.hpp:17-38 */
+extern const int ORC_EX[19], ORC_EY[19], ORC_EZ[19];
+extern const double ORC_W[19];
+
+/* units.hpp:25-26 */
+double orc_tau(double dx, double dt, double nu);
+
+/* lattice.hpp:41-45 */
+double orc_equilibrium_dir(int i, double rho, const double u[3]);
+/* lattice.hpp:107-116 */
+void orc_initialize(const int dims[3], const double* rho, const double* u, double* f);
+
+/* solver.hpp:25-51 ; returns n_nonpositive_rho */
+int orc_macroscopic(const int dims[3], const double* f, const double* F, double* rho, double* u);
+/* solver.hpp:65-97 */
+void orc_apply_open_boundary(const int dims[3], double* f);
+/* solver.hpp:103-178 : reads fa, writes fb (then caller swaps), applies the
+ * open boundary to fb when !periodic. */
+void orc_collide_and_stream(const int dims[3], int periodic, double tau, const double* fa,
+                            double* fb, const double* F, int* finite, double* min_f);
+/* solver.hpp:181-200 */
+double orc_total_mass(const int dims[3], const double* f);
+void orc_total_momentum(const int dims[3], const double* f, double p[3]);
+
+/* kernel.hpp:22-40, coupling.hpp:18-24 ; kernel 0 = Peskin4, 1 = Roma3 */
+double orc_phi(int kernel, double r);
+void orc_range(int kernel, double x, int* lo, int* hi);
+int orc_marker_in_bounds(int kernel, const int dims[3], const double x[3]);
+/* coupling.hpp:27-48 */
+void orc_interpolate(int kernel, const int dims[3], const double* ufield, const double x[3],
+                     double out[3]);
+/* coupling.hpp:52-71 */
+void orc_spread(int kernel, const int dims[3], double* F, const double x[3], const double f[3]);
+/* coupling.hpp:80-85 ; wall 0 = Slip, 1 = NoSlip */
+void orc_direct_forcing(const double ub[3], const double uf[3], const double n[3], double rho,
+                        double area, double h, double dt, int wall, double out[3]);
+
+/* Frame constants derived from a world-frame FrameState (frame.hpp:13-53).
+ * q = (w,x,y,z).  R is row-major. */
+typedef struct {
+  double p[3], pd[3], pdd[3], q[4], omega[3], alpha[3];
+} orc_frame_state;
+typedef struct {
+  double R[9];       /* rotation() = q.toRotationMatrix()           */
+  double a0[3];      /* R^T pdd                                     */
+  double omega_f[3]; /* R^T omega                                   */
+  double alpha_f[3]; /* R^T alpha                                   */
+} orc_frame_consts;
+void orc_frame_consts_of(const orc_frame_state* fs, orc_frame_consts* fc);
+/* frame.hpp:47-53 */
+void orc_virtual_force(const orc_frame_consts* fc, const double x[3], const double u[3],
+                       double out[3]);
+/* frame.hpp:132-154 : dst <- src shifted, caller swaps; advances fs->p */
+void orc_recenter(const int dims[3], double dx, const double* src, double* dst, const int shift[3],
+                  orc_frame_state* fs);
+
+/* Session: the fluid half of CoupledSession::step (session.hpp:94-166). */
+typedef struct orc_session orc_session;
+orc_session* orc_session_create(const int dims[3], double dx, double dt, double rho, double nu,
+                                int periodic, int kernel, int wall, int frame_mode);
+void orc_session_destroy(orc_session* s);
+double* orc_session_f(orc_session* s);     /* current (post-stream) f, 19*n */
+double* orc_session_force(orc_session* s); /* F from the last step, 3*n     */
+double* orc_session_rho(orc_session* s);   /* bare macro of the last step   */
+double* orc_session_u(orc_session* s);
+void orc_session_set_frame(orc_session* s, const orc_frame_state* fs);
+void orc_session_get_frame(orc_session* s, orc_frame_state* fs);
+/* stats per body: fluid force[3], body force[3], power ; returns nonpos count */
+int orc_session_step(orc_session* s, int n_bodies, const int64_t* body_offsets,
+                     const double* points, const double* velocities, const double* normals,
+                     const double* areas, double* force_world, int* valid, double* stats,
+                     int* finite, double* min_f);
+void orc_session_recenter(orc_session* s, const int shift[3]);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

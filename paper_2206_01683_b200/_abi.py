@@ -1,0 +1,130 @@
+"""ctypes binding of the C ABI in include/fsg.h (libfsg.so, built in-tree).
+
+There is deliberately no fallback: if libfsg.so is missing or no CUDA device
+is visible the calls fail loudly (FsgError).  The CPU oracle lives in
+oracle/ and is never imported from here.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libfsg.so")
+
+FSG_OK, FSG_EINPUT, FSG_ECUDA, FSG_ESTATE = 0, 1, 2, 3
+
+
+class FsgError(RuntimeError):
+    """Raised for every non-zero fsg_* return code."""
+
+    def __init__(self, code: int, msg: str):
+        super().__init__(f"[fsg code {code}] {msg}")
+        self.code = code
+
+
+class InputError(FsgError, ValueError):
+    """Invalid configuration (the reference throws fishsim::InputError, types.hpp:27-30)."""
+
+
+class fsg_config(C.Structure):
+    _fields_ = [("dims", C.c_int * 3), ("dx", C.c_double), ("dt", C.c_double),
+                ("rho", C.c_double), ("nu", C.c_double), ("boundary", C.c_int),
+                ("kernel", C.c_int), ("wall", C.c_int), ("frame_mode", C.c_int),
+                ("precision", C.c_int), ("device", C.c_int), ("max_markers", C.c_int),
+                ("z_offset", C.c_int), ("nz_global", C.c_int)]
+
+
+class fsg_status(C.Structure):
+    _fields_ = [("finite", C.c_int), ("min_f", C.c_double), ("n_nonpositive_rho", C.c_int),
+                ("out_of_bounds_markers", C.c_int), ("stable", C.c_int)]
+
+
+class fsg_frame_state(C.Structure):
+    _fields_ = [("p", C.c_double * 3), ("pd", C.c_double * 3), ("pdd", C.c_double * 3),
+                ("q", C.c_double * 4), ("omega", C.c_double * 3), ("alpha", C.c_double * 3)]
+
+
+_dp = C.POINTER(C.c_double)
+_ip = C.POINTER(C.c_int)
+_i64p = C.POINTER(C.c_int64)
+_vp = C.c_void_p
+
+# name -> (restype, argtypes); this is the complete exported surface of fsg.h
+SIGNATURES = {
+    "fsg_last_error": (C.c_char_p, []),
+    "fsg_abi_version": (C.c_int, []),
+    "fsg_config_default": (None, [C.POINTER(fsg_config)]),
+    "fsg_tau": (C.c_double, [C.c_double, C.c_double, C.c_double]),
+    "fsg_create": (C.c_int, [C.POINTER(fsg_config), C.POINTER(_vp)]),
+    "fsg_destroy": (C.c_int, [_vp]),
+    "fsg_stream": (_vp, [_vp]),
+    "fsg_reset_rest": (C.c_int, [_vp]),
+    "fsg_initialize": (C.c_int, [_vp, _dp, _dp]),
+    "fsg_set_f": (C.c_int, [_vp, _dp]),
+    "fsg_get_f": (C.c_int, [_vp, _dp]),
+    "fsg_set_force": (C.c_int, [_vp, _dp]),
+    "fsg_collide_and_stream": (C.c_int, [_vp, C.POINTER(fsg_status)]),
+    "fsg_macroscopic": (C.c_int, [_vp, _dp, _dp, _ip]),
+    "fsg_total_mass": (C.c_int, [_vp, _dp]),
+    "fsg_total_momentum": (C.c_int, [_vp, _dp]),
+    "fsg_set_frame": (C.c_int, [_vp, C.POINTER(fsg_frame_state)]),
+    "fsg_get_frame": (C.c_int, [_vp, C.POINTER(fsg_frame_state)]),
+    "fsg_recenter": (C.c_int, [_vp, _ip]),
+    "fsg_set_markers": (C.c_int, [_vp, C.c_int, _i64p, _dp, _dp, _dp, _dp]),
+    "fsg_set_markers_device": (C.c_int, [_vp, C.c_int, _i64p, _vp, _vp, _vp, _vp]),
+    "fsg_step": (C.c_int, [_vp, C.POINTER(fsg_status)]),
+    "fsg_step_async": (C.c_int, [_vp]),
+    "fsg_last_status": (C.c_int, [_vp, C.POINTER(fsg_status)]),
+    "fsg_get_marker_forces": (C.c_int, [_vp, _dp, _ip, _dp]),
+    "fsg_get_macro": (C.c_int, [_vp, _dp, _dp]),
+    "fsg_get_force": (C.c_int, [_vp, _dp]),
+    "fsg_get_stencils": (C.c_int, [_vp, _ip]),
+    "fsg_halo_bytes": (C.c_size_t, [_vp]),
+    "fsg_halo_pack": (C.c_int, [_vp, _vp, _vp]),
+    "fsg_halo_unpack": (C.c_int, [_vp, _vp, _vp]),
+}
+
+_lib = None
+
+
+def lib() -> C.CDLL:
+    """Load libfsg.so (raises if it was not built: there is no CPU fallback)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise FsgError(FSG_ECUDA, f"{LIB_PATH} not built; run __graft_entry__.build() "
+                                      "(the B200 path has no CPU fallback)")
+        L = C.CDLL(LIB_PATH)
+        for name, (res, args) in SIGNATURES.items():
+            fn = getattr(L, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = L
+    return _lib
+
+
+def check(rc: int) -> None:
+    if rc != FSG_OK:
+        msg = lib().fsg_last_error().decode(errors="replace")
+        if rc == FSG_EINPUT:
+            raise InputError(rc, msg)
+        raise FsgError(rc, msg)
+
+
+def dptr(a: np.ndarray | None):
+    if a is None:
+        return None
+    if a.dtype != np.float64 or not a.flags.c_contiguous:
+        raise TypeError("expected a C-contiguous float64 array")
+    return a.ctypes.data_as(_dp)
+
+
+def iptr(a: np.ndarray | None):
+    if a is None:
+        return None
+    if a.dtype != np.int32 or not a.flags.c_contiguous:
+        raise TypeError("expected a C-contiguous int32 array")
+    return a.ctypes.data_as(_ip)

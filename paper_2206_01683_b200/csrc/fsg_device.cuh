@@ -1,0 +1,175 @@
+// fsg_device.cuh -- shared device-side definitions for the FishGym IB-LBM
+// hot path on B200 (sm_100a).  Included by the two precision translation
+// units (fsg_kernels_fp32.cu, fsg_kernels_fp64.cu) and by the host session.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace fsg {
+
+// ----------------------------------------------------------------- D3Q19 --
+// lattice.hpp:17-38 : 0 rest, 1-6 axes (+x,-x,+y,-y,+z,-z), 7-18 diagonals.
+__host__ __device__ __forceinline__ constexpr int ex_of(int i) {
+  constexpr int t[19] = {0, 1, -1, 0, 0, 0, 0, 1, -1, 1, -1, 1, -1, 1, -1, 0, 0, 0, 0};
+  return t[i];
+}
+__host__ __device__ __forceinline__ constexpr int ey_of(int i) {
+  constexpr int t[19] = {0, 0, 0, 1, -1, 0, 0, 1, -1, -1, 1, 0, 0, 0, 0, 1, -1, 1, -1};
+  return t[i];
+}
+__host__ __device__ __forceinline__ constexpr int ez_of(int i) {
+  constexpr int t[19] = {0, 0, 0, 0, 0, 1, -1, 0, 0, 0, 0, 1, -1, -1, 1, 1, -1, -1, 1};
+  return t[i];
+}
+__host__ __device__ __forceinline__ constexpr double w_of(int i) {
+  return i == 0 ? 1.0 / 3.0 : (i <= 6 ? 1.0 / 18.0 : 1.0 / 36.0);
+}
+constexpr int Q = 19;
+
+// --------------------------------------------------------------- layout --
+// One direction plane holds the slab's owned cells plus `zpad` halo planes
+// below and above (z-slab decomposition).  Element (i, x, y, z_local) lives at
+//   i*stride + x + nx*(y + ny*(z_local + zpad)).
+struct Grid {
+  int nx, ny, nz;    // local (owned) dims
+  int nzg, z0;       // global z extent, global z of local plane 0
+  int zpad;          // halo planes per side (0 single GPU, 1 slab)
+  int periodic;
+  int _pad;
+  long long n;       // owned cells nx*ny*nz
+  long long plane;   // nx*ny
+  long long stride;  // elements per direction array (>= plane*(nz+2*zpad), 32-aligned)
+};
+
+__host__ __device__ __forceinline__ long long mem_index(const Grid& g, int x, int y, int z) {
+  return (long long)x + (long long)g.nx * ((long long)y + (long long)g.ny * (long long)(z + g.zpad));
+}
+
+// ------------------------------------------------------ device constants --
+// Per-session constants (host-computed in fp64 exactly as the reference).
+struct SessionConsts {
+  double omega;      // 1/tau                            solver.hpp:109
+  double guo;        // 1 - omega/2                      solver.hpp:110
+  double dx, dt, rho_phys;
+  double v2p;        // dx/dt          vel_to_physical  units.hpp:31
+  double acc;        // dt*dt/dx       session.hpp:149
+  double f2l;        // dt^2/(rho dx^4) session.hpp:128
+  double hd[3];      // 0.5*(d-1)      session.hpp:79-85 (global dims)
+  int dims_g[3];     // global dims (marker_in_bounds)
+  int kernel;        // 0 Peskin4, 1 Roma3
+  int wall;          // 0 slip, 1 no-slip
+  int frame_on;      // frame_mode != None
+};
+
+// Per-step frame constants (frame.hpp:21-53), host-computed in fp64.
+struct StepConsts {
+  double R[9];       // row-major rotation()
+  double p[3], pd[3];
+  double a0[3];      // R^T pdd
+  double wf[3];      // R^T omega
+  double af[3];      // R^T alpha
+};
+
+// Per-step scratch, reset to all-zero bytes before every step.  Encodings are
+// chosen so that zero bytes == "empty": min via max of ~key, bbox lo via max
+// of (LO_BIAS - lo), bbox hi via max of (hi + 1).
+struct StepScratch {
+  unsigned long long neg_min_key;  // ~ordered_key(min post), 0 == +inf
+  int nonfinite;                   // 1 if any cell had non-finite rho+u2
+  int nonpos;                      // count of rho <= 0 cells
+  int oob;                         // out-of-bounds markers
+  int band_overflow;               // bbox exceeded band capacity
+  int bbox_lo_enc[3];
+  int bbox_hi_enc[3];
+  int _pad[2];
+};
+constexpr int LO_BIAS = 0x40000000;
+
+__host__ __device__ __forceinline__ unsigned long long ordered_key(double v) {
+#ifdef __CUDA_ARCH__
+  unsigned long long b = (unsigned long long)__double_as_longlong(v);
+#else
+  unsigned long long b;
+  __builtin_memcpy(&b, &v, 8);
+#endif
+  return (b >> 63) ? ~b : (b | 0x8000000000000000ull);
+}
+__host__ __device__ __forceinline__ double key_to_double(unsigned long long k) {
+  unsigned long long b = (k >> 63) ? (k & 0x7fffffffffffffffull) : ~k;
+#ifdef __CUDA_ARCH__
+  return __longlong_as_double((long long)b);
+#else
+  double v;
+  __builtin_memcpy(&v, &b, 8);
+  return v;
+#endif
+}
+
+// Per-marker stencil record written by the prepare kernel.
+struct MarkerStencil {
+  double xf[3];      // frame position (m)
+  double xl[3];      // lattice position
+  double ph[3][5];   // phi(k - x_a) for k = lo_a .. hi_a (kernel.hpp:22-33)
+  double fl[3];      // lattice force to spread (session.hpp:128, :136-138)
+  int lo[3], hi[3];  // inclusive ranges (kernel.hpp:36-40)
+  int valid;
+  int _pad;
+};
+
+// Marker input arrays (SI world frame, session.hpp:113-126).
+struct Markers {
+  const double* pts;
+  const double* vel;
+  const double* nrm;
+  const double* area;
+  int m;
+};
+
+// Compact IB band (bounding box of all valid stencils, local coordinates).
+struct Band {
+  double* u;         // bare velocity, 3 per band cell
+  double* F;         // spread IB force, 3 per band cell
+  long long cap;     // capacity in cells
+};
+
+// ---------------------------------------------------------- kernel table --
+// Launchers exported by each precision translation unit.
+struct Launchers {
+  void (*fill_rest)(const Grid&, void* A, cudaStream_t);
+  void (*set_f)(const Grid&, const double* f, void* A, cudaStream_t);
+  void (*init_eq)(const Grid&, const double* rho, const double* u, void* A, cudaStream_t);
+  // S readback (post-stream state) into double f[19*n]
+  void (*get_f)(const Grid&, const void* A, int pulled, double* f, cudaStream_t);
+  // moments of S with optional external force (SoA 3 x n, math type); rho[n], u[3n]
+  void (*macroscopic)(const Grid&, const void* A, int pulled, const void* Fext, double* rho,
+                      double* u, StepScratch*, cudaStream_t);
+  // collide + stream (+ open BC via clamped pull) A -> B
+  void (*collide)(const Grid&, const void* A, int pulled, void* B, const void* Fext,
+                  const Band*, const StepScratch*, const SessionConsts*, const StepConsts*,
+                  StepScratch*, int session_force, int frame_on, cudaStream_t);
+  // full F readback of a session step: IB band + virtual force, AoS double
+  void (*session_force)(const Grid&, const void* A, int pulled, const Band*, const StepScratch*,
+                        const SessionConsts*, const StepConsts*, int frame_on, double* F,
+                        cudaStream_t);
+  void (*recenter)(const Grid&, const void* A, int pulled, void* B, int sx, int sy, int sz,
+                   cudaStream_t);
+  // IB
+  void (*markers_prepare)(const Grid&, Markers, const SessionConsts*, const StepConsts*,
+                          MarkerStencil*, StepScratch*, cudaStream_t);
+  void (*band_moments)(const Grid&, const void* A, int pulled, Band, const StepScratch*,
+                       StepScratch*, cudaStream_t);
+  void (*markers_force)(const Grid&, Markers, const SessionConsts*, const StepConsts*,
+                        MarkerStencil*, Band, const StepScratch*, double* fworld, cudaStream_t);
+  void (*spread)(const Grid&, int m, const MarkerStencil*, Band, const StepScratch*, cudaStream_t);
+  // halo planes (z-slab): pack owned boundary planes / unpack into halo planes
+  void (*halo_pack)(const Grid&, const void* B, void* send_lo, void* send_hi, cudaStream_t);
+  void (*halo_unpack)(const Grid&, void* B, const void* recv_lo, const void* recv_hi,
+                      cudaStream_t);
+  int elem_bytes;
+};
+
+const Launchers& launchers_fp32();
+const Launchers& launchers_fp64();
+
+}  // namespace fsg

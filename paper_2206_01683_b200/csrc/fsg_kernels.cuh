@@ -1,0 +1,932 @@
+// fsg_kernels.cuh -- the IB-LBM hot-path kernels, written once and compiled
+// twice (included by fsg_kernels_fp32.cu and fsg_kernels_fp64.cu with
+// FSG_PREC set to 32 or 64).
+//
+//   FSG_PREC == 64 : parity mode.  f stored as fp64; every expression keeps
+//                    the reference's operation order and the TU is built
+//                    with --fmad=false, so results are bit-identical to the
+//                    reference (oracle/_ref) on the same inputs.
+//   FSG_PREC == 32 : throughput mode.  f stored as fp32 deviations
+//                    g_i = f_i - w_i (152 B per cell update); the collision is
+//                    evaluated in deviation form, so rounding is relative to
+//                    O(|u|) quantities rather than O(1) ones.
+//
+// Streaming is PULL (gather) with the reference's push + open-boundary
+// semantics re-expressed as clamped gathers (solver.hpp:59-97, :157-169):
+//   source(c, i) = c - e_i                        if c - e_i is inside the box
+//                = wrap(c - e_i)                  periodic
+//                = clamp(c, 1, n-2) - e_i         open (neighbour copy)
+// The stored array therefore holds POST-COLLISION populations P_n; the
+// reference's post-stream state S_{n+1} is gather(P_n).  After set/init/
+// recenter the array holds S directly ("pulled" == 0) and the next step is
+// collide-only.
+#pragma once
+
+#include <float.h>
+#include <math.h>
+
+#include "fsg_device.cuh"
+
+#ifndef FSG_PREC
+#error "define FSG_PREC to 32 or 64"
+#endif
+
+namespace fsg {
+#if FSG_PREC == 64
+namespace p64 {
+using Store = double;
+using Real = double;
+#else
+namespace p32 {
+using Store = float;
+using Real = float;
+#endif
+
+// -------------------------------------------------------------- helpers --
+template <int i>
+__device__ __forceinline__ double to_abs(Store s) {
+#if FSG_PREC == 64
+  return s;
+#else
+  return (double)s + w_of(i);
+#endif
+}
+template <int i>
+__device__ __forceinline__ Store from_abs(double f) {
+#if FSG_PREC == 64
+  return f;
+#else
+  return (float)(f - w_of(i));
+#endif
+}
+
+__device__ __forceinline__ int clampi(int v, int lo, int hi) { return v < lo ? lo : (v > hi ? hi : v); }
+
+/// Memory index of the population that streams into (x,y,z) along i
+/// (pull form of solver.hpp:157-169 + apply_open_boundary :65-97).
+template <int i>
+__device__ __forceinline__ long long pull_src(const Grid& g, int x, int y, int z, bool interior) {
+  constexpr int ex = ex_of(i), ey = ey_of(i), ez = ez_of(i);
+  if (interior) return mem_index(g, x - ex, y - ey, z - ez);
+  const int sx = x - ex, sy = y - ey, sz = z - ez;
+  const int szg = g.z0 + sz;
+  const bool known = (unsigned)sx < (unsigned)g.nx && (unsigned)sy < (unsigned)g.ny &&
+                     (unsigned)szg < (unsigned)g.nzg;
+  if (known) return mem_index(g, sx, sy, sz);
+  if (g.periodic) {
+    const int wx = (sx + g.nx) % g.nx, wy = (sy + g.ny) % g.ny;
+    const int wz = g.zpad == 0 ? (sz + g.nz) % g.nz : sz;  // slab: halo holds the wrap
+    return mem_index(g, wx, wy, wz);
+  }
+  const int cx = clampi(x, 1, g.nx - 2), cy = clampi(y, 1, g.ny - 2);
+  const int cz = clampi(g.z0 + z, 1, g.nzg - 2) - g.z0;
+  return mem_index(g, cx - ex, cy - ey, cz - ez);
+}
+
+__device__ __forceinline__ bool is_interior(const Grid& g, int x, int y, int z) {
+  const int zg = g.z0 + z;
+  return x > 0 && x < g.nx - 1 && y > 0 && y < g.ny - 1 && zg > 0 && zg < g.nzg - 1;
+}
+
+/// Gather the 19 post-stream populations S(x,y,z) in storage form.
+template <bool PULLED>
+__device__ __forceinline__ void gather(const Grid& g, const Store* __restrict__ A, int x, int y,
+                                       int z, Store s[Q]) {
+  if (!PULLED) {
+    const long long m = mem_index(g, x, y, z);
+#pragma unroll
+    for (int i = 0; i < Q; ++i) s[i] = A[i * g.stride + m];
+  } else {
+    const bool interior = is_interior(g, x, y, z);
+    s[0] = A[pull_src<0>(g, x, y, z, interior)];
+#define FSG_G(I) s[I] = A[(long long)(I)*g.stride + pull_src<I>(g, x, y, z, interior)];
+    FSG_G(1) FSG_G(2) FSG_G(3) FSG_G(4) FSG_G(5) FSG_G(6) FSG_G(7) FSG_G(8) FSG_G(9)
+    FSG_G(10) FSG_G(11) FSG_G(12) FSG_G(13) FSG_G(14) FSG_G(15) FSG_G(16) FSG_G(17) FSG_G(18)
+#undef FSG_G
+  }
+}
+
+template <int a, int b, int c, class T>
+__device__ __forceinline__ T edot(T x, T y, T z) {
+  // e.v for a D3Q19 direction without multiplying by zero components
+  if constexpr (a == 0 && b == 0 && c == 0) return T(0);
+  else if constexpr (b == 0 && c == 0) return a > 0 ? x : -x;
+  else if constexpr (a == 0 && c == 0) return b > 0 ? y : -y;
+  else if constexpr (a == 0 && b == 0) return c > 0 ? z : -z;
+  else if constexpr (c == 0) return (a > 0 ? x : -x) + (b > 0 ? y : -y);
+  else if constexpr (b == 0) return (a > 0 ? x : -x) + (c > 0 ? z : -z);
+  else return (b > 0 ? y : -y) + (c > 0 ? z : -z);
+}
+
+// ---------------------------------------------------- cell moments -------
+#if FSG_PREC == 64
+/// rho, (mx,my,mz) in the reference's accumulation order (solver.hpp:129-136).
+__device__ __forceinline__ void moments(const Store s[Q], double& rho, double& mx, double& my,
+                                        double& mz) {
+  rho = 0.0;
+  mx = 0.0;
+  my = 0.0;
+  mz = 0.0;
+#pragma unroll
+  for (int i = 0; i < Q; ++i) {
+    rho += s[i];
+    mx += s[i] * (double)ex_of(i);
+    my += s[i] * (double)ey_of(i);
+    mz += s[i] * (double)ez_of(i);
+  }
+}
+#else
+/// deviation moments: drho = sum g, m = sum e g (sum w e = 0 exactly)
+__device__ __forceinline__ void moments_dev(const Store g[Q], float& drho, float& mx, float& my,
+                                            float& mz) {
+  drho = ((g[0] + (g[1] + g[2])) + ((g[3] + g[4]) + (g[5] + g[6]))) +
+         (((g[7] + g[8]) + (g[9] + g[10])) + ((g[11] + g[12]) + (g[13] + g[14]))) +
+         ((g[15] + g[16]) + (g[17] + g[18]));
+  mx = ((g[1] - g[2]) + (g[7] - g[8])) + ((g[9] - g[10]) + ((g[11] - g[12]) + (g[13] - g[14])));
+  my = ((g[3] - g[4]) + (g[7] - g[8])) + ((g[10] - g[9]) + ((g[15] - g[16]) + (g[17] - g[18])));
+  mz = ((g[5] - g[6]) + (g[11] - g[12])) + ((g[14] - g[13]) + ((g[15] - g[16]) + (g[18] - g[17])));
+}
+#endif
+
+// ------------------------------------------------------- virtual force ---
+/// frame.hpp:47-53 with the session's lattice scaling (session.hpp:148-163):
+/// returns rho*acc*a for the cell at lattice (i,j,k) with bare velocity u.
+template <class T>
+__device__ __forceinline__ void vf_term(const SessionConsts& sc, const StepConsts& st, int i,
+                                        int j, int k, T rho, T ubx, T uby, T ubz, T& fx, T& fy,
+                                        T& fz) {
+  const T dx = (T)sc.dx, v2p = (T)sc.v2p;
+  // cell_frame_position (session.hpp:77-81)
+  const T x0 = ((T)i - (T)sc.hd[0]) * dx;
+  const T x1 = ((T)j - (T)sc.hd[1]) * dx;
+  const T x2 = ((T)k - (T)sc.hd[2]) * dx;
+  const T u0 = ubx * v2p, u1 = uby * v2p, u2 = ubz * v2p;
+  const T w0 = (T)st.wf[0], w1 = (T)st.wf[1], w2 = (T)st.wf[2];
+  const T a0 = (T)st.af[0], a1 = (T)st.af[1], a2 = (T)st.af[2];
+  // alpha' x x
+  const T ax0 = a1 * x2 - a2 * x1, ax1 = a2 * x0 - a0 * x2, ax2 = a0 * x1 - a1 * x0;
+  // omega' x x, omega' x (omega' x x)
+  const T wx0 = w1 * x2 - w2 * x1, wx1 = w2 * x0 - w0 * x2, wx2 = w0 * x1 - w1 * x0;
+  const T ww0 = w1 * wx2 - w2 * wx1, ww1 = w2 * wx0 - w0 * wx2, ww2 = w0 * wx1 - w1 * wx0;
+  // omega' x u
+  const T wu0 = w1 * u2 - w2 * u1, wu1 = w2 * u0 - w0 * u2, wu2 = w0 * u1 - w1 * u0;
+  const T A0 = -(T)st.a0[0] - ax0 - ww0 - (T)2 * wu0;
+  const T A1 = -(T)st.a0[1] - ax1 - ww1 - (T)2 * wu1;
+  const T A2 = -(T)st.a0[2] - ax2 - ww2 - (T)2 * wu2;
+  const T ra = rho * (T)sc.acc;
+  fx = ra * A0;
+  fy = ra * A1;
+  fz = ra * A2;
+}
+
+__device__ __forceinline__ void decode_bbox(const StepScratch* sc, int lo[3], int hi[3]) {
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    lo[a] = LO_BIAS - sc->bbox_lo_enc[a];
+    hi[a] = sc->bbox_hi_enc[a] - 1;
+  }
+}
+
+// ------------------------------------------------------ block reduction --
+__device__ __forceinline__ void report_min(StepScratch* out, double v) {
+  // warp min, then one lane per warp does check-then-atomic (few atomics/step)
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmin(v, __shfl_xor_sync(0xffffffffu, v, o));
+  if ((threadIdx.x & 31) == 0 && !isnan(v)) {
+    const unsigned long long nk = ~ordered_key(v);
+    const unsigned long long cur = *(volatile unsigned long long*)&out->neg_min_key;
+    if (nk > cur) atomicMax(&out->neg_min_key, nk);
+  }
+}
+
+// =============================================================== K4 ======
+// Fused: [moments of S] + [virtual force] + [IB band force] + BGK/Guo
+// collide (solver.hpp:103-178) + pull stream + open/periodic BC.
+// FMODE: 0 no force, 1 external full-grid force (SoA, Real), 2 session force
+// (IB band from K_d, plus virtual force when frame_on).
+template <bool PULLED, int FMODE, bool VF>
+__global__ void __launch_bounds__(128) k_collide(Grid g, const Store* __restrict__ A,
+                                                 Store* __restrict__ B,
+                                                 const Real* __restrict__ Fext, Band band,
+                                                 const StepScratch* __restrict__ bscr,
+                                                 const SessionConsts* __restrict__ scp,
+                                                 const StepConsts* __restrict__ stp,
+                                                 StepScratch* __restrict__ out) {
+  const int x = blockIdx.x * blockDim.x + threadIdx.x;
+  const int y = blockIdx.y * blockDim.y + threadIdx.y;
+  const int z = blockIdx.z;
+  const bool live = x < g.nx && y < g.ny;
+  double vmin = DBL_MAX;
+  if (live) {
+    Store s[Q];
+    gather<PULLED>(g, A, x, y, z, s);
+    const long long m = mem_index(g, x, y, z);
+    const SessionConsts& sc = *scp;
+    // -------- force F for this cell
+    Real Fx = 0, Fy = 0, Fz = 0;
+    if constexpr (FMODE == 1) {
+      const long long c = (long long)x + (long long)g.nx * ((long long)y + (long long)g.ny * z);
+      Fx = Fext[c];
+      Fy = Fext[g.n + c];
+      Fz = Fext[2 * g.n + c];
+    }
+    bool in_band = false;
+    long long lc = 0;
+    if constexpr (FMODE == 2) {
+      int lo[3], hi[3];
+      decode_bbox(bscr, lo, hi);
+      in_band = x >= lo[0] && x <= hi[0] && y >= lo[1] && y <= hi[1] && z >= lo[2] && z <= hi[2];
+      if (in_band)
+        lc = (long long)(x - lo[0]) +
+             (long long)(hi[0] - lo[0] + 1) * ((long long)(y - lo[1]) + (long long)(hi[1] - lo[1] + 1) * (z - lo[2]));
+    }
+#if FSG_PREC == 64
+    double rho, mx, my, mz;
+    moments(s, rho, mx, my, mz);
+    if constexpr (FMODE == 2) {
+      // BodyForceField cleared to zero, IB spread accumulated (K_d), then the
+      // virtual force added on top (session.hpp:95, :129-144, :148-163)
+      Fx = in_band ? band.F[3 * lc] : 0.0;
+      Fy = in_band ? band.F[3 * lc + 1] : 0.0;
+      Fz = in_band ? band.F[3 * lc + 2] : 0.0;
+      if constexpr (VF) {
+        double bx = 0.0, by = 0.0, bz = 0.0;
+        if (rho > 0.0) {  // macroscopic_into with F = 0 (solver.hpp:42-48)
+          bx = (mx + 0.5 * 0.0) / rho;
+          by = (my + 0.5 * 0.0) / rho;
+          bz = (mz + 0.5 * 0.0) / rho;
+        }
+        double vx, vy, vz;
+        vf_term<double>(sc, *stp, x, y, g.z0 + z, rho, bx, by, bz, vx, vy, vz);
+        Fx = Fx + vx;
+        Fy = Fy + vy;
+        Fz = Fz + vz;
+      }
+      if (!(rho > 0.0)) atomicAdd(&out->nonpos, 1);
+    }
+    const double omega = sc.omega, guo = sc.guo;
+    const double inv_rho = 1.0 / rho;
+    const double ux = (mx + 0.5 * Fx) * inv_rho;
+    const double uy = (my + 0.5 * Fy) * inv_rho;
+    const double uz = (mz + 0.5 * Fz) * inv_rho;
+    const double u2 = ux * ux + uy * uy + uz * uz;
+    if (!isfinite(rho + u2)) out->nonfinite = 1;
+#pragma unroll
+    for (int i = 0; i < Q; ++i) {
+      const double exd = ex_of(i), eyd = ey_of(i), ezd = ez_of(i);
+      const double eu = exd * ux + eyd * uy + ezd * uz;
+      const double feq = w_of(i) * rho * (1.0 + 3.0 * eu + 4.5 * eu * eu - 1.5 * u2);
+      const double sx = 3.0 * (exd - ux) + 9.0 * eu * exd;
+      const double sy = 3.0 * (eyd - uy) + 9.0 * eu * eyd;
+      const double sz = 3.0 * (ezd - uz) + 9.0 * eu * ezd;
+      const double src = guo * w_of(i) * (sx * Fx + sy * Fy + sz * Fz);
+      const double post = s[i] - omega * (s[i] - feq) + src;
+      vmin = post < vmin ? post : vmin;
+      B[i * g.stride + m] = post;
+    }
+#else
+    float drho, mx, my, mz;
+    moments_dev(s, drho, mx, my, mz);
+    const float rho = 1.0f + drho;
+    if constexpr (FMODE == 2) {
+      Fx = in_band ? (float)band.F[3 * lc] : 0.0f;
+      Fy = in_band ? (float)band.F[3 * lc + 1] : 0.0f;
+      Fz = in_band ? (float)band.F[3 * lc + 2] : 0.0f;
+      if constexpr (VF) {
+        float bx = 0.f, by = 0.f, bz = 0.f;
+        if (rho > 0.0f) {
+          const float ir = 1.0f / rho;
+          bx = mx * ir;
+          by = my * ir;
+          bz = mz * ir;
+        }
+        float vx, vy, vz;
+        vf_term<float>(sc, *stp, x, y, g.z0 + z, rho, bx, by, bz, vx, vy, vz);
+        Fx += vx;
+        Fy += vy;
+        Fz += vz;
+      }
+      if (!(rho > 0.0f)) atomicAdd(&out->nonpos, 1);
+    }
+    const float omega = (float)sc.omega;
+    const float om1 = (float)(1.0 - sc.omega);
+    const float inv_rho = 1.0f / rho;
+    const float ux = (mx + 0.5f * Fx) * inv_rho;
+    const float uy = (my + 0.5f * Fy) * inv_rho;
+    const float uz = (mz + 0.5f * Fz) * inv_rho;
+    const float u2 = ux * ux + uy * uy + uz * uz;
+    if (!isfinite(rho + u2)) out->nonfinite = 1;
+    const float uF = ux * Fx + uy * Fy + uz * Fz;
+    const float h15u2 = 1.5f * u2;
+    // weight classes: 0 rest, 1 axes, 2 diagonals
+    const float ow[3] = {(float)(sc.omega * (1.0 / 3.0)), (float)(sc.omega * (1.0 / 18.0)),
+                         (float)(sc.omega * (1.0 / 36.0))};
+    const float gw[3] = {(float)(sc.guo * (1.0 / 3.0)), (float)(sc.guo * (1.0 / 18.0)),
+                         (float)(sc.guo * (1.0 / 36.0))};
+    float fmin_dev = FLT_MAX;  // min over (post - w_i) per weight class is not enough; track abs
+    (void)omega;
+#define FSG_DIR(I)                                                                        \
+  {                                                                                       \
+    constexpr int a = ex_of(I), b = ey_of(I), c = ez_of(I);                               \
+    constexpr int cls = (I) == 0 ? 0 : ((I) <= 6 ? 1 : 2);                                \
+    const float eu = edot<a, b, c, float>(ux, uy, uz);                                    \
+    const float eF = edot<a, b, c, float>(Fx, Fy, Fz);                                    \
+    const float X = fmaf(eu, fmaf(4.5f, eu, 3.0f), -h15u2);                               \
+    const float geq_w = fmaf(rho, X, drho);                                               \
+    const float srcw = fmaf(fmaf(9.0f, eu, 3.0f), eF, -3.0f * uF);                        \
+    const float gp = fmaf(om1, s[I], fmaf(ow[cls], geq_w, gw[cls] * srcw));               \
+    fmin_dev = fminf(fmin_dev, gp + (float)w_of(I));                                      \
+    B[(long long)(I)*g.stride + m] = gp;                                                  \
+  }
+    FSG_DIR(0) FSG_DIR(1) FSG_DIR(2) FSG_DIR(3) FSG_DIR(4) FSG_DIR(5) FSG_DIR(6)
+    FSG_DIR(7) FSG_DIR(8) FSG_DIR(9) FSG_DIR(10) FSG_DIR(11) FSG_DIR(12) FSG_DIR(13)
+    FSG_DIR(14) FSG_DIR(15) FSG_DIR(16) FSG_DIR(17) FSG_DIR(18)
+#undef FSG_DIR
+    vmin = (double)fmin_dev;
+#endif
+  }
+  report_min(out, vmin);
+}
+
+// ====================================================== small kernels =====
+__global__ void k_fill_rest(Grid g, Store* A) {
+  const long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (t >= g.n) return;
+  const int x = (int)(t % g.nx);
+  const int y = (int)((t / g.nx) % g.ny);
+  const int z = (int)(t / g.plane);
+  const long long m = mem_index(g, x, y, z);
+  // LatticeGrid::reset_to_rest (lattice.hpp:98-104): f_i = w_i (deviation 0)
+#pragma unroll
+  for (int i = 0; i < Q; ++i) {
+#if FSG_PREC == 64
+    A[i * g.stride + m] = w_of(i);
+#else
+    A[i * g.stride + m] = 0.0f;
+#endif
+  }
+}
+
+__global__ void k_set_f(Grid g, const double* __restrict__ f, Store* A) {
+  const long long c = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (c >= g.n) return;
+  const int x = (int)(c % g.nx);
+  const int y = (int)((c / g.nx) % g.ny);
+  const int z = (int)(c / g.plane);
+  const long long m = mem_index(g, x, y, z);
+#define FSG_S(I) A[(long long)(I)*g.stride + m] = from_abs<I>(f[(long long)(I)*g.n + c]);
+  FSG_S(0) FSG_S(1) FSG_S(2) FSG_S(3) FSG_S(4) FSG_S(5) FSG_S(6) FSG_S(7) FSG_S(8) FSG_S(9)
+  FSG_S(10) FSG_S(11) FSG_S(12) FSG_S(13) FSG_S(14) FSG_S(15) FSG_S(16) FSG_S(17) FSG_S(18)
+#undef FSG_S
+}
+
+/// LatticeGrid::initialize (lattice.hpp:107-116) with equilibrium_dir (:41-45).
+__global__ void k_init_eq(Grid g, const double* __restrict__ rho, const double* __restrict__ u,
+                          Store* A) {
+  const long long c = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (c >= g.n) return;
+  const int x = (int)(c % g.nx);
+  const int y = (int)((c / g.nx) % g.ny);
+  const int z = (int)(c / g.plane);
+  const long long m = mem_index(g, x, y, z);
+  const double r = rho[c], ux = u[3 * c], uy = u[3 * c + 1], uz = u[3 * c + 2];
+#pragma unroll
+  for (int i = 0; i < Q; ++i) {
+    const double eu = ex_of(i) * ux + ey_of(i) * uy + ez_of(i) * uz;
+    const double u2 = ux * ux + uy * uy + uz * uz;
+    const double feq = w_of(i) * r * (1.0 + 3.0 * eu + 4.5 * eu * eu - 1.5 * u2);
+#if FSG_PREC == 64
+    A[i * g.stride + m] = feq;
+#else
+    // deviation computed without cancellation: w*(r-1 + r*(3eu + 4.5eu^2 - 1.5u2))
+    A[i * g.stride + m] = (float)(w_of(i) * ((r - 1.0) + r * (3.0 * eu + 4.5 * eu * eu - 1.5 * u2)));
+    (void)feq;
+#endif
+  }
+}
+
+template <bool PULLED>
+__global__ void k_get_f(Grid g, const Store* __restrict__ A, double* __restrict__ f) {
+  const long long c = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (c >= g.n) return;
+  const int x = (int)(c % g.nx);
+  const int y = (int)((c / g.nx) % g.ny);
+  const int z = (int)(c / g.plane);
+  Store s[Q];
+  gather<PULLED>(g, A, x, y, z, s);
+#define FSG_O(I) f[(long long)(I)*g.n + c] = to_abs<I>(s[I]);
+  FSG_O(0) FSG_O(1) FSG_O(2) FSG_O(3) FSG_O(4) FSG_O(5) FSG_O(6) FSG_O(7) FSG_O(8) FSG_O(9)
+  FSG_O(10) FSG_O(11) FSG_O(12) FSG_O(13) FSG_O(14) FSG_O(15) FSG_O(16) FSG_O(17) FSG_O(18)
+#undef FSG_O
+}
+
+/// Moments of S (solver.hpp:25-51) into rho[n], u[3n] (fp64 out).
+template <bool PULLED, bool BARE>
+__device__ __forceinline__ void cell_moments(const Grid& g, const Store* __restrict__ A, int x,
+                                             int y, int z, double Fx, double Fy, double Fz,
+                                             double& rho_o, double& ux, double& uy, double& uz,
+                                             bool& bad) {
+  Store s[Q];
+  gather<PULLED>(g, A, x, y, z, s);
+#if FSG_PREC == 64
+  double rho, mx, my, mz;
+  moments(s, rho, mx, my, mz);
+  rho_o = rho;
+  bad = !(rho > 0.0);
+  if (bad) {
+    ux = uy = uz = 0.0;
+    return;
+  }
+  ux = (mx + 0.5 * Fx) / rho;
+  uy = (my + 0.5 * Fy) / rho;
+  uz = (mz + 0.5 * Fz) / rho;
+#else
+  float drho, mx, my, mz;
+  moments_dev(s, drho, mx, my, mz);
+  const float rho = 1.0f + drho;
+  rho_o = 1.0 + (double)drho;
+  bad = !(rho > 0.0f);
+  if (bad) {
+    ux = uy = uz = 0.0;
+    return;
+  }
+  ux = (mx + 0.5f * (float)Fx) / rho;
+  uy = (my + 0.5f * (float)Fy) / rho;
+  uz = (mz + 0.5f * (float)Fz) / rho;
+#endif
+  (void)BARE;
+}
+
+template <bool PULLED>
+__global__ void k_macroscopic(Grid g, const Store* __restrict__ A, const Real* __restrict__ Fext,
+                              double* __restrict__ rho, double* __restrict__ u, StepScratch* out) {
+  const long long c = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (c >= g.n) return;
+  const int x = (int)(c % g.nx);
+  const int y = (int)((c / g.nx) % g.ny);
+  const int z = (int)(c / g.plane);
+  const double Fx = Fext ? (double)Fext[c] : 0.0, Fy = Fext ? (double)Fext[g.n + c] : 0.0,
+               Fz = Fext ? (double)Fext[2 * g.n + c] : 0.0;
+  double r, ux, uy, uz;
+  bool bad;
+  cell_moments<PULLED, false>(g, A, x, y, z, Fx, Fy, Fz, r, ux, uy, uz, bad);
+  rho[c] = r;
+  u[3 * c] = ux;
+  u[3 * c + 1] = uy;
+  u[3 * c + 2] = uz;
+  if (bad) atomicAdd(&out->nonpos, 1);
+}
+
+/// Session BodyForceField readback: band IB force + virtual force (AoS).
+template <bool PULLED>
+__global__ void k_session_force(Grid g, const Store* __restrict__ A, Band band,
+                                const StepScratch* __restrict__ bscr,
+                                const SessionConsts* __restrict__ scp,
+                                const StepConsts* __restrict__ stp, int frame_on,
+                                double* __restrict__ F) {
+  const long long c = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (c >= g.n) return;
+  const int x = (int)(c % g.nx);
+  const int y = (int)((c / g.nx) % g.ny);
+  const int z = (int)(c / g.plane);
+  int lo[3], hi[3];
+  decode_bbox(bscr, lo, hi);
+  double Fx = 0.0, Fy = 0.0, Fz = 0.0;
+  if (x >= lo[0] && x <= hi[0] && y >= lo[1] && y <= hi[1] && z >= lo[2] && z <= hi[2]) {
+    const long long lc = (long long)(x - lo[0]) +
+                         (long long)(hi[0] - lo[0] + 1) *
+                             ((long long)(y - lo[1]) + (long long)(hi[1] - lo[1] + 1) * (z - lo[2]));
+    Fx = band.F[3 * lc];
+    Fy = band.F[3 * lc + 1];
+    Fz = band.F[3 * lc + 2];
+  }
+  if (frame_on) {
+    double r, ux, uy, uz;
+    bool bad;
+    cell_moments<PULLED, true>(g, A, x, y, z, 0.0, 0.0, 0.0, r, ux, uy, uz, bad);
+    double vx, vy, vz;
+#if FSG_PREC == 64
+    vf_term<double>(*scp, *stp, x, y, g.z0 + z, r, ux, uy, uz, vx, vy, vz);
+#else
+    float fx, fy, fz;
+    vf_term<float>(*scp, *stp, x, y, g.z0 + z, (float)r, (float)ux, (float)uy, (float)uz, fx, fy,
+                   fz);
+    vx = fx;
+    vy = fy;
+    vz = fz;
+#endif
+    Fx = Fx + vx;
+    Fy = Fy + vy;
+    Fz = Fz + vz;
+  }
+  F[3 * c] = Fx;
+  F[3 * c + 1] = Fy;
+  F[3 * c + 2] = Fz;
+}
+
+/// frame::recenter (frame.hpp:132-154): B(x) = S(clamp(x + shift)).
+template <bool PULLED>
+__global__ void k_recenter(Grid g, const Store* __restrict__ A, Store* __restrict__ B, int sx,
+                           int sy, int sz) {
+  const long long c = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (c >= g.n) return;
+  const int x = (int)(c % g.nx);
+  const int y = (int)((c / g.nx) % g.ny);
+  const int z = (int)(c / g.plane);
+  const int qx = clampi(x + sx, 0, g.nx - 1), qy = clampi(y + sy, 0, g.ny - 1),
+            qz = clampi(z + sz, 0, g.nz - 1);
+  Store s[Q];
+  gather<PULLED>(g, A, qx, qy, qz, s);
+  const long long m = mem_index(g, x, y, z);
+#pragma unroll
+  for (int i = 0; i < Q; ++i) B[i * g.stride + m] = s[i];
+}
+
+// ====================================================== IB kernels =======
+/// IBKernel::phi (kernel.hpp:22-33), fp64.
+__device__ __forceinline__ double ib_phi(int kernel, double r) {
+  const double a = fabs(r);
+  if (kernel == 0) {
+    if (a >= 2.0) return 0.0;
+    if (a <= 1.0) return 0.125 * (3.0 - 2.0 * a + sqrt(1.0 + 4.0 * a - 4.0 * a * a));
+    return 0.125 * (5.0 - 2.0 * a - sqrt(-7.0 + 12.0 * a - 4.0 * a * a));
+  }
+  if (a <= 0.5) return (1.0 + sqrt(1.0 - 3.0 * r * r)) / 3.0;
+  if (a <= 1.5) return (5.0 - 3.0 * a - sqrt(-3.0 * (1.0 - a) * (1.0 - a) + 1.0)) / 6.0;
+  return 0.0;
+}
+
+/// r = R^T v in Eigen's coefficient order (R row-major).
+__device__ __forceinline__ void mat_t_vec(const double* R, const double* v, double* r) {
+#pragma unroll
+  for (int i = 0; i < 3; ++i) r[i] = R[i] * v[0] + R[3 + i] * v[1] + R[6 + i] * v[2];
+}
+__device__ __forceinline__ void mat_vec(const double* R, const double* v, double* r) {
+#pragma unroll
+  for (int i = 0; i < 3; ++i) r[i] = R[3 * i] * v[0] + R[3 * i + 1] * v[1] + R[3 * i + 2] * v[2];
+}
+
+/// K_a: per marker world->frame->lattice (frame.hpp:24-26, session.hpp:82-85),
+/// marker_in_bounds (coupling.hpp:18-24), stencil ranges (kernel.hpp:36-40),
+/// per-axis phi values, band bounding box.
+__global__ void k_markers_prepare(Grid g, Markers mk, const SessionConsts* __restrict__ scp,
+                                  const StepConsts* __restrict__ stp, MarkerStencil* st,
+                                  StepScratch* out) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= mk.m) return;
+  const SessionConsts& sc = *scp;
+  const StepConsts& fs = *stp;
+  MarkerStencil r;
+  double xw[3];
+#pragma unroll
+  for (int k = 0; k < 3; ++k) xw[k] = mk.pts[3 * t + k] - fs.p[k];
+  mat_t_vec(fs.R, xw, r.xf);
+#pragma unroll
+  for (int k = 0; k < 3; ++k) r.xl[k] = r.xf[k] / sc.dx + sc.hd[k];
+  const double margin = 0.5 * (sc.kernel == 0 ? 4 : 3);
+  bool ok = true;
+#pragma unroll
+  for (int a = 0; a < 3; ++a)
+    if (r.xl[a] < margin || r.xl[a] > sc.dims_g[a] - 1 - margin) ok = false;
+  r.valid = ok ? 1 : 0;
+  if (!ok) {
+    atomicAdd(&out->oob, 1);
+    st[t] = r;
+    return;
+  }
+  const double half = 0.5 * (sc.kernel == 0 ? 4 : 3);
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    r.lo[a] = (int)ceil(r.xl[a] - half);
+    r.hi[a] = (int)floor(r.xl[a] + half);
+    // valid markers never touch the box edge; the clip of coupling.hpp:35-39 is a no-op
+#pragma unroll
+    for (int q = 0; q < 5; ++q) r.ph[a][q] = q <= r.hi[a] - r.lo[a] ? ib_phi(sc.kernel, (r.lo[a] + q) - r.xl[a]) : 0.0;
+  }
+  r.fl[0] = r.fl[1] = r.fl[2] = 0.0;
+  st[t] = r;
+  // bounding box in local z for slabs
+  atomicMax(&out->bbox_lo_enc[0], LO_BIAS - r.lo[0]);
+  atomicMax(&out->bbox_lo_enc[1], LO_BIAS - r.lo[1]);
+  atomicMax(&out->bbox_lo_enc[2], LO_BIAS - max(r.lo[2] - g.z0, 0));
+  atomicMax(&out->bbox_hi_enc[0], r.hi[0] + 1);
+  atomicMax(&out->bbox_hi_enc[1], r.hi[1] + 1);
+  atomicMax(&out->bbox_hi_enc[2], min(r.hi[2] - g.z0, g.nz - 1) + 1);
+}
+
+/// K_b: bare moments (macroscopic_into with F = 0, session.hpp:95-96) over the band.
+template <bool PULLED>
+__global__ void k_band_moments(Grid g, const Store* __restrict__ A, Band band,
+                               const StepScratch* __restrict__ bscr, StepScratch* out) {
+  int lo[3], hi[3];
+  decode_bbox(bscr, lo, hi);
+  if (hi[0] < lo[0] || hi[1] < lo[1] || hi[2] < lo[2]) return;
+  const long long bnx = hi[0] - lo[0] + 1, bny = hi[1] - lo[1] + 1, bnz = hi[2] - lo[2] + 1;
+  const long long nb = bnx * bny * bnz;
+  if (nb > band.cap) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) out->band_overflow = 1;
+    return;
+  }
+  for (long long lc = blockIdx.x * (long long)blockDim.x + threadIdx.x; lc < nb;
+       lc += (long long)gridDim.x * blockDim.x) {
+    const int x = lo[0] + (int)(lc % bnx);
+    const int y = lo[1] + (int)((lc / bnx) % bny);
+    const int z = lo[2] + (int)(lc / (bnx * bny));
+    double r, ux, uy, uz;
+    bool bad;
+    cell_moments<PULLED, true>(g, A, x, y, z, 0.0, 0.0, 0.0, r, ux, uy, uz, bad);
+    band.u[3 * lc] = ux;
+    band.u[3 * lc + 1] = uy;
+    band.u[3 * lc + 2] = uz;
+  }
+}
+
+/// K_c: interpolate_velocity (coupling.hpp:27-48), body_velocity_to_frame
+/// (frame.hpp:39-42), direct_forcing (coupling.hpp:80-85), world force and
+/// the lattice force to spread (session.hpp:113-138).  One thread per marker,
+/// serial stencil sum in the reference's k, j, i order.
+__global__ void k_markers_force(Grid g, Markers mk, const SessionConsts* __restrict__ scp,
+                                const StepConsts* __restrict__ stp, MarkerStencil* st, Band band,
+                                const StepScratch* __restrict__ bscr, double* __restrict__ fworld) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= mk.m) return;
+  MarkerStencil& r = st[t];
+  if (!r.valid) {
+    fworld[3 * t] = fworld[3 * t + 1] = fworld[3 * t + 2] = 0.0;
+    return;
+  }
+  const SessionConsts& sc = *scp;
+  const StepConsts& fs = *stp;
+  int lo[3], hi[3];
+  decode_bbox(bscr, lo, hi);
+  const long long bnx = hi[0] - lo[0] + 1, bny = hi[1] - lo[1] + 1;
+  double u0 = 0.0, u1 = 0.0, u2 = 0.0;
+  for (int k = r.lo[2]; k <= r.hi[2]; ++k) {
+    const double wz = r.ph[2][k - r.lo[2]];
+    for (int j = r.lo[1]; j <= r.hi[1]; ++j) {
+      const double wyz = wz * r.ph[1][j - r.lo[1]];
+      for (int i = r.lo[0]; i <= r.hi[0]; ++i) {
+        const double w = wyz * r.ph[0][i - r.lo[0]];
+        const long long lc = (long long)(i - lo[0]) + bnx * ((long long)(j - lo[1]) + bny * (long long)(k - g.z0 - lo[2]));
+        u0 = u0 + w * band.u[3 * lc];
+        u1 = u1 + w * band.u[3 * lc + 1];
+        u2 = u2 + w * band.u[3 * lc + 2];
+      }
+    }
+  }
+  const double uf[3] = {u0 * sc.v2p, u1 * sc.v2p, u2 * sc.v2p};
+  double vw[3], vf[3], ub[3], nf[3], fl[3], fw[3], ff[3];
+#pragma unroll
+  for (int k = 0; k < 3; ++k) vw[k] = mk.vel[3 * t + k] - fs.pd[k];
+  mat_t_vec(fs.R, vw, vf);
+  const double wx0 = fs.wf[1] * r.xf[2] - fs.wf[2] * r.xf[1];
+  const double wx1 = fs.wf[2] * r.xf[0] - fs.wf[0] * r.xf[2];
+  const double wx2 = fs.wf[0] * r.xf[1] - fs.wf[1] * r.xf[0];
+  ub[0] = vf[0] - wx0;
+  ub[1] = vf[1] - wx1;
+  ub[2] = vf[2] - wx2;
+  mat_t_vec(fs.R, mk.nrm + 3 * t, nf);
+  double du[3] = {ub[0] - uf[0], ub[1] - uf[1], ub[2] - uf[2]};
+  if (sc.wall == 0) {
+    const double s = du[0] * nf[0] + du[1] * nf[1] + du[2] * nf[2];
+    du[0] = s * nf[0];
+    du[1] = s * nf[1];
+    du[2] = s * nf[2];
+  }
+  const double kf = sc.rho_phys * mk.area[t] * sc.dx / sc.dt;
+  fl[0] = kf * du[0];
+  fl[1] = kf * du[1];
+  fl[2] = kf * du[2];
+  mat_vec(fs.R, fl, fw);
+  fworld[3 * t] = fw[0];
+  fworld[3 * t + 1] = fw[1];
+  fworld[3 * t + 2] = fw[2];
+  mat_t_vec(fs.R, fw, ff);
+  r.fl[0] = ff[0] * sc.f2l;
+  r.fl[1] = ff[1] * sc.f2l;
+  r.fl[2] = ff[2] * sc.f2l;
+}
+
+/// K_d: spread_force (coupling.hpp:52-71) driven serially in ascending marker
+/// order (session.hpp:129-144), re-expressed as a gather: each band cell sums
+/// its contributions in ascending marker order, after a per-tile ordered cull
+/// of the marker list.  Deterministic, no float atomics, bit-identical to the
+/// serial loop.
+constexpr int SP_TX = 8, SP_TY = 4, SP_TZ = 4, SP_THREADS = 128, SP_CAP = 1024;
+__global__ void __launch_bounds__(SP_THREADS) k_spread(Grid g, int m, const MarkerStencil* __restrict__ st,
+                                                      Band band, const StepScratch* __restrict__ bscr) {
+  __shared__ int list[SP_CAP];
+  __shared__ int warp_tot[SP_THREADS / 32];
+  __shared__ int count_s;
+  int lo[3], hi[3];
+  decode_bbox(bscr, lo, hi);
+  if (hi[0] < lo[0] || hi[1] < lo[1] || hi[2] < lo[2]) return;
+  const int bnx = hi[0] - lo[0] + 1, bny = hi[1] - lo[1] + 1, bnz = hi[2] - lo[2] + 1;
+  if ((long long)bnx * bny * bnz > band.cap) return;
+  const int tnx = (bnx + SP_TX - 1) / SP_TX, tny = (bny + SP_TY - 1) / SP_TY, tnz = (bnz + SP_TZ - 1) / SP_TZ;
+  const int ntiles = tnx * tny * tnz;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const int tx0 = lo[0] + (tile % tnx) * SP_TX;
+    const int ty0 = lo[1] + ((tile / tnx) % tny) * SP_TY;
+    const int tz0 = lo[2] + (tile / (tnx * tny)) * SP_TZ;  // local z
+    const int tx1 = min(tx0 + SP_TX - 1, hi[0]), ty1 = min(ty0 + SP_TY - 1, hi[1]),
+              tz1 = min(tz0 + SP_TZ - 1, hi[2]);
+    const int cx = tx0 + (threadIdx.x % SP_TX);
+    const int cy = ty0 + ((threadIdx.x / SP_TX) % SP_TY);
+    const int cz = tz0 + threadIdx.x / (SP_TX * SP_TY);
+    const int czg = cz + g.z0;
+    double F0 = 0.0, F1 = 0.0, F2 = 0.0;
+    if (threadIdx.x == 0) count_s = 0;
+    __syncthreads();
+    for (int base = 0; base < m; base += SP_THREADS) {
+      const int mi = base + threadIdx.x;
+      bool hit = false;
+      if (mi < m) {
+        const MarkerStencil& r = st[mi];
+        hit = r.valid && r.lo[0] <= tx1 && r.hi[0] >= tx0 && r.lo[1] <= ty1 && r.hi[1] >= ty0 &&
+              r.lo[2] - g.z0 <= tz1 && r.hi[2] - g.z0 >= tz0;
+      }
+      const unsigned bal = __ballot_sync(0xffffffffu, hit);
+      if (lane == 0) warp_tot[wid] = __popc(bal);
+      __syncthreads();
+      int off = count_s;
+      for (int w = 0; w < wid; ++w) off += warp_tot[w];
+      if (hit) list[off + __popc(bal & ((1u << lane) - 1u))] = mi;
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        int tot = 0;
+        for (int w = 0; w < SP_THREADS / 32; ++w) tot += warp_tot[w];
+        count_s += tot;
+      }
+      __syncthreads();
+      const int cnt = count_s;
+      if (cnt > SP_CAP - SP_THREADS || base + SP_THREADS >= m) {
+        // drain the list in ascending marker order
+        for (int q = 0; q < cnt; ++q) {
+          const MarkerStencil& r = st[list[q]];
+          if (cx >= r.lo[0] && cx <= r.hi[0] && cy >= r.lo[1] && cy <= r.hi[1] && czg >= r.lo[2] &&
+              czg <= r.hi[2]) {
+            const double w = (r.ph[2][czg - r.lo[2]] * r.ph[1][cy - r.lo[1]]) * r.ph[0][cx - r.lo[0]];
+            F0 = F0 + w * r.fl[0];
+            F1 = F1 + w * r.fl[1];
+            F2 = F2 + w * r.fl[2];
+          }
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) count_s = 0;
+        __syncthreads();
+      }
+    }
+    if (cx <= tx1 && cy <= ty1 && cz <= tz1) {
+      const long long lc = (long long)(cx - lo[0]) + (long long)bnx * ((long long)(cy - lo[1]) + (long long)bny * (cz - lo[2]));
+      band.F[3 * lc] = F0;
+      band.F[3 * lc + 1] = F1;
+      band.F[3 * lc + 2] = F2;
+    }
+    __syncthreads();
+  }
+}
+
+// ======================================================= halo (slabs) ====
+// Populations crossing a z face (lattice.hpp:25-26): ez=+1 {5,11,14,15,18},
+// ez=-1 {6,12,13,16,17}.
+__device__ __forceinline__ int up_dir(int k) { return k == 0 ? 5 : k == 1 ? 11 : k == 2 ? 14 : k == 3 ? 15 : 18; }
+__device__ __forceinline__ int dn_dir(int k) { return k == 0 ? 6 : k == 1 ? 12 : k == 2 ? 13 : k == 3 ? 16 : 17; }
+
+__global__ void k_halo_pack(Grid g, const Store* __restrict__ B, Store* send_lo, Store* send_hi) {
+  const long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (t >= 5 * g.plane) return;
+  const int k = (int)(t / g.plane);
+  const long long xy = t % g.plane;
+  // top owned plane, ez=+1 populations -> upper neighbour
+  send_hi[t] = B[up_dir(k) * g.stride + g.plane * (g.nz - 1 + g.zpad) + xy];
+  // bottom owned plane, ez=-1 populations -> lower neighbour
+  send_lo[t] = B[dn_dir(k) * g.stride + g.plane * (0 + g.zpad) + xy];
+}
+__global__ void k_halo_unpack(Grid g, Store* B, const Store* __restrict__ recv_lo,
+                              const Store* __restrict__ recv_hi) {
+  const long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (t >= 5 * g.plane) return;
+  const int k = (int)(t / g.plane);
+  const long long xy = t % g.plane;
+  // lower neighbour's top plane (ez=+1) -> halo plane z = -1
+  if (recv_lo) B[up_dir(k) * g.stride + xy] = recv_lo[t];
+  // upper neighbour's bottom plane (ez=-1) -> halo plane z = nz
+  if (recv_hi) B[dn_dir(k) * g.stride + g.plane * (g.nz + g.zpad) + xy] = recv_hi[t];
+}
+
+// ======================================================== launchers =====
+inline dim3 cell_block(const Grid& g) {
+  int bx = g.nx >= 128 ? 128 : ((g.nx + 31) / 32) * 32;
+  if (bx > 128) bx = 128;
+  return dim3(bx, 128 / bx, 1);
+}
+inline dim3 cell_grid(const Grid& g, dim3 b) {
+  return dim3((g.nx + b.x - 1) / b.x, (g.ny + b.y - 1) / b.y, g.nz);
+}
+inline unsigned lin_blocks(long long n, int t) { return (unsigned)((n + t - 1) / t); }
+
+static void L_fill_rest(const Grid& g, void* A, cudaStream_t s) {
+  k_fill_rest<<<lin_blocks(g.n, 256), 256, 0, s>>>(g, (Store*)A);
+}
+static void L_set_f(const Grid& g, const double* f, void* A, cudaStream_t s) {
+  k_set_f<<<lin_blocks(g.n, 256), 256, 0, s>>>(g, f, (Store*)A);
+}
+static void L_init_eq(const Grid& g, const double* rho, const double* u, void* A, cudaStream_t s) {
+  k_init_eq<<<lin_blocks(g.n, 256), 256, 0, s>>>(g, rho, u, (Store*)A);
+}
+static void L_get_f(const Grid& g, const void* A, int pulled, double* f, cudaStream_t s) {
+  if (pulled)
+    k_get_f<true><<<lin_blocks(g.n, 128), 128, 0, s>>>(g, (const Store*)A, f);
+  else
+    k_get_f<false><<<lin_blocks(g.n, 128), 128, 0, s>>>(g, (const Store*)A, f);
+}
+static void L_macroscopic(const Grid& g, const void* A, int pulled, const void* Fext, double* rho,
+                          double* u, StepScratch* out, cudaStream_t s) {
+  if (pulled)
+    k_macroscopic<true><<<lin_blocks(g.n, 128), 128, 0, s>>>(g, (const Store*)A, (const Real*)Fext, rho, u, out);
+  else
+    k_macroscopic<false><<<lin_blocks(g.n, 128), 128, 0, s>>>(g, (const Store*)A, (const Real*)Fext, rho, u, out);
+}
+template <bool P, int FM, bool VF>
+static void launch_collide_t(const Grid& g, const void* A, void* B, const void* Fext,
+                             const Band* band, const StepScratch* bscr, const SessionConsts* sc,
+                             const StepConsts* st, StepScratch* out, cudaStream_t s) {
+  const dim3 b = cell_block(g);
+  Band bd = band ? *band : Band{nullptr, nullptr, 0};
+  k_collide<P, FM, VF><<<cell_grid(g, b), b, 0, s>>>(g, (const Store*)A, (Store*)B, (const Real*)Fext,
+                                                     bd, bscr, sc, st, out);
+}
+static void L_collide(const Grid& g, const void* A, int pulled, void* B, const void* Fext,
+                      const Band* band, const StepScratch* bscr, const SessionConsts* sc,
+                      const StepConsts* st, StepScratch* out, int session_force, int frame_on,
+                      cudaStream_t s) {
+  const int fm = session_force ? 2 : (Fext ? 1 : 0);
+#define FSG_LC(P, FM, VF) launch_collide_t<P, FM, VF>(g, A, B, Fext, band, bscr, sc, st, out, s)
+  if (pulled) {
+    if (fm == 0) FSG_LC(true, 0, false);
+    else if (fm == 1) FSG_LC(true, 1, false);
+    else if (frame_on) FSG_LC(true, 2, true);
+    else FSG_LC(true, 2, false);
+  } else {
+    if (fm == 0) FSG_LC(false, 0, false);
+    else if (fm == 1) FSG_LC(false, 1, false);
+    else if (frame_on) FSG_LC(false, 2, true);
+    else FSG_LC(false, 2, false);
+  }
+#undef FSG_LC
+}
+static void L_session_force(const Grid& g, const void* A, int pulled, const Band* band,
+                            const StepScratch* bscr, const SessionConsts* sc, const StepConsts* st,
+                            int frame_on, double* F, cudaStream_t s) {
+  if (pulled)
+    k_session_force<true><<<lin_blocks(g.n, 128), 128, 0, s>>>(g, (const Store*)A, *band, bscr, sc, st, frame_on, F);
+  else
+    k_session_force<false><<<lin_blocks(g.n, 128), 128, 0, s>>>(g, (const Store*)A, *band, bscr, sc, st, frame_on, F);
+}
+static void L_recenter(const Grid& g, const void* A, int pulled, void* B, int sx, int sy, int sz,
+                       cudaStream_t s) {
+  if (pulled)
+    k_recenter<true><<<lin_blocks(g.n, 128), 128, 0, s>>>(g, (const Store*)A, (Store*)B, sx, sy, sz);
+  else
+    k_recenter<false><<<lin_blocks(g.n, 128), 128, 0, s>>>(g, (const Store*)A, (Store*)B, sx, sy, sz);
+}
+static void L_markers_prepare(const Grid& g, Markers mk, const SessionConsts* sc,
+                              const StepConsts* st, MarkerStencil* ms, StepScratch* out,
+                              cudaStream_t s) {
+  if (mk.m == 0) return;
+  k_markers_prepare<<<lin_blocks(mk.m, 128), 128, 0, s>>>(g, mk, sc, st, ms, out);
+}
+static void L_band_moments(const Grid& g, const void* A, int pulled, Band band,
+                           const StepScratch* bscr, StepScratch* out, cudaStream_t s) {
+  if (pulled)
+    k_band_moments<true><<<296, 128, 0, s>>>(g, (const Store*)A, band, bscr, out);
+  else
+    k_band_moments<false><<<296, 128, 0, s>>>(g, (const Store*)A, band, bscr, out);
+}
+static void L_markers_force(const Grid& g, Markers mk, const SessionConsts* sc,
+                            const StepConsts* st, MarkerStencil* ms, Band band,
+                            const StepScratch* bscr, double* fworld, cudaStream_t s) {
+  if (mk.m == 0) return;
+  k_markers_force<<<lin_blocks(mk.m, 64), 64, 0, s>>>(g, mk, sc, st, ms, band, bscr, fworld);
+}
+static void L_spread(const Grid& g, int m, const MarkerStencil* ms, Band band,
+                     const StepScratch* bscr, cudaStream_t s) {
+  if (m == 0) return;
+  k_spread<<<296, SP_THREADS, 0, s>>>(g, m, ms, band, bscr);
+}
+static void L_halo_pack(const Grid& g, const void* B, void* lo, void* hi, cudaStream_t s) {
+  k_halo_pack<<<lin_blocks(5 * g.plane, 256), 256, 0, s>>>(g, (const Store*)B, (Store*)lo, (Store*)hi);
+}
+static void L_halo_unpack(const Grid& g, void* B, const void* lo, const void* hi, cudaStream_t s) {
+  k_halo_unpack<<<lin_blocks(5 * g.plane, 256), 256, 0, s>>>(g, (Store*)B, (const Store*)lo, (const Store*)hi);
+}
+
+static const Launchers kLaunchers = {
+    L_fill_rest,    L_set_f,          L_init_eq,      L_get_f,         L_macroscopic,
+    L_collide,      L_session_force,  L_recenter,     L_markers_prepare, L_band_moments,
+    L_markers_force, L_spread,        L_halo_pack,    L_halo_unpack,   (int)sizeof(Store)};
+
+}  // namespace p32 / p64
+}  // namespace fsg

@@ -1,0 +1,301 @@
+"""Python mirror of the reference's hot-path API over the C ABI.
+
+Names and argument meaning follow FishGym's C++ API so that tests read like
+the reference's own Catch2 tests:
+
+* ``SessionConfig``            <- sim::SessionConfig (session.hpp:12-24) + UnitMap (units.hpp:18-23)
+* ``CoupledSession``           <- sim::CoupledSession (session.hpp:29-224), fluid half of step()
+* ``CoupledSession.collide_and_stream / macroscopic / total_mass / total_momentum``
+                               <- lbm::collide_and_stream etc. (solver.hpp:25-206)
+* ``FrameState``               <- frame::FrameState (frame.hpp:13-43)
+* ``StepStatus``               <- lbm::StepStatus (solver.hpp:13-20) / StepOutcome (backend.hpp:37-40)
+
+Errors: invalid configuration raises ``InputError`` (reference: InputError),
+instability is reported in the returned status, never raised.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _abi
+from ._abi import check, dptr, iptr
+
+BOUNDARY = {"periodic": 0, "open": 1}
+KERNEL = {"peskin4": 0, "roma3": 1}
+WALL = {"slip": 0, "noslip": 1}
+FRAME = {"none": 0, "translation": 1, "translation_yaw": 2, "full": 3}
+PRECISION = {"fp32": 0, "fp64": 1}
+
+
+def tau_of(dx: float, dt: float, nu: float) -> float:
+    """UnitMap::tau (units.hpp:25): 3 nu dt/dx^2 + 1/2."""
+    return _abi.lib().fsg_tau(dx, dt, nu)
+
+
+@dataclass
+class SessionConfig:
+    dims: tuple = (64, 64, 64)
+    dx: float = 0.01
+    dt: float = 0.004
+    rho: float = 1000.0
+    nu: float = 0.00089
+    boundary: str = "open"
+    kernel: str = "peskin4"
+    wall: str = "slip"
+    frame_mode: str = "translation_yaw"
+    precision: str = "fp32"
+    device: int = 0
+    max_markers: int = 65536
+    z_offset: int = 0
+    nz_global: int = 0
+
+    @staticmethod
+    def lattice_units(dims, tau: float, **kw) -> "SessionConfig":
+        """dx = dt = rho = 1 with nu chosen to hit tau (test_lattice.cpp:16-24)."""
+        return SessionConfig(dims=tuple(dims), dx=1.0, dt=1.0, rho=1.0, nu=(tau - 0.5) / 3.0, **kw)
+
+    def to_c(self) -> _abi.fsg_config:
+        c = _abi.fsg_config()
+        for k in range(3):
+            c.dims[k] = int(self.dims[k])
+        c.dx, c.dt, c.rho, c.nu = float(self.dx), float(self.dt), float(self.rho), float(self.nu)
+        c.boundary = BOUNDARY[self.boundary]
+        c.kernel = KERNEL[self.kernel]
+        c.wall = WALL[self.wall]
+        c.frame_mode = FRAME[self.frame_mode]
+        c.precision = PRECISION[self.precision]
+        c.device = int(self.device)
+        c.max_markers = int(self.max_markers)
+        c.z_offset = int(self.z_offset)
+        c.nz_global = int(self.nz_global)
+        return c
+
+    @property
+    def tau(self) -> float:
+        return tau_of(self.dx, self.dt, self.nu)
+
+
+@dataclass
+class StepStatus:
+    finite: bool
+    min_f: float
+    n_nonpositive_rho: int = 0
+    out_of_bounds_markers: int = 0
+    ok: bool = True
+
+    def stable(self, negative_tolerance: float = 1e-3) -> bool:
+        """solver.hpp:17-19 (plus the session's rho check, session.hpp:97)."""
+        return self.finite and self.min_f > -negative_tolerance and self.n_nonpositive_rho == 0
+
+    @classmethod
+    def of(cls, s: _abi.fsg_status) -> "StepStatus":
+        return cls(bool(s.finite), float(s.min_f), int(s.n_nonpositive_rho),
+                   int(s.out_of_bounds_markers), bool(s.stable))
+
+
+@dataclass
+class FrameState:
+    """frame::FrameState (frame.hpp:13-20), world frame; q = (w, x, y, z)."""
+
+    p: np.ndarray = field(default_factory=lambda: np.zeros(3))
+    pd: np.ndarray = field(default_factory=lambda: np.zeros(3))
+    pdd: np.ndarray = field(default_factory=lambda: np.zeros(3))
+    q: np.ndarray = field(default_factory=lambda: np.array([1.0, 0.0, 0.0, 0.0]))
+    omega: np.ndarray = field(default_factory=lambda: np.zeros(3))
+    alpha: np.ndarray = field(default_factory=lambda: np.zeros(3))
+
+    def to_c(self) -> _abi.fsg_frame_state:
+        c = _abi.fsg_frame_state()
+        for name in ("p", "pd", "pdd", "q", "omega", "alpha"):
+            arr = getattr(c, name)
+            for k, v in enumerate(np.asarray(getattr(self, name), dtype=np.float64)):
+                arr[k] = float(v)
+        return c
+
+    @classmethod
+    def of(cls, c: _abi.fsg_frame_state) -> "FrameState":
+        return cls(*(np.array(list(getattr(c, n))) for n in ("p", "pd", "pdd", "q", "omega", "alpha")))
+
+
+class CoupledSession:
+    """One device-resident IB-LBM domain (sim::CoupledSession, session.hpp:29-224)."""
+
+    def __init__(self, cfg: SessionConfig):
+        self.cfg = cfg
+        L = _abi.lib()
+        h = C.c_void_p()
+        check(L.fsg_create(C.byref(cfg.to_c()), C.byref(h)))
+        self._h = h
+        self.dims = tuple(int(d) for d in cfg.dims)
+        self.n_cells = int(np.prod(self.dims))
+        self.m = 0
+        self.n_bodies = 0
+
+    # -- lifetime --------------------------------------------------------
+    def close(self) -> None:
+        if getattr(self, "_h", None):
+            _abi.lib().fsg_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+    @property
+    def handle(self):
+        return self._h
+
+    @property
+    def stream(self) -> int:
+        return _abi.lib().fsg_stream(self._h) or 0
+
+    # -- LatticeGrid -----------------------------------------------------
+    def reset_to_rest(self) -> None:
+        check(_abi.lib().fsg_reset_rest(self._h))
+
+    def initialize(self, rho: np.ndarray, u: np.ndarray) -> None:
+        """LatticeGrid::initialize (lattice.hpp:107-116); rho[n], u[n,3] in cell order."""
+        rho = np.ascontiguousarray(rho, dtype=np.float64).reshape(-1)
+        u = np.ascontiguousarray(u, dtype=np.float64).reshape(-1)
+        assert rho.size == self.n_cells and u.size == 3 * self.n_cells
+        check(_abi.lib().fsg_initialize(self._h, dptr(rho), dptr(u)))
+
+    def set_f(self, f: np.ndarray) -> None:
+        f = np.ascontiguousarray(f, dtype=np.float64).reshape(-1)
+        assert f.size == 19 * self.n_cells
+        check(_abi.lib().fsg_set_f(self._h, dptr(f)))
+
+    def get_f(self) -> np.ndarray:
+        """LatticeGrid::front() (post-stream state), direction-major [19*n]."""
+        out = np.empty(19 * self.n_cells)
+        check(_abi.lib().fsg_get_f(self._h, dptr(out)))
+        return out
+
+    # -- lbm::solver -----------------------------------------------------
+    def set_force(self, F: np.ndarray | None) -> None:
+        if F is None:
+            check(_abi.lib().fsg_set_force(self._h, None))
+            return
+        F = np.ascontiguousarray(F, dtype=np.float64).reshape(-1)
+        assert F.size == 3 * self.n_cells
+        check(_abi.lib().fsg_set_force(self._h, dptr(F)))
+
+    def collide_and_stream(self) -> StepStatus:
+        st = _abi.fsg_status()
+        check(_abi.lib().fsg_collide_and_stream(self._h, C.byref(st)))
+        return StepStatus.of(st)
+
+    def macroscopic(self):
+        """lbm::macroscopic_into with the stored force -> (rho[n], u[n,3], n_nonpositive)."""
+        rho = np.empty(self.n_cells)
+        u = np.empty(3 * self.n_cells)
+        bad = C.c_int(0)
+        check(_abi.lib().fsg_macroscopic(self._h, dptr(rho), dptr(u), C.byref(bad)))
+        return rho, u.reshape(-1, 3), bad.value
+
+    def total_mass(self) -> float:
+        v = C.c_double()
+        check(_abi.lib().fsg_total_mass(self._h, C.byref(v)))
+        return v.value
+
+    def total_momentum(self) -> np.ndarray:
+        v = np.zeros(3)
+        check(_abi.lib().fsg_total_momentum(self._h, dptr(v)))
+        return v
+
+    # -- frame -----------------------------------------------------------
+    def set_frame(self, fs: FrameState) -> None:
+        check(_abi.lib().fsg_set_frame(self._h, C.byref(fs.to_c())))
+
+    def frame_state(self) -> FrameState:
+        c = _abi.fsg_frame_state()
+        check(_abi.lib().fsg_get_frame(self._h, C.byref(c)))
+        return FrameState.of(c)
+
+    def recenter(self, shift) -> None:
+        sh = np.ascontiguousarray(np.asarray(shift, dtype=np.int32))
+        check(_abi.lib().fsg_recenter(self._h, iptr(sh)))
+
+    # -- coupled step ------------------------------------------------------
+    def set_markers(self, body_offsets, points, velocities, normals, areas) -> None:
+        off = np.ascontiguousarray(np.asarray(body_offsets, dtype=np.int64))
+        pts = np.ascontiguousarray(points, dtype=np.float64).reshape(-1)
+        vel = np.ascontiguousarray(velocities, dtype=np.float64).reshape(-1)
+        nrm = np.ascontiguousarray(normals, dtype=np.float64).reshape(-1)
+        ar = np.ascontiguousarray(areas, dtype=np.float64).reshape(-1)
+        nb = len(off) - 1
+        check(_abi.lib().fsg_set_markers(self._h, nb, off.ctypes.data_as(_abi._i64p), dptr(pts),
+                                         dptr(vel), dptr(nrm), dptr(ar)))
+        self.m = int(off[-1]) if nb > 0 else 0
+        self.n_bodies = nb
+
+    def set_markers_device(self, body_offsets, d_points: int, d_velocities: int, d_normals: int,
+                           d_areas: int) -> None:
+        off = np.ascontiguousarray(np.asarray(body_offsets, dtype=np.int64))
+        nb = len(off) - 1
+        check(_abi.lib().fsg_set_markers_device(self._h, nb, off.ctypes.data_as(_abi._i64p),
+                                                d_points, d_velocities, d_normals, d_areas))
+        self.m = int(off[-1]) if nb > 0 else 0
+        self.n_bodies = nb
+
+    def step(self) -> StepStatus:
+        """Fluid half of CoupledSession::step (session.hpp:94-166)."""
+        st = _abi.fsg_status()
+        check(_abi.lib().fsg_step(self._h, C.byref(st)))
+        return StepStatus.of(st)
+
+    def step_async(self) -> None:
+        check(_abi.lib().fsg_step_async(self._h))
+
+    def last_status(self) -> StepStatus:
+        st = _abi.fsg_status()
+        check(_abi.lib().fsg_last_status(self._h, C.byref(st)))
+        return StepStatus.of(st)
+
+    def marker_forces(self):
+        """-> (force_world[m,3] on the fluid, valid[m], stats[n_bodies,7])."""
+        fw = np.zeros(3 * self.m)
+        valid = np.zeros(self.m, dtype=np.int32)
+        stats = np.zeros(7 * max(self.n_bodies, 1))
+        check(_abi.lib().fsg_get_marker_forces(self._h, dptr(fw), iptr(valid), dptr(stats)))
+        return fw.reshape(-1, 3), valid, stats[: 7 * self.n_bodies].reshape(-1, 7)
+
+    def macro(self):
+        """CoupledSession::macro() after step(): bare (rho[n], u[n,3])."""
+        rho = np.empty(self.n_cells)
+        u = np.empty(3 * self.n_cells)
+        check(_abi.lib().fsg_get_macro(self._h, dptr(rho), dptr(u)))
+        return rho, u.reshape(-1, 3)
+
+    def force(self) -> np.ndarray:
+        """BodyForceField of the last step (IB + virtual force), [n,3]."""
+        F = np.empty(3 * self.n_cells)
+        check(_abi.lib().fsg_get_force(self._h, dptr(F)))
+        return F.reshape(-1, 3)
+
+    def stencils(self) -> np.ndarray:
+        """Integer stencil ranges of the last step: [m, 6] = lo(x,y,z), hi(x,y,z)."""
+        out = np.zeros(6 * self.m, dtype=np.int32)
+        check(_abi.lib().fsg_get_stencils(self._h, iptr(out)))
+        return out.reshape(-1, 6)
+
+    # -- z-slab halos ----------------------------------------------------------
+    def halo_bytes(self) -> int:
+        return int(_abi.lib().fsg_halo_bytes(self._h))
+
+    def halo_pack(self, d_send_lo: int, d_send_hi: int) -> None:
+        check(_abi.lib().fsg_halo_pack(self._h, d_send_lo, d_send_hi))
+
+    def halo_unpack(self, d_recv_lo: int | None, d_recv_hi: int | None) -> None:
+        check(_abi.lib().fsg_halo_unpack(self._h, d_recv_lo, d_recv_hi))
