@@ -40,7 +40,19 @@ struct Grid {
   long long n;       // owned cells nx*ny*nz
   long long plane;   // nx*ny
   long long stride;  // elements per direction array (>= plane*(nz+2*zpad), 32-aligned)
+  // per-direction element offsets relative to the cell's own slot (host-made,
+  // land in the constant bank): own[i] = i*stride, pull[i] = i*stride - off_i
+  // with off_i = ex + nx*(ey + ny*ez) (interior pull source)
+  long long own[19];
+  long long pull[19];
 };
+
+inline void grid_offsets(Grid& g) {
+  for (int i = 0; i < 19; ++i) {
+    g.own[i] = (long long)i * g.stride;
+    g.pull[i] = g.own[i] - ((long long)ex_of(i) + (long long)g.nx * ((long long)ey_of(i) + (long long)g.ny * ez_of(i)));
+  }
+}
 
 __host__ __device__ __forceinline__ long long mem_index(const Grid& g, int x, int y, int z) {
   return (long long)x + (long long)g.nx * ((long long)y + (long long)g.ny * (long long)(z + g.zpad));
@@ -60,6 +72,11 @@ struct SessionConsts {
   int kernel;        // 0 Peskin4, 1 Roma3
   int wall;          // 0 slip, 1 no-slip
   int frame_on;      // frame_mode != None
+  // fp32 collision constants (throughput mode), rounded once on the host
+  float om1_f;       // 1 - omega
+  float ow_f[3];     // omega * w  for w in {1/3, 1/18, 1/36}
+  float gw_f[3];     // guo * w
+  float dx_f, v2p_f, acc_f, hd_f[3];
 };
 
 // Per-step frame constants (frame.hpp:21-53), host-computed in fp64.
@@ -69,6 +86,8 @@ struct StepConsts {
   double a0[3];      // R^T pdd
   double wf[3];      // R^T omega
   double af[3];      // R^T alpha
+  float a0_f[3], wf_f[3], af_f[3];  // fp32 copies for the throughput kernels
+  float _padf;
 };
 
 // Per-step scratch, reset to all-zero bytes before every step.  Encodings are
@@ -106,15 +125,21 @@ __host__ __device__ __forceinline__ double key_to_double(unsigned long long k) {
 #endif
 }
 
-// Per-marker stencil record written by the prepare kernel.
-struct MarkerStencil {
-  double xf[3];      // frame position (m)
-  double xl[3];      // lattice position
+// Per-marker stencil record written by the marker kernel.
+struct __align__(16) MarkerStencil {
   double ph[3][5];   // phi(k - x_a) for k = lo_a .. hi_a (kernel.hpp:22-33)
   double fl[3];      // lattice force to spread (session.hpp:128, :136-138)
-  int lo[3], hi[3];  // inclusive ranges (kernel.hpp:36-40)
+  int lo[3], hi[3];  // inclusive global ranges (kernel.hpp:36-40)
   int valid;
   int _pad;
+};
+
+// Compact stencil box (local coordinates) for the spread kernel's cull.
+struct __align__(16) MarkerBox {
+  short lo[3];
+  short valid;
+  short hi[3];
+  short _pad;
 };
 
 // Marker input arrays (SI world frame, session.hpp:113-126).
@@ -128,7 +153,6 @@ struct Markers {
 
 // Compact IB band (bounding box of all valid stencils, local coordinates).
 struct Band {
-  double* u;         // bare velocity, 3 per band cell
   double* F;         // spread IB force, 3 per band cell
   long long cap;     // capacity in cells
 };
@@ -154,14 +178,12 @@ struct Launchers {
                         cudaStream_t);
   void (*recenter)(const Grid&, const void* A, int pulled, void* B, int sx, int sy, int sz,
                    cudaStream_t);
-  // IB
-  void (*markers_prepare)(const Grid&, Markers, const SessionConsts*, const StepConsts*,
-                          MarkerStencil*, StepScratch*, cudaStream_t);
-  void (*band_moments)(const Grid&, const void* A, int pulled, Band, const StepScratch*,
-                       StepScratch*, cudaStream_t);
-  void (*markers_force)(const Grid&, Markers, const SessionConsts*, const StepConsts*,
-                        MarkerStencil*, Band, const StepScratch*, double* fworld, cudaStream_t);
-  void (*spread)(const Grid&, int m, const MarkerStencil*, Band, const StepScratch*, cudaStream_t);
+  // IB: per-marker fused kernel, then the ordered spread into the band
+  void (*markers)(const Grid&, const void* A, int pulled, Markers, const SessionConsts*,
+                  const StepConsts*, MarkerStencil*, MarkerBox*, double* fworld,
+                  double* fworld_host, int* valid_host, StepScratch*, cudaStream_t);
+  void (*spread)(const Grid&, int m, const MarkerStencil*, const MarkerBox*, Band,
+                 const StepScratch*, cudaStream_t);
   // halo planes (z-slab): pack owned boundary planes / unpack into halo planes
   void (*halo_pack)(const Grid&, const void* B, void* send_lo, void* send_hi, cudaStream_t);
   void (*halo_unpack)(const Grid&, void* B, const void* recv_lo, const void* recv_hi,

@@ -89,17 +89,22 @@ __device__ __forceinline__ bool is_interior(const Grid& g, int x, int y, int z) 
 }
 
 /// Gather the 19 post-stream populations S(x,y,z) in storage form.
+/// Interior cells (the overwhelming majority) take one branch with constant
+/// 32-bit neighbour offsets; boundary cells take the general clamped path.
 template <bool PULLED>
 __device__ __forceinline__ void gather(const Grid& g, const Store* __restrict__ A, int x, int y,
                                        int z, Store s[Q]) {
+  const int m = (int)mem_index(g, x, y, z);  // < 2^31 for every supported grid
+  const Store* __restrict__ base = A + m;
   if (!PULLED) {
-    const long long m = mem_index(g, x, y, z);
 #pragma unroll
-    for (int i = 0; i < Q; ++i) s[i] = A[i * g.stride + m];
+    for (int i = 0; i < Q; ++i) s[i] = base[g.own[i]];
+  } else if (is_interior(g, x, y, z)) {
+#pragma unroll
+    for (int i = 0; i < Q; ++i) s[i] = base[g.pull[i]];
   } else {
-    const bool interior = is_interior(g, x, y, z);
-    s[0] = A[pull_src<0>(g, x, y, z, interior)];
-#define FSG_G(I) s[I] = A[(long long)(I)*g.stride + pull_src<I>(g, x, y, z, interior)];
+    s[0] = A[pull_src<0>(g, x, y, z, false)];
+#define FSG_G(I) s[I] = A[(long long)(I)*g.stride + pull_src<I>(g, x, y, z, false)];
     FSG_G(1) FSG_G(2) FSG_G(3) FSG_G(4) FSG_G(5) FSG_G(6) FSG_G(7) FSG_G(8) FSG_G(9)
     FSG_G(10) FSG_G(11) FSG_G(12) FSG_G(13) FSG_G(14) FSG_G(15) FSG_G(16) FSG_G(17) FSG_G(18)
 #undef FSG_G
@@ -179,6 +184,27 @@ __device__ __forceinline__ void vf_term(const SessionConsts& sc, const StepConst
   fz = ra * A2;
 }
 
+/// vf_term with the host-rounded fp32 constants (throughput mode).
+__device__ __forceinline__ void vf_term32(const SessionConsts& sc, const StepConsts& st, int i,
+                                          int j, int k, float rho, float ubx, float uby, float ubz,
+                                          float& fx, float& fy, float& fz) {
+  const float dx = sc.dx_f, v2p = sc.v2p_f;
+  const float x0 = ((float)i - sc.hd_f[0]) * dx;
+  const float x1 = ((float)j - sc.hd_f[1]) * dx;
+  const float x2 = ((float)k - sc.hd_f[2]) * dx;
+  const float u0 = ubx * v2p, u1 = uby * v2p, u2 = ubz * v2p;
+  const float w0 = st.wf_f[0], w1 = st.wf_f[1], w2 = st.wf_f[2];
+  const float a0 = st.af_f[0], a1 = st.af_f[1], a2 = st.af_f[2];
+  const float ax0 = a1 * x2 - a2 * x1, ax1 = a2 * x0 - a0 * x2, ax2 = a0 * x1 - a1 * x0;
+  const float wx0 = w1 * x2 - w2 * x1, wx1 = w2 * x0 - w0 * x2, wx2 = w0 * x1 - w1 * x0;
+  const float ww0 = w1 * wx2 - w2 * wx1, ww1 = w2 * wx0 - w0 * wx2, ww2 = w0 * wx1 - w1 * wx0;
+  const float wu0 = w1 * u2 - w2 * u1, wu1 = w2 * u0 - w0 * u2, wu2 = w0 * u1 - w1 * u0;
+  const float ra = rho * sc.acc_f;
+  fx = ra * (-st.a0_f[0] - ax0 - ww0 - 2.0f * wu0);
+  fy = ra * (-st.a0_f[1] - ax1 - ww1 - 2.0f * wu1);
+  fz = ra * (-st.a0_f[2] - ax2 - ww2 - 2.0f * wu2);
+}
+
 __device__ __forceinline__ void decode_bbox(const StepScratch* sc, int lo[3], int hi[3]) {
 #pragma unroll
   for (int a = 0; a < 3; ++a) {
@@ -190,14 +216,89 @@ __device__ __forceinline__ void decode_bbox(const StepScratch* sc, int lo[3], in
 // ------------------------------------------------------ block reduction --
 __device__ __forceinline__ void report_min(StepScratch* out, double v) {
   // warp min, then one lane per warp does check-then-atomic (few atomics/step)
+#if FSG_PREC == 32
+  float vf = (float)v;  // fp32 mode: post values are fp32 already
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) vf = fminf(vf, __shfl_xor_sync(0xffffffffu, vf, o));
+  v = vf == FLT_MAX ? DBL_MAX : (double)vf;
+#else
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v = fmin(v, __shfl_xor_sync(0xffffffffu, v, o));
+#endif
   if ((threadIdx.x & 31) == 0 && !isnan(v)) {
     const unsigned long long nk = ~ordered_key(v);
     const unsigned long long cur = *(volatile unsigned long long*)&out->neg_min_key;
     if (nk > cur) atomicMax(&out->neg_min_key, nk);
   }
 }
+
+#if FSG_PREC == 32
+/// fp32 BGK + Guo collision of one cell in deviation form (solver.hpp:129-154
+/// restated for g_i = f_i - w_i), with the session force assembled as the
+/// reference does (IB band force, then + virtual force, session.hpp:148-163).
+/// Overwrites s with the post-collision deviations; returns min(post f).
+template <int FMODE, bool VF>
+__device__ __forceinline__ float collide_cell32(float (&s)[Q], int x, int y, int z, const Grid& g,
+                                                float Fx, float Fy, float Fz, bool in_band,
+                                                long long lc, const Band& band,
+                                                const SessionConsts& sc, const StepConsts& st,
+                                                StepScratch* out) {
+  float drho, mx, my, mz;
+  moments_dev(s, drho, mx, my, mz);
+  const float rho = 1.0f + drho;
+  if constexpr (FMODE == 2) {
+    Fx = in_band ? (float)band.F[3 * lc] : 0.0f;
+    Fy = in_band ? (float)band.F[3 * lc + 1] : 0.0f;
+    Fz = in_band ? (float)band.F[3 * lc + 2] : 0.0f;
+    if constexpr (VF) {
+      float bx = 0.f, by = 0.f, bz = 0.f;
+      if (rho > 0.0f) {
+        const float ir = 1.0f / rho;
+        bx = mx * ir;
+        by = my * ir;
+        bz = mz * ir;
+      }
+      float vx, vy, vz;
+      vf_term32(sc, st, x, y, g.z0 + z, rho, bx, by, bz, vx, vy, vz);
+      Fx += vx;
+      Fy += vy;
+      Fz += vz;
+    }
+    if (!(rho > 0.0f)) atomicAdd(&out->nonpos, 1);
+  }
+  const float om1 = sc.om1_f;
+  const float inv_rho = 1.0f / rho;
+  const float ux = (mx + 0.5f * Fx) * inv_rho;
+  const float uy = (my + 0.5f * Fy) * inv_rho;
+  const float uz = (mz + 0.5f * Fz) * inv_rho;
+  const float u2 = ux * ux + uy * uy + uz * uz;
+  if (!isfinite(rho + u2)) out->nonfinite = 1;
+  const float uF = ux * Fx + uy * Fy + uz * Fz;
+  const float h15u2 = 1.5f * u2;
+  // weight classes: 0 rest, 1 axes, 2 diagonals
+  const float ow[3] = {sc.ow_f[0], sc.ow_f[1], sc.ow_f[2]};
+  const float gw[3] = {sc.gw_f[0], sc.gw_f[1], sc.gw_f[2]};
+  float fmin_dev = FLT_MAX;
+#define FSG_DIR(I)                                                                        \
+  {                                                                                       \
+    constexpr int a = ex_of(I), b = ey_of(I), c = ez_of(I);                               \
+    constexpr int cls = (I) == 0 ? 0 : ((I) <= 6 ? 1 : 2);                                \
+    const float eu = edot<a, b, c, float>(ux, uy, uz);                                    \
+    const float eF = edot<a, b, c, float>(Fx, Fy, Fz);                                    \
+    const float X = fmaf(eu, fmaf(4.5f, eu, 3.0f), -h15u2);                               \
+    const float geq_w = fmaf(rho, X, drho);                                               \
+    const float srcw = fmaf(fmaf(9.0f, eu, 3.0f), eF, -3.0f * uF);                        \
+    const float gp = fmaf(om1, s[I], fmaf(ow[cls], geq_w, gw[cls] * srcw));               \
+    fmin_dev = fminf(fmin_dev, gp + (float)w_of(I));                                      \
+    s[I] = gp;                                                                            \
+  }
+  FSG_DIR(0) FSG_DIR(1) FSG_DIR(2) FSG_DIR(3) FSG_DIR(4) FSG_DIR(5) FSG_DIR(6)
+  FSG_DIR(7) FSG_DIR(8) FSG_DIR(9) FSG_DIR(10) FSG_DIR(11) FSG_DIR(12) FSG_DIR(13)
+  FSG_DIR(14) FSG_DIR(15) FSG_DIR(16) FSG_DIR(17) FSG_DIR(18)
+#undef FSG_DIR
+  return fmin_dev;
+}
+#endif
 
 // =============================================================== K4 ======
 // Fused: [moments of S] + [virtual force] + [IB band force] + BGK/Guo
@@ -220,7 +321,7 @@ __global__ void __launch_bounds__(128) k_collide(Grid g, const Store* __restrict
   if (live) {
     Store s[Q];
     gather<PULLED>(g, A, x, y, z, s);
-    const long long m = mem_index(g, x, y, z);
+    const int m = (int)mem_index(g, x, y, z);
     const SessionConsts& sc = *scp;
     // -------- force F for this cell
     Real Fx = 0, Fy = 0, Fz = 0;
@@ -282,71 +383,23 @@ __global__ void __launch_bounds__(128) k_collide(Grid g, const Store* __restrict
       const double src = guo * w_of(i) * (sx * Fx + sy * Fy + sz * Fz);
       const double post = s[i] - omega * (s[i] - feq) + src;
       vmin = post < vmin ? post : vmin;
-      B[i * g.stride + m] = post;
+      B[g.own[i] + m] = post;
     }
 #else
-    float drho, mx, my, mz;
-    moments_dev(s, drho, mx, my, mz);
-    const float rho = 1.0f + drho;
-    if constexpr (FMODE == 2) {
-      Fx = in_band ? (float)band.F[3 * lc] : 0.0f;
-      Fy = in_band ? (float)band.F[3 * lc + 1] : 0.0f;
-      Fz = in_band ? (float)band.F[3 * lc + 2] : 0.0f;
-      if constexpr (VF) {
-        float bx = 0.f, by = 0.f, bz = 0.f;
-        if (rho > 0.0f) {
-          const float ir = 1.0f / rho;
-          bx = mx * ir;
-          by = my * ir;
-          bz = mz * ir;
-        }
-        float vx, vy, vz;
-        vf_term<float>(sc, *stp, x, y, g.z0 + z, rho, bx, by, bz, vx, vy, vz);
-        Fx += vx;
-        Fy += vy;
-        Fz += vz;
-      }
-      if (!(rho > 0.0f)) atomicAdd(&out->nonpos, 1);
-    }
-    const float omega = (float)sc.omega;
-    const float om1 = (float)(1.0 - sc.omega);
-    const float inv_rho = 1.0f / rho;
-    const float ux = (mx + 0.5f * Fx) * inv_rho;
-    const float uy = (my + 0.5f * Fy) * inv_rho;
-    const float uz = (mz + 0.5f * Fz) * inv_rho;
-    const float u2 = ux * ux + uy * uy + uz * uz;
-    if (!isfinite(rho + u2)) out->nonfinite = 1;
-    const float uF = ux * Fx + uy * Fy + uz * Fz;
-    const float h15u2 = 1.5f * u2;
-    // weight classes: 0 rest, 1 axes, 2 diagonals
-    const float ow[3] = {(float)(sc.omega * (1.0 / 3.0)), (float)(sc.omega * (1.0 / 18.0)),
-                         (float)(sc.omega * (1.0 / 36.0))};
-    const float gw[3] = {(float)(sc.guo * (1.0 / 3.0)), (float)(sc.guo * (1.0 / 18.0)),
-                         (float)(sc.guo * (1.0 / 36.0))};
-    float fmin_dev = FLT_MAX;  // min over (post - w_i) per weight class is not enough; track abs
-    (void)omega;
-#define FSG_DIR(I)                                                                        \
-  {                                                                                       \
-    constexpr int a = ex_of(I), b = ey_of(I), c = ez_of(I);                               \
-    constexpr int cls = (I) == 0 ? 0 : ((I) <= 6 ? 1 : 2);                                \
-    const float eu = edot<a, b, c, float>(ux, uy, uz);                                    \
-    const float eF = edot<a, b, c, float>(Fx, Fy, Fz);                                    \
-    const float X = fmaf(eu, fmaf(4.5f, eu, 3.0f), -h15u2);                               \
-    const float geq_w = fmaf(rho, X, drho);                                               \
-    const float srcw = fmaf(fmaf(9.0f, eu, 3.0f), eF, -3.0f * uF);                        \
-    const float gp = fmaf(om1, s[I], fmaf(ow[cls], geq_w, gw[cls] * srcw));               \
-    fmin_dev = fminf(fmin_dev, gp + (float)w_of(I));                                      \
-    B[(long long)(I)*g.stride + m] = gp;                                                  \
-  }
-    FSG_DIR(0) FSG_DIR(1) FSG_DIR(2) FSG_DIR(3) FSG_DIR(4) FSG_DIR(5) FSG_DIR(6)
-    FSG_DIR(7) FSG_DIR(8) FSG_DIR(9) FSG_DIR(10) FSG_DIR(11) FSG_DIR(12) FSG_DIR(13)
-    FSG_DIR(14) FSG_DIR(15) FSG_DIR(16) FSG_DIR(17) FSG_DIR(18)
-#undef FSG_DIR
+    const float fmin_dev = collide_cell32<FMODE, VF>(s, x, y, z, g, Fx, Fy, Fz, in_band, lc, band,
+                                                     sc, *stp, out);
+    Store* __restrict__ ob = B + m;
+#pragma unroll
+    for (int i = 0; i < Q; ++i) ob[g.own[i]] = s[i];
     vmin = (double)fmin_dev;
 #endif
   }
   report_min(out, vmin);
 }
+
+#if FSG_PREC == 32
+#include "fsg_k4v4.cuh"
+#endif
 
 // ====================================================== small kernels =====
 __global__ void k_fill_rest(Grid g, Store* A) {
@@ -457,6 +510,33 @@ __device__ __forceinline__ void cell_moments(const Grid& g, const Store* __restr
   (void)BARE;
 }
 
+/// Bare velocity of gathered populations: macroscopic_into with F = 0
+/// (solver.hpp:42-48, session.hpp:95-96); u = 0 where rho <= 0.
+__device__ __forceinline__ void bare_velocity(const Store s[Q], double& ux, double& uy, double& uz) {
+#if FSG_PREC == 64
+  double rho, mx, my, mz;
+  moments(s, rho, mx, my, mz);
+  if (!(rho > 0.0)) {
+    ux = uy = uz = 0.0;
+    return;
+  }
+  ux = (mx + 0.5 * 0.0) / rho;
+  uy = (my + 0.5 * 0.0) / rho;
+  uz = (mz + 0.5 * 0.0) / rho;
+#else
+  float drho, mx, my, mz;
+  moments_dev(s, drho, mx, my, mz);
+  const float rho = 1.0f + drho;
+  if (!(rho > 0.0f)) {
+    ux = uy = uz = 0.0;
+    return;
+  }
+  ux = (mx + 0.0f) / rho;
+  uy = (my + 0.0f) / rho;
+  uz = (mz + 0.0f) / rho;
+#endif
+}
+
 template <bool PULLED>
 __global__ void k_macroscopic(Grid g, const Store* __restrict__ A, const Real* __restrict__ Fext,
                               double* __restrict__ rho, double* __restrict__ u, StepScratch* out) {
@@ -543,250 +623,7 @@ __global__ void k_recenter(Grid g, const Store* __restrict__ A, Store* __restric
 }
 
 // ====================================================== IB kernels =======
-/// IBKernel::phi (kernel.hpp:22-33), fp64.
-__device__ __forceinline__ double ib_phi(int kernel, double r) {
-  const double a = fabs(r);
-  if (kernel == 0) {
-    if (a >= 2.0) return 0.0;
-    if (a <= 1.0) return 0.125 * (3.0 - 2.0 * a + sqrt(1.0 + 4.0 * a - 4.0 * a * a));
-    return 0.125 * (5.0 - 2.0 * a - sqrt(-7.0 + 12.0 * a - 4.0 * a * a));
-  }
-  if (a <= 0.5) return (1.0 + sqrt(1.0 - 3.0 * r * r)) / 3.0;
-  if (a <= 1.5) return (5.0 - 3.0 * a - sqrt(-3.0 * (1.0 - a) * (1.0 - a) + 1.0)) / 6.0;
-  return 0.0;
-}
-
-/// r = R^T v in Eigen's coefficient order (R row-major).
-__device__ __forceinline__ void mat_t_vec(const double* R, const double* v, double* r) {
-#pragma unroll
-  for (int i = 0; i < 3; ++i) r[i] = R[i] * v[0] + R[3 + i] * v[1] + R[6 + i] * v[2];
-}
-__device__ __forceinline__ void mat_vec(const double* R, const double* v, double* r) {
-#pragma unroll
-  for (int i = 0; i < 3; ++i) r[i] = R[3 * i] * v[0] + R[3 * i + 1] * v[1] + R[3 * i + 2] * v[2];
-}
-
-/// K_a: per marker world->frame->lattice (frame.hpp:24-26, session.hpp:82-85),
-/// marker_in_bounds (coupling.hpp:18-24), stencil ranges (kernel.hpp:36-40),
-/// per-axis phi values, band bounding box.
-__global__ void k_markers_prepare(Grid g, Markers mk, const SessionConsts* __restrict__ scp,
-                                  const StepConsts* __restrict__ stp, MarkerStencil* st,
-                                  StepScratch* out) {
-  const int t = blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= mk.m) return;
-  const SessionConsts& sc = *scp;
-  const StepConsts& fs = *stp;
-  MarkerStencil r;
-  double xw[3];
-#pragma unroll
-  for (int k = 0; k < 3; ++k) xw[k] = mk.pts[3 * t + k] - fs.p[k];
-  mat_t_vec(fs.R, xw, r.xf);
-#pragma unroll
-  for (int k = 0; k < 3; ++k) r.xl[k] = r.xf[k] / sc.dx + sc.hd[k];
-  const double margin = 0.5 * (sc.kernel == 0 ? 4 : 3);
-  bool ok = true;
-#pragma unroll
-  for (int a = 0; a < 3; ++a)
-    if (r.xl[a] < margin || r.xl[a] > sc.dims_g[a] - 1 - margin) ok = false;
-  r.valid = ok ? 1 : 0;
-  if (!ok) {
-    atomicAdd(&out->oob, 1);
-    st[t] = r;
-    return;
-  }
-  const double half = 0.5 * (sc.kernel == 0 ? 4 : 3);
-#pragma unroll
-  for (int a = 0; a < 3; ++a) {
-    r.lo[a] = (int)ceil(r.xl[a] - half);
-    r.hi[a] = (int)floor(r.xl[a] + half);
-    // valid markers never touch the box edge; the clip of coupling.hpp:35-39 is a no-op
-#pragma unroll
-    for (int q = 0; q < 5; ++q) r.ph[a][q] = q <= r.hi[a] - r.lo[a] ? ib_phi(sc.kernel, (r.lo[a] + q) - r.xl[a]) : 0.0;
-  }
-  r.fl[0] = r.fl[1] = r.fl[2] = 0.0;
-  st[t] = r;
-  // bounding box in local z for slabs
-  atomicMax(&out->bbox_lo_enc[0], LO_BIAS - r.lo[0]);
-  atomicMax(&out->bbox_lo_enc[1], LO_BIAS - r.lo[1]);
-  atomicMax(&out->bbox_lo_enc[2], LO_BIAS - max(r.lo[2] - g.z0, 0));
-  atomicMax(&out->bbox_hi_enc[0], r.hi[0] + 1);
-  atomicMax(&out->bbox_hi_enc[1], r.hi[1] + 1);
-  atomicMax(&out->bbox_hi_enc[2], min(r.hi[2] - g.z0, g.nz - 1) + 1);
-}
-
-/// K_b: bare moments (macroscopic_into with F = 0, session.hpp:95-96) over the band.
-template <bool PULLED>
-__global__ void k_band_moments(Grid g, const Store* __restrict__ A, Band band,
-                               const StepScratch* __restrict__ bscr, StepScratch* out) {
-  int lo[3], hi[3];
-  decode_bbox(bscr, lo, hi);
-  if (hi[0] < lo[0] || hi[1] < lo[1] || hi[2] < lo[2]) return;
-  const long long bnx = hi[0] - lo[0] + 1, bny = hi[1] - lo[1] + 1, bnz = hi[2] - lo[2] + 1;
-  const long long nb = bnx * bny * bnz;
-  if (nb > band.cap) {
-    if (blockIdx.x == 0 && threadIdx.x == 0) out->band_overflow = 1;
-    return;
-  }
-  for (long long lc = blockIdx.x * (long long)blockDim.x + threadIdx.x; lc < nb;
-       lc += (long long)gridDim.x * blockDim.x) {
-    const int x = lo[0] + (int)(lc % bnx);
-    const int y = lo[1] + (int)((lc / bnx) % bny);
-    const int z = lo[2] + (int)(lc / (bnx * bny));
-    double r, ux, uy, uz;
-    bool bad;
-    cell_moments<PULLED, true>(g, A, x, y, z, 0.0, 0.0, 0.0, r, ux, uy, uz, bad);
-    band.u[3 * lc] = ux;
-    band.u[3 * lc + 1] = uy;
-    band.u[3 * lc + 2] = uz;
-  }
-}
-
-/// K_c: interpolate_velocity (coupling.hpp:27-48), body_velocity_to_frame
-/// (frame.hpp:39-42), direct_forcing (coupling.hpp:80-85), world force and
-/// the lattice force to spread (session.hpp:113-138).  One thread per marker,
-/// serial stencil sum in the reference's k, j, i order.
-__global__ void k_markers_force(Grid g, Markers mk, const SessionConsts* __restrict__ scp,
-                                const StepConsts* __restrict__ stp, MarkerStencil* st, Band band,
-                                const StepScratch* __restrict__ bscr, double* __restrict__ fworld) {
-  const int t = blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= mk.m) return;
-  MarkerStencil& r = st[t];
-  if (!r.valid) {
-    fworld[3 * t] = fworld[3 * t + 1] = fworld[3 * t + 2] = 0.0;
-    return;
-  }
-  const SessionConsts& sc = *scp;
-  const StepConsts& fs = *stp;
-  int lo[3], hi[3];
-  decode_bbox(bscr, lo, hi);
-  const long long bnx = hi[0] - lo[0] + 1, bny = hi[1] - lo[1] + 1;
-  double u0 = 0.0, u1 = 0.0, u2 = 0.0;
-  for (int k = r.lo[2]; k <= r.hi[2]; ++k) {
-    const double wz = r.ph[2][k - r.lo[2]];
-    for (int j = r.lo[1]; j <= r.hi[1]; ++j) {
-      const double wyz = wz * r.ph[1][j - r.lo[1]];
-      for (int i = r.lo[0]; i <= r.hi[0]; ++i) {
-        const double w = wyz * r.ph[0][i - r.lo[0]];
-        const long long lc = (long long)(i - lo[0]) + bnx * ((long long)(j - lo[1]) + bny * (long long)(k - g.z0 - lo[2]));
-        u0 = u0 + w * band.u[3 * lc];
-        u1 = u1 + w * band.u[3 * lc + 1];
-        u2 = u2 + w * band.u[3 * lc + 2];
-      }
-    }
-  }
-  const double uf[3] = {u0 * sc.v2p, u1 * sc.v2p, u2 * sc.v2p};
-  double vw[3], vf[3], ub[3], nf[3], fl[3], fw[3], ff[3];
-#pragma unroll
-  for (int k = 0; k < 3; ++k) vw[k] = mk.vel[3 * t + k] - fs.pd[k];
-  mat_t_vec(fs.R, vw, vf);
-  const double wx0 = fs.wf[1] * r.xf[2] - fs.wf[2] * r.xf[1];
-  const double wx1 = fs.wf[2] * r.xf[0] - fs.wf[0] * r.xf[2];
-  const double wx2 = fs.wf[0] * r.xf[1] - fs.wf[1] * r.xf[0];
-  ub[0] = vf[0] - wx0;
-  ub[1] = vf[1] - wx1;
-  ub[2] = vf[2] - wx2;
-  mat_t_vec(fs.R, mk.nrm + 3 * t, nf);
-  double du[3] = {ub[0] - uf[0], ub[1] - uf[1], ub[2] - uf[2]};
-  if (sc.wall == 0) {
-    const double s = du[0] * nf[0] + du[1] * nf[1] + du[2] * nf[2];
-    du[0] = s * nf[0];
-    du[1] = s * nf[1];
-    du[2] = s * nf[2];
-  }
-  const double kf = sc.rho_phys * mk.area[t] * sc.dx / sc.dt;
-  fl[0] = kf * du[0];
-  fl[1] = kf * du[1];
-  fl[2] = kf * du[2];
-  mat_vec(fs.R, fl, fw);
-  fworld[3 * t] = fw[0];
-  fworld[3 * t + 1] = fw[1];
-  fworld[3 * t + 2] = fw[2];
-  mat_t_vec(fs.R, fw, ff);
-  r.fl[0] = ff[0] * sc.f2l;
-  r.fl[1] = ff[1] * sc.f2l;
-  r.fl[2] = ff[2] * sc.f2l;
-}
-
-/// K_d: spread_force (coupling.hpp:52-71) driven serially in ascending marker
-/// order (session.hpp:129-144), re-expressed as a gather: each band cell sums
-/// its contributions in ascending marker order, after a per-tile ordered cull
-/// of the marker list.  Deterministic, no float atomics, bit-identical to the
-/// serial loop.
-constexpr int SP_TX = 8, SP_TY = 4, SP_TZ = 4, SP_THREADS = 128, SP_CAP = 1024;
-__global__ void __launch_bounds__(SP_THREADS) k_spread(Grid g, int m, const MarkerStencil* __restrict__ st,
-                                                      Band band, const StepScratch* __restrict__ bscr) {
-  __shared__ int list[SP_CAP];
-  __shared__ int warp_tot[SP_THREADS / 32];
-  __shared__ int count_s;
-  int lo[3], hi[3];
-  decode_bbox(bscr, lo, hi);
-  if (hi[0] < lo[0] || hi[1] < lo[1] || hi[2] < lo[2]) return;
-  const int bnx = hi[0] - lo[0] + 1, bny = hi[1] - lo[1] + 1, bnz = hi[2] - lo[2] + 1;
-  if ((long long)bnx * bny * bnz > band.cap) return;
-  const int tnx = (bnx + SP_TX - 1) / SP_TX, tny = (bny + SP_TY - 1) / SP_TY, tnz = (bnz + SP_TZ - 1) / SP_TZ;
-  const int ntiles = tnx * tny * tnz;
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-    const int tx0 = lo[0] + (tile % tnx) * SP_TX;
-    const int ty0 = lo[1] + ((tile / tnx) % tny) * SP_TY;
-    const int tz0 = lo[2] + (tile / (tnx * tny)) * SP_TZ;  // local z
-    const int tx1 = min(tx0 + SP_TX - 1, hi[0]), ty1 = min(ty0 + SP_TY - 1, hi[1]),
-              tz1 = min(tz0 + SP_TZ - 1, hi[2]);
-    const int cx = tx0 + (threadIdx.x % SP_TX);
-    const int cy = ty0 + ((threadIdx.x / SP_TX) % SP_TY);
-    const int cz = tz0 + threadIdx.x / (SP_TX * SP_TY);
-    const int czg = cz + g.z0;
-    double F0 = 0.0, F1 = 0.0, F2 = 0.0;
-    if (threadIdx.x == 0) count_s = 0;
-    __syncthreads();
-    for (int base = 0; base < m; base += SP_THREADS) {
-      const int mi = base + threadIdx.x;
-      bool hit = false;
-      if (mi < m) {
-        const MarkerStencil& r = st[mi];
-        hit = r.valid && r.lo[0] <= tx1 && r.hi[0] >= tx0 && r.lo[1] <= ty1 && r.hi[1] >= ty0 &&
-              r.lo[2] - g.z0 <= tz1 && r.hi[2] - g.z0 >= tz0;
-      }
-      const unsigned bal = __ballot_sync(0xffffffffu, hit);
-      if (lane == 0) warp_tot[wid] = __popc(bal);
-      __syncthreads();
-      int off = count_s;
-      for (int w = 0; w < wid; ++w) off += warp_tot[w];
-      if (hit) list[off + __popc(bal & ((1u << lane) - 1u))] = mi;
-      __syncthreads();
-      if (threadIdx.x == 0) {
-        int tot = 0;
-        for (int w = 0; w < SP_THREADS / 32; ++w) tot += warp_tot[w];
-        count_s += tot;
-      }
-      __syncthreads();
-      const int cnt = count_s;
-      if (cnt > SP_CAP - SP_THREADS || base + SP_THREADS >= m) {
-        // drain the list in ascending marker order
-        for (int q = 0; q < cnt; ++q) {
-          const MarkerStencil& r = st[list[q]];
-          if (cx >= r.lo[0] && cx <= r.hi[0] && cy >= r.lo[1] && cy <= r.hi[1] && czg >= r.lo[2] &&
-              czg <= r.hi[2]) {
-            const double w = (r.ph[2][czg - r.lo[2]] * r.ph[1][cy - r.lo[1]]) * r.ph[0][cx - r.lo[0]];
-            F0 = F0 + w * r.fl[0];
-            F1 = F1 + w * r.fl[1];
-            F2 = F2 + w * r.fl[2];
-          }
-        }
-        __syncthreads();
-        if (threadIdx.x == 0) count_s = 0;
-        __syncthreads();
-      }
-    }
-    if (cx <= tx1 && cy <= ty1 && cz <= tz1) {
-      const long long lc = (long long)(cx - lo[0]) + (long long)bnx * ((long long)(cy - lo[1]) + (long long)bny * (cz - lo[2]));
-      band.F[3 * lc] = F0;
-      band.F[3 * lc + 1] = F1;
-      band.F[3 * lc + 2] = F2;
-    }
-    __syncthreads();
-  }
-}
+#include "fsg_ib.cuh"
 
 // ======================================================= halo (slabs) ====
 // Populations crossing a z face (lattice.hpp:25-26): ez=+1 {5,11,14,15,18},
@@ -853,8 +690,20 @@ template <bool P, int FM, bool VF>
 static void launch_collide_t(const Grid& g, const void* A, void* B, const void* Fext,
                              const Band* band, const StepScratch* bscr, const SessionConsts* sc,
                              const StepConsts* st, StepScratch* out, cudaStream_t s) {
+  Band bd = band ? *band : Band{nullptr, 0};
   const dim3 b = cell_block(g);
-  Band bd = band ? *band : Band{nullptr, nullptr, 0};
+#if FSG_PREC == 32
+  if (P) {
+    DirPtrs dp;
+    for (int i = 0; i < Q; ++i) {
+      dp.a[i] = (const float*)A + g.pull[i];
+      dp.b[i] = (float*)B + g.own[i];
+    }
+    k_collide_fast<FM, VF><<<cell_grid(g, b), b, 0, s>>>(g, dp, (const float*)A, (const float*)Fext,
+                                                         bd, bscr, sc, st, out);
+    return;
+  }
+#endif
   k_collide<P, FM, VF><<<cell_grid(g, b), b, 0, s>>>(g, (const Store*)A, (Store*)B, (const Real*)Fext,
                                                      bd, bscr, sc, st, out);
 }
@@ -892,29 +741,23 @@ static void L_recenter(const Grid& g, const void* A, int pulled, void* B, int sx
   else
     k_recenter<false><<<lin_blocks(g.n, 128), 128, 0, s>>>(g, (const Store*)A, (Store*)B, sx, sy, sz);
 }
-static void L_markers_prepare(const Grid& g, Markers mk, const SessionConsts* sc,
-                              const StepConsts* st, MarkerStencil* ms, StepScratch* out,
-                              cudaStream_t s) {
+static void L_markers(const Grid& g, const void* A, int pulled, Markers mk,
+                      const SessionConsts* sc, const StepConsts* st, MarkerStencil* ms,
+                      MarkerBox* boxes, double* fworld, double* fworld_h, int* valid_h,
+                      StepScratch* out, cudaStream_t s) {
   if (mk.m == 0) return;
-  k_markers_prepare<<<lin_blocks(mk.m, 128), 128, 0, s>>>(g, mk, sc, st, ms, out);
-}
-static void L_band_moments(const Grid& g, const void* A, int pulled, Band band,
-                           const StepScratch* bscr, StepScratch* out, cudaStream_t s) {
+  const unsigned nb = (unsigned)((mk.m + MK_PER_BLOCK - 1) / MK_PER_BLOCK);
   if (pulled)
-    k_band_moments<true><<<296, 128, 0, s>>>(g, (const Store*)A, band, bscr, out);
+    k_markers<true><<<nb, 128, 0, s>>>(g, (const Store*)A, mk, sc, st, ms, boxes, fworld, fworld_h,
+                                       valid_h, out);
   else
-    k_band_moments<false><<<296, 128, 0, s>>>(g, (const Store*)A, band, bscr, out);
+    k_markers<false><<<nb, 128, 0, s>>>(g, (const Store*)A, mk, sc, st, ms, boxes, fworld, fworld_h,
+                                        valid_h, out);
 }
-static void L_markers_force(const Grid& g, Markers mk, const SessionConsts* sc,
-                            const StepConsts* st, MarkerStencil* ms, Band band,
-                            const StepScratch* bscr, double* fworld, cudaStream_t s) {
-  if (mk.m == 0) return;
-  k_markers_force<<<lin_blocks(mk.m, 64), 64, 0, s>>>(g, mk, sc, st, ms, band, bscr, fworld);
-}
-static void L_spread(const Grid& g, int m, const MarkerStencil* ms, Band band,
-                     const StepScratch* bscr, cudaStream_t s) {
+static void L_spread(const Grid& g, int m, const MarkerStencil* ms, const MarkerBox* boxes,
+                     Band band, const StepScratch* bscr, cudaStream_t s) {
   if (m == 0) return;
-  k_spread<<<296, SP_THREADS, 0, s>>>(g, m, ms, band, bscr);
+  k_spread<<<296, SP_THREADS, 0, s>>>(g, m, ms, boxes, band, bscr);
 }
 static void L_halo_pack(const Grid& g, const void* B, void* lo, void* hi, cudaStream_t s) {
   k_halo_pack<<<lin_blocks(5 * g.plane, 256), 256, 0, s>>>(g, (const Store*)B, (Store*)lo, (Store*)hi);
@@ -925,8 +768,8 @@ static void L_halo_unpack(const Grid& g, void* B, const void* lo, const void* hi
 
 static const Launchers kLaunchers = {
     L_fill_rest,    L_set_f,          L_init_eq,      L_get_f,         L_macroscopic,
-    L_collide,      L_session_force,  L_recenter,     L_markers_prepare, L_band_moments,
-    L_markers_force, L_spread,        L_halo_pack,    L_halo_unpack,   (int)sizeof(Store)};
+    L_collide,      L_session_force,  L_recenter,     L_markers,       L_spread,
+    L_halo_pack,    L_halo_unpack,    (int)sizeof(Store)};
 
 }  // namespace p32 / p64
 }  // namespace fsg

@@ -6,6 +6,14 @@
 // functions the reference's tests drive directly.  All fp64 host arithmetic
 // (UnitMap, frame constants, recenter origin update) keeps the reference's
 // operation order.
+//
+// The coupled step is replayed as a CUDA graph:
+//   [H2D marker state] -> [H2D frame constants] -> [reset step scratch]
+//   -> K_m markers -> K_s spread -> K4 collide/stream -> [D2H status]
+// Host staging (pinned), step scratch and the status readback slot are
+// double-buffered by the parity of the A/B pair, so step n+1 can be
+// enqueued while step n still runs; each graph bakes in its parity's
+// buffers.
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -23,6 +31,7 @@
 using fsg::Band;
 using fsg::Grid;
 using fsg::Launchers;
+using fsg::MarkerBox;
 using fsg::MarkerStencil;
 using fsg::Markers;
 using fsg::SessionConsts;
@@ -78,6 +87,12 @@ void mat_vec(const double* R, const double* v, double* r) {
   for (int i = 0; i < 3; ++i) r[i] = R[3 * i] * v[0] + R[3 * i + 1] * v[1] + R[3 * i + 2] * v[2];
 }
 
+struct GraphEntry {
+  int par, pulled, m, copy_mk, frame_on;
+  const void* mkp;
+  cudaGraphExec_t exec;
+};
+
 }  // namespace
 
 struct fsg_session {
@@ -85,42 +100,52 @@ struct fsg_session {
   const Launchers* L = nullptr;
   Grid g{};
   cudaStream_t stream = nullptr;
-  void* A = nullptr;
-  void* B = nullptr;
+  void* buf[2] = {nullptr, nullptr};
+  int par = 0;     // A = buf[par], B = buf[par ^ 1]
   int pulled = 0;  // A holds post-collision P (1) or post-stream S (0)
-  // last session step, for macro()/force readbacks (the buffer it read)
+  // last coupled step, for macro()/force readbacks (the buffer it read)
   bool last_valid = false;
-  void* prevA = nullptr;
+  int last_par = 0;
   int prev_pulled = 0;
   bool last_frame_on = false;
+  bool stepped = false;
   void* Fext = nullptr;  // SoA 3*n in the storage's math type
   SessionConsts hsc{};
   SessionConsts* d_sc = nullptr;
   StepConsts* d_st = nullptr;
-  StepConsts* h_st = nullptr;  // pinned
-  StepScratch* d_scr = nullptr;
-  StepScratch* h_scr = nullptr;  // pinned
+  // per-parity resources
+  StepConsts* h_st[2] = {nullptr, nullptr};     // pinned
+  StepScratch* d_scr[2] = {nullptr, nullptr};
+  StepScratch* h_scr[2] = {nullptr, nullptr};   // pinned
+  double* h_mk[2] = {nullptr, nullptr};         // pinned marker slots (read in place)
+  double* h_fw[2] = {nullptr, nullptr};         // pinned marker forces (written in place)
+  int* h_valid[2] = {nullptr, nullptr};
+  cudaEvent_t ev[2] = {nullptr, nullptr};       // last graph of that parity done
+  cudaEvent_t ev_mk[2] = {nullptr, nullptr};    // last step that read marker slot k done
+  int mk_slot = -1;                             // slot the current marker pointers read
   fsg_frame_state frame{};
   // markers
   int cap = 0;
   int m = 0;
   int n_bodies = 0;
   std::vector<int64_t> offsets;
-  double* d_mk = nullptr;   // owned [pts 3cap | vel 3cap | nrm 3cap | area cap]
-  double* h_mk = nullptr;   // pinned staging
+  double* d_mk = nullptr;  // owned [pts 3cap | vel 3cap | nrm 3cap | area cap]
   Markers mk{};
-  bool mk_host_vel = false;
+  bool mk_host = false;
+  bool mk_dirty = false;
   std::vector<double> h_vel;  // for CouplingStats power
   MarkerStencil* d_stencil = nullptr;
+  MarkerBox* d_boxes = nullptr;
   double* d_fworld = nullptr;
   Band band{};
-  double* d_tmp = nullptr;  // readback staging, 19*n doubles (lazy)
+  double* d_tmp = nullptr;  // readback staging (lazy)
   size_t tmp_bytes = 0;
   double* d_red = nullptr;  // reduction scratch
-  StepScratch* d_junk = nullptr;
-  cudaEvent_t ev_st = nullptr;  // h_st consumed
-  cudaEvent_t ev_mk = nullptr;  // h_mk consumed
+  std::vector<GraphEntry> graphs;
   fsg_status last{};
+
+  void* A() const { return buf[par]; }
+  void* B() const { return buf[par ^ 1]; }
 };
 
 namespace {
@@ -144,6 +169,12 @@ void frame_consts(const fsg_frame_state& f, StepConsts& st) {
   mat_t_vec(st.R, f.pdd, st.a0);
   mat_t_vec(st.R, f.omega, st.wf);
   mat_t_vec(st.R, f.alpha, st.af);
+  for (int k = 0; k < 3; ++k) {
+    st.a0_f[k] = (float)st.a0[k];
+    st.wf_f[k] = (float)st.wf[k];
+    st.af_f[k] = (float)st.af[k];
+  }
+  st._padf = 0.0f;
 }
 
 void decode_status(const StepScratch& sc, fsg_status* st, bool session) {
@@ -175,7 +206,7 @@ int plane_sums(fsg_session* s, double out[19]) {
   const long long n = s->g.n;
   int rc = ensure_tmp(s, sizeof(double) * 19 * (size_t)n);
   if (rc) return rc;
-  s->L->get_f(s->g, s->A, s->pulled, s->d_tmp, s->stream);
+  s->L->get_f(s->g, s->A(), s->pulled, s->d_tmp, s->stream);
   CU_LAUNCH();
   const int nblk = 256;
   if (!s->d_red) CU(cudaMalloc(&s->d_red, sizeof(double) * 19 * nblk));
@@ -193,11 +224,84 @@ int plane_sums(fsg_session* s, double out[19]) {
   return FSG_OK;
 }
 
-int upload_step_consts(fsg_session* s) {
-  CU(cudaEventSynchronize(s->ev_st));  // previous copy out of the pinned buffer done
-  frame_consts(s->frame, *s->h_st);
-  CU(cudaMemcpyAsync(s->d_st, s->h_st, sizeof(StepConsts), cudaMemcpyHostToDevice, s->stream));
-  CU(cudaEventRecord(s->ev_st, s->stream));
+// Step prologue: pull the frame constants from mapped pinned host memory and
+// reset the step scratch (one tiny kernel instead of a copy + a memset node).
+__global__ void k_step_begin(const StepConsts* __restrict__ h_st, StepConsts* d_st,
+                             StepScratch* d_scr) {
+  constexpr int NW = (int)(sizeof(StepConsts) / 4), NS = (int)(sizeof(StepScratch) / 4);
+  for (int k = threadIdx.x; k < NW; k += blockDim.x)
+    reinterpret_cast<int*>(d_st)[k] = reinterpret_cast<const volatile int*>(h_st)[k];
+  for (int k = threadIdx.x; k < NS; k += blockDim.x) reinterpret_cast<int*>(d_scr)[k] = 0;
+}
+// Step epilogue: publish the step status into mapped pinned host memory.
+__global__ void k_step_end(const StepScratch* __restrict__ d_scr, StepScratch* h_scr) {
+  constexpr int NS = (int)(sizeof(StepScratch) / 4);
+  for (int k = threadIdx.x; k < NS; k += blockDim.x)
+    reinterpret_cast<volatile int*>(h_scr)[k] = reinterpret_cast<const int*>(d_scr)[k];
+  __threadfence_system();
+}
+
+// Enqueue the body of one coupled step for parity p on the session stream
+// (used both for graph capture and, with FSG_NO_GRAPH set, direct launch).
+void enqueue_step(fsg_session* s, int p, bool copy_mk, bool frame_on) {
+  const Grid& g = s->g;
+  const size_t m = (size_t)s->m;
+  (void)copy_mk;  // host markers are read in place from mapped pinned memory
+  k_step_begin<<<1, 64, 0, s->stream>>>(s->h_st[p], s->d_st, s->d_scr[p]);
+  if (m) {
+    s->L->markers(g, s->buf[p], s->pulled, s->mk, s->d_sc, s->d_st, s->d_stencil, s->d_boxes,
+                  s->d_fworld, s->h_fw[p], s->h_valid[p], s->d_scr[p], s->stream);
+    s->L->spread(g, s->m, s->d_stencil, s->d_boxes, s->band, s->d_scr[p], s->stream);
+  }
+  s->L->collide(g, s->buf[p], s->pulled, s->buf[p ^ 1], nullptr, &s->band, s->d_scr[p], s->d_sc,
+                s->d_st, s->d_scr[p], 1, frame_on ? 1 : 0, s->stream);
+  k_step_end<<<1, 32, 0, s->stream>>>(s->d_scr[p], s->h_scr[p]);
+}
+
+bool use_graphs() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = std::getenv("FSG_NO_GRAPH");
+    v = (e && e[0] && e[0] != '0') ? 0 : 1;
+  }
+  return v == 1;
+}
+
+void clear_graphs(fsg_session* s) {
+  for (auto& e : s->graphs) cudaGraphExecDestroy(e.exec);
+  s->graphs.clear();
+}
+
+int launch_step(fsg_session* s, int p, bool copy_mk, bool frame_on) {
+  if (!use_graphs()) {
+    enqueue_step(s, p, copy_mk, frame_on);
+    CU_LAUNCH();
+    return FSG_OK;
+  }
+  const void* mkp = s->mk.pts;
+  for (auto& e : s->graphs)
+    if (e.par == p && e.pulled == s->pulled && e.m == s->m && e.copy_mk == (int)copy_mk &&
+        e.frame_on == (int)frame_on && e.mkp == mkp) {
+      CU(cudaGraphLaunch(e.exec, s->stream));
+      return FSG_OK;
+    }
+  if (s->graphs.size() >= 16) clear_graphs(s);
+  cudaGraph_t graph = nullptr;
+  CU(cudaStreamBeginCapture(s->stream, cudaStreamCaptureModeThreadLocal));
+  enqueue_step(s, p, copy_mk, frame_on);
+  const cudaError_t cap_err = cudaGetLastError();
+  cudaError_t e = cudaStreamEndCapture(s->stream, &graph);
+  if (cap_err != cudaSuccess || e != cudaSuccess) {
+    if (graph) cudaGraphDestroy(graph);
+    return set_err(FSG_ECUDA, "step graph capture failed: %s",
+                   cudaGetErrorString(cap_err != cudaSuccess ? cap_err : e));
+  }
+  cudaGraphExec_t exec = nullptr;
+  e = cudaGraphInstantiate(&exec, graph, 0);
+  cudaGraphDestroy(graph);
+  if (e != cudaSuccess) return set_err(FSG_ECUDA, "graph instantiate: %s", cudaGetErrorString(e));
+  s->graphs.push_back(GraphEntry{p, s->pulled, s->m, (int)copy_mk, (int)frame_on, mkp, exec});
+  CU(cudaGraphLaunch(exec, s->stream));
   return FSG_OK;
 }
 
@@ -249,6 +353,8 @@ int fsg_create(const fsg_config* cfg_in, fsg_session** out) {
   if (cfg.dims[2] < (slab ? 2 : 8) || cfg.z_offset < 0 || cfg.z_offset + cfg.dims[2] > cfg.nz_global)
     return set_err(FSG_EINPUT, "bad z slab: offset %d depth %d of %d", cfg.z_offset, cfg.dims[2],
                    cfg.nz_global);
+  if ((long long)cfg.dims[0] * cfg.dims[1] * (cfg.dims[2] + 2) >= (1ll << 31))
+    return set_err(FSG_EINPUT, "slab too large: a direction plane must hold < 2^31 cells");
   if (cfg.boundary != FSG_BOUNDARY_OPEN && cfg.boundary != FSG_BOUNDARY_PERIODIC)
     return set_err(FSG_EINPUT, "unknown boundary mode %d", cfg.boundary);
   if (cfg.kernel != FSG_KERNEL_PESKIN4 && cfg.kernel != FSG_KERNEL_ROMA3)
@@ -282,6 +388,7 @@ int fsg_create(const fsg_config* cfg_in, fsg_session** out) {
   g.plane = (long long)g.nx * g.ny;
   g.n = g.plane * g.nz;
   g.stride = ((g.plane * (g.nz + 2 * g.zpad) + 31) / 32) * 32;
+  fsg::grid_offsets(g);
 
   // session constants, host fp64 in the reference's order
   SessionConsts& sc = s->hsc;
@@ -297,13 +404,22 @@ int fsg_create(const fsg_config* cfg_in, fsg_session** out) {
   for (int a = 0; a < 3; ++a) {
     sc.hd[a] = 0.5 * (dg[a] - 1);
     sc.dims_g[a] = dg[a];
+    sc.hd_f[a] = (float)sc.hd[a];
   }
+  sc.dx_f = (float)sc.dx;
+  sc.v2p_f = (float)sc.v2p;
+  sc.acc_f = (float)sc.acc;
   sc.kernel = cfg.kernel;
   sc.wall = cfg.wall;
   sc.frame_on = cfg.frame_mode != FSG_FRAME_NONE;
+  const double wcls[3] = {1.0 / 3.0, 1.0 / 18.0, 1.0 / 36.0};
+  sc.om1_f = (float)(1.0 - sc.omega);
+  for (int k = 0; k < 3; ++k) {
+    sc.ow_f[k] = (float)(sc.omega * wcls[k]);
+    sc.gw_f[k] = (float)(sc.guo * wcls[k]);
+  }
   s->frame.q[0] = 1.0;
 
-  int rc = FSG_OK;
   auto fail = [&](int code) {
     fsg_destroy(s);
     return code;
@@ -316,37 +432,40 @@ int fsg_create(const fsg_config* cfg_in, fsg_session** out) {
   } while (0)
   CUF(cudaStreamCreateWithFlags(&s->stream, cudaStreamNonBlocking));
   const size_t fbytes = (size_t)s->L->elem_bytes * 19 * (size_t)g.stride;
-  CUF(cudaMalloc(&s->A, fbytes));
-  CUF(cudaMalloc(&s->B, fbytes));
-  CUF(cudaMemsetAsync(s->A, 0, fbytes, s->stream));
-  CUF(cudaMemsetAsync(s->B, 0, fbytes, s->stream));
+  for (int k = 0; k < 2; ++k) {
+    CUF(cudaMalloc(&s->buf[k], fbytes));
+    CUF(cudaMemsetAsync(s->buf[k], 0, fbytes, s->stream));
+    CUF(cudaMalloc(&s->d_scr[k], sizeof(StepScratch)));
+    CUF(cudaMemsetAsync(s->d_scr[k], 0, sizeof(StepScratch), s->stream));
+    CUF(cudaMallocHost(&s->h_st[k], sizeof(StepConsts)));
+    CUF(cudaMallocHost(&s->h_scr[k], sizeof(StepScratch)));
+    std::memset(s->h_scr[k], 0, sizeof(StepScratch));
+    CUF(cudaEventCreateWithFlags(&s->ev[k], cudaEventDisableTiming));
+    CUF(cudaEventRecord(s->ev[k], s->stream));
+  }
   CUF(cudaMalloc(&s->d_sc, sizeof(SessionConsts)));
   CUF(cudaMalloc(&s->d_st, sizeof(StepConsts)));
-  CUF(cudaMalloc(&s->d_scr, sizeof(StepScratch)));
-  CUF(cudaMallocHost(&s->h_st, sizeof(StepConsts)));
-  CUF(cudaMallocHost(&s->h_scr, sizeof(StepScratch)));
   CUF(cudaMemcpyAsync(s->d_sc, &s->hsc, sizeof(SessionConsts), cudaMemcpyHostToDevice, s->stream));
-  CUF(cudaMemsetAsync(s->d_scr, 0, sizeof(StepScratch), s->stream));
   s->cap = cfg.max_markers;
   CUF(cudaMalloc(&s->d_mk, sizeof(double) * 10 * (size_t)s->cap));
-  CUF(cudaMallocHost(&s->h_mk, sizeof(double) * 10 * (size_t)s->cap));
+  for (int k = 0; k < 2; ++k) {
+    CUF(cudaMallocHost(&s->h_mk[k], sizeof(double) * 10 * (size_t)s->cap));
+    CUF(cudaMallocHost(&s->h_fw[k], sizeof(double) * 3 * (size_t)s->cap));
+    CUF(cudaMallocHost(&s->h_valid[k], sizeof(int) * (size_t)s->cap));
+    CUF(cudaEventCreateWithFlags(&s->ev_mk[k], cudaEventDisableTiming));
+    CUF(cudaEventRecord(s->ev_mk[k], s->stream));
+  }
   CUF(cudaMalloc(&s->d_stencil, sizeof(MarkerStencil) * (size_t)s->cap));
+  CUF(cudaMalloc(&s->d_boxes, sizeof(MarkerBox) * (size_t)s->cap));
   CUF(cudaMalloc(&s->d_fworld, sizeof(double) * 3 * (size_t)s->cap));
   s->band.cap = std::min<long long>(g.n, 16ll << 20);
-  CUF(cudaMalloc(&s->band.u, sizeof(double) * 3 * (size_t)s->band.cap));
   CUF(cudaMalloc(&s->band.F, sizeof(double) * 3 * (size_t)s->band.cap));
-  CUF(cudaMalloc(&s->d_junk, sizeof(StepScratch)));
-  CUF(cudaEventCreateWithFlags(&s->ev_st, cudaEventDisableTiming));
-  CUF(cudaEventCreateWithFlags(&s->ev_mk, cudaEventDisableTiming));
-  CUF(cudaEventRecord(s->ev_st, s->stream));
-  CUF(cudaEventRecord(s->ev_mk, s->stream));
-#undef CUF
-  s->L->fill_rest(g, s->A, s->stream);
+  s->L->fill_rest(g, s->A(), s->stream);
   if (cudaGetLastError() != cudaSuccess) return fail(set_err(FSG_ECUDA, "fill_rest launch failed"));
   if (cudaStreamSynchronize(s->stream) != cudaSuccess)
     return fail(set_err(FSG_ECUDA, "session init failed"));
+#undef CUF
   s->pulled = 0;
-  (void)rc;
   *out = s;
   return FSG_OK;
 }
@@ -355,25 +474,28 @@ int fsg_destroy(fsg_session* s) {
   if (!s) return FSG_OK;
   cudaSetDevice(s->cfg.device);
   if (s->stream) cudaStreamSynchronize(s->stream);
-  cudaFree(s->A);
-  cudaFree(s->B);
+  clear_graphs(s);
+  for (int k = 0; k < 2; ++k) {
+    cudaFree(s->buf[k]);
+    cudaFree(s->d_scr[k]);
+    if (s->h_st[k]) cudaFreeHost(s->h_st[k]);
+    if (s->h_scr[k]) cudaFreeHost(s->h_scr[k]);
+    if (s->h_mk[k]) cudaFreeHost(s->h_mk[k]);
+    if (s->h_fw[k]) cudaFreeHost(s->h_fw[k]);
+    if (s->h_valid[k]) cudaFreeHost(s->h_valid[k]);
+    if (s->ev[k]) cudaEventDestroy(s->ev[k]);
+    if (s->ev_mk[k]) cudaEventDestroy(s->ev_mk[k]);
+  }
   cudaFree(s->Fext);
   cudaFree(s->d_sc);
   cudaFree(s->d_st);
-  cudaFree(s->d_scr);
-  if (s->h_st) cudaFreeHost(s->h_st);
-  if (s->h_scr) cudaFreeHost(s->h_scr);
   cudaFree(s->d_mk);
-  if (s->h_mk) cudaFreeHost(s->h_mk);
   cudaFree(s->d_stencil);
+  cudaFree(s->d_boxes);
   cudaFree(s->d_fworld);
-  cudaFree(s->band.u);
   cudaFree(s->band.F);
   cudaFree(s->d_tmp);
   cudaFree(s->d_red);
-  cudaFree(s->d_junk);
-  if (s->ev_st) cudaEventDestroy(s->ev_st);
-  if (s->ev_mk) cudaEventDestroy(s->ev_mk);
   if (s->stream) cudaStreamDestroy(s->stream);
   delete s;
   return FSG_OK;
@@ -382,12 +504,17 @@ int fsg_destroy(fsg_session* s) {
 void* fsg_stream(fsg_session* s) { return s ? (void*)s->stream : nullptr; }
 
 // --------------------------------------------------------------- state --
+static void state_changed(fsg_session* s) {
+  s->last_valid = false;
+  s->stepped = false;
+}
+
 int fsg_reset_rest(fsg_session* s) {
   CU(cudaSetDevice(s->cfg.device));
-  s->L->fill_rest(s->g, s->A, s->stream);
+  s->L->fill_rest(s->g, s->A(), s->stream);
   CU_LAUNCH();
   s->pulled = 0;
-  s->last_valid = false;
+  state_changed(s);
   CU(cudaStreamSynchronize(s->stream));
   return FSG_OK;
 }
@@ -400,10 +527,10 @@ int fsg_initialize(fsg_session* s, const double* rho, const double* u) {
   if (rc) return rc;
   CU(cudaMemcpyAsync(s->d_tmp, rho, sizeof(double) * n, cudaMemcpyHostToDevice, s->stream));
   CU(cudaMemcpyAsync(s->d_tmp + n, u, sizeof(double) * 3 * n, cudaMemcpyHostToDevice, s->stream));
-  s->L->init_eq(s->g, s->d_tmp, s->d_tmp + n, s->A, s->stream);
+  s->L->init_eq(s->g, s->d_tmp, s->d_tmp + n, s->A(), s->stream);
   CU_LAUNCH();
   s->pulled = 0;
-  s->last_valid = false;
+  state_changed(s);
   CU(cudaStreamSynchronize(s->stream));
   return FSG_OK;
 }
@@ -415,10 +542,10 @@ int fsg_set_f(fsg_session* s, const double* f) {
   int rc = ensure_tmp(s, sizeof(double) * 19 * n);
   if (rc) return rc;
   CU(cudaMemcpyAsync(s->d_tmp, f, sizeof(double) * 19 * n, cudaMemcpyHostToDevice, s->stream));
-  s->L->set_f(s->g, s->d_tmp, s->A, s->stream);
+  s->L->set_f(s->g, s->d_tmp, s->A(), s->stream);
   CU_LAUNCH();
   s->pulled = 0;
-  s->last_valid = false;
+  state_changed(s);
   CU(cudaStreamSynchronize(s->stream));
   return FSG_OK;
 }
@@ -429,7 +556,7 @@ int fsg_get_f(fsg_session* s, double* f) {
   const size_t n = (size_t)s->g.n;
   int rc = ensure_tmp(s, sizeof(double) * 19 * n);
   if (rc) return rc;
-  s->L->get_f(s->g, s->A, s->pulled, s->d_tmp, s->stream);
+  s->L->get_f(s->g, s->A(), s->pulled, s->d_tmp, s->stream);
   CU_LAUNCH();
   CU(cudaMemcpyAsync(f, s->d_tmp, sizeof(double) * 19 * n, cudaMemcpyDeviceToHost, s->stream));
   CU(cudaStreamSynchronize(s->stream));
@@ -463,16 +590,20 @@ int fsg_set_force(fsg_session* s, const double* F) {
 
 int fsg_collide_and_stream(fsg_session* s, fsg_status* st) {
   CU(cudaSetDevice(s->cfg.device));
-  CU(cudaMemsetAsync(s->d_scr, 0, sizeof(StepScratch), s->stream));
-  s->L->collide(s->g, s->A, s->pulled, s->B, s->Fext, nullptr, nullptr, s->d_sc, s->d_st, s->d_scr,
-                0, 0, s->stream);
+  const int p = s->par;
+  CU(cudaEventSynchronize(s->ev[p]));
+  CU(cudaMemsetAsync(s->d_scr[p], 0, sizeof(StepScratch), s->stream));
+  s->L->collide(s->g, s->A(), s->pulled, s->B(), s->Fext, nullptr, nullptr, s->d_sc, s->d_st,
+                s->d_scr[p], 0, 0, s->stream);
   CU_LAUNCH();
-  CU(cudaMemcpyAsync(s->h_scr, s->d_scr, sizeof(StepScratch), cudaMemcpyDeviceToHost, s->stream));
+  CU(cudaMemcpyAsync(s->h_scr[p], s->d_scr[p], sizeof(StepScratch), cudaMemcpyDeviceToHost,
+                     s->stream));
+  CU(cudaEventRecord(s->ev[p], s->stream));
   CU(cudaStreamSynchronize(s->stream));
-  std::swap(s->A, s->B);
+  s->par ^= 1;
   s->pulled = 1;
-  s->last_valid = false;
-  decode_status(*s->h_scr, &s->last, false);
+  state_changed(s);
+  decode_status(*s->h_scr[p], &s->last, false);
   if (st) *st = s->last;
   return FSG_OK;
 }
@@ -482,15 +613,18 @@ int fsg_macroscopic(fsg_session* s, double* rho, double* u, int* nonpos) {
   const size_t n = (size_t)s->g.n;
   int rc = ensure_tmp(s, sizeof(double) * 4 * n);
   if (rc) return rc;
-  CU(cudaMemsetAsync(s->d_scr, 0, sizeof(StepScratch), s->stream));
-  s->L->macroscopic(s->g, s->A, s->pulled, s->Fext, s->d_tmp, s->d_tmp + n, s->d_scr, s->stream);
+  const int p = s->par;
+  CU(cudaStreamSynchronize(s->stream));
+  CU(cudaMemsetAsync(s->d_scr[p], 0, sizeof(StepScratch), s->stream));
+  s->L->macroscopic(s->g, s->A(), s->pulled, s->Fext, s->d_tmp, s->d_tmp + n, s->d_scr[p], s->stream);
   CU_LAUNCH();
   if (rho) CU(cudaMemcpyAsync(rho, s->d_tmp, sizeof(double) * n, cudaMemcpyDeviceToHost, s->stream));
   if (u) CU(cudaMemcpyAsync(u, s->d_tmp + n, sizeof(double) * 3 * n, cudaMemcpyDeviceToHost, s->stream));
-  CU(cudaMemcpyAsync(s->h_scr, s->d_scr, sizeof(StepScratch), cudaMemcpyDeviceToHost, s->stream));
+  StepScratch sc;
+  CU(cudaMemcpyAsync(&sc, s->d_scr[p], sizeof(StepScratch), cudaMemcpyDeviceToHost, s->stream));
   CU(cudaStreamSynchronize(s->stream));
-  if (nonpos) *nonpos = s->h_scr->nonpos;
-  s->last_valid = false;  // scratch reused
+  if (nonpos) *nonpos = sc.nonpos;
+  s->last_valid = false;  // the step scratch of parity p was reused
   return FSG_OK;
 }
 
@@ -535,12 +669,12 @@ int fsg_get_frame(fsg_session* s, fsg_frame_state* fs) {
 int fsg_recenter(fsg_session* s, const int shift[3]) {
   if (s->g.zpad) return set_err(FSG_EINPUT, "recenter is not defined for z-slab sessions");
   CU(cudaSetDevice(s->cfg.device));
-  s->L->recenter(s->g, s->A, s->pulled, s->B, shift[0], shift[1], shift[2], s->stream);
+  s->L->recenter(s->g, s->A(), s->pulled, s->B(), shift[0], shift[1], shift[2], s->stream);
   CU_LAUNCH();
   CU(cudaStreamSynchronize(s->stream));
-  std::swap(s->A, s->B);
+  s->par ^= 1;
   s->pulled = 0;
-  s->last_valid = false;
+  state_changed(s);
   // frame.hpp:152-153: p += R * (shift * dx)
   double R[9];
   quat_to_R(s->frame.q, R);
@@ -573,21 +707,24 @@ int fsg_set_markers(fsg_session* s, int n_bodies, const int64_t* off, const doub
   if (rc) return rc;
   const size_t m = (size_t)s->m;
   CU(cudaSetDevice(s->cfg.device));
+  // pinned slot the marker kernel reads in place (zero-copy): alternate slots so
+  // the host fills one while a queued step may still read the other
+  const int p = s->mk_slot < 0 ? 0 : (s->mk_slot ^ 1);
   if (m) {
     if (!pts || !vel || !nrm || !area) return set_err(FSG_EINPUT, "fsg_set_markers: null array");
-    // one pinned staging buffer [pts | vel | nrm | area] -> one H2D copy
-    CU(cudaEventSynchronize(s->ev_mk));
-    double* h = s->h_mk;
+    CU(cudaEventSynchronize(s->ev_mk[p]));  // last step that read this slot is done
+    double* h = s->h_mk[p];
     std::memcpy(h, pts, sizeof(double) * 3 * m);
     std::memcpy(h + 3 * m, vel, sizeof(double) * 3 * m);
     std::memcpy(h + 6 * m, nrm, sizeof(double) * 3 * m);
     std::memcpy(h + 9 * m, area, sizeof(double) * m);
-    CU(cudaMemcpyAsync(s->d_mk, h, sizeof(double) * 10 * m, cudaMemcpyHostToDevice, s->stream));
-    CU(cudaEventRecord(s->ev_mk, s->stream));
     s->h_vel.assign(vel, vel + 3 * m);
   }
-  s->mk = Markers{s->d_mk, s->d_mk + 3 * m, s->d_mk + 6 * m, s->d_mk + 9 * m, (int)m};
-  s->mk_host_vel = true;
+  double* h = s->h_mk[p];
+  s->mk = Markers{h, h + 3 * m, h + 6 * m, h + 9 * m, (int)m};
+  s->mk_slot = p;
+  s->mk_host = true;
+  s->mk_dirty = m > 0;
   return FSG_OK;
 }
 
@@ -596,44 +733,46 @@ int fsg_set_markers_device(fsg_session* s, int n_bodies, const int64_t* off, con
   int rc = set_markers_common(s, n_bodies, off);
   if (rc) return rc;
   s->mk = Markers{pts, vel, nrm, area, s->m};
-  s->mk_host_vel = false;
+  s->mk_host = false;
+  s->mk_slot = -1;
+  s->mk_dirty = false;
   return FSG_OK;
 }
 
 // ----------------------------------------------------------------- step --
 int fsg_step_async(fsg_session* s) {
   CU(cudaSetDevice(s->cfg.device));
-  const Grid& g = s->g;
-  int rc = upload_step_consts(s);
-  if (rc) return rc;
-  CU(cudaMemsetAsync(s->d_scr, 0, sizeof(StepScratch), s->stream));
+  const int p = s->par;
+  CU(cudaEventSynchronize(s->ev[p]));  // pinned slots of parity p are free again
+  frame_consts(s->frame, *s->h_st[p]);
   const bool frame_on = s->cfg.frame_mode != FSG_FRAME_NONE;
-  if (s->m > 0) {
-    s->L->markers_prepare(g, s->mk, s->d_sc, s->d_st, s->d_stencil, s->d_scr, s->stream);
-    s->L->band_moments(g, s->A, s->pulled, s->band, s->d_scr, s->d_scr, s->stream);
-    s->L->markers_force(g, s->mk, s->d_sc, s->d_st, s->d_stencil, s->band, s->d_scr, s->d_fworld,
-                        s->stream);
-    s->L->spread(g, s->m, s->d_stencil, s->band, s->d_scr, s->stream);
-  }
-  s->L->collide(g, s->A, s->pulled, s->B, nullptr, &s->band, s->d_scr, s->d_sc, s->d_st, s->d_scr,
-                1, frame_on ? 1 : 0, s->stream);
-  CU_LAUNCH();
-  CU(cudaMemcpyAsync(s->h_scr, s->d_scr, sizeof(StepScratch), cudaMemcpyDeviceToHost, s->stream));
-  s->prevA = s->A;
+  const bool copy_mk = s->mk_host && s->mk_dirty;
+  int rc = launch_step(s, p, copy_mk, frame_on);
+  if (rc) return rc;
+  CU(cudaEventRecord(s->ev[p], s->stream));
+  if (s->mk_host && s->mk_slot >= 0) CU(cudaEventRecord(s->ev_mk[s->mk_slot], s->stream));
+  s->last_par = p;
   s->prev_pulled = s->pulled;
   s->last_frame_on = frame_on;
-  std::swap(s->A, s->B);
+  s->par ^= 1;
   s->pulled = 1;
   s->last_valid = true;
+  s->stepped = true;
+  s->mk_dirty = false;
   return FSG_OK;
 }
 
 int fsg_last_status(fsg_session* s, fsg_status* st) {
   CU(cudaStreamSynchronize(s->stream));
-  if (s->h_scr->band_overflow)
+  if (!s->stepped) {
+    if (st) *st = s->last;
+    return FSG_OK;
+  }
+  const StepScratch& sc = *s->h_scr[s->last_par];
+  if (sc.band_overflow)
     return set_err(FSG_ESTATE, "IB band bounding box exceeds capacity (%lld cells)",
                    (long long)s->band.cap);
-  decode_status(*s->h_scr, &s->last, true);
+  decode_status(sc, &s->last, true);
   if (st) *st = s->last;
   return FSG_OK;
 }
@@ -647,21 +786,17 @@ int fsg_step(fsg_session* s, fsg_status* st) {
 int fsg_get_marker_forces(fsg_session* s, double* fw, int* valid, double* stats) {
   CU(cudaSetDevice(s->cfg.device));
   const size_t m = (size_t)s->m;
-  std::vector<double> f(3 * m);
-  std::vector<MarkerStencil> st(m);
-  if (m) {
-    CU(cudaMemcpyAsync(f.data(), s->d_fworld, sizeof(double) * 3 * m, cudaMemcpyDeviceToHost, s->stream));
-    CU(cudaMemcpyAsync(st.data(), s->d_stencil, sizeof(MarkerStencil) * m, cudaMemcpyDeviceToHost,
-                       s->stream));
-  }
+  // the marker kernel wrote the forces straight into mapped pinned memory
   CU(cudaStreamSynchronize(s->stream));
-  if (fw) std::memcpy(fw, f.data(), sizeof(double) * 3 * m);
-  if (valid)
-    for (size_t i = 0; i < m; ++i) valid[i] = st[i].valid;
+  if (!s->stepped) return set_err(FSG_ESTATE, "no coupled step yet");
+  const double* f = s->h_fw[s->last_par];
+  const int* vv = s->h_valid[s->last_par];
+  if (fw) std::memcpy(fw, f, sizeof(double) * 3 * m);
+  if (valid) std::memcpy(valid, vv, sizeof(int) * m);
   if (stats) {
     std::vector<double> vel;
     const double* v = nullptr;
-    if (s->mk_host_vel) {
+    if (s->mk_host) {
       v = s->h_vel.data();
     } else if (m) {
       vel.resize(3 * m);
@@ -672,7 +807,7 @@ int fsg_get_marker_forces(fsg_session* s, double* fw, int* valid, double* stats)
     for (int b = 0; b < s->n_bodies; ++b) {
       double tf[3] = {0, 0, 0}, tb[3] = {0, 0, 0}, power = 0.0;
       for (int64_t i = s->offsets[b]; i < s->offsets[b + 1]; ++i) {
-        if (!st[i].valid) continue;
+        if (!vv[i]) continue;
         const double* w = &f[3 * i];
         for (int k = 0; k < 3; ++k) {
           tf[k] = tf[k] + w[k];
@@ -694,14 +829,17 @@ int fsg_get_stencils(fsg_session* s, int* lo_hi) {
   CU(cudaSetDevice(s->cfg.device));
   const size_t m = (size_t)s->m;
   std::vector<MarkerStencil> st(m);
-  if (m)
+  std::vector<MarkerBox> bx(m);
+  if (m) {
     CU(cudaMemcpyAsync(st.data(), s->d_stencil, sizeof(MarkerStencil) * m, cudaMemcpyDeviceToHost,
                        s->stream));
+    CU(cudaMemcpyAsync(bx.data(), s->d_boxes, sizeof(MarkerBox) * m, cudaMemcpyDeviceToHost, s->stream));
+  }
   CU(cudaStreamSynchronize(s->stream));
   for (size_t i = 0; i < m; ++i)
     for (int a = 0; a < 3; ++a) {
-      lo_hi[6 * i + a] = st[i].valid ? st[i].lo[a] : 0;
-      lo_hi[6 * i + 3 + a] = st[i].valid ? st[i].hi[a] : -1;
+      lo_hi[6 * i + a] = bx[i].valid ? st[i].lo[a] : 0;
+      lo_hi[6 * i + 3 + a] = bx[i].valid ? st[i].hi[a] : -1;
     }
   return FSG_OK;
 }
@@ -712,8 +850,10 @@ int fsg_get_macro(fsg_session* s, double* rho, double* u) {
   const size_t n = (size_t)s->g.n;
   int rc = ensure_tmp(s, sizeof(double) * 4 * n);
   if (rc) return rc;
-  s->L->macroscopic(s->g, s->prevA, s->prev_pulled, nullptr, s->d_tmp, s->d_tmp + n, s->d_junk,
-                    s->stream);
+  CU(cudaStreamSynchronize(s->stream));
+  StepScratch* junk = s->d_scr[s->last_par ^ 1];  // not read back by anyone
+  s->L->macroscopic(s->g, s->buf[s->last_par], s->prev_pulled, nullptr, s->d_tmp, s->d_tmp + n,
+                    junk, s->stream);
   CU_LAUNCH();
   if (rho) CU(cudaMemcpyAsync(rho, s->d_tmp, sizeof(double) * n, cudaMemcpyDeviceToHost, s->stream));
   if (u) CU(cudaMemcpyAsync(u, s->d_tmp + n, sizeof(double) * 3 * n, cudaMemcpyDeviceToHost, s->stream));
@@ -727,8 +867,8 @@ int fsg_get_force(fsg_session* s, double* F) {
   const size_t n = (size_t)s->g.n;
   int rc = ensure_tmp(s, sizeof(double) * 3 * n);
   if (rc) return rc;
-  s->L->session_force(s->g, s->prevA, s->prev_pulled, &s->band, s->d_scr, s->d_sc, s->d_st,
-                      s->last_frame_on ? 1 : 0, s->d_tmp, s->stream);
+  s->L->session_force(s->g, s->buf[s->last_par], s->prev_pulled, &s->band, s->d_scr[s->last_par],
+                      s->d_sc, s->d_st, s->last_frame_on ? 1 : 0, s->d_tmp, s->stream);
   CU_LAUNCH();
   CU(cudaMemcpyAsync(F, s->d_tmp, sizeof(double) * 3 * n, cudaMemcpyDeviceToHost, s->stream));
   CU(cudaStreamSynchronize(s->stream));
@@ -741,7 +881,7 @@ size_t fsg_halo_bytes(fsg_session* s) { return (size_t)5 * s->g.plane * s->L->el
 int fsg_halo_pack(fsg_session* s, void* lo, void* hi) {
   if (!s->g.zpad) return set_err(FSG_EINPUT, "not a z-slab session");
   CU(cudaSetDevice(s->cfg.device));
-  s->L->halo_pack(s->g, s->A, lo, hi, s->stream);
+  s->L->halo_pack(s->g, s->A(), lo, hi, s->stream);
   CU_LAUNCH();
   return FSG_OK;
 }
@@ -749,7 +889,7 @@ int fsg_halo_pack(fsg_session* s, void* lo, void* hi) {
 int fsg_halo_unpack(fsg_session* s, const void* lo, const void* hi) {
   if (!s->g.zpad) return set_err(FSG_EINPUT, "not a z-slab session");
   CU(cudaSetDevice(s->cfg.device));
-  s->L->halo_unpack(s->g, s->A, lo, hi, s->stream);
+  s->L->halo_unpack(s->g, s->A(), lo, hi, s->stream);
   CU_LAUNCH();
   return FSG_OK;
 }

@@ -43,7 +43,8 @@ def test_collide_and_stream_fp64_bit_exact(mk):
     assert r["nonpos"] == g["nonpos"]
     # reductions: deterministic tree order vs the reference's serial order
     assert abs(r["mass"] - g["mass"]) <= 1e-13 * abs(g["mass"])
-    assert np.abs(r["momentum"] - g["momentum"]).max() <= 1e-13 * max(1.0, np.abs(g["momentum"]).max())
+    # (momentum: cancellation over 19 n terms of O(w); scale by the mass)
+    assert np.abs(r["momentum"] - g["momentum"]).max() <= 1e-13 * abs(g["mass"])
 
 
 @pytest.mark.parametrize("mk", [K.case_lbm_open, K.case_lbm_periodic])
