@@ -101,9 +101,24 @@ struct StepScratch {
   int band_overflow;               // bbox exceeded band capacity
   int bbox_lo_enc[3];
   int bbox_hi_enc[3];
-  int _pad[2];
+  unsigned blocks_done;              // K4 last-block detection (status publish)
+  int _pad;
 };
 constexpr int LO_BIAS = 0x40000000;
+constexpr int TICKET_GROUPS = 1024;  // K4 last-block detection: group counters + 1 global
+
+// Throughput-mode IB force field: 64-bit fixed point (2^-40 lattice force
+// units), accumulated with integer atomics -- associative, hence bit-
+// deterministic whatever the order -- over 4x4x4 tiles flagged per step.
+constexpr double FIX_SCALE = 1099511627776.0;        // 2^40
+constexpr double FIX_INV = 1.0 / 1099511627776.0;   // 2^-40
+struct FixBand {
+  unsigned long long* F;     // 3 per owned cell (x + nx*(y + ny*z))
+  unsigned char* flag_cur;   // tiles touched this step (read by K4)
+  unsigned char* flag_prev;  // tiles of the previous step (cleared by K4)
+  int tnx, tny, tnz;         // tile grid (4^3 cells per tile)
+  int _pad;
+};
 
 __host__ __device__ __forceinline__ unsigned long long ordered_key(double v) {
 #ifdef __CUDA_ARCH__
@@ -184,6 +199,15 @@ struct Launchers {
                   double* fworld_host, int* valid_host, StepScratch*, cudaStream_t);
   void (*spread)(const Grid&, int m, const MarkerStencil*, const MarkerBox*, Band,
                  const StepScratch*, cudaStream_t);
+  // throughput path (fp32 only; nullptr in the fp64 table): markers scatter
+  // fixed-point forces; K4 consumes them and publishes the step status
+  void (*markers_fix)(const Grid&, const void* A, int pulled, Markers, const SessionConsts*,
+                      const StepConsts& st, MarkerStencil*, double* fworld, double* fworld_host,
+                      int* valid_host, FixBand, StepScratch*, cudaStream_t);
+  void (*collide_fix)(const Grid&, const void* A, int pulled, void* B, FixBand,
+                      const SessionConsts*, const StepConsts& st, int frame_on, int has_ib,
+                      StepScratch* scr, StepScratch* scr_next, StepScratch* publish,
+                      unsigned* tickets, unsigned* tickets_next, cudaStream_t);
   // halo planes (z-slab): pack owned boundary planes / unpack into halo planes
   void (*halo_pack)(const Grid&, const void* B, void* send_lo, void* send_hi, cudaStream_t);
   void (*halo_unpack)(const Grid&, void* B, const void* recv_lo, const void* recv_hi,

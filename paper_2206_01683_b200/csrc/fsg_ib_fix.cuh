@@ -1,0 +1,185 @@
+// fsg_ib_fix.cuh -- throughput-mode immersed boundary (fp32 session), included
+// inside namespace fsg::p32 after fsg_ib.cuh.
+//
+// One half-warp per marker does the whole reference chain of
+// session.hpp:113-138 (position, bounds, stencil, bare moments of the
+// stencil cells, interpolate_velocity, body velocity, direct forcing) and then
+// SPREADS its own force: every stencil contribution w * f (coupling.hpp:52-71)
+// is converted to 64-bit fixed point (2^-40) and added with an integer atomic.
+// Integer addition is associative, so the accumulated field is bit-identical
+// run to run whatever order the atomics land in -- deterministic without a
+// separate ordered-spread kernel.  Touched 4^3 tiles are flagged; K4 reads
+// (and re-zeroes) only flagged tiles.  The interpolation sum uses a fixed
+// half-warp butterfly (deterministic); the fp64 parity path keeps the
+// reference's serial order instead (fsg_ib.cuh).
+
+__device__ __forceinline__ unsigned long long to_fix(double v) {
+  return (unsigned long long)__double2ll_rn(v * FIX_SCALE);
+}
+
+template <bool PULLED>
+__global__ void __launch_bounds__(128)
+    k_markers_fix(Grid g, const float* __restrict__ A, Markers mk, const SessionConsts* __restrict__ scp,
+                  const StepConsts st, MarkerStencil* __restrict__ rec_out, double* __restrict__ fworld,
+                  double* fworld_h, int* valid_h, FixBand fb, StepScratch* out) {
+  __shared__ double phs[MK_PER_BLOCK][3][5];
+  const int hl = threadIdx.x & (MK_LANES - 1);
+  const int slot = threadIdx.x / MK_LANES;
+  const unsigned hmask = 0xFFFFu << (threadIdx.x & 16);
+  const int t = blockIdx.x * MK_PER_BLOCK + slot;
+  if (t >= mk.m) return;  // uniform over the half-warp
+  const SessionConsts& sc = *scp;
+  // marker state: broadcast loads (may be mapped pinned host memory)
+  double xw[3], vel[3], nrm[3];
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    xw[k] = mk.pts[3 * t + k] - st.p[k];
+    vel[k] = mk.vel[3 * t + k];
+    nrm[k] = mk.nrm[3 * t + k];
+  }
+  const double area = mk.area[t];
+  double xf[3], xl[3];
+  mat_t_vec(st.R, xw, xf);
+#pragma unroll
+  for (int k = 0; k < 3; ++k) xl[k] = xf[k] / sc.dx + sc.hd[k];
+  const double half = 0.5 * (sc.kernel == 0 ? 4 : 3);
+  bool ok = true;
+#pragma unroll
+  for (int a = 0; a < 3; ++a)
+    if (xl[a] < half || xl[a] > sc.dims_g[a] - 1 - half) ok = false;  // coupling.hpp:18-24
+  if (!ok) {
+    if (hl == 0) {
+      rec_out[t].valid = 0;
+      fworld[3 * t] = fworld[3 * t + 1] = fworld[3 * t + 2] = 0.0;
+      if (fworld_h) {
+        fworld_h[3 * t] = fworld_h[3 * t + 1] = fworld_h[3 * t + 2] = 0.0;
+        valid_h[t] = 0;
+      }
+      atomicAdd(&out->oob, 1);
+    }
+    return;
+  }
+  int lo[3], hi[3], cnt[3];
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    lo[a] = (int)ceil(xl[a] - half);  // kernel.hpp:36-40
+    hi[a] = (int)floor(xl[a] + half);
+    cnt[a] = hi[a] - lo[a] + 1;
+  }
+  if (hl < 15) {
+    const int a = hl / 5, q = hl % 5;
+    const int la = a == 0 ? lo[0] : (a == 1 ? lo[1] : lo[2]);
+    const double xa = a == 0 ? xl[0] : (a == 1 ? xl[1] : xl[2]);
+    const int ca = a == 0 ? cnt[0] : (a == 1 ? cnt[1] : cnt[2]);
+    phs[slot][a][q] = q < ca ? ib_phi(sc.kernel, (la + q) - xa) : 0.0;
+  }
+  __syncwarp(hmask);
+  const int ncell = cnt[0] * cnt[1] * cnt[2];
+  const float r0 = 1.0f / (float)cnt[0], r01 = 1.0f / (float)(cnt[0] * cnt[1]);
+  double a0 = 0.0, a1 = 0.0, a2 = 0.0;
+  // this lane's cells c = hl + 16 r (r < 8): gathered 4 at a time
+  for (int c0 = 0; c0 < ncell; c0 += 4 * MK_LANES) {
+    float sv[4][Q];
+    int cio[4], cjo[4], cko[4];
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      const int c = c0 + hl + MK_LANES * r;
+      const int ko = (int)(((float)c + 0.5f) * r01);
+      const int rem = c - ko * cnt[0] * cnt[1];
+      const int jo = (int)(((float)rem + 0.5f) * r0);
+      cio[r] = rem - jo * cnt[0];
+      cjo[r] = jo;
+      cko[r] = ko;
+      if (c < ncell) gather_cell<PULLED>(g, A, lo[0] + cio[r], lo[1] + jo, lo[2] + ko - g.z0, sv[r]);
+    }
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      const int c = c0 + hl + MK_LANES * r;
+      if (c < ncell) {
+        float drho, mx, my, mz;
+        moments_dev(sv[r], drho, mx, my, mz);
+        const float rho = 1.0f + drho;
+        const float ir = rho > 0.0f ? 1.0f / rho : 0.0f;  // bare u; 0 where rho <= 0
+        const double w = (phs[slot][2][cko[r]] * phs[slot][1][cjo[r]]) * phs[slot][0][cio[r]];
+        a0 += w * (double)(mx * ir);
+        a1 += w * (double)(my * ir);
+        a2 += w * (double)(mz * ir);
+      }
+    }
+  }
+#pragma unroll
+  for (int o = MK_LANES / 2; o > 0; o >>= 1) {  // fixed butterfly: every lane gets the total
+    a0 += __shfl_xor_sync(hmask, a0, o, MK_LANES);
+    a1 += __shfl_xor_sync(hmask, a1, o, MK_LANES);
+    a2 += __shfl_xor_sync(hmask, a2, o, MK_LANES);
+  }
+  // body velocity, direct forcing, world force (identical on every lane)
+  const double uf[3] = {a0 * sc.v2p, a1 * sc.v2p, a2 * sc.v2p};
+  double vw[3], vf[3], nf[3], fl[3], fw[3], ff[3];
+#pragma unroll
+  for (int k = 0; k < 3; ++k) vw[k] = vel[k] - st.pd[k];
+  mat_t_vec(st.R, vw, vf);
+  double du[3] = {vf[0] - (st.wf[1] * xf[2] - st.wf[2] * xf[1]) - uf[0],
+                  vf[1] - (st.wf[2] * xf[0] - st.wf[0] * xf[2]) - uf[1],
+                  vf[2] - (st.wf[0] * xf[1] - st.wf[1] * xf[0]) - uf[2]};
+  mat_t_vec(st.R, nrm, nf);
+  if (sc.wall == 0) {
+    const double s = du[0] * nf[0] + du[1] * nf[1] + du[2] * nf[2];
+    du[0] = s * nf[0];
+    du[1] = s * nf[1];
+    du[2] = s * nf[2];
+  }
+  const double kf = sc.rho_phys * area * sc.dx / sc.dt;
+  fl[0] = kf * du[0];
+  fl[1] = kf * du[1];
+  fl[2] = kf * du[2];
+  mat_vec(st.R, fl, fw);
+  mat_t_vec(st.R, fw, ff);
+  const double fx = ff[0] * sc.f2l, fy = ff[1] * sc.f2l, fz = ff[2] * sc.f2l;
+  if (hl == 0) {
+    fworld[3 * t] = fw[0];
+    fworld[3 * t + 1] = fw[1];
+    fworld[3 * t + 2] = fw[2];
+    if (fworld_h) {
+      fworld_h[3 * t] = fw[0];
+      fworld_h[3 * t + 1] = fw[1];
+      fworld_h[3 * t + 2] = fw[2];
+      valid_h[t] = 1;
+    }
+    MarkerStencil r;  // kept for diagnostics (fsg_get_force / fsg_get_stencils)
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+#pragma unroll
+      for (int q = 0; q < 5; ++q) r.ph[a][q] = phs[slot][a][q];
+      r.lo[a] = lo[a];
+      r.hi[a] = hi[a];
+    }
+    r.fl[0] = fx;
+    r.fl[1] = fy;
+    r.fl[2] = fz;
+    r.valid = 1;
+    r._pad = 0;
+    rec_out[t] = r;
+  }
+  // flag the (<= 2x2x2) tiles the stencil touches
+  if (hl < 8) {
+    const int tx = ((hl & 1) ? hi[0] : lo[0]) >> 2;
+    const int ty = ((hl & 2) ? hi[1] : lo[1]) >> 2;
+    const int tz = ((hl & 4) ? hi[2] - g.z0 : lo[2] - g.z0) >> 2;
+    fb.flag_cur[tx + fb.tnx * (ty + fb.tny * tz)] = 1;
+  }
+  // spread: this lane's own cells, fixed-point integer atomics
+  for (int c = hl; c < ncell; c += MK_LANES) {
+    const int ko = (int)(((float)c + 0.5f) * r01);
+    const int rem = c - ko * cnt[0] * cnt[1];
+    const int jo = (int)(((float)rem + 0.5f) * r0);
+    const int io = rem - jo * cnt[0];
+    const double w = (phs[slot][2][ko] * phs[slot][1][jo]) * phs[slot][0][io];
+    const long long cell = (long long)(lo[0] + io) +
+                           (long long)g.nx * ((long long)(lo[1] + jo) + (long long)g.ny * (lo[2] + ko - g.z0));
+    unsigned long long* F = fb.F + 3 * cell;
+    atomicAdd(F, to_fix(w * fx));
+    atomicAdd(F + 1, to_fix(w * fy));
+    atomicAdd(F + 2, to_fix(w * fz));
+  }
+}

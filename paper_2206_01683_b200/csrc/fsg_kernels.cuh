@@ -228,7 +228,10 @@ __device__ __forceinline__ void report_min(StepScratch* out, double v) {
   if ((threadIdx.x & 31) == 0 && !isnan(v)) {
     const unsigned long long nk = ~ordered_key(v);
     const unsigned long long cur = *(volatile unsigned long long*)&out->neg_min_key;
-    if (nk > cur) atomicMax(&out->neg_min_key, nk);
+    if (nk > cur) {
+      atomicMax(&out->neg_min_key, nk);
+      __threadfence();
+    }
   }
 }
 
@@ -246,10 +249,12 @@ __device__ __forceinline__ float collide_cell32(float (&s)[Q], int x, int y, int
   float drho, mx, my, mz;
   moments_dev(s, drho, mx, my, mz);
   const float rho = 1.0f + drho;
-  if constexpr (FMODE == 2) {
-    Fx = in_band ? (float)band.F[3 * lc] : 0.0f;
-    Fy = in_band ? (float)band.F[3 * lc + 1] : 0.0f;
-    Fz = in_band ? (float)band.F[3 * lc + 2] : 0.0f;
+  if constexpr (FMODE == 2 || FMODE == 3) {  // 3: IB force already in Fx..Fz (fixed-point band)
+    if constexpr (FMODE == 2) {
+      Fx = in_band ? (float)band.F[3 * lc] : 0.0f;
+      Fy = in_band ? (float)band.F[3 * lc + 1] : 0.0f;
+      Fz = in_band ? (float)band.F[3 * lc + 2] : 0.0f;
+    }
     if constexpr (VF) {
       float bx = 0.f, by = 0.f, bz = 0.f;
       if (rho > 0.0f) {
@@ -264,7 +269,10 @@ __device__ __forceinline__ float collide_cell32(float (&s)[Q], int x, int y, int
       Fy += vy;
       Fz += vz;
     }
-    if (!(rho > 0.0f)) atomicAdd(&out->nonpos, 1);
+    if (!(rho > 0.0f)) {
+      atomicAdd(&out->nonpos, 1);
+      __threadfence();
+    }
   }
   const float om1 = sc.om1_f;
   const float inv_rho = 1.0f / rho;
@@ -272,7 +280,10 @@ __device__ __forceinline__ float collide_cell32(float (&s)[Q], int x, int y, int
   const float uy = (my + 0.5f * Fy) * inv_rho;
   const float uz = (mz + 0.5f * Fz) * inv_rho;
   const float u2 = ux * ux + uy * uy + uz * uz;
-  if (!isfinite(rho + u2)) out->nonfinite = 1;
+  if (!isfinite(rho + u2)) {
+    out->nonfinite = 1;
+    __threadfence();
+  }
   const float uF = ux * Fx + uy * Fy + uz * Fz;
   const float h15u2 = 1.5f * u2;
   // weight classes: 0 rest, 1 axes, 2 diagonals
@@ -624,6 +635,9 @@ __global__ void k_recenter(Grid g, const Store* __restrict__ A, Store* __restric
 
 // ====================================================== IB kernels =======
 #include "fsg_ib.cuh"
+#if FSG_PREC == 32
+#include "fsg_ib_fix.cuh"
+#endif
 
 // ======================================================= halo (slabs) ====
 // Populations crossing a z face (lattice.hpp:25-26): ez=+1 {5,11,14,15,18},
@@ -766,9 +780,68 @@ static void L_halo_unpack(const Grid& g, void* B, const void* lo, const void* hi
   k_halo_unpack<<<lin_blocks(5 * g.plane, 256), 256, 0, s>>>(g, (Store*)B, (const Store*)lo, (const Store*)hi);
 }
 
+#if FSG_PREC == 32
+static void L_markers_fix(const Grid& g, const void* A, int pulled, Markers mk,
+                          const SessionConsts* sc, const StepConsts& st, MarkerStencil* rec,
+                          double* fworld, double* fworld_h, int* valid_h, FixBand fb,
+                          StepScratch* out, cudaStream_t s) {
+  if (mk.m == 0) return;
+  const unsigned nb = (unsigned)((mk.m + MK_PER_BLOCK - 1) / MK_PER_BLOCK);
+  if (pulled)
+    k_markers_fix<true><<<nb, 128, 0, s>>>(g, (const float*)A, mk, sc, st, rec, fworld, fworld_h,
+                                           valid_h, fb, out);
+  else
+    k_markers_fix<false><<<nb, 128, 0, s>>>(g, (const float*)A, mk, sc, st, rec, fworld, fworld_h,
+                                            valid_h, fb, out);
+}
+static void L_collide_fix(const Grid& g, const void* A, int pulled, void* B, FixBand fb,
+                          const SessionConsts* sc, const StepConsts& st, int frame_on, int has_ib,
+                          StepScratch* scr, StepScratch* scr_next, StepScratch* publish,
+                          unsigned* tickets, unsigned* tickets_next, cudaStream_t s) {
+  DirPtrs dp;
+  for (int i = 0; i < Q; ++i) {
+    dp.a[i] = (const float*)A + (pulled ? g.pull[i] : g.own[i]);
+    dp.b[i] = (float*)B + g.own[i];
+  }
+  const dim3 b = cell_block(g), g3 = cell_grid(g, b);
+  const long long ntile = (long long)g3.x * g3.y * g3.z;
+  static int resident = 0;  // blocks of k_collide_fix resident per SM (same for all variants)
+  static int nsm = 0;
+  if (!resident) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&resident, k_collide_fix<true, true>, 128, 0);
+    if (resident < 1) resident = 1;
+  }
+  const long long grid = std::min<long long>(ntile, (long long)nsm * resident);
+  const dim3 gr((unsigned)grid);
+  // z chunk: ~8 work items per resident block for balance
+  const long long ncol = (long long)g3.x * g3.y;
+  const long long nzc_want = (8 * grid + ncol - 1) / ncol;
+  const int zc = (int)std::max<long long>(1, g.nz / std::max<long long>(1, nzc_want));
+#define FSG_LF(P, V) \
+  k_collide_fix<P, V><<<gr, b, 0, s>>>(g, dp, (const float*)A, fb, has_ib, sc, st, scr, scr_next, \
+                                       publish, tickets, tickets_next, zc)
+  if (pulled) {
+    if (frame_on) FSG_LF(true, true);
+    else FSG_LF(true, false);
+  } else {
+    if (frame_on) FSG_LF(false, true);
+    else FSG_LF(false, false);
+  }
+#undef FSG_LF
+}
+#endif
+
 static const Launchers kLaunchers = {
     L_fill_rest,    L_set_f,          L_init_eq,      L_get_f,         L_macroscopic,
     L_collide,      L_session_force,  L_recenter,     L_markers,       L_spread,
+#if FSG_PREC == 32
+    L_markers_fix,  L_collide_fix,
+#else
+    nullptr,        nullptr,
+#endif
     L_halo_pack,    L_halo_unpack,    (int)sizeof(Store)};
 
 }  // namespace p32 / p64

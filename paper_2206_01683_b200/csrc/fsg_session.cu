@@ -143,6 +143,14 @@ struct fsg_session {
   double* d_red = nullptr;  // reduction scratch
   std::vector<GraphEntry> graphs;
   fsg_status last{};
+  // throughput (fp32) IB: fixed-point tile band
+  fsg::FixBand fix{};
+  unsigned char* flags[2] = {nullptr, nullptr};
+  unsigned* tickets[2] = {nullptr, nullptr};  // K4 hierarchical last-block counters
+  bool fix_active = false;  // markers were spread at least once
+  bool scr_dirty[2] = {false, false};  // d_scr[k] not known to be zero
+  StepConsts last_st{};     // frame constants of the last step (diagnostics)
+  StepScratch* d_diag = nullptr;
 
   void* A() const { return buf[par]; }
   void* B() const { return buf[par ^ 1]; }
@@ -460,6 +468,22 @@ int fsg_create(const fsg_config* cfg_in, fsg_session** out) {
   CUF(cudaMalloc(&s->d_fworld, sizeof(double) * 3 * (size_t)s->cap));
   s->band.cap = std::min<long long>(g.n, 16ll << 20);
   CUF(cudaMalloc(&s->band.F, sizeof(double) * 3 * (size_t)s->band.cap));
+  CUF(cudaMalloc(&s->d_diag, sizeof(StepScratch)));
+  if (s->L->markers_fix) {
+    fsg::FixBand& fb = s->fix;
+    fb.tnx = (g.nx + 3) / 4;
+    fb.tny = (g.ny + 3) / 4;
+    fb.tnz = (g.nz + 3) / 4;
+    const size_t ntile = (size_t)fb.tnx * fb.tny * fb.tnz;
+    CUF(cudaMalloc(&fb.F, sizeof(unsigned long long) * 3 * (size_t)g.n));
+    CUF(cudaMemsetAsync(fb.F, 0, sizeof(unsigned long long) * 3 * (size_t)g.n, s->stream));
+    for (int k = 0; k < 2; ++k) {
+      CUF(cudaMalloc(&s->flags[k], ntile));
+      CUF(cudaMemsetAsync(s->flags[k], 0, ntile, s->stream));
+      CUF(cudaMalloc(&s->tickets[k], sizeof(unsigned) * (fsg::TICKET_GROUPS + 1)));
+      CUF(cudaMemsetAsync(s->tickets[k], 0, sizeof(unsigned) * (fsg::TICKET_GROUPS + 1), s->stream));
+    }
+  }
   s->L->fill_rest(g, s->A(), s->stream);
   if (cudaGetLastError() != cudaSuccess) return fail(set_err(FSG_ECUDA, "fill_rest launch failed"));
   if (cudaStreamSynchronize(s->stream) != cudaSuccess)
@@ -494,6 +518,12 @@ int fsg_destroy(fsg_session* s) {
   cudaFree(s->d_boxes);
   cudaFree(s->d_fworld);
   cudaFree(s->band.F);
+  cudaFree(s->fix.F);
+  cudaFree(s->flags[0]);
+  cudaFree(s->flags[1]);
+  cudaFree(s->tickets[0]);
+  cudaFree(s->tickets[1]);
+  cudaFree(s->d_diag);
   cudaFree(s->d_tmp);
   cudaFree(s->d_red);
   if (s->stream) cudaStreamDestroy(s->stream);
@@ -604,6 +634,7 @@ int fsg_collide_and_stream(fsg_session* s, fsg_status* st) {
   s->pulled = 1;
   state_changed(s);
   decode_status(*s->h_scr[p], &s->last, false);
+  s->scr_dirty[p] = true;
   if (st) *st = s->last;
   return FSG_OK;
 }
@@ -624,6 +655,7 @@ int fsg_macroscopic(fsg_session* s, double* rho, double* u, int* nonpos) {
   CU(cudaMemcpyAsync(&sc, s->d_scr[p], sizeof(StepScratch), cudaMemcpyDeviceToHost, s->stream));
   CU(cudaStreamSynchronize(s->stream));
   if (nonpos) *nonpos = sc.nonpos;
+  s->scr_dirty[p] = true;
   s->last_valid = false;  // the step scratch of parity p was reused
   return FSG_OK;
 }
@@ -747,8 +779,32 @@ int fsg_step_async(fsg_session* s) {
   frame_consts(s->frame, *s->h_st[p]);
   const bool frame_on = s->cfg.frame_mode != FSG_FRAME_NONE;
   const bool copy_mk = s->mk_host && s->mk_dirty;
-  int rc = launch_step(s, p, copy_mk, frame_on);
-  if (rc) return rc;
+  if (s->L->markers_fix) {
+    // throughput path: two kernels, frame constants by value, status
+    // published by K4's last block into mapped pinned memory
+    const StepConsts st = *s->h_st[p];
+    s->last_st = st;
+    if (s->scr_dirty[p]) CU(cudaMemsetAsync(s->d_scr[p], 0, sizeof(StepScratch), s->stream));
+    fsg::FixBand fb = s->fix;
+    fb.flag_cur = s->flags[p];
+    fb.flag_prev = s->flags[p ^ 1];
+    if (s->m) {
+      s->L->markers_fix(s->g, s->buf[p], s->pulled, s->mk, s->d_sc, st, s->d_stencil, s->d_fworld,
+                        s->h_fw[p], s->h_valid[p], fb, s->d_scr[p], s->stream);
+      s->fix_active = true;
+    }
+    if (s->scr_dirty[p])
+      CU(cudaMemsetAsync(s->tickets[p], 0, sizeof(unsigned) * (fsg::TICKET_GROUPS + 1), s->stream));
+    s->L->collide_fix(s->g, s->buf[p], s->pulled, s->buf[p ^ 1], fb, s->d_sc, st, frame_on ? 1 : 0,
+                      s->fix_active ? 1 : 0, s->d_scr[p], s->d_scr[p ^ 1], s->h_scr[p],
+                      s->tickets[p], s->tickets[p ^ 1], s->stream);
+    CU_LAUNCH();
+    s->scr_dirty[p] = true;       // holds this step's status
+    s->scr_dirty[p ^ 1] = false;  // reset by K4 for the next step
+  } else {
+    int rc = launch_step(s, p, copy_mk, frame_on);
+    if (rc) return rc;
+  }
   CU(cudaEventRecord(s->ev[p], s->stream));
   if (s->mk_host && s->mk_slot >= 0) CU(cudaEventRecord(s->ev_mk[s->mk_slot], s->stream));
   s->last_par = p;
@@ -838,8 +894,8 @@ int fsg_get_stencils(fsg_session* s, int* lo_hi) {
   CU(cudaStreamSynchronize(s->stream));
   for (size_t i = 0; i < m; ++i)
     for (int a = 0; a < 3; ++a) {
-      lo_hi[6 * i + a] = bx[i].valid ? st[i].lo[a] : 0;
-      lo_hi[6 * i + 3 + a] = bx[i].valid ? st[i].hi[a] : -1;
+      lo_hi[6 * i + a] = st[i].valid ? st[i].lo[a] : 0;
+      lo_hi[6 * i + 3 + a] = st[i].valid ? st[i].hi[a] : -1;
     }
   return FSG_OK;
 }
@@ -851,7 +907,7 @@ int fsg_get_macro(fsg_session* s, double* rho, double* u) {
   int rc = ensure_tmp(s, sizeof(double) * 4 * n);
   if (rc) return rc;
   CU(cudaStreamSynchronize(s->stream));
-  StepScratch* junk = s->d_scr[s->last_par ^ 1];  // not read back by anyone
+  StepScratch* junk = s->d_diag;  // nonpos count not needed here
   s->L->macroscopic(s->g, s->buf[s->last_par], s->prev_pulled, nullptr, s->d_tmp, s->d_tmp + n,
                     junk, s->stream);
   CU_LAUNCH();
@@ -867,7 +923,43 @@ int fsg_get_force(fsg_session* s, double* F) {
   const size_t n = (size_t)s->g.n;
   int rc = ensure_tmp(s, sizeof(double) * 3 * n);
   if (rc) return rc;
-  s->L->session_force(s->g, s->buf[s->last_par], s->prev_pulled, &s->band, s->d_scr[s->last_par],
+  StepScratch* bscr = s->d_scr[s->last_par];
+  if (s->L->markers_fix) {
+    // Throughput path: K4 consumed (and re-zeroed) the fixed-point band, so
+    // this diagnostic rebuilds the IB field from the stored stencil records
+    // with the ordered spread kernel (agrees with the fixed-point sum to
+    // ~1e-12 relative) and restores the step's frame constants.
+    const size_t m = (size_t)s->m;
+    std::vector<MarkerStencil> st(m);
+    std::vector<MarkerBox> bx(m);
+    if (m)
+      CU(cudaMemcpy(st.data(), s->d_stencil, sizeof(MarkerStencil) * m, cudaMemcpyDeviceToHost));
+    StepScratch sc{};
+    int lo[3] = {1 << 29, 1 << 29, 1 << 29}, hi[3] = {-1, -1, -1};
+    for (size_t i = 0; i < m; ++i) {
+      bx[i] = MarkerBox{};
+      bx[i].valid = (short)st[i].valid;
+      for (int a = 0; a < 3; ++a) {
+        const int off = a == 2 ? s->g.z0 : 0;
+        bx[i].lo[a] = (short)(st[i].lo[a] - off);
+        bx[i].hi[a] = (short)(st[i].hi[a] - off);
+        if (st[i].valid) {
+          lo[a] = std::min(lo[a], st[i].lo[a] - off);
+          hi[a] = std::max(hi[a], st[i].hi[a] - off);
+        }
+      }
+    }
+    for (int a = 0; a < 3; ++a) {
+      sc.bbox_lo_enc[a] = hi[a] >= 0 ? fsg::LO_BIAS - lo[a] : 0;
+      sc.bbox_hi_enc[a] = hi[a] >= 0 ? hi[a] + 1 : 0;
+    }
+    if (m) CU(cudaMemcpy(s->d_boxes, bx.data(), sizeof(MarkerBox) * m, cudaMemcpyHostToDevice));
+    CU(cudaMemcpy(s->d_diag, &sc, sizeof sc, cudaMemcpyHostToDevice));
+    CU(cudaMemcpy(s->d_st, &s->last_st, sizeof(StepConsts), cudaMemcpyHostToDevice));
+    s->L->spread(s->g, s->m, s->d_stencil, s->d_boxes, s->band, s->d_diag, s->stream);
+    bscr = s->d_diag;
+  }
+  s->L->session_force(s->g, s->buf[s->last_par], s->prev_pulled, &s->band, bscr,
                       s->d_sc, s->d_st, s->last_frame_on ? 1 : 0, s->d_tmp, s->stream);
   CU_LAUNCH();
   CU(cudaMemcpyAsync(F, s->d_tmp, sizeof(double) * 3 * n, cudaMemcpyDeviceToHost, s->stream));
