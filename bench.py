@@ -1,0 +1,379 @@
+#!/usr/bin/env python
+"""bench.py -- throughput of the coupled IB-LBM step on B200.
+
+Metric (BASELINE.json): "MLUPS (whole box) and % of HBM roofline at 1/2/4/8
+B200 vs CPU ref".  One "step" is one coupled fluid step of the hot path
+(markers -> interpolation/forcing/spread -> virtual force -> collide/stream
+/open BC) over the synthetic scene of the workload; MLUPS = cells x steps /
+time.
+
+  value     : device time (CUDA events on the session stream, per step, L2
+              flushed between steps), marker state and frames already
+              resident in HBM; whole-job MLUPS (sum over ranks, max time).
+  e2e       : the same metric through the public API with HOST buffers:
+              every step uploads marker state + frame (pinned, zero-copy),
+              runs fsg_step (synchronous status readback) and reads the
+              marker forces back (wall clock per step, L2 flushed between).
+  roofline  : the collide-stream kernel (dominant), 152 B per cell update,
+              timed with CUDA events on its launching stream.
+  cpu_baseline : the reference's own CPU code (oracle/_ref, the reference
+              headers compiled unmodified) on a bounded sample of the same
+              workload on this box's cores.
+
+Workloads (BASELINE.json configs): c1 64^3 sphere, c2 128x64x64 koi in an
+accelerating frame (default, configs[1]), c3 256x128x128 two-koi school,
+c5 96x48x48 env.  Under torchrun every rank runs an independent replica
+(weak scaling, no data-path collective).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                  [--workload c2] [--no-cpu-baseline]
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "MLUPS (whole box) and % of HBM roofline at 1/2/4/8 B200 vs CPU ref"
+BYTES_PER_CELL = 152  # 19 fp32 populations read + 19 written
+
+
+def parse_args():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=1000)
+    ap.add_argument("--warmup", type=int, default=20)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="c2", choices=["c1", "c2", "c3", "c5"])
+    ap.add_argument("--e2e-steps", type=int, default=100)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    return ap.parse_args()
+
+
+def dist_env():
+    return (int(os.environ.get("RANK", "0")), int(os.environ.get("LOCAL_RANK", "0")),
+            int(os.environ.get("WORLD_SIZE", "1")))
+
+
+def measured_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+# ----------------------------------------------------------------- clocks --
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.th = threading.Thread(target=self._read, daemon=True)
+            self.th.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, smax, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            p = [x.strip() for x in ln.split(",")]
+            if len(p) < 9:
+                continue
+            try:
+                sm.append(float(p[1]))
+                smax = float(p[2])
+            except ValueError:
+                continue
+            for nm, v in zip(names, p[5:9]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"]}
+        sm.sort()
+        return {"sm_mhz": sm[len(sm) // 2], "sm_max_mhz": smax, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ------------------------------------------------------------ CPU (ref) ----
+def cpu_reference_mlups(scene, seconds: float, max_steps: int = 400):
+    """The reference's own CPU code (oracle/_ref: the reference headers compiled
+    unmodified, OpenMP over this box's cores) driving the fluid half of
+    CoupledSession::step on the same synthetic scene.  Falls back to the C
+    restatement (oracle/liboracle.so) when _ref was not built."""
+    import numpy as np
+    from oracle import bind as B
+    kind = "reference" if B.have_ref() else "port"
+    fm = {"none": 0, "translation": 1, "translation_yaw": 2, "full": 3}[scene.frame_mode]
+    m = scene.m
+    nb = len(scene.bodies)
+    off = scene.offsets
+    if kind == "reference":
+        R = B.ref()
+        h = R.ref_session_create(*scene.dims, scene.dx, scene.dt, scene.rho, scene.nu, 0, 0, 0, fm)
+    else:
+        O = B.oracle()
+        h = O.orc_session_create(B.iptr(B.dims_arr(scene.dims)), scene.dx, scene.dt, scene.rho,
+                                 scene.nu, 0, 0, 0, fm)
+    fw = np.zeros(3 * max(m, 1))
+    valid = np.zeros(max(m, 1), np.int32)
+    stats = np.zeros(7 * max(nb, 1))
+    fin = np.zeros(1, np.int32)
+    mf = np.zeros(1)
+    mk = [scene.markers(k) for k in range(8)] if m else None
+
+    def one(k):
+        f = scene.frame(k)
+        if kind == "reference":
+            R.ref_set_frame(h, *(B.dptr(np.ascontiguousarray(v, dtype=np.float64)) for v in
+                                 (f.p, f.pd, f.pdd, f.q, f.omega, f.alpha)))
+        else:
+            O.orc_session_set_frame(h, B.FrameState.make(p=f.p, pd=f.pd, pdd=f.pdd, q=f.q,
+                                                         omega=f.omega, alpha=f.alpha))
+        args = (h, nb, B.i64ptr(off))
+        if m:
+            pts, vel, nrm, area = mk[k % 8]
+            marr = (B.dptr(pts.reshape(-1)), B.dptr(vel.reshape(-1)), B.dptr(nrm.reshape(-1)),
+                    B.dptr(area))
+        else:
+            marr = (None, None, None, None)
+        fn = R.ref_session_step if kind == "reference" else O.orc_session_step
+        fn(*args, *marr, B.dptr(fw), B.iptr(valid), B.dptr(stats), B.iptr(fin), B.dptr(mf))
+
+    one(0)  # warm-up (page-in, OpenMP pool)
+    t0 = time.perf_counter()
+    n = 0
+    while n < max_steps and (time.perf_counter() - t0) < seconds:
+        one(n + 1)
+        n += 1
+    dt = time.perf_counter() - t0
+    if kind == "reference":
+        R.ref_session_destroy(h)
+    else:
+        O.orc_session_destroy(h)
+    cores = int(os.environ.get("OMP_NUM_THREADS", os.cpu_count() or 1))
+    return {"value": scene.n_cells * n / dt / 1e6, "unit": "MLUPS", "cores": cores, "kind": kind,
+            "sample": f"{n} coupled steps of {scene.name} ({dt:.1f} s wall, fp64, OpenMP)"}
+
+
+# ------------------------------------------------------------------ ours ---
+def run_ours(args, scene, rank, local, world):
+    import numpy as np
+    import torch
+    from paper_2206_01683_b200 import CoupledSession, SessionConfig
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    cfg = SessionConfig(dims=scene.dims, dx=scene.dx, dt=scene.dt, rho=scene.rho, nu=scene.nu,
+                        frame_mode=scene.frame_mode, precision="fp32", device=local,
+                        max_markers=max(scene.m, 1))
+    s = CoupledSession(cfg)
+    stream = torch.cuda.ExternalStream(s.stream, device=dev)
+    W, K = args.warmup, args.steps
+    nsteps = W + K
+    m = scene.m
+    # marker state of every step, resident in HBM before timing
+    mk_dev = None
+    if m:
+        P = np.zeros((nsteps, 4, 3 * m))
+        for k in range(nsteps):
+            pts, vel, nrm, area = scene.markers(k)
+            P[k, 0], P[k, 1], P[k, 2] = pts.reshape(-1), vel.reshape(-1), nrm.reshape(-1)
+            P[k, 3, :m] = area
+        mk_dev = torch.tensor(P, dtype=torch.float64, device=dev)
+    frames = [scene.frame(k) for k in range(nsteps)]
+    off = scene.offsets
+    # L2 flush: write then read buffers larger than L2 (126 MB), outside timing
+    l2 = torch.cuda.get_device_properties(dev).L2_cache_size
+    nflush = max(2 * l2, 256 << 20) // 4
+    fw_buf = torch.empty(nflush, dtype=torch.float32, device=dev)
+    fr_buf = torch.ones(nflush, dtype=torch.float32, device=dev)
+    sink = torch.zeros(1, dtype=torch.float32, device=dev)
+
+    def flush():
+        fw_buf.fill_(1.0)
+        torch.sum(fr_buf, dim=0, out=sink[0])
+
+    def set_step(k):
+        s.set_frame(frames[k])
+        if m:
+            r = mk_dev[k]
+            s.set_markers_device(off, r[0].data_ptr(), r[1].data_ptr(), r[2].data_ptr(),
+                                 r[3].data_ptr())
+
+    with torch.cuda.stream(stream):
+        for k in range(W):
+            set_step(k)
+            s.step_async()
+        st = s.last_status()
+        torch.cuda.synchronize(dev)
+        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+              for _ in range(K)]
+        s.profile(True)
+        if world > 1:
+            import torch.distributed as dist
+            dist.barrier()
+        torch.cuda.synchronize(dev)
+        with ClockSampler(local) as clk:
+            time.sleep(0.4)  # let nvidia-smi start sampling before the timed region
+            for k in range(K):
+                flush()
+                set_step(W + k)
+                ev[k][0].record(stream)
+                s.step_async()
+                ev[k][1].record(stream)
+            torch.cuda.synchronize(dev)
+            time.sleep(0.15)
+        st = s.last_status()
+        mk_ms, k4_ms, nprof = s.profile_read()
+        s.profile(False)
+        step_ms = sum(a.elapsed_time(b) for a, b in ev) / K
+    t_total = step_ms * K / 1e3
+    if world > 1:
+        import torch.distributed as dist
+        t = torch.tensor([t_total], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        t_total = float(t.item())
+    value = scene.n_cells * K * world / t_total / 1e6
+
+    # ---- end to end through the public API with host buffers
+    E = min(args.e2e_steps, K)
+    mk_host = [scene.markers(k) for k in range(8)] if m else None
+    e2e_t = 0.0
+    with torch.cuda.stream(stream):
+        s.reset_to_rest()
+        for k in range(3):
+            s.set_frame(frames[k])
+            if m:
+                s.set_markers(off, *mk_host[k % 8])
+            s.step()
+            if m:
+                s.marker_forces()
+        for k in range(E):
+            flush()
+            torch.cuda.synchronize(dev)
+            t0 = time.perf_counter()
+            s.set_frame(frames[k % nsteps])
+            if m:
+                s.set_markers(off, *mk_host[k % 8])
+            st_e = s.step()
+            if m:
+                s.marker_forces()
+            e2e_t += time.perf_counter() - t0
+    e2e_val = scene.n_cells * E / e2e_t / 1e6
+    if world > 1:
+        import torch.distributed as dist
+        t = torch.tensor([e2e_t], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_val = scene.n_cells * E * world / float(t.item()) / 1e6
+    h2d = 80 * m + 232          # marker state (pts, vel, nrm 3x8 B, area 8 B) + frame consts
+    d2h = 28 * m + 64           # marker forces (3x8 B) + validity (4 B) + step status
+    s.close()
+
+    peak, peak_src = measured_peaks()
+    k4_avg_s = (k4_ms / max(nprof, 1)) / 1e3
+    achieved = BYTES_PER_CELL * scene.n_cells / k4_avg_s / 1e9
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "k4_traffic.json")) as f:
+            tr = json.load(f)
+        if tr.get("workload") == args.workload:
+            traffic = tr.get("dram_bytes_per_launch")
+    except Exception:
+        pass
+    out = {
+        "metric": METRIC, "value": round(value, 1), "unit": "MLUPS", "n_gpus": world,
+        "steps": K, "warmup": W, "ms_per_step": round(step_ms, 4), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f32 (fp32 storage of f - w_i)",
+        "data": "synthetic (prescribed-kinematics bodies, fluid at rest; SURVEY.md §8(d))",
+        "config": {"workload": scene.name, "dims": list(scene.dims), "markers": m,
+                   "frame": scene.frame_mode, "l2": "flushed between timed steps",
+                   "parallelism": f"replicas x{world}" if world > 1 else "single GPU"},
+        "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                     "frac": round(achieved / peak, 4), "traffic": traffic,
+                     "kernel": "k_collide_fix (collide+stream+open BC+VF+IB band)",
+                     "peak_source": peak_src,
+                     "per_step_ms": {"markers": round(mk_ms / max(nprof, 1), 4),
+                                     "collide": round(k4_avg_s * 1e3, 4)}},
+        "e2e": {"value": round(e2e_val, 1), "unit": "MLUPS", "h2d_bytes_per_step": h2d,
+                "d2h_bytes_per_step": d2h, "steps": E},
+        "gpu_launches": K * (2 if m else 1),
+        "status": {"stable": bool(st.stable()), "min_f": st.min_f},
+        "clocks": clk.summary(),
+    }
+    return out
+
+
+def main():
+    args = parse_args()
+    rank, local, world = dist_env()
+    from paper_2206_01683_b200.scenes import make_scene
+    scene = make_scene(args.workload)
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        cb = cpu_reference_mlups(scene, seconds=max(5.0, args.cpu_seconds))
+        out = {"metric": METRIC, "value": round(cb["value"], 3), "unit": "MLUPS", "n_gpus": world,
+               "steps": args.steps, "warmup": args.warmup, "higher_is_better": True,
+               "scaling": "weak", "vs_baseline": None, "dtype": "f64", "impl": "reference",
+               "data": "synthetic", "config": {"workload": scene.name, "dims": list(scene.dims),
+                                               "markers": scene.m},
+               "cpu_baseline": cb,
+               "e2e": {"value": round(cb["value"], 3), "unit": "MLUPS", "h2d_bytes_per_step": 0,
+                       "d2h_bytes_per_step": 0}}
+        print(json.dumps(out))
+        return
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl")
+    out = run_ours(args, scene, rank, local, world)
+    if rank == 0:
+        if not args.no_cpu_baseline:
+            out["cpu_baseline"] = cpu_reference_mlups(scene, seconds=args.cpu_seconds)
+        print(json.dumps(out))
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

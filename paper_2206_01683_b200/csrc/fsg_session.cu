@@ -151,6 +151,11 @@ struct fsg_session {
   bool scr_dirty[2] = {false, false};  // d_scr[k] not known to be zero
   StepConsts last_st{};     // frame constants of the last step (diagnostics)
   StepScratch* d_diag = nullptr;
+  // measurement: event triplets (before markers, before K4, after K4) per step
+  static constexpr int PROF_CAP = 4096;
+  bool prof = false;
+  std::vector<cudaEvent_t> prof_ev;
+  int prof_n = 0;
 
   void* A() const { return buf[par]; }
   void* B() const { return buf[par ^ 1]; }
@@ -499,6 +504,7 @@ int fsg_destroy(fsg_session* s) {
   cudaSetDevice(s->cfg.device);
   if (s->stream) cudaStreamSynchronize(s->stream);
   clear_graphs(s);
+  for (auto& e : s->prof_ev) cudaEventDestroy(e);
   for (int k = 0; k < 2; ++k) {
     cudaFree(s->buf[k]);
     cudaFree(s->d_scr[k]);
@@ -788,17 +794,25 @@ int fsg_step_async(fsg_session* s) {
     fsg::FixBand fb = s->fix;
     fb.flag_cur = s->flags[p];
     fb.flag_prev = s->flags[p ^ 1];
+    const bool prof = s->prof && s->prof_n < fsg_session::PROF_CAP;
+    cudaEvent_t* pe = prof ? &s->prof_ev[3 * (size_t)s->prof_n] : nullptr;
+    if (prof) CU(cudaEventRecord(pe[0], s->stream));
     if (s->m) {
       s->L->markers_fix(s->g, s->buf[p], s->pulled, s->mk, s->d_sc, st, s->d_stencil, s->d_fworld,
                         s->h_fw[p], s->h_valid[p], fb, s->d_scr[p], s->stream);
       s->fix_active = true;
     }
+    if (prof) CU(cudaEventRecord(pe[1], s->stream));
     if (s->scr_dirty[p])
       CU(cudaMemsetAsync(s->tickets[p], 0, sizeof(unsigned) * (fsg::TICKET_GROUPS + 1), s->stream));
     s->L->collide_fix(s->g, s->buf[p], s->pulled, s->buf[p ^ 1], fb, s->d_sc, st, frame_on ? 1 : 0,
                       s->fix_active ? 1 : 0, s->d_scr[p], s->d_scr[p ^ 1], s->h_scr[p],
                       s->tickets[p], s->tickets[p ^ 1], s->stream);
     CU_LAUNCH();
+    if (prof) {
+      CU(cudaEventRecord(pe[2], s->stream));
+      ++s->prof_n;
+    }
     s->scr_dirty[p] = true;       // holds this step's status
     s->scr_dirty[p ^ 1] = false;  // reset by K4 for the next step
   } else {
@@ -964,6 +978,35 @@ int fsg_get_force(fsg_session* s, double* F) {
   CU_LAUNCH();
   CU(cudaMemcpyAsync(F, s->d_tmp, sizeof(double) * 3 * n, cudaMemcpyDeviceToHost, s->stream));
   CU(cudaStreamSynchronize(s->stream));
+  return FSG_OK;
+}
+
+// --------------------------------------------------------- measurement --
+int fsg_profile_enable(fsg_session* s, int enable) {
+  CU(cudaSetDevice(s->cfg.device));
+  if (enable && s->prof_ev.empty()) {
+    s->prof_ev.resize(3 * (size_t)fsg_session::PROF_CAP);
+    for (auto& e : s->prof_ev) CU(cudaEventCreate(&e));
+  }
+  s->prof = enable != 0;
+  s->prof_n = 0;
+  return FSG_OK;
+}
+
+int fsg_profile_read(fsg_session* s, double* markers_ms, double* collide_ms, int* steps) {
+  CU(cudaStreamSynchronize(s->stream));
+  double a = 0.0, b = 0.0;
+  for (int k = 0; k < s->prof_n; ++k) {
+    float t0 = 0.f, t1 = 0.f;
+    CU(cudaEventElapsedTime(&t0, s->prof_ev[3 * k], s->prof_ev[3 * k + 1]));
+    CU(cudaEventElapsedTime(&t1, s->prof_ev[3 * k + 1], s->prof_ev[3 * k + 2]));
+    a += t0;
+    b += t1;
+  }
+  if (markers_ms) *markers_ms = a;
+  if (collide_ms) *collide_ms = b;
+  if (steps) *steps = s->prof_n;
+  s->prof_n = 0;
   return FSG_OK;
 }
 

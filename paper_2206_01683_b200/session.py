@@ -290,6 +290,19 @@ class CoupledSession:
         check(_abi.lib().fsg_get_stencils(self._h, iptr(out)))
         return out.reshape(-1, 6)
 
+    # -- measurement -----------------------------------------------------------
+    def profile(self, enable: bool = True) -> None:
+        """Bracket each coupled step's marker and collide kernels with CUDA events."""
+        check(_abi.lib().fsg_profile_enable(self._h, 1 if enable else 0))
+
+    def profile_read(self):
+        """-> (marker-kernel ms, collide-kernel ms, timed steps) accumulated since enable/read."""
+        a = C.c_double()
+        b = C.c_double()
+        n = C.c_int()
+        check(_abi.lib().fsg_profile_read(self._h, C.byref(a), C.byref(b), C.byref(n)))
+        return a.value, b.value, n.value
+
     # -- z-slab halos ----------------------------------------------------------
     def halo_bytes(self) -> int:
         return int(_abi.lib().fsg_halo_bytes(self._h))
