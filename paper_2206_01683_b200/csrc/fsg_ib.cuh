@@ -47,10 +47,10 @@ constexpr int MK_LANES = 16;      // lanes per marker (half a warp)
 constexpr int MK_PER_BLOCK = 8;   // markers per 128-thread block
 constexpr int MK_MAXC = 125;      // 5^3 (Peskin4 with x +- 2 integral)
 
-/// Boundary-cell gather, out of line (rare for stencil cells; keeps the
-/// marker kernel's code small).
+/// Boundary-cell gather (rare for stencil cells).  Inline: an out-of-line
+/// call forces the caller's gathered values through local memory.
 template <bool PULLED>
-__device__ __noinline__ void gather_slow(const Grid& g, const Store* __restrict__ A, int x, int y,
+__device__ __forceinline__ void gather_slow(const Grid& g, const Store* __restrict__ A, int x, int y,
                                          int z, Store* s) {
   Store t[Q];
   gather<PULLED>(g, A, x, y, z, t);

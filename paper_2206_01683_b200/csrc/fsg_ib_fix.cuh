@@ -13,6 +13,10 @@
 // half-warp butterfly (deterministic); the fp64 parity path keeps the
 // reference's serial order instead (fsg_ib.cuh).
 
+constexpr int FX_LANES = 32;     // one warp per marker
+constexpr int FX_PER_BLOCK = 4;  // markers per 128-thread block
+constexpr int FX_CPL = 2;        // stencil cells per lane per round (64 per round trip)
+
 __device__ __forceinline__ unsigned long long to_fix(double v) {
   return (unsigned long long)__double2ll_rn(v * FIX_SCALE);
 }
@@ -22,11 +26,11 @@ __global__ void __launch_bounds__(128)
     k_markers_fix(Grid g, const float* __restrict__ A, Markers mk, const SessionConsts* __restrict__ scp,
                   const StepConsts st, MarkerStencil* __restrict__ rec_out, double* __restrict__ fworld,
                   double* fworld_h, int* valid_h, FixBand fb, StepScratch* out) {
-  __shared__ double phs[MK_PER_BLOCK][3][5];
-  const int hl = threadIdx.x & (MK_LANES - 1);
-  const int slot = threadIdx.x / MK_LANES;
-  const unsigned hmask = 0xFFFFu << (threadIdx.x & 16);
-  const int t = blockIdx.x * MK_PER_BLOCK + slot;
+  __shared__ double phs[FX_PER_BLOCK][3][5];
+  const int hl = threadIdx.x & (FX_LANES - 1);
+  const int slot = threadIdx.x / FX_LANES;
+  constexpr unsigned hmask = 0xFFFFFFFFu;
+  const int t = blockIdx.x * FX_PER_BLOCK + slot;
   if (t >= mk.m) return;  // uniform over the half-warp
   const SessionConsts& sc = *scp;
   // marker state: broadcast loads (may be mapped pinned host memory)
@@ -78,12 +82,12 @@ __global__ void __launch_bounds__(128)
   const float r0 = 1.0f / (float)cnt[0], r01 = 1.0f / (float)(cnt[0] * cnt[1]);
   double a0 = 0.0, a1 = 0.0, a2 = 0.0;
   // this lane's cells c = hl + 16 r (r < 8): gathered 4 at a time
-  for (int c0 = 0; c0 < ncell; c0 += 4 * MK_LANES) {
-    float sv[4][Q];
-    int cio[4], cjo[4], cko[4];
+  for (int c0 = 0; c0 < ncell; c0 += FX_CPL * FX_LANES) {
+    float sv[FX_CPL][Q];
+    int cio[FX_CPL], cjo[FX_CPL], cko[FX_CPL];
 #pragma unroll
-    for (int r = 0; r < 4; ++r) {
-      const int c = c0 + hl + MK_LANES * r;
+    for (int r = 0; r < FX_CPL; ++r) {
+      const int c = c0 + hl + FX_LANES * r;
       const int ko = (int)(((float)c + 0.5f) * r01);
       const int rem = c - ko * cnt[0] * cnt[1];
       const int jo = (int)(((float)rem + 0.5f) * r0);
@@ -93,8 +97,8 @@ __global__ void __launch_bounds__(128)
       if (c < ncell) gather_cell<PULLED>(g, A, lo[0] + cio[r], lo[1] + jo, lo[2] + ko - g.z0, sv[r]);
     }
 #pragma unroll
-    for (int r = 0; r < 4; ++r) {
-      const int c = c0 + hl + MK_LANES * r;
+    for (int r = 0; r < FX_CPL; ++r) {
+      const int c = c0 + hl + FX_LANES * r;
       if (c < ncell) {
         float drho, mx, my, mz;
         moments_dev(sv[r], drho, mx, my, mz);
@@ -108,10 +112,10 @@ __global__ void __launch_bounds__(128)
     }
   }
 #pragma unroll
-  for (int o = MK_LANES / 2; o > 0; o >>= 1) {  // fixed butterfly: every lane gets the total
-    a0 += __shfl_xor_sync(hmask, a0, o, MK_LANES);
-    a1 += __shfl_xor_sync(hmask, a1, o, MK_LANES);
-    a2 += __shfl_xor_sync(hmask, a2, o, MK_LANES);
+  for (int o = FX_LANES / 2; o > 0; o >>= 1) {  // fixed butterfly: every lane gets the total
+    a0 += __shfl_xor_sync(hmask, a0, o);
+    a1 += __shfl_xor_sync(hmask, a1, o);
+    a2 += __shfl_xor_sync(hmask, a2, o);
   }
   // body velocity, direct forcing, world force (identical on every lane)
   const double uf[3] = {a0 * sc.v2p, a1 * sc.v2p, a2 * sc.v2p};
@@ -169,7 +173,7 @@ __global__ void __launch_bounds__(128)
     fb.flag_cur[tx + fb.tnx * (ty + fb.tny * tz)] = 1;
   }
   // spread: this lane's own cells, fixed-point integer atomics
-  for (int c = hl; c < ncell; c += MK_LANES) {
+  for (int c = hl; c < ncell; c += FX_LANES) {
     const int ko = (int)(((float)c + 0.5f) * r01);
     const int rem = c - ko * cnt[0] * cnt[1];
     const int jo = (int)(((float)rem + 0.5f) * r0);

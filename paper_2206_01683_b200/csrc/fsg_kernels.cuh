@@ -786,7 +786,7 @@ static void L_markers_fix(const Grid& g, const void* A, int pulled, Markers mk,
                           double* fworld, double* fworld_h, int* valid_h, FixBand fb,
                           StepScratch* out, cudaStream_t s) {
   if (mk.m == 0) return;
-  const unsigned nb = (unsigned)((mk.m + MK_PER_BLOCK - 1) / MK_PER_BLOCK);
+  const unsigned nb = (unsigned)((mk.m + FX_PER_BLOCK - 1) / FX_PER_BLOCK);
   if (pulled)
     k_markers_fix<true><<<nb, 128, 0, s>>>(g, (const float*)A, mk, sc, st, rec, fworld, fworld_h,
                                            valid_h, fb, out);
