@@ -246,8 +246,15 @@ __device__ __forceinline__ float collide_cell32(float (&s)[Q], int x, int y, int
                                                 long long lc, const Band& band,
                                                 const SessionConsts& sc, const StepConsts& st,
                                                 StepScratch* out) {
-  float drho, mx, my, mz;
-  moments_dev(s, drho, mx, my, mz);
+  // moments from opposite-pair sums/differences (pairs (1,2),(3,4),...,(17,18))
+  const float d1 = s[1] - s[2], d3 = s[3] - s[4], d5 = s[5] - s[6], d7 = s[7] - s[8],
+              d9 = s[9] - s[10], d11 = s[11] - s[12], d13 = s[13] - s[14], d15 = s[15] - s[16],
+              d17 = s[17] - s[18];
+  const float drho = ((s[0] + ((s[1] + s[2]) + (s[3] + s[4]))) + ((s[5] + s[6]) + (s[7] + s[8]))) +
+                     (((s[9] + s[10]) + (s[11] + s[12])) + ((s[13] + s[14]) + ((s[15] + s[16]) + (s[17] + s[18]))));
+  const float mx = (d1 + d7) + (d9 + (d11 + d13));
+  const float my = (d3 + d7) + ((d15 + d17) - d9);
+  const float mz = (d5 + d11) + ((d15 - d13) - d17);
   const float rho = 1.0f + drho;
   if constexpr (FMODE == 2 || FMODE == 3) {  // 3: IB force already in Fx..Fz (fixed-point band)
     if constexpr (FMODE == 2) {
@@ -274,7 +281,6 @@ __device__ __forceinline__ float collide_cell32(float (&s)[Q], int x, int y, int
       __threadfence();
     }
   }
-  const float om1 = sc.om1_f;
   const float inv_rho = 1.0f / rho;
   const float ux = (mx + 0.5f * Fx) * inv_rho;
   const float uy = (my + 0.5f * Fy) * inv_rho;
@@ -284,30 +290,47 @@ __device__ __forceinline__ float collide_cell32(float (&s)[Q], int x, int y, int
     out->nonfinite = 1;
     __threadfence();
   }
-  const float uF = ux * Fx + uy * Fy + uz * Fz;
+  const float uF3 = 3.0f * (ux * Fx + uy * Fy + uz * Fz);
   const float h15u2 = 1.5f * u2;
-  // weight classes: 0 rest, 1 axes, 2 diagonals
-  const float ow[3] = {sc.ow_f[0], sc.ow_f[1], sc.ow_f[2]};
-  const float gw[3] = {sc.gw_f[0], sc.gw_f[1], sc.gw_f[2]};
-  float fmin_dev = FLT_MAX;
-#define FSG_DIR(I)                                                                        \
+  // Pair form of  g'_i = (1-w) g_i + w w_i (drho + rho X_i) + guo w_i S_i  with
+  // X = 3 eu + 4.5 eu^2 - 1.5 u^2 and S = 3(e-u).F + 9 eu e.F: for e_j = -e_i the
+  // even parts (4.5 t^2 - 1.5u^2, 9 t q - 3 u.F) are shared and the odd parts
+  // (3t, 3q) flip sign, t = e.u, q = e.F.
+  const float om1 = sc.om1_f;
+  const float owr1 = sc.ow_f[1] * rho, owr2 = sc.ow_f[2] * rho;
+  const float owt1 = 3.0f * owr1, owt2 = 3.0f * owr2;
+  const float owd1 = fmaf(sc.ow_f[1], drho, -sc.gw_f[1] * uF3);
+  const float owd2 = fmaf(sc.ow_f[2], drho, -sc.gw_f[2] * uF3);
+  const float g9_1 = 9.0f * sc.gw_f[1], g9_2 = 9.0f * sc.gw_f[2];
+  const float g3_1 = 3.0f * sc.gw_f[1], g3_2 = 3.0f * sc.gw_f[2];
+  const float p0 = fmaf(om1, s[0], fmaf(sc.ow_f[0], fmaf(rho, -h15u2, drho), -sc.gw_f[0] * uF3));
+  s[0] = p0;
+  float min1 = FLT_MAX, min2 = FLT_MAX;
+#define FSG_PAIR(I, OWR, OWT, OWD, G9, G3, MN)                                            \
   {                                                                                       \
     constexpr int a = ex_of(I), b = ey_of(I), c = ez_of(I);                               \
-    constexpr int cls = (I) == 0 ? 0 : ((I) <= 6 ? 1 : 2);                                \
-    const float eu = edot<a, b, c, float>(ux, uy, uz);                                    \
-    const float eF = edot<a, b, c, float>(Fx, Fy, Fz);                                    \
-    const float X = fmaf(eu, fmaf(4.5f, eu, 3.0f), -h15u2);                               \
-    const float geq_w = fmaf(rho, X, drho);                                               \
-    const float srcw = fmaf(fmaf(9.0f, eu, 3.0f), eF, -3.0f * uF);                        \
-    const float gp = fmaf(om1, s[I], fmaf(ow[cls], geq_w, gw[cls] * srcw));               \
-    fmin_dev = fminf(fmin_dev, gp + (float)w_of(I));                                      \
-    s[I] = gp;                                                                            \
+    const float t = edot<a, b, c, float>(ux, uy, uz);                                     \
+    const float q = edot<a, b, c, float>(Fx, Fy, Fz);                                     \
+    const float S = fmaf(G9, t * q, fmaf(OWR, fmaf(4.5f * t, t, -h15u2), OWD));           \
+    const float A = fmaf(OWT, t, G3 * q);                                                 \
+    const float gi = fmaf(om1, s[I], S + A);                                              \
+    const float gj = fmaf(om1, s[(I) + 1], S - A);                                        \
+    s[I] = gi;                                                                            \
+    s[(I) + 1] = gj;                                                                      \
+    MN = fminf(MN, fminf(gi, gj));                                                        \
   }
-  FSG_DIR(0) FSG_DIR(1) FSG_DIR(2) FSG_DIR(3) FSG_DIR(4) FSG_DIR(5) FSG_DIR(6)
-  FSG_DIR(7) FSG_DIR(8) FSG_DIR(9) FSG_DIR(10) FSG_DIR(11) FSG_DIR(12) FSG_DIR(13)
-  FSG_DIR(14) FSG_DIR(15) FSG_DIR(16) FSG_DIR(17) FSG_DIR(18)
-#undef FSG_DIR
-  return fmin_dev;
+  FSG_PAIR(1, owr1, owt1, owd1, g9_1, g3_1, min1)
+  FSG_PAIR(3, owr1, owt1, owd1, g9_1, g3_1, min1)
+  FSG_PAIR(5, owr1, owt1, owd1, g9_1, g3_1, min1)
+  FSG_PAIR(7, owr2, owt2, owd2, g9_2, g3_2, min2)
+  FSG_PAIR(9, owr2, owt2, owd2, g9_2, g3_2, min2)
+  FSG_PAIR(11, owr2, owt2, owd2, g9_2, g3_2, min2)
+  FSG_PAIR(13, owr2, owt2, owd2, g9_2, g3_2, min2)
+  FSG_PAIR(15, owr2, owt2, owd2, g9_2, g3_2, min2)
+  FSG_PAIR(17, owr2, owt2, owd2, g9_2, g3_2, min2)
+#undef FSG_PAIR
+  // min over post-collision f = g' + w_i, per weight class (monotone in g')
+  return fminf(p0 + (float)(1.0 / 3.0), fminf(min1 + (float)(1.0 / 18.0), min2 + (float)(1.0 / 36.0)));
 }
 #endif
 
