@@ -153,11 +153,12 @@ int fsg_get_force(fsg_session* s, double* F);
 int fsg_get_stencils(fsg_session* s, int* lo_hi);
 
 /* ---- measurement ---------------------------------------------------------
- * When enabled, every coupled step brackets its marker kernel and its
- * collide-stream kernel with CUDA events on the session stream; read back the
- * accumulated device times (ms) and the number of timed steps. */
+ * When enabled, every step is bracketed with CUDA events on the session
+ * stream (the marker kernel and the banded collide/stream kernel overlap, so
+ * the step is one interval); read back the accumulated device time (ms) and
+ * the number of timed steps. */
 int fsg_profile_enable(fsg_session* s, int enable);
-int fsg_profile_read(fsg_session* s, double* markers_ms, double* collide_ms, int* steps);
+int fsg_profile_read(fsg_session* s, double* step_ms, int* steps);
 
 /* ---- z-slab halo exchange ------------------------------
  * In a slab session the 5 populations that cross each z face are packed into

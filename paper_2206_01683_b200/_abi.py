@@ -83,7 +83,7 @@ SIGNATURES = {
     "fsg_get_force": (C.c_int, [_vp, _dp]),
     "fsg_get_stencils": (C.c_int, [_vp, _ip]),
     "fsg_profile_enable": (C.c_int, [_vp, C.c_int]),
-    "fsg_profile_read": (C.c_int, [_vp, _dp, _dp, _ip]),
+    "fsg_profile_read": (C.c_int, [_vp, _dp, _ip]),
     "fsg_halo_bytes": (C.c_size_t, [_vp]),
     "fsg_halo_pack": (C.c_int, [_vp, _vp, _vp]),
     "fsg_halo_unpack": (C.c_int, [_vp, _vp, _vp]),

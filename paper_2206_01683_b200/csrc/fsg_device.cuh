@@ -101,11 +101,9 @@ struct StepScratch {
   int band_overflow;               // bbox exceeded band capacity
   int bbox_lo_enc[3];
   int bbox_hi_enc[3];
-  unsigned blocks_done;              // K4 last-block detection (status publish)
-  int _pad;
+  unsigned work[2];                  // banded K4: dynamic work counters (phase A, B)
 };
 constexpr int LO_BIAS = 0x40000000;
-constexpr int TICKET_GROUPS = 1024;  // K4 last-block detection: group counters + 1 global
 
 // Throughput-mode IB force field: 64-bit fixed point (2^-40 lattice force
 // units), accumulated with integer atomics -- associative, hence bit-
@@ -114,11 +112,35 @@ constexpr double FIX_SCALE = 1099511627776.0;        // 2^40
 constexpr double FIX_INV = 1.0 / 1099511627776.0;   // 2^-40
 struct FixBand {
   unsigned long long* F;     // 3 per owned cell (x + nx*(y + ny*z))
-  unsigned char* flag_cur;   // tiles touched this step (read by K4)
-  unsigned char* flag_prev;  // tiles of the previous step (cleared by K4)
   int tnx, tny, tnz;         // tile grid (4^3 cells per tile)
-  int _pad;
+  unsigned stamp;            // step stamp (step index + 1; 0 = never)
+  // per-tile step stamps
+  unsigned* tflag;           // touched by a stencil at this step
+  unsigned* tdil;            // predicted band of this step (previous stencils dilated by 1 cell)
+  unsigned* tdiln;           // predicted band of the next step (written by the marker kernel)
+  unsigned* tdone;           // processed by the band phase of this step
+  int* listT;                // tiles touched this step            (count *cntT)
+  int* listD;                // tiles predicted for this step      (count *cntD)
+  int* listDn;               // tiles predicted for the next step  (count *cntDn)
+  unsigned* cntT;            // the counters live in a ring of three steps, so K4 can
+  unsigned* cntD;            // zero the next step's from block 0 (no last-block
+  unsigned* cntDn;           // detection): see fix_counters()
+  unsigned* zero0;           // counters K4 of this step zeroes for later steps
+  unsigned* zero1;
 };
+
+// Counter ring [6] = cntT[3] | cntD[3], indexed by stamp mod 3.  Step s: the
+// marker kernel appends to cntT[s] and cntDn = cntD[s+1]; K4 reads cntT[s],
+// cntD[s] and zeroes cntT[s+1] (next marker kernel) and cntD[s+2] (its
+// cntDn) -- both last used by steps that completed before this K4 started.
+__host__ __device__ inline void fix_counters(FixBand& fb, unsigned* ring) {
+  const unsigned s = fb.stamp;
+  fb.cntT = ring + s % 3;
+  fb.cntD = ring + 3 + s % 3;
+  fb.cntDn = ring + 3 + (s + 1) % 3;
+  fb.zero0 = ring + (s + 1) % 3;
+  fb.zero1 = ring + 3 + (s + 2) % 3;
+}
 
 __host__ __device__ __forceinline__ unsigned long long ordered_key(double v) {
 #ifdef __CUDA_ARCH__
@@ -200,14 +222,20 @@ struct Launchers {
   void (*spread)(const Grid&, int m, const MarkerStencil*, const MarkerBox*, Band,
                  const StepScratch*, cudaStream_t);
   // throughput path (fp32 only; nullptr in the fp64 table): markers scatter
-  // fixed-point forces; K4 consumes them and publishes the step status
+  // fixed-point forces; K4 consumes them.  Both K4 variants reset the next
+  // step's scratch from block 0; the host copies the status out on demand.
   void (*markers_fix)(const Grid&, const void* A, int pulled, Markers, const SessionConsts*,
                       const StepConsts& st, MarkerStencil*, double* fworld, double* fworld_host,
                       int* valid_host, FixBand, StepScratch*, cudaStream_t);
-  void (*collide_fix)(const Grid&, const void* A, int pulled, void* B, FixBand,
-                      const SessionConsts*, const StepConsts& st, int frame_on, int has_ib,
-                      StepScratch* scr, StepScratch* scr_next, StepScratch* publish,
-                      unsigned* tickets, unsigned* tickets_next, cudaStream_t);
+  // pure-fluid step (no IB band)
+  void (*collide_fix)(const Grid&, const void* A, int pulled, void* B, const SessionConsts*,
+                      const StepConsts& st, int frame_on, StepScratch* scr, StepScratch* scr_next,
+                      cudaStream_t);
+  // banded coupled step: one K4 launch, a programmatic dependent (pdl != 0)
+  // of the marker kernel launched just before it on the same stream
+  void (*collide_band)(const Grid&, const void* A, int pulled, void* B, FixBand,
+                       const SessionConsts*, const StepConsts& st, int frame_on,
+                       StepScratch* scr, StepScratch* scr_next, int pdl, cudaStream_t);
   // halo planes (z-slab): pack owned boundary planes / unpack into halo planes
   void (*halo_pack)(const Grid&, const void* B, void* send_lo, void* send_hi, cudaStream_t);
   void (*halo_unpack)(const Grid&, void* B, const void* recv_lo, const void* recv_hi,

@@ -27,6 +27,9 @@ __global__ void __launch_bounds__(128)
                   const StepConsts st, MarkerStencil* __restrict__ rec_out, double* __restrict__ fworld,
                   double* fworld_h, int* valid_h, FixBand fb, StepScratch* out) {
   __shared__ double phs[FX_PER_BLOCK][3][5];
+  // let the banded K4 (programmatic dependent) start its non-band cells now;
+  // it waits for this grid's completion before touching the band
+  asm volatile("griddepcontrol.launch_dependents;");
   const int hl = threadIdx.x & (FX_LANES - 1);
   const int slot = threadIdx.x / FX_LANES;
   constexpr unsigned hmask = 0xFFFFFFFFu;
@@ -165,12 +168,26 @@ __global__ void __launch_bounds__(128)
     r._pad = 0;
     rec_out[t] = r;
   }
-  // flag the (<= 2x2x2) tiles the stencil touches
+  // stamp + list the touched tiles (this step: <= 2x2x2, the stencil spans
+  // <= 5 cells) and the tiles of the stencil dilated by one cell (predicted
+  // band of the next step: markers move < 1 cell per step)
   if (hl < 8) {
     const int tx = ((hl & 1) ? hi[0] : lo[0]) >> 2;
     const int ty = ((hl & 2) ? hi[1] : lo[1]) >> 2;
     const int tz = ((hl & 4) ? hi[2] - g.z0 : lo[2] - g.z0) >> 2;
-    fb.flag_cur[tx + fb.tnx * (ty + fb.tny * tz)] = 1;
+    const int T = tx + fb.tnx * (ty + fb.tny * tz);
+    if (atomicExch(&fb.tflag[T], fb.stamp) != fb.stamp) fb.listT[atomicAdd(fb.cntT, 1u)] = T;
+  }
+  if (hl < 27) {
+    const int ex0 = max(lo[0] - 1, 0) >> 2, ex1 = min(hi[0] + 1, g.nx - 1) >> 2;
+    const int ey0 = max(lo[1] - 1, 0) >> 2, ey1 = min(hi[1] + 1, g.ny - 1) >> 2;
+    const int ez0 = max(lo[2] - g.z0 - 1, 0) >> 2, ez1 = min(hi[2] - g.z0 + 1, g.nz - 1) >> 2;
+    const int tx = ex0 + hl % 3, ty = ey0 + (hl / 3) % 3, tz = ez0 + hl / 9;
+    if (tx <= ex1 && ty <= ey1 && tz <= ez1) {
+      const int T = tx + fb.tnx * (ty + fb.tny * tz);
+      if (atomicExch(&fb.tdiln[T], fb.stamp + 1u) != fb.stamp + 1u)
+        fb.listDn[atomicAdd(fb.cntDn, 1u)] = T;
+    }
   }
   // spread: this lane's own cells, fixed-point integer atomics
   for (int c = hl; c < ncell; c += FX_LANES) {

@@ -55,104 +55,161 @@ __global__ void __launch_bounds__(128)
   report_min(out, vmin == FLT_MAX ? DBL_MAX : (double)vmin);
 }
 
-// Coupled-step K4 of the throughput session: IB force from the fixed-point
-// tile band (read and re-zeroed), virtual force inline, then collide/stream.
-// Block (0,0,0) resets the next step's scratch; the last block to finish
-// publishes the step status into mapped pinned host memory.
+/// One cell: pull gather (x faces on the fast path), collide, store.
+template <bool PULLED, bool VF>
+__device__ __forceinline__ float cell_update(const Grid& g, const DirPtrs& dp,
+                                             const float* __restrict__ A, int x, int y, int z,
+                                             float Fx, float Fy, float Fz,
+                                             const SessionConsts& sc, const StepConsts& st,
+                                             StepScratch* out) {
+  const int m = (int)mem_index(g, x, y, z);
+  const int zg = g.z0 + z;
+  float s[Q];
+  if (!PULLED) {
+#pragma unroll
+    for (int i = 0; i < Q; ++i) s[i] = __ldg(dp.a[i] + m);
+  } else if (y > 0 && y < g.ny - 1 && zg > 0 && zg < g.nzg - 1) {
+    // x faces stay on the fast path: the pull source of an unknown population
+    // moves by +-1 (open: clamped copy, solver.hpp:59-97) or +-nx (periodic)
+    const int cxp = x == 0 ? (g.periodic ? g.nx : 1) : 0;
+    const int cxm = x == g.nx - 1 ? (g.periodic ? -g.nx : -1) : 0;
+#pragma unroll
+    for (int i = 0; i < Q; ++i) {
+      const int cx = ex_of(i) > 0 ? cxp : (ex_of(i) < 0 ? cxm : 0);
+      s[i] = __ldg(dp.a[i] + (m + cx));
+    }
+  } else {
+    gather<true>(g, A, x, y, z, s);  // y/z face rows (warp-uniform)
+  }
+  Band none{nullptr, 0};
+  const float v = collide_cell32<3, VF>(s, x, y, z, g, Fx, Fy, Fz, false, 0, none, sc, st, out);
+#pragma unroll
+  for (int i = 0; i < Q; ++i) dp.b[i][m] = s[i];
+  return v;
+}
+
+/// Block 0 zeroes the next step's scratch (status + work counters).  Nothing
+/// is published from the kernel: the host copies the status out of the
+/// device scratch when it asks for it, after a stream sync, so the kernel
+/// needs no last-block detection and no system-scope fence on its tail.
+__device__ __forceinline__ void reset_next(StepScratch* next, int tid) {
+  constexpr int NS = (int)(sizeof(StepScratch) / 4);
+  if (blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && tid < NS)
+    reinterpret_cast<int*>(next)[tid] = 0;
+}
+
+// Pure-fluid K4 of the throughput session (no IB band): virtual force inline,
+// collide/stream.  Persistent: work item = (xy column, chunk of zc planes).
 template <bool PULLED, bool VF>
 __global__ void __launch_bounds__(128)
-    k_collide_fix(Grid g, DirPtrs dp, const float* __restrict__ A, FixBand fb, int has_ib,
+    k_collide_fix(Grid g, DirPtrs dp, const float* __restrict__ A,
                   const SessionConsts* __restrict__ scp, const StepConsts st,
-                  StepScratch* __restrict__ out, StepScratch* __restrict__ next,
-                  StepScratch* publish, unsigned* tickets, unsigned* tickets_next, int zc) {
-  constexpr int NS = (int)(sizeof(StepScratch) / 4);
+                  StepScratch* __restrict__ out, StepScratch* __restrict__ next, int zc) {
   const int tid = threadIdx.x + blockDim.x * threadIdx.y;
-  if (blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0) {
-    if (tid < NS) reinterpret_cast<int*>(next)[tid] = 0;
-    for (int k = tid; k <= TICKET_GROUPS; k += blockDim.x * blockDim.y) tickets_next[k] = 0u;
+  reset_next(next, tid);
+  const int tx_n = (g.nx + blockDim.x - 1) / blockDim.x;
+  const int ty_n = (g.ny + blockDim.y - 1) / blockDim.y;
+  const int ncol = tx_n * ty_n, nzc = (g.nz + zc - 1) / zc;
+  const int nitem = ncol * nzc;
+  const SessionConsts& sc = *scp;
+  float vmin = FLT_MAX;
+  for (int it = blockIdx.x; it < nitem; it += gridDim.x) {
+    const int col = it % ncol, zk = it / ncol;
+    const int x = (col % tx_n) * blockDim.x + threadIdx.x;
+    const int y = (col / tx_n) * blockDim.y + threadIdx.y;
+    const int z0 = zk * zc, z1 = min(g.nz, z0 + zc);
+    if (x >= g.nx || y >= g.ny) continue;
+    for (int z = z0; z < z1; ++z)
+      vmin = fminf(vmin, cell_update<PULLED, VF>(g, dp, A, x, y, z, 0.f, 0.f, 0.f, sc, st, out));
   }
-  // persistent: work item = (xy tile column, chunk of zc planes); a block
-  // walks its items, stepping z by one plane (no per-cell index division)
+  report_min(out, vmin == FLT_MAX ? DBL_MAX : (double)vmin);
+}
+
+// ---------------------------------------------------------------------------
+// Banded coupled K4 (one launch per step).  Launched on the session stream as
+// a programmatic dependent of the marker kernel, which triggers its
+// dependents on entry: K4 starts while the markers still run and updates
+// every cell OUTSIDE the predicted band (phase A: tiles of the previous
+// step's stencils dilated by one cell -- markers move < 1 cell per step),
+// with dynamic work fetch so blocks that land late on SMs freed by the marker
+// kernel take less.  It then waits for the marker grid (griddepcontrol.wait:
+// completion + memory visibility) and updates the union of the touched and
+// predicted tiles with the fresh IB forces (phase B).  A touched tile that
+// was not predicted (first step, recentring) is simply recomputed by phase
+// B: K4 reads A and writes B, so a recomputation is idempotent.
+
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
+template <bool PULLED, bool VF>
+__global__ void __launch_bounds__(128)
+    k_collide_band(Grid g, DirPtrs dp, const float* __restrict__ A, FixBand fb,
+                   const SessionConsts* __restrict__ scp, const StepConsts st,
+                   StepScratch* __restrict__ out, StepScratch* __restrict__ next, int zc) {
+  __shared__ int item;
+  __shared__ int take[2];
+  const int tid = threadIdx.x + blockDim.x * threadIdx.y;
+  reset_next(next, tid);
+  if (blockIdx.x == 0 && tid == 0) {  // counter ring: see fix_counters()
+    *fb.zero0 = 0u;
+    *fb.zero1 = 0u;
+  }
+  const SessionConsts& sc = *scp;
+  // ---- phase A: cells outside the predicted band (no IB force)
   const int tx_n = (g.nx + blockDim.x - 1) / blockDim.x;
   const int ty_n = (g.ny + blockDim.y - 1) / blockDim.y;
   const int ncol = tx_n * ty_n, nzc = (g.nz + zc - 1) / zc;
   const int nitem = ncol * nzc;
   float vmin = FLT_MAX;
-  for (int it = blockIdx.x; it < nitem; it += gridDim.x) {
-  const int col = it % ncol, zk = it / ncol;
-  const int x = (col % tx_n) * blockDim.x + threadIdx.x;
-  const int y = (col / tx_n) * blockDim.y + threadIdx.y;
-  const int z0 = zk * zc, z1 = min(g.nz, z0 + zc);
-  if (x < g.nx && y < g.ny) {
-  const bool yin = y > 0 && y < g.ny - 1;
-  // x faces stay on the fast path: the pull source of an unknown population
-  // moves by +-1 (open: clamped copy, solver.hpp:59-97) or +-nx (periodic)
-  const int cxp = x == 0 ? (g.periodic ? g.nx : 1) : 0;             // ex = +1
-  const int cxm = x == g.nx - 1 ? (g.periodic ? -g.nx : -1) : 0;    // ex = -1
-  int m = (int)mem_index(g, x, y, z0);
-  for (int z = z0; z < z1; ++z, m += (int)g.plane) {
-    float s[Q];
-    const int zg = g.z0 + z;
-    if (!PULLED) {
-#pragma unroll
-      for (int i = 0; i < Q; ++i) s[i] = __ldg(dp.a[i] + m);  // dp.a = A + own[i]
-    } else if (yin && zg > 0 && zg < g.nzg - 1) {
-#pragma unroll
-      for (int i = 0; i < Q; ++i) {  // dp.a = A + pull[i]
-        const int cx = ex_of(i) > 0 ? cxp : (ex_of(i) < 0 ? cxm : 0);
-        s[i] = __ldg(dp.a[i] + (m + cx));
-      }
-    } else {
-      gather<true>(g, A, x, y, z, s);  // y/z face rows (warp-uniform)
-    }
-    float Fx = 0.f, Fy = 0.f, Fz = 0.f;
-    if (has_ib) {
-      const int tile = (x >> 2) + fb.tnx * ((y >> 2) + fb.tny * (z >> 2));
-      if (fb.flag_cur[tile]) {
-        unsigned long long* F = fb.F + 3 * ((long long)x + (long long)g.nx * ((long long)y + (long long)g.ny * z));
-        const long long f0 = (long long)F[0], f1 = (long long)F[1], f2 = (long long)F[2];
-        F[0] = 0ull;
-        F[1] = 0ull;
-        F[2] = 0ull;
-        Fx = (float)((double)f0 * FIX_INV);
-        Fy = (float)((double)f1 * FIX_INV);
-        Fz = (float)((double)f2 * FIX_INV);
-      }
-      if (((x | y | z) & 3) == 0) fb.flag_prev[tile] = 0;  // the previous step's flags
-    }
-    Band none{nullptr, 0};
-    vmin = fminf(vmin, collide_cell32<3, VF>(s, x, y, z, g, Fx, Fy, Fz, false, 0, none, *scp, st, out));
-#pragma unroll
-    for (int i = 0; i < Q; ++i) dp.b[i][m] = s[i];
-  }  // z
-  }  // live column
-  }  // work items
-  report_min(out, vmin == FLT_MAX ? DBL_MAX : (double)vmin);
-  if (publish) {
-    __shared__ int last;
-    // status writers (report_min's lane 0, rare nonfinite/nonpos stores)
-    // fence themselves; the ticket below orders the block after them
+  for (;;) {
+    if (tid == 0) item = (int)atomicAdd(&out->work[0], 1u);
     __syncthreads();
-    if (tid == 0) {
-      // hierarchical ticket: one same-address atomic per block would
-      // serialise ~n/128 atomics on one L2 slice
-      const unsigned nblk = gridDim.x * gridDim.y * gridDim.z;
-      const unsigned bid = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);
-      const unsigned G = max(64u, (nblk + TICKET_GROUPS - 1) / TICKET_GROUPS);
-      const unsigned grp = bid / G, ngrp = (nblk + G - 1) / G;
-      const unsigned gsize = min(G, nblk - grp * G);
-      __threadfence();
-      last = 0;
-      if (atomicAdd(&tickets[grp], 1u) == gsize - 1) {
-        __threadfence();
-        last = atomicAdd(&tickets[TICKET_GROUPS], 1u) == ngrp - 1;
-      }
-    }
+    const int it = item;
     __syncthreads();
-    if (last && tid < NS) {
-      __threadfence();
-      reinterpret_cast<volatile int*>(publish)[tid] = reinterpret_cast<volatile int*>(out)[tid];
-      __threadfence_system();
+    if (it >= nitem) break;
+    const int col = it % ncol, zk = it / ncol;
+    const int x = (col % tx_n) * blockDim.x + threadIdx.x;
+    const int y = (col / tx_n) * blockDim.y + threadIdx.y;
+    const int z0 = zk * zc, z1 = min(g.nz, z0 + zc);
+    if (x >= g.nx || y >= g.ny) continue;
+    const int trow = (x >> 2) + fb.tnx * (y >> 2);
+    for (int z = z0; z < z1; ++z) {
+      if (fb.tdil[trow + fb.tnx * fb.tny * (z >> 2)] == fb.stamp) continue;  // predicted band
+      vmin = fminf(vmin, cell_update<PULLED, VF>(g, dp, A, x, y, z, 0.f, 0.f, 0.f, sc, st, out));
     }
   }
+  // ---- phase B: touched + predicted tiles, after the marker grid completed
+  pdl_wait();
+  const int nT = (int)*(volatile unsigned*)fb.cntT, nD = (int)*(volatile unsigned*)fb.cntD;
+  const int half = tid >> 6, lt = tid & 63;  // two 4^3 tiles per fetch
+  for (;;) {
+    if (tid == 0) item = (int)atomicAdd(&out->work[1], 2u);
+    __syncthreads();
+    const int e = item + half;
+    __syncthreads();
+    if (e - half >= nT + nD) break;  // block-uniform
+    const int T = e >= nT + nD ? -1 : (e < nT ? fb.listT[e] : fb.listD[e - nT]);
+    // a tile listed twice (touched and predicted) is processed once: lane 0
+    // of the half claims it
+    if (lt == 0) take[half] = T >= 0 && atomicExch(&fb.tdone[T], fb.stamp) != fb.stamp;
+    __syncthreads();
+    const bool go = take[half];
+    __syncthreads();
+    if (!go) continue;
+    const int tx = T % fb.tnx, ty = (T / fb.tnx) % fb.tny, tz = T / (fb.tnx * fb.tny);
+    const int x = 4 * tx + (lt & 3), y = 4 * ty + ((lt >> 2) & 3), z = 4 * tz + (lt >> 4);
+    if (x >= g.nx || y >= g.ny || z >= g.nz) continue;
+    float Fx = 0.f, Fy = 0.f, Fz = 0.f;
+    if (fb.tflag[T] == fb.stamp) {  // consume and re-zero the fixed-point force
+      unsigned long long* F = fb.F + 3 * ((long long)x + (long long)g.nx * ((long long)y + (long long)g.ny * z));
+      const long long f0 = (long long)F[0], f1 = (long long)F[1], f2 = (long long)F[2];
+      F[0] = 0ull;
+      F[1] = 0ull;
+      F[2] = 0ull;
+      Fx = (float)((double)f0 * FIX_INV);
+      Fy = (float)((double)f1 * FIX_INV);
+      Fz = (float)((double)f2 * FIX_INV);
+    }
+    vmin = fminf(vmin, cell_update<PULLED, VF>(g, dp, A, x, y, z, Fx, Fy, Fz, sc, st, out));
+  }
+  report_min(out, vmin == FLT_MAX ? DBL_MAX : (double)vmin);
 }

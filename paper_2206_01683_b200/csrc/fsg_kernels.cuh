@@ -817,10 +817,9 @@ static void L_markers_fix(const Grid& g, const void* A, int pulled, Markers mk,
     k_markers_fix<false><<<nb, 128, 0, s>>>(g, (const float*)A, mk, sc, st, rec, fworld, fworld_h,
                                             valid_h, fb, out);
 }
-static void L_collide_fix(const Grid& g, const void* A, int pulled, void* B, FixBand fb,
-                          const SessionConsts* sc, const StepConsts& st, int frame_on, int has_ib,
-                          StepScratch* scr, StepScratch* scr_next, StepScratch* publish,
-                          unsigned* tickets, unsigned* tickets_next, cudaStream_t s) {
+static void L_collide_fix(const Grid& g, const void* A, int pulled, void* B,
+                          const SessionConsts* sc, const StepConsts& st, int frame_on,
+                          StepScratch* scr, StepScratch* scr_next, cudaStream_t s) {
   DirPtrs dp;
   for (int i = 0; i < Q; ++i) {
     dp.a[i] = (const float*)A + (pulled ? g.pull[i] : g.own[i]);
@@ -844,8 +843,7 @@ static void L_collide_fix(const Grid& g, const void* A, int pulled, void* B, Fix
   const long long nzc_want = (8 * grid + ncol - 1) / ncol;
   const int zc = (int)std::max<long long>(1, g.nz / std::max<long long>(1, nzc_want));
 #define FSG_LF(P, V) \
-  k_collide_fix<P, V><<<gr, b, 0, s>>>(g, dp, (const float*)A, fb, has_ib, sc, st, scr, scr_next, \
-                                       publish, tickets, tickets_next, zc)
+  k_collide_fix<P, V><<<gr, b, 0, s>>>(g, dp, (const float*)A, sc, st, scr, scr_next, zc)
   if (pulled) {
     if (frame_on) FSG_LF(true, true);
     else FSG_LF(true, false);
@@ -855,15 +853,61 @@ static void L_collide_fix(const Grid& g, const void* A, int pulled, void* B, Fix
   }
 #undef FSG_LF
 }
+
+// Banded K4 as a programmatic dependent of the marker kernel just launched on
+// the same stream (see k_collide_band).
+static void L_collide_band(const Grid& g, const void* A, int pulled, void* B, FixBand fb,
+                           const SessionConsts* sc, const StepConsts& st, int frame_on,
+                           StepScratch* scr, StepScratch* scr_next, int pdl, cudaStream_t s) {
+  DirPtrs dp;
+  for (int i = 0; i < Q; ++i) {
+    dp.a[i] = (const float*)A + (pulled ? g.pull[i] : g.own[i]);
+    dp.b[i] = (float*)B + g.own[i];
+  }
+  static int nsm = 0, res = 0;
+  if (!nsm) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&res, k_collide_band<true, true>, 128, 0);
+    res = std::max(res, 1);
+  }
+  const dim3 b = cell_block(g);
+  const int zc = 4;  // one tile layer per work item
+  const long long nitem =
+      (long long)((g.nx + b.x - 1) / b.x) * ((g.ny + b.y - 1) / b.y) * ((g.nz + zc - 1) / zc);
+  const unsigned grid = (unsigned)std::min<long long>(nitem, (long long)nsm * res);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = b;
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = pdl ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+#define FSG_PB(P, V)                                                                     \
+  cudaLaunchKernelEx(&cfg, k_collide_band<P, V>, g, dp, (const float*)A, fb, sc, st, scr, \
+                     scr_next, zc)
+  if (pulled) {
+    if (frame_on) FSG_PB(true, true);
+    else FSG_PB(true, false);
+  } else {
+    if (frame_on) FSG_PB(false, true);
+    else FSG_PB(false, false);
+  }
+#undef FSG_PB
+}
 #endif
 
 static const Launchers kLaunchers = {
     L_fill_rest,    L_set_f,          L_init_eq,      L_get_f,         L_macroscopic,
     L_collide,      L_session_force,  L_recenter,     L_markers,       L_spread,
 #if FSG_PREC == 32
-    L_markers_fix,  L_collide_fix,
+    L_markers_fix,  L_collide_fix,    L_collide_band,
 #else
-    nullptr,        nullptr,
+    nullptr,        nullptr,          nullptr,
 #endif
     L_halo_pack,    L_halo_unpack,    (int)sizeof(Store)};
 

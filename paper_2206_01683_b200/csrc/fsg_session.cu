@@ -7,13 +7,18 @@
 // (UnitMap, frame constants, recenter origin update) keeps the reference's
 // operation order.
 //
-// The coupled step is replayed as a CUDA graph:
+// Parity mode (fp64): the coupled step is replayed as a CUDA graph:
 //   [H2D marker state] -> [H2D frame constants] -> [reset step scratch]
 //   -> K_m markers -> K_s spread -> K4 collide/stream -> [D2H status]
 // Host staging (pinned), step scratch and the status readback slot are
 // double-buffered by the parity of the A/B pair, so step n+1 can be
 // enqueued while step n still runs; each graph bakes in its parity's
 // buffers.
+// Throughput mode (fp32): two direct launches per coupled step, frame
+// constants by value -- the marker kernel (fixed-point spread) and the
+// banded K4 as its programmatic dependent (fsg_k4v4.cuh) -- or one K4 when
+// there are no markers.  The host never waits before enqueueing; the status
+// is copied out of the device scratch only when asked for.
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -145,13 +150,16 @@ struct fsg_session {
   fsg_status last{};
   // throughput (fp32) IB: fixed-point tile band
   fsg::FixBand fix{};
-  unsigned char* flags[2] = {nullptr, nullptr};
-  unsigned* tickets[2] = {nullptr, nullptr};  // K4 hierarchical last-block counters
-  bool fix_active = false;  // markers were spread at least once
+  // banded step: per-tile step stamps, tile lists, counter ring
+  unsigned* tstamp = nullptr;  // [4 * ntile]: tflag | tdil[2] | tdone
+  int* tlists = nullptr;       // [3 * ntile]: listT | listD[2]
+  unsigned* tcnt = nullptr;    // [6]: cntT[3] | cntD[3] (fix_counters)
+  unsigned stamp = 0;          // step stamp (step index + 1)
+  size_t ntile = 0;
   bool scr_dirty[2] = {false, false};  // d_scr[k] not known to be zero
   StepConsts last_st{};     // frame constants of the last step (diagnostics)
   StepScratch* d_diag = nullptr;
-  // measurement: event triplets (before markers, before K4, after K4) per step
+  // measurement: an event pair around every step
   static constexpr int PROF_CAP = 4096;
   bool prof = false;
   std::vector<cudaEvent_t> prof_ev;
@@ -482,12 +490,12 @@ int fsg_create(const fsg_config* cfg_in, fsg_session** out) {
     const size_t ntile = (size_t)fb.tnx * fb.tny * fb.tnz;
     CUF(cudaMalloc(&fb.F, sizeof(unsigned long long) * 3 * (size_t)g.n));
     CUF(cudaMemsetAsync(fb.F, 0, sizeof(unsigned long long) * 3 * (size_t)g.n, s->stream));
-    for (int k = 0; k < 2; ++k) {
-      CUF(cudaMalloc(&s->flags[k], ntile));
-      CUF(cudaMemsetAsync(s->flags[k], 0, ntile, s->stream));
-      CUF(cudaMalloc(&s->tickets[k], sizeof(unsigned) * (fsg::TICKET_GROUPS + 1)));
-      CUF(cudaMemsetAsync(s->tickets[k], 0, sizeof(unsigned) * (fsg::TICKET_GROUPS + 1), s->stream));
-    }
+    s->ntile = ntile;
+    CUF(cudaMalloc(&s->tstamp, sizeof(unsigned) * 4 * ntile));
+    CUF(cudaMemsetAsync(s->tstamp, 0, sizeof(unsigned) * 4 * ntile, s->stream));
+    CUF(cudaMalloc(&s->tlists, sizeof(int) * 3 * ntile));
+    CUF(cudaMalloc(&s->tcnt, sizeof(unsigned) * 6));
+    CUF(cudaMemsetAsync(s->tcnt, 0, sizeof(unsigned) * 6, s->stream));
   }
   s->L->fill_rest(g, s->A(), s->stream);
   if (cudaGetLastError() != cudaSuccess) return fail(set_err(FSG_ECUDA, "fill_rest launch failed"));
@@ -525,10 +533,9 @@ int fsg_destroy(fsg_session* s) {
   cudaFree(s->d_fworld);
   cudaFree(s->band.F);
   cudaFree(s->fix.F);
-  cudaFree(s->flags[0]);
-  cudaFree(s->flags[1]);
-  cudaFree(s->tickets[0]);
-  cudaFree(s->tickets[1]);
+  cudaFree(s->tstamp);
+  cudaFree(s->tlists);
+  cudaFree(s->tcnt);
   cudaFree(s->d_diag);
   cudaFree(s->d_tmp);
   cudaFree(s->d_red);
@@ -781,36 +788,53 @@ int fsg_set_markers_device(fsg_session* s, int n_bodies, const int64_t* off, con
 int fsg_step_async(fsg_session* s) {
   CU(cudaSetDevice(s->cfg.device));
   const int p = s->par;
-  CU(cudaEventSynchronize(s->ev[p]));  // pinned slots of parity p are free again
+  // the fp64 graph reads its frame constants from pinned slot p: wait until
+  // the step that last used it is done.  The throughput path passes them by
+  // value and the device only WRITES its pinned slots (status, marker
+  // forces), which the host reads after a stream sync -- no wait, so the
+  // host can run several steps ahead.
+  if (!s->L->markers_fix) CU(cudaEventSynchronize(s->ev[p]));
   frame_consts(s->frame, *s->h_st[p]);
   const bool frame_on = s->cfg.frame_mode != FSG_FRAME_NONE;
   const bool copy_mk = s->mk_host && s->mk_dirty;
   if (s->L->markers_fix) {
-    // throughput path: two kernels, frame constants by value, status
-    // published by K4's last block into mapped pinned memory
+    // throughput path: frame constants by value; the status stays in the
+    // device scratch until the host asks for it (fsg_last_status)
     const StepConsts st = *s->h_st[p];
     s->last_st = st;
     if (s->scr_dirty[p]) CU(cudaMemsetAsync(s->d_scr[p], 0, sizeof(StepScratch), s->stream));
-    fsg::FixBand fb = s->fix;
-    fb.flag_cur = s->flags[p];
-    fb.flag_prev = s->flags[p ^ 1];
     const bool prof = s->prof && s->prof_n < fsg_session::PROF_CAP;
-    cudaEvent_t* pe = prof ? &s->prof_ev[3 * (size_t)s->prof_n] : nullptr;
+    cudaEvent_t* pe = prof ? &s->prof_ev[2 * (size_t)s->prof_n] : nullptr;
     if (prof) CU(cudaEventRecord(pe[0], s->stream));
     if (s->m) {
-      s->L->markers_fix(s->g, s->buf[p], s->pulled, s->mk, s->d_sc, st, s->d_stencil, s->d_fworld,
-                        s->h_fw[p], s->h_valid[p], fb, s->d_scr[p], s->stream);
-      s->fix_active = true;
+      // coupled step: markers, then the banded K4 as their programmatic
+      // dependent (no event between the two, or the overlap is lost).  The
+      // fixed-point force field is consumed (re-zeroed) by that K4, so a step
+      // without markers is the plain fluid K4 below.
+      fsg::FixBand fb = s->fix;
+      const unsigned stamp = ++s->stamp;
+      const int q = (int)(stamp & 1u);
+      const size_t nt = s->ntile;
+      fb.stamp = stamp;
+      fb.tflag = s->tstamp;
+      fb.tdil = s->tstamp + nt * (size_t)(1 + q);
+      fb.tdiln = s->tstamp + nt * (size_t)(1 + (q ^ 1));
+      fb.tdone = s->tstamp + 3 * nt;
+      fb.listT = s->tlists;
+      fb.listD = s->tlists + nt * (size_t)(1 + q);
+      fb.listDn = s->tlists + nt * (size_t)(1 + (q ^ 1));
+      fsg::fix_counters(fb, s->tcnt);
+      s->L->markers_fix(s->g, s->buf[p], s->pulled, s->mk, s->d_sc, st, s->d_stencil,
+                        s->d_fworld, s->h_fw[p], s->h_valid[p], fb, s->d_scr[p], s->stream);
+      s->L->collide_band(s->g, s->buf[p], s->pulled, s->buf[p ^ 1], fb, s->d_sc, st,
+                         frame_on ? 1 : 0, s->d_scr[p], s->d_scr[p ^ 1], 1, s->stream);
+    } else {
+      s->L->collide_fix(s->g, s->buf[p], s->pulled, s->buf[p ^ 1], s->d_sc, st, frame_on ? 1 : 0,
+                        s->d_scr[p], s->d_scr[p ^ 1], s->stream);
     }
-    if (prof) CU(cudaEventRecord(pe[1], s->stream));
-    if (s->scr_dirty[p])
-      CU(cudaMemsetAsync(s->tickets[p], 0, sizeof(unsigned) * (fsg::TICKET_GROUPS + 1), s->stream));
-    s->L->collide_fix(s->g, s->buf[p], s->pulled, s->buf[p ^ 1], fb, s->d_sc, st, frame_on ? 1 : 0,
-                      s->fix_active ? 1 : 0, s->d_scr[p], s->d_scr[p ^ 1], s->h_scr[p],
-                      s->tickets[p], s->tickets[p ^ 1], s->stream);
     CU_LAUNCH();
     if (prof) {
-      CU(cudaEventRecord(pe[2], s->stream));
+      CU(cudaEventRecord(pe[1], s->stream));
       ++s->prof_n;
     }
     s->scr_dirty[p] = true;       // holds this step's status
@@ -833,6 +857,12 @@ int fsg_step_async(fsg_session* s) {
 }
 
 int fsg_last_status(fsg_session* s, fsg_status* st) {
+  if (s->stepped && s->L->markers_fix) {
+    // throughput path: the last step's status is still in its device
+    // scratch (the next K4 would reset it, but none is enqueued)
+    CU(cudaMemcpyAsync(s->h_scr[s->last_par], s->d_scr[s->last_par], sizeof(StepScratch),
+                       cudaMemcpyDeviceToHost, s->stream));
+  }
   CU(cudaStreamSynchronize(s->stream));
   if (!s->stepped) {
     if (st) *st = s->last;
@@ -985,7 +1015,7 @@ int fsg_get_force(fsg_session* s, double* F) {
 int fsg_profile_enable(fsg_session* s, int enable) {
   CU(cudaSetDevice(s->cfg.device));
   if (enable && s->prof_ev.empty()) {
-    s->prof_ev.resize(3 * (size_t)fsg_session::PROF_CAP);
+    s->prof_ev.resize(2 * (size_t)fsg_session::PROF_CAP);
     for (auto& e : s->prof_ev) CU(cudaEventCreate(&e));
   }
   s->prof = enable != 0;
@@ -993,18 +1023,16 @@ int fsg_profile_enable(fsg_session* s, int enable) {
   return FSG_OK;
 }
 
-int fsg_profile_read(fsg_session* s, double* markers_ms, double* collide_ms, int* steps) {
+int fsg_profile_read(fsg_session* s, double* step_ms, int* steps) {
   CU(cudaStreamSynchronize(s->stream));
-  double a = 0.0, b = 0.0;
+  double a = 0.0;
   for (int k = 0; k < s->prof_n; ++k) {
-    float t0 = 0.f, t1 = 0.f;
-    CU(cudaEventElapsedTime(&t0, s->prof_ev[3 * k], s->prof_ev[3 * k + 1]));
-    CU(cudaEventElapsedTime(&t1, s->prof_ev[3 * k + 1], s->prof_ev[3 * k + 2]));
-    a += t0;
-    b += t1;
+    float t = 0.f;
+    const cudaEvent_t* e = &s->prof_ev[2 * (size_t)k];
+    CU(cudaEventElapsedTime(&t, e[0], e[1]));
+    a += t;
   }
-  if (markers_ms) *markers_ms = a;
-  if (collide_ms) *collide_ms = b;
+  if (step_ms) *step_ms = a;
   if (steps) *steps = s->prof_n;
   s->prof_n = 0;
   return FSG_OK;

@@ -107,13 +107,16 @@ class FrameState:
     omega: np.ndarray = field(default_factory=lambda: np.zeros(3))
     alpha: np.ndarray = field(default_factory=lambda: np.zeros(3))
 
+    def packed(self) -> np.ndarray:
+        """The 19 doubles of fsg_frame_state in field order."""
+        buf = np.concatenate([np.asarray(getattr(self, n), dtype=np.float64).reshape(-1)
+                              for n in ("p", "pd", "pdd", "q", "omega", "alpha")])
+        if buf.size != 19:
+            raise ValueError("FrameState: p, pd, pdd, omega, alpha need 3 values, q needs 4")
+        return buf
+
     def to_c(self) -> _abi.fsg_frame_state:
-        c = _abi.fsg_frame_state()
-        for name in ("p", "pd", "pdd", "q", "omega", "alpha"):
-            arr = getattr(c, name)
-            for k, v in enumerate(np.asarray(getattr(self, name), dtype=np.float64)):
-                arr[k] = float(v)
-        return c
+        return _abi.fsg_frame_state.from_buffer_copy(self.packed())
 
     @classmethod
     def of(cls, c: _abi.fsg_frame_state) -> "FrameState":
@@ -129,6 +132,10 @@ class CoupledSession:
         h = C.c_void_p()
         check(L.fsg_create(C.byref(cfg.to_c()), C.byref(h)))
         self._h = h
+        self._L = L
+        self._fs_c = _abi.fsg_frame_state()
+        self._fs_ref = C.byref(self._fs_c)
+        self._fs_view = np.frombuffer(self._fs_c, dtype=np.float64)
         self.dims = tuple(int(d) for d in cfg.dims)
         self.n_cells = int(np.prod(self.dims))
         self.m = 0
@@ -216,7 +223,16 @@ class CoupledSession:
 
     # -- frame -----------------------------------------------------------
     def set_frame(self, fs: FrameState) -> None:
-        check(_abi.lib().fsg_set_frame(self._h, C.byref(fs.to_c())))
+        a = self._fs_view  # per-step path: slice copies into a reused struct
+        a[0:3] = fs.p
+        a[3:6] = fs.pd
+        a[6:9] = fs.pdd
+        a[9:13] = fs.q
+        a[13:16] = fs.omega
+        a[16:19] = fs.alpha
+        rc = self._L.fsg_set_frame(self._h, self._fs_ref)
+        if rc:
+            check(rc)
 
     def frame_state(self) -> FrameState:
         c = _abi.fsg_frame_state()
@@ -256,7 +272,9 @@ class CoupledSession:
         return StepStatus.of(st)
 
     def step_async(self) -> None:
-        check(_abi.lib().fsg_step_async(self._h))
+        rc = self._L.fsg_step_async(self._h)
+        if rc:
+            check(rc)
 
     def last_status(self) -> StepStatus:
         st = _abi.fsg_status()
@@ -292,16 +310,15 @@ class CoupledSession:
 
     # -- measurement -----------------------------------------------------------
     def profile(self, enable: bool = True) -> None:
-        """Bracket each coupled step's marker and collide kernels with CUDA events."""
+        """Bracket every step's kernels with CUDA events on the session stream."""
         check(_abi.lib().fsg_profile_enable(self._h, 1 if enable else 0))
 
     def profile_read(self):
-        """-> (marker-kernel ms, collide-kernel ms, timed steps) accumulated since enable/read."""
+        """-> (device ms of the timed steps, timed steps) accumulated since enable/read."""
         a = C.c_double()
-        b = C.c_double()
         n = C.c_int()
-        check(_abi.lib().fsg_profile_read(self._h, C.byref(a), C.byref(b), C.byref(n)))
-        return a.value, b.value, n.value
+        check(_abi.lib().fsg_profile_read(self._h, C.byref(a), C.byref(n)))
+        return a.value, n.value
 
     # -- z-slab halos ----------------------------------------------------------
     def halo_bytes(self) -> int:
