@@ -12,7 +12,8 @@ import os
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libfsg.so")
+# FSG_LIB: alternative build of the same ABI (dev A/B runs); the default is the in-tree libfsg.so
+LIB_PATH = os.environ.get("FSG_LIB") or os.path.join(HERE, "libfsg.so")
 
 FSG_OK, FSG_EINPUT, FSG_ECUDA, FSG_ESTATE = 0, 1, 2, 3
 

@@ -6,6 +6,15 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+// minimum resident 128-thread blocks per SM asked of ptxas for the
+// throughput K4 and marker kernels (register caps: 65536 / (128 * MINB))
+#ifndef FSG_K4_MINB
+#define FSG_K4_MINB 6
+#endif
+#ifndef FSG_KM_MINB
+#define FSG_KM_MINB 6
+#endif
+
 namespace fsg {
 
 // ----------------------------------------------------------------- D3Q19 --
@@ -101,7 +110,8 @@ struct StepScratch {
   int band_overflow;               // bbox exceeded band capacity
   int bbox_lo_enc[3];
   int bbox_hi_enc[3];
-  unsigned work[2];                  // banded K4: dynamic work counters (phase A, B)
+  unsigned work;                     // banded K4: phase-A dynamic work counter
+  int _pad;
 };
 constexpr int LO_BIAS = 0x40000000;
 
@@ -112,35 +122,10 @@ constexpr double FIX_SCALE = 1099511627776.0;        // 2^40
 constexpr double FIX_INV = 1.0 / 1099511627776.0;   // 2^-40
 struct FixBand {
   unsigned long long* F;     // 3 per owned cell (x + nx*(y + ny*z))
-  int tnx, tny, tnz;         // tile grid (4^3 cells per tile)
-  unsigned stamp;            // step stamp (step index + 1; 0 = never)
-  // per-tile step stamps
-  unsigned* tflag;           // touched by a stencil at this step
-  unsigned* tdil;            // predicted band of this step (previous stencils dilated by 1 cell)
-  unsigned* tdiln;           // predicted band of the next step (written by the marker kernel)
-  unsigned* tdone;           // processed by the band phase of this step
-  int* listT;                // tiles touched this step            (count *cntT)
-  int* listD;                // tiles predicted for this step      (count *cntD)
-  int* listDn;               // tiles predicted for the next step  (count *cntDn)
-  unsigned* cntT;            // the counters live in a ring of three steps, so K4 can
-  unsigned* cntD;            // zero the next step's from block 0 (no last-block
-  unsigned* cntDn;           // detection): see fix_counters()
-  unsigned* zero0;           // counters K4 of this step zeroes for later steps
-  unsigned* zero1;
+  unsigned* tflag;           // per 4^3 tile: stamp of the last step a stencil touched it
+  int tnx, tny, tnz;         // tile grid
+  unsigned stamp;            // step stamp (coupled step index + 1; 0 = never)
 };
-
-// Counter ring [6] = cntT[3] | cntD[3], indexed by stamp mod 3.  Step s: the
-// marker kernel appends to cntT[s] and cntDn = cntD[s+1]; K4 reads cntT[s],
-// cntD[s] and zeroes cntT[s+1] (next marker kernel) and cntD[s+2] (its
-// cntDn) -- both last used by steps that completed before this K4 started.
-__host__ __device__ inline void fix_counters(FixBand& fb, unsigned* ring) {
-  const unsigned s = fb.stamp;
-  fb.cntT = ring + s % 3;
-  fb.cntD = ring + 3 + s % 3;
-  fb.cntDn = ring + 3 + (s + 1) % 3;
-  fb.zero0 = ring + (s + 1) % 3;
-  fb.zero1 = ring + 3 + (s + 2) % 3;
-}
 
 __host__ __device__ __forceinline__ unsigned long long ordered_key(double v) {
 #ifdef __CUDA_ARCH__

@@ -1,59 +1,77 @@
 // fsg_ib_fix.cuh -- throughput-mode immersed boundary (fp32 session), included
 // inside namespace fsg::p32 after fsg_ib.cuh.
 //
-// One half-warp per marker does the whole reference chain of
+// One warp per marker does the whole reference chain of
 // session.hpp:113-138 (position, bounds, stencil, bare moments of the
 // stencil cells, interpolate_velocity, body velocity, direct forcing) and then
 // SPREADS its own force: every stencil contribution w * f (coupling.hpp:52-71)
 // is converted to 64-bit fixed point (2^-40) and added with an integer atomic.
 // Integer addition is associative, so the accumulated field is bit-identical
 // run to run whatever order the atomics land in -- deterministic without a
-// separate ordered-spread kernel.  Touched 4^3 tiles are flagged; K4 reads
-// (and re-zeroes) only flagged tiles.  The interpolation sum uses a fixed
-// half-warp butterfly (deterministic); the fp64 parity path keeps the
-// reference's serial order instead (fsg_ib.cuh).
+// separate ordered-spread kernel.  Touched 4^3 tiles are stamped first
+// thing; K4 reads (and re-zeroes) the force only in stamped tiles.  The
+// interpolation sum uses a fixed warp butterfly (deterministic); the fp64
+// parity path keeps the reference's serial order instead (fsg_ib.cuh).
 
 constexpr int FX_LANES = 32;     // one warp per marker
 constexpr int FX_PER_BLOCK = 4;  // markers per 128-thread block
-constexpr int FX_CPL = 2;        // stencil cells per lane per round (64 per round trip)
+constexpr int FX_CPL = 1;        // stencil cells per lane per round trip (register pressure)
 
 __device__ __forceinline__ unsigned long long to_fix(double v) {
   return (unsigned long long)__double2ll_rn(v * FIX_SCALE);
 }
 
 template <bool PULLED>
-__global__ void __launch_bounds__(128)
+__global__ void __launch_bounds__(128, FSG_KM_MINB)
     k_markers_fix(Grid g, const float* __restrict__ A, Markers mk, const SessionConsts* __restrict__ scp,
                   const StepConsts st, MarkerStencil* __restrict__ rec_out, double* __restrict__ fworld,
                   double* fworld_h, int* valid_h, FixBand fb, StepScratch* out) {
   __shared__ double phs[FX_PER_BLOCK][3][5];
-  // let the banded K4 (programmatic dependent) start its non-band cells now;
-  // it waits for this grid's completion before touching the band
-  asm volatile("griddepcontrol.launch_dependents;");
   const int hl = threadIdx.x & (FX_LANES - 1);
   const int slot = threadIdx.x / FX_LANES;
   constexpr unsigned hmask = 0xFFFFFFFFu;
   const int t = blockIdx.x * FX_PER_BLOCK + slot;
-  if (t >= mk.m) return;  // uniform over the half-warp
+  const bool live = t < mk.m;  // uniform over the warp
   const SessionConsts& sc = *scp;
-  // marker state: broadcast loads (may be mapped pinned host memory)
-  double xw[3], vel[3], nrm[3];
-#pragma unroll
-  for (int k = 0; k < 3; ++k) {
-    xw[k] = mk.pts[3 * t + k] - st.p[k];
-    vel[k] = mk.vel[3 * t + k];
-    nrm[k] = mk.nrm[3 * t + k];
-  }
-  const double area = mk.area[t];
-  double xf[3], xl[3];
-  mat_t_vec(st.R, xw, xf);
-#pragma unroll
-  for (int k = 0; k < 3; ++k) xl[k] = xf[k] / sc.dx + sc.hd[k];
   const double half = 0.5 * (sc.kernel == 0 ? 4 : 3);
-  bool ok = true;
+  // marker state: broadcast loads (may be mapped pinned host memory)
+  double xw[3] = {0.0, 0.0, 0.0}, xf[3], xl[3];
+  bool ok = false;
+  int lo[3] = {0, 0, 0}, hi[3] = {0, 0, 0}, cnt[3] = {1, 1, 1};
+  if (live) {
 #pragma unroll
-  for (int a = 0; a < 3; ++a)
-    if (xl[a] < half || xl[a] > sc.dims_g[a] - 1 - half) ok = false;  // coupling.hpp:18-24
+    for (int k = 0; k < 3; ++k) {
+      xw[k] = mk.pts[3 * t + k] - st.p[k];
+    }
+    mat_t_vec(st.R, xw, xf);
+#pragma unroll
+    for (int k = 0; k < 3; ++k) xl[k] = xf[k] / sc.dx + sc.hd[k];
+    ok = true;
+#pragma unroll
+    for (int a = 0; a < 3; ++a)
+      if (xl[a] < half || xl[a] > sc.dims_g[a] - 1 - half) ok = false;  // coupling.hpp:18-24
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      lo[a] = (int)ceil(xl[a] - half);  // kernel.hpp:36-40
+      hi[a] = (int)floor(xl[a] + half);
+      cnt[a] = hi[a] - lo[a] + 1;
+    }
+    // stamp the touched tiles (<= 2x2x2: the stencil spans <= 5 cells)
+    if (ok && hl < 8) {
+      const int tx = ((hl & 1) ? hi[0] : lo[0]) >> 2;
+      const int ty = ((hl & 2) ? hi[1] : lo[1]) >> 2;
+      const int tz = ((hl & 4) ? hi[2] - g.z0 : lo[2] - g.z0) >> 2;
+      fb.tflag[tx + fb.tnx * (ty + fb.tny * tz)] = fb.stamp;
+    }
+  }
+  // every warp's stamps are visible before this block lets the banded K4
+  // (programmatic dependent) launch: K4's first phase skips stamped tiles and
+  // waits for this grid's completion before updating them
+  __syncthreads();
+  if (threadIdx.x == 0) __threadfence();
+  __syncthreads();
+  asm volatile("griddepcontrol.launch_dependents;");
+  if (!live) return;
   if (!ok) {
     if (hl == 0) {
       rec_out[t].valid = 0;
@@ -66,13 +84,6 @@ __global__ void __launch_bounds__(128)
     }
     return;
   }
-  int lo[3], hi[3], cnt[3];
-#pragma unroll
-  for (int a = 0; a < 3; ++a) {
-    lo[a] = (int)ceil(xl[a] - half);  // kernel.hpp:36-40
-    hi[a] = (int)floor(xl[a] + half);
-    cnt[a] = hi[a] - lo[a] + 1;
-  }
   if (hl < 15) {
     const int a = hl / 5, q = hl % 5;
     const int la = a == 0 ? lo[0] : (a == 1 ? lo[1] : lo[2]);
@@ -84,7 +95,7 @@ __global__ void __launch_bounds__(128)
   const int ncell = cnt[0] * cnt[1] * cnt[2];
   const float r0 = 1.0f / (float)cnt[0], r01 = 1.0f / (float)(cnt[0] * cnt[1]);
   double a0 = 0.0, a1 = 0.0, a2 = 0.0;
-  // this lane's cells c = hl + 16 r (r < 8): gathered 4 at a time
+  // this lane's cells c = hl + 32 r: FX_CPL gathered per round trip
   for (int c0 = 0; c0 < ncell; c0 += FX_CPL * FX_LANES) {
     float sv[FX_CPL][Q];
     int cio[FX_CPL], cjo[FX_CPL], cko[FX_CPL];
@@ -120,9 +131,16 @@ __global__ void __launch_bounds__(128)
     a1 += __shfl_xor_sync(hmask, a1, o);
     a2 += __shfl_xor_sync(hmask, a2, o);
   }
-  // body velocity, direct forcing, world force (identical on every lane)
+  // body velocity, direct forcing, world force (identical on every lane);
+  // the rest of the marker state is loaded only now (register pressure)
   const double uf[3] = {a0 * sc.v2p, a1 * sc.v2p, a2 * sc.v2p};
-  double vw[3], vf[3], nf[3], fl[3], fw[3], ff[3];
+  double vel[3], nrm[3], vw[3], vf[3], nf[3], fl[3], fw[3], ff[3];
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    vel[k] = mk.vel[3 * t + k];
+    nrm[k] = mk.nrm[3 * t + k];
+  }
+  const double area = mk.area[t];
 #pragma unroll
   for (int k = 0; k < 3; ++k) vw[k] = vel[k] - st.pd[k];
   mat_t_vec(st.R, vw, vf);
@@ -167,27 +185,6 @@ __global__ void __launch_bounds__(128)
     r.valid = 1;
     r._pad = 0;
     rec_out[t] = r;
-  }
-  // stamp + list the touched tiles (this step: <= 2x2x2, the stencil spans
-  // <= 5 cells) and the tiles of the stencil dilated by one cell (predicted
-  // band of the next step: markers move < 1 cell per step)
-  if (hl < 8) {
-    const int tx = ((hl & 1) ? hi[0] : lo[0]) >> 2;
-    const int ty = ((hl & 2) ? hi[1] : lo[1]) >> 2;
-    const int tz = ((hl & 4) ? hi[2] - g.z0 : lo[2] - g.z0) >> 2;
-    const int T = tx + fb.tnx * (ty + fb.tny * tz);
-    if (atomicExch(&fb.tflag[T], fb.stamp) != fb.stamp) fb.listT[atomicAdd(fb.cntT, 1u)] = T;
-  }
-  if (hl < 27) {
-    const int ex0 = max(lo[0] - 1, 0) >> 2, ex1 = min(hi[0] + 1, g.nx - 1) >> 2;
-    const int ey0 = max(lo[1] - 1, 0) >> 2, ey1 = min(hi[1] + 1, g.ny - 1) >> 2;
-    const int ez0 = max(lo[2] - g.z0 - 1, 0) >> 2, ez1 = min(hi[2] - g.z0 + 1, g.nz - 1) >> 2;
-    const int tx = ex0 + hl % 3, ty = ey0 + (hl / 3) % 3, tz = ez0 + hl / 9;
-    if (tx <= ex1 && ty <= ey1 && tz <= ez1) {
-      const int T = tx + fb.tnx * (ty + fb.tny * tz);
-      if (atomicExch(&fb.tdiln[T], fb.stamp + 1u) != fb.stamp + 1u)
-        fb.listDn[atomicAdd(fb.cntDn, 1u)] = T;
-    }
   }
   // spread: this lane's own cells, fixed-point integer atomics
   for (int c = hl; c < ncell; c += FX_LANES) {

@@ -101,7 +101,7 @@ __device__ __forceinline__ void reset_next(StepScratch* next, int tid) {
 // Pure-fluid K4 of the throughput session (no IB band): virtual force inline,
 // collide/stream.  Persistent: work item = (xy column, chunk of zc planes).
 template <bool PULLED, bool VF>
-__global__ void __launch_bounds__(128)
+__global__ void __launch_bounds__(128, FSG_K4_MINB)
     k_collide_fix(Grid g, DirPtrs dp, const float* __restrict__ A,
                   const SessionConsts* __restrict__ scp, const StepConsts st,
                   StepScratch* __restrict__ out, StepScratch* __restrict__ next, int zc) {
@@ -127,45 +127,46 @@ __global__ void __launch_bounds__(128)
 
 // ---------------------------------------------------------------------------
 // Banded coupled K4 (one launch per step).  Launched on the session stream as
-// a programmatic dependent of the marker kernel, which triggers its
-// dependents on entry: K4 starts while the markers still run and updates
-// every cell OUTSIDE the predicted band (phase A: tiles of the previous
-// step's stencils dilated by one cell -- markers move < 1 cell per step),
-// with dynamic work fetch so blocks that land late on SMs freed by the marker
-// kernel take less.  It then waits for the marker grid (griddepcontrol.wait:
-// completion + memory visibility) and updates the union of the touched and
-// predicted tiles with the fresh IB forces (phase B).  A touched tile that
-// was not predicted (first step, recentring) is simply recomputed by phase
-// B: K4 reads A and writes B, so a recomputation is idempotent.
+// a programmatic dependent of the marker kernel, whose blocks stamp the 4^3
+// tiles their stencils touch, fence, and only then trigger their dependents
+// -- before their slow part (gathers, forcing, spread).  So K4 starts while
+// the markers still run, with every stamp of this step visible, and
+//   phase A  updates every cell outside the stamped tiles (no IB force), with
+//            dynamic work fetch (prefetched one item ahead) so blocks that
+//            land late on SMs freed by the marker kernel take less;
+//   phase B  waits for the marker grid (griddepcontrol.wait: completion +
+//            memory visibility) and updates the stamped tiles with the fresh
+//            fixed-point IB force, found by an interleaved scan of the stamps.
+// Each cell is written exactly once per step.
 
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 
 template <bool PULLED, bool VF>
-__global__ void __launch_bounds__(128)
+__global__ void __launch_bounds__(128, FSG_K4_MINB)
     k_collide_band(Grid g, DirPtrs dp, const float* __restrict__ A, FixBand fb,
                    const SessionConsts* __restrict__ scp, const StepConsts st,
                    StepScratch* __restrict__ out, StepScratch* __restrict__ next, int zc) {
   __shared__ int item;
-  __shared__ int take[2];
+  __shared__ int tl[128];
+  __shared__ int ntl;
   const int tid = threadIdx.x + blockDim.x * threadIdx.y;
   reset_next(next, tid);
-  if (blockIdx.x == 0 && tid == 0) {  // counter ring: see fix_counters()
-    *fb.zero0 = 0u;
-    *fb.zero1 = 0u;
-  }
   const SessionConsts& sc = *scp;
-  // ---- phase A: cells outside the predicted band (no IB force)
   const int tx_n = (g.nx + blockDim.x - 1) / blockDim.x;
   const int ty_n = (g.ny + blockDim.y - 1) / blockDim.y;
   const int ncol = tx_n * ty_n, nzc = (g.nz + zc - 1) / zc;
   const int nitem = ncol * nzc;
+  int nxt = 0;
+  if (tid == 0) nxt = (int)atomicAdd(&out->work, 1u);
+  // ---- phase A: cells outside the stamped tiles (no IB force)
   float vmin = FLT_MAX;
   for (;;) {
-    if (tid == 0) item = (int)atomicAdd(&out->work[0], 1u);
+    if (tid == 0) item = nxt;
     __syncthreads();
     const int it = item;
     __syncthreads();
     if (it >= nitem) break;
+    if (tid == 0) nxt = (int)atomicAdd(&out->work, 1u);  // consumed next iteration
     const int col = it % ncol, zk = it / ncol;
     const int x = (col % tx_n) * blockDim.x + threadIdx.x;
     const int y = (col / tx_n) * blockDim.y + threadIdx.y;
@@ -173,43 +174,43 @@ __global__ void __launch_bounds__(128)
     if (x >= g.nx || y >= g.ny) continue;
     const int trow = (x >> 2) + fb.tnx * (y >> 2);
     for (int z = z0; z < z1; ++z) {
-      if (fb.tdil[trow + fb.tnx * fb.tny * (z >> 2)] == fb.stamp) continue;  // predicted band
+      if (__ldcg(fb.tflag + trow + fb.tnx * fb.tny * (z >> 2)) == fb.stamp) continue;  // band: phase B
       vmin = fminf(vmin, cell_update<PULLED, VF>(g, dp, A, x, y, z, 0.f, 0.f, 0.f, sc, st, out));
     }
   }
-  // ---- phase B: touched + predicted tiles, after the marker grid completed
+  // ---- phase B: the stamped tiles, after the marker grid completed.  Block b
+  // scans tiles b, b + G, b + 2G ... (G = gridDim.x), one per thread per
+  // chunk, so a body's clustered tiles spread over all blocks; each 64
+  // threads take one stamped tile per pass.
   pdl_wait();
-  const int nT = (int)*(volatile unsigned*)fb.cntT, nD = (int)*(volatile unsigned*)fb.cntD;
-  const int half = tid >> 6, lt = tid & 63;  // two 4^3 tiles per fetch
-  for (;;) {
-    if (tid == 0) item = (int)atomicAdd(&out->work[1], 2u);
+  const int ntile = fb.tnx * fb.tny * fb.tnz;
+  const int nthr = blockDim.x * blockDim.y;  // 96 or 128 (cell_block)
+  const int tpp = nthr >> 6;                 // tiles per pass (64 threads each)
+  const int half = tid >> 6, lt = tid & 63;
+  for (int base = 0; (long long)base * gridDim.x < ntile; base += nthr) {
+    if (tid == 0) ntl = 0;
     __syncthreads();
-    const int e = item + half;
+    const long long T0 = (long long)blockIdx.x + (long long)gridDim.x * (base + tid);
+    if (T0 < ntile && fb.tflag[T0] == fb.stamp) tl[atomicAdd(&ntl, 1)] = (int)T0;
     __syncthreads();
-    if (e - half >= nT + nD) break;  // block-uniform
-    const int T = e >= nT + nD ? -1 : (e < nT ? fb.listT[e] : fb.listD[e - nT]);
-    // a tile listed twice (touched and predicted) is processed once: lane 0
-    // of the half claims it
-    if (lt == 0) take[half] = T >= 0 && atomicExch(&fb.tdone[T], fb.stamp) != fb.stamp;
-    __syncthreads();
-    const bool go = take[half];
-    __syncthreads();
-    if (!go) continue;
-    const int tx = T % fb.tnx, ty = (T / fb.tnx) % fb.tny, tz = T / (fb.tnx * fb.tny);
-    const int x = 4 * tx + (lt & 3), y = 4 * ty + ((lt >> 2) & 3), z = 4 * tz + (lt >> 4);
-    if (x >= g.nx || y >= g.ny || z >= g.nz) continue;
-    float Fx = 0.f, Fy = 0.f, Fz = 0.f;
-    if (fb.tflag[T] == fb.stamp) {  // consume and re-zero the fixed-point force
+    const int n = half < tpp ? ntl : 0;
+    for (int k = half; k < n; k += tpp) {
+      const int T = tl[k];
+      const int tx = T % fb.tnx, ty = (T / fb.tnx) % fb.tny, tz = T / (fb.tnx * fb.tny);
+      const int x = 4 * tx + (lt & 3), y = 4 * ty + ((lt >> 2) & 3), z = 4 * tz + (lt >> 4);
+      if (x >= g.nx || y >= g.ny || z >= g.nz) continue;
+      // consume and re-zero the fixed-point force
       unsigned long long* F = fb.F + 3 * ((long long)x + (long long)g.nx * ((long long)y + (long long)g.ny * z));
       const long long f0 = (long long)F[0], f1 = (long long)F[1], f2 = (long long)F[2];
       F[0] = 0ull;
       F[1] = 0ull;
       F[2] = 0ull;
-      Fx = (float)((double)f0 * FIX_INV);
-      Fy = (float)((double)f1 * FIX_INV);
-      Fz = (float)((double)f2 * FIX_INV);
+      const float Fx = (float)((double)f0 * FIX_INV);
+      const float Fy = (float)((double)f1 * FIX_INV);
+      const float Fz = (float)((double)f2 * FIX_INV);
+      vmin = fminf(vmin, cell_update<PULLED, VF>(g, dp, A, x, y, z, Fx, Fy, Fz, sc, st, out));
     }
-    vmin = fminf(vmin, cell_update<PULLED, VF>(g, dp, A, x, y, z, Fx, Fy, Fz, sc, st, out));
+    __syncthreads();
   }
   report_min(out, vmin == FLT_MAX ? DBL_MAX : (double)vmin);
 }

@@ -150,12 +150,7 @@ struct fsg_session {
   fsg_status last{};
   // throughput (fp32) IB: fixed-point tile band
   fsg::FixBand fix{};
-  // banded step: per-tile step stamps, tile lists, counter ring
-  unsigned* tstamp = nullptr;  // [4 * ntile]: tflag | tdil[2] | tdone
-  int* tlists = nullptr;       // [3 * ntile]: listT | listD[2]
-  unsigned* tcnt = nullptr;    // [6]: cntT[3] | cntD[3] (fix_counters)
-  unsigned stamp = 0;          // step stamp (step index + 1)
-  size_t ntile = 0;
+  unsigned stamp = 0;          // coupled step stamp (fix.tflag)
   bool scr_dirty[2] = {false, false};  // d_scr[k] not known to be zero
   StepConsts last_st{};     // frame constants of the last step (diagnostics)
   StepScratch* d_diag = nullptr;
@@ -490,12 +485,8 @@ int fsg_create(const fsg_config* cfg_in, fsg_session** out) {
     const size_t ntile = (size_t)fb.tnx * fb.tny * fb.tnz;
     CUF(cudaMalloc(&fb.F, sizeof(unsigned long long) * 3 * (size_t)g.n));
     CUF(cudaMemsetAsync(fb.F, 0, sizeof(unsigned long long) * 3 * (size_t)g.n, s->stream));
-    s->ntile = ntile;
-    CUF(cudaMalloc(&s->tstamp, sizeof(unsigned) * 4 * ntile));
-    CUF(cudaMemsetAsync(s->tstamp, 0, sizeof(unsigned) * 4 * ntile, s->stream));
-    CUF(cudaMalloc(&s->tlists, sizeof(int) * 3 * ntile));
-    CUF(cudaMalloc(&s->tcnt, sizeof(unsigned) * 6));
-    CUF(cudaMemsetAsync(s->tcnt, 0, sizeof(unsigned) * 6, s->stream));
+    CUF(cudaMalloc(&fb.tflag, sizeof(unsigned) * ntile));
+    CUF(cudaMemsetAsync(fb.tflag, 0, sizeof(unsigned) * ntile, s->stream));
   }
   s->L->fill_rest(g, s->A(), s->stream);
   if (cudaGetLastError() != cudaSuccess) return fail(set_err(FSG_ECUDA, "fill_rest launch failed"));
@@ -533,9 +524,7 @@ int fsg_destroy(fsg_session* s) {
   cudaFree(s->d_fworld);
   cudaFree(s->band.F);
   cudaFree(s->fix.F);
-  cudaFree(s->tstamp);
-  cudaFree(s->tlists);
-  cudaFree(s->tcnt);
+  cudaFree(s->fix.tflag);
   cudaFree(s->d_diag);
   cudaFree(s->d_tmp);
   cudaFree(s->d_red);
@@ -812,18 +801,7 @@ int fsg_step_async(fsg_session* s) {
       // fixed-point force field is consumed (re-zeroed) by that K4, so a step
       // without markers is the plain fluid K4 below.
       fsg::FixBand fb = s->fix;
-      const unsigned stamp = ++s->stamp;
-      const int q = (int)(stamp & 1u);
-      const size_t nt = s->ntile;
-      fb.stamp = stamp;
-      fb.tflag = s->tstamp;
-      fb.tdil = s->tstamp + nt * (size_t)(1 + q);
-      fb.tdiln = s->tstamp + nt * (size_t)(1 + (q ^ 1));
-      fb.tdone = s->tstamp + 3 * nt;
-      fb.listT = s->tlists;
-      fb.listD = s->tlists + nt * (size_t)(1 + q);
-      fb.listDn = s->tlists + nt * (size_t)(1 + (q ^ 1));
-      fsg::fix_counters(fb, s->tcnt);
+      fb.stamp = ++s->stamp;
       s->L->markers_fix(s->g, s->buf[p], s->pulled, s->mk, s->d_sc, st, s->d_stencil,
                         s->d_fworld, s->h_fw[p], s->h_valid[p], fb, s->d_scr[p], s->stream);
       s->L->collide_band(s->g, s->buf[p], s->pulled, s->buf[p ^ 1], fb, s->d_sc, st,

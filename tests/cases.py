@@ -151,6 +151,7 @@ def marker_state(case, step):
     dt = case["units"]["dt"]
     t = step * dt
     shift = np.array([0.004 * math.sin(20 * t), 0.002 * math.cos(15 * t), 0.0])
+    shift = shift + np.asarray(case.get("jumps", {}).get(step, (0.0, 0.0, 0.0)))  # teleports
     vel = np.tile([0.08 * math.cos(20 * t), -0.03 * math.sin(15 * t), 0.01], (len(case["area"]), 1))
     return (np.ascontiguousarray(case["pts0"] + shift), np.ascontiguousarray(vel),
             np.ascontiguousarray(case["nrm"]), np.ascontiguousarray(case["area"]))
