@@ -161,12 +161,28 @@ int fsg_profile_enable(fsg_session* s, int enable);
 int fsg_profile_read(fsg_session* s, double* step_ms, int* steps);
 
 /* ---- z-slab halo exchange ------------------------------
- * In a slab session the 5 populations that cross each z face are packed into
- * a caller-visible device buffer after each step and the neighbour's planes
- * are unpacked from it before the next step.  Sizes in bytes. */
+ * A slab session (cfg.z_offset / cfg.nz_global) owns planes [z_offset,
+ * z_offset + dims[2]) of a global grid plus one halo plane per side.  Per
+ * step, the 5 populations that cross each z face (5 * nx * ny elements per
+ * face) go to the neighbour slab:
+ *   fsg_step_async  updates the two boundary planes first, packs them into the
+ *                   session's send buffers, then updates the interior planes;
+ *   fsg_halo_begin  makes comm_stream wait until those planes are packed;
+ *                   the caller moves send_hi -> upper neighbour's recv_lo and
+ *                   send_lo -> lower neighbour's recv_hi on comm_stream (NCCL
+ *                   or peer copies), overlapping the interior update;
+ *   fsg_halo_end    makes the session stream wait for comm_stream and unpacks
+ *                   the received planes (have_lo/have_hi: a neighbour exists)
+ *                   into the halo before the next step.
+ * fsg_halo_pack/unpack are the unordered primitives on the current state
+ * (caller buffers).  Sizes in bytes. */
 size_t fsg_halo_bytes(fsg_session* s);
 int fsg_halo_pack(fsg_session* s, void* d_send_lo, void* d_send_hi);
 int fsg_halo_unpack(fsg_session* s, const void* d_recv_lo, const void* d_recv_hi);
+int fsg_halo_buffers(fsg_session* s, void** d_send_lo, void** d_send_hi, void** d_recv_lo,
+                     void** d_recv_hi);
+int fsg_halo_begin(fsg_session* s, void* comm_stream);
+int fsg_halo_end(fsg_session* s, void* comm_stream, int have_lo, int have_hi);
 
 #ifdef __cplusplus
 }

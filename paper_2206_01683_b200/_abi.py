@@ -88,6 +88,10 @@ SIGNATURES = {
     "fsg_halo_bytes": (C.c_size_t, [_vp]),
     "fsg_halo_pack": (C.c_int, [_vp, _vp, _vp]),
     "fsg_halo_unpack": (C.c_int, [_vp, _vp, _vp]),
+    "fsg_halo_buffers": (C.c_int, [_vp, C.POINTER(_vp), C.POINTER(_vp), C.POINTER(_vp),
+                                   C.POINTER(_vp)]),
+    "fsg_halo_begin": (C.c_int, [_vp, _vp]),
+    "fsg_halo_end": (C.c_int, [_vp, _vp, C.c_int, C.c_int]),
 }
 
 _lib = None

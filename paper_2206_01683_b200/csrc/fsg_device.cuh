@@ -212,10 +212,11 @@ struct Launchers {
   void (*markers_fix)(const Grid&, const void* A, int pulled, Markers, const SessionConsts*,
                       const StepConsts& st, MarkerStencil*, double* fworld, double* fworld_host,
                       int* valid_host, FixBand, StepScratch*, cudaStream_t);
-  // pure-fluid step (no IB band)
+  // pure-fluid step (no IB band); planes: 0 all, 1 the two z-boundary planes,
+  // 2 the interior planes (z-slab step: boundary first, halo send, interior)
   void (*collide_fix)(const Grid&, const void* A, int pulled, void* B, const SessionConsts*,
                       const StepConsts& st, int frame_on, StepScratch* scr, StepScratch* scr_next,
-                      cudaStream_t);
+                      int planes, cudaStream_t);
   // banded coupled step: one K4 launch, a programmatic dependent (pdl != 0)
   // of the marker kernel launched just before it on the same stream
   void (*collide_band)(const Grid&, const void* A, int pulled, void* B, FixBand,

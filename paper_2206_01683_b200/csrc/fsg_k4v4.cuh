@@ -99,17 +99,24 @@ __device__ __forceinline__ void reset_next(StepScratch* next, int tid) {
 }
 
 // Pure-fluid K4 of the throughput session (no IB band): virtual force inline,
-// collide/stream.  Persistent: work item = (xy column, chunk of zc planes).
+// collide/stream.  Persistent: work item = (xy column, chunk of zc planes)
+// over the planes z = zr.lo + q * zr.step < zr.hi (all planes; or, in a z-slab
+// step, the two boundary planes first and the interior behind the halo send).
+struct ZRange {
+  int lo, hi, step;
+};
+
 template <bool PULLED, bool VF>
 __global__ void __launch_bounds__(128, FSG_K4_MINB)
     k_collide_fix(Grid g, DirPtrs dp, const float* __restrict__ A,
                   const SessionConsts* __restrict__ scp, const StepConsts st,
-                  StepScratch* __restrict__ out, StepScratch* __restrict__ next, int zc) {
+                  StepScratch* __restrict__ out, StepScratch* __restrict__ next, int zc, ZRange zr) {
   const int tid = threadIdx.x + blockDim.x * threadIdx.y;
   reset_next(next, tid);
   const int tx_n = (g.nx + blockDim.x - 1) / blockDim.x;
   const int ty_n = (g.ny + blockDim.y - 1) / blockDim.y;
-  const int ncol = tx_n * ty_n, nzc = (g.nz + zc - 1) / zc;
+  const int nq = (zr.hi - zr.lo + zr.step - 1) / zr.step;
+  const int ncol = tx_n * ty_n, nzc = (nq + zc - 1) / zc;
   const int nitem = ncol * nzc;
   const SessionConsts& sc = *scp;
   float vmin = FLT_MAX;
@@ -117,10 +124,11 @@ __global__ void __launch_bounds__(128, FSG_K4_MINB)
     const int col = it % ncol, zk = it / ncol;
     const int x = (col % tx_n) * blockDim.x + threadIdx.x;
     const int y = (col / tx_n) * blockDim.y + threadIdx.y;
-    const int z0 = zk * zc, z1 = min(g.nz, z0 + zc);
+    const int q0 = zk * zc, q1 = min(nq, q0 + zc);
     if (x >= g.nx || y >= g.ny) continue;
-    for (int z = z0; z < z1; ++z)
-      vmin = fminf(vmin, cell_update<PULLED, VF>(g, dp, A, x, y, z, 0.f, 0.f, 0.f, sc, st, out));
+    for (int q = q0; q < q1; ++q)
+      vmin = fminf(vmin, cell_update<PULLED, VF>(g, dp, A, x, y, zr.lo + q * zr.step, 0.f, 0.f, 0.f,
+                                                 sc, st, out));
   }
   report_min(out, vmin == FLT_MAX ? DBL_MAX : (double)vmin);
 }

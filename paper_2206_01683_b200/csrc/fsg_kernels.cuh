@@ -819,14 +819,20 @@ static void L_markers_fix(const Grid& g, const void* A, int pulled, Markers mk,
 }
 static void L_collide_fix(const Grid& g, const void* A, int pulled, void* B,
                           const SessionConsts* sc, const StepConsts& st, int frame_on,
-                          StepScratch* scr, StepScratch* scr_next, cudaStream_t s) {
+                          StepScratch* scr, StepScratch* scr_next, int planes, cudaStream_t s) {
   DirPtrs dp;
   for (int i = 0; i < Q; ++i) {
     dp.a[i] = (const float*)A + (pulled ? g.pull[i] : g.own[i]);
     dp.b[i] = (float*)B + g.own[i];
   }
+  // planes: 0 all, 1 the two boundary planes (z-slab), 2 the interior planes
+  ZRange zr{0, g.nz, 1};
+  if (planes == 1) zr = ZRange{0, g.nz, std::max(1, g.nz - 1)};
+  if (planes == 2) zr = ZRange{1, g.nz - 1, 1};
+  const int nq = (zr.hi - zr.lo + zr.step - 1) / zr.step;
+  if (nq <= 0) return;
   const dim3 b = cell_block(g), g3 = cell_grid(g, b);
-  const long long ntile = (long long)g3.x * g3.y * g3.z;
+  const long long ntile = (long long)g3.x * g3.y * nq;
   static int resident = 0;  // blocks of k_collide_fix resident per SM (same for all variants)
   static int nsm = 0;
   if (!resident) {
@@ -841,9 +847,9 @@ static void L_collide_fix(const Grid& g, const void* A, int pulled, void* B,
   // z chunk: ~8 work items per resident block for balance
   const long long ncol = (long long)g3.x * g3.y;
   const long long nzc_want = (8 * grid + ncol - 1) / ncol;
-  const int zc = (int)std::max<long long>(1, g.nz / std::max<long long>(1, nzc_want));
+  const int zc = (int)std::max<long long>(1, nq / std::max<long long>(1, nzc_want));
 #define FSG_LF(P, V) \
-  k_collide_fix<P, V><<<gr, b, 0, s>>>(g, dp, (const float*)A, sc, st, scr, scr_next, zc)
+  k_collide_fix<P, V><<<gr, b, 0, s>>>(g, dp, (const float*)A, sc, st, scr, scr_next, zc, zr)
   if (pulled) {
     if (frame_on) FSG_LF(true, true);
     else FSG_LF(true, false);

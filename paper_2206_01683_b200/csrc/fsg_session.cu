@@ -151,6 +151,11 @@ struct fsg_session {
   // throughput (fp32) IB: fixed-point tile band
   fsg::FixBand fix{};
   unsigned stamp = 0;          // coupled step stamp (fix.tflag)
+  // z-slab halo exchange: session-owned device planes and the event after
+  // which this step's boundary planes are packed
+  void* d_hsend[2] = {nullptr, nullptr};  // lo, hi
+  void* d_hrecv[2] = {nullptr, nullptr};
+  cudaEvent_t ev_hpack = nullptr, ev_hrecv = nullptr;
   bool scr_dirty[2] = {false, false};  // d_scr[k] not known to be zero
   StepConsts last_st{};     // frame constants of the last step (diagnostics)
   StepScratch* d_diag = nullptr;
@@ -488,6 +493,16 @@ int fsg_create(const fsg_config* cfg_in, fsg_session** out) {
     CUF(cudaMalloc(&fb.tflag, sizeof(unsigned) * ntile));
     CUF(cudaMemsetAsync(fb.tflag, 0, sizeof(unsigned) * ntile, s->stream));
   }
+  if (g.zpad) {
+    const size_t hb = (size_t)5 * g.plane * s->L->elem_bytes;
+    for (int k = 0; k < 2; ++k) {
+      CUF(cudaMalloc(&s->d_hsend[k], hb));
+      CUF(cudaMalloc(&s->d_hrecv[k], hb));
+    }
+    CUF(cudaEventCreateWithFlags(&s->ev_hpack, cudaEventDisableTiming));
+    CUF(cudaEventCreateWithFlags(&s->ev_hrecv, cudaEventDisableTiming));
+    CUF(cudaEventRecord(s->ev_hpack, s->stream));
+  }
   s->L->fill_rest(g, s->A(), s->stream);
   if (cudaGetLastError() != cudaSuccess) return fail(set_err(FSG_ECUDA, "fill_rest launch failed"));
   if (cudaStreamSynchronize(s->stream) != cudaSuccess)
@@ -525,6 +540,12 @@ int fsg_destroy(fsg_session* s) {
   cudaFree(s->band.F);
   cudaFree(s->fix.F);
   cudaFree(s->fix.tflag);
+  for (int k = 0; k < 2; ++k) {
+    cudaFree(s->d_hsend[k]);
+    cudaFree(s->d_hrecv[k]);
+  }
+  if (s->ev_hpack) cudaEventDestroy(s->ev_hpack);
+  if (s->ev_hrecv) cudaEventDestroy(s->ev_hrecv);
   cudaFree(s->d_diag);
   cudaFree(s->d_tmp);
   cudaFree(s->d_red);
@@ -722,6 +743,9 @@ int fsg_recenter(fsg_session* s, const int shift[3]) {
 // -------------------------------------------------------------- markers --
 static int set_markers_common(fsg_session* s, int n_bodies, const int64_t* off) {
   if (n_bodies < 0) return set_err(FSG_EINPUT, "negative body count");
+  if (n_bodies > 0 && s->g.zpad)
+    return set_err(FSG_EINPUT, "IB markers on a z-slab session are not supported (the sharded "
+                               "config is pure LBM, SURVEY.md 8(e))");
   if (n_bodies > 0 && !off) return set_err(FSG_EINPUT, "null body offsets");
   const int64_t m = n_bodies > 0 ? off[n_bodies] : 0;
   if (n_bodies > 0 && off[0] != 0) return set_err(FSG_EINPUT, "body_offsets[0] must be 0");
@@ -806,9 +830,18 @@ int fsg_step_async(fsg_session* s) {
                         s->d_fworld, s->h_fw[p], s->h_valid[p], fb, s->d_scr[p], s->stream);
       s->L->collide_band(s->g, s->buf[p], s->pulled, s->buf[p ^ 1], fb, s->d_sc, st,
                          frame_on ? 1 : 0, s->d_scr[p], s->d_scr[p ^ 1], 1, s->stream);
+    } else if (s->g.zpad) {
+      // z-slab: the two boundary planes first, packed for the neighbours
+      // (fsg_halo_begin lets a comm stream start on them), then the interior
+      s->L->collide_fix(s->g, s->buf[p], s->pulled, s->buf[p ^ 1], s->d_sc, st, frame_on ? 1 : 0,
+                        s->d_scr[p], s->d_scr[p ^ 1], 1, s->stream);
+      s->L->halo_pack(s->g, s->buf[p ^ 1], s->d_hsend[0], s->d_hsend[1], s->stream);
+      CU(cudaEventRecord(s->ev_hpack, s->stream));
+      s->L->collide_fix(s->g, s->buf[p], s->pulled, s->buf[p ^ 1], s->d_sc, st, frame_on ? 1 : 0,
+                        s->d_scr[p], s->d_scr[p ^ 1], 2, s->stream);
     } else {
       s->L->collide_fix(s->g, s->buf[p], s->pulled, s->buf[p ^ 1], s->d_sc, st, frame_on ? 1 : 0,
-                        s->d_scr[p], s->d_scr[p ^ 1], s->stream);
+                        s->d_scr[p], s->d_scr[p ^ 1], 0, s->stream);
     }
     CU_LAUNCH();
     if (prof) {
@@ -820,6 +853,10 @@ int fsg_step_async(fsg_session* s) {
   } else {
     int rc = launch_step(s, p, copy_mk, frame_on);
     if (rc) return rc;
+    if (s->g.zpad) {  // parity mode: the whole step, then the planes for the neighbours
+      s->L->halo_pack(s->g, s->buf[p ^ 1], s->d_hsend[0], s->d_hsend[1], s->stream);
+      CU(cudaEventRecord(s->ev_hpack, s->stream));
+    }
   }
   CU(cudaEventRecord(s->ev[p], s->stream));
   if (s->mk_host && s->mk_slot >= 0) CU(cudaEventRecord(s->ev_mk[s->mk_slot], s->stream));
@@ -1032,6 +1069,36 @@ int fsg_halo_unpack(fsg_session* s, const void* lo, const void* hi) {
   CU(cudaSetDevice(s->cfg.device));
   s->L->halo_unpack(s->g, s->A(), lo, hi, s->stream);
   CU_LAUNCH();
+  return FSG_OK;
+}
+
+int fsg_halo_buffers(fsg_session* s, void** send_lo, void** send_hi, void** recv_lo,
+                     void** recv_hi) {
+  if (!s->g.zpad) return set_err(FSG_EINPUT, "not a z-slab session");
+  if (send_lo) *send_lo = s->d_hsend[0];
+  if (send_hi) *send_hi = s->d_hsend[1];
+  if (recv_lo) *recv_lo = s->d_hrecv[0];
+  if (recv_hi) *recv_hi = s->d_hrecv[1];
+  return FSG_OK;
+}
+
+int fsg_halo_begin(fsg_session* s, void* comm_stream) {
+  if (!s->g.zpad) return set_err(FSG_EINPUT, "not a z-slab session");
+  CU(cudaSetDevice(s->cfg.device));
+  CU(cudaStreamWaitEvent((cudaStream_t)comm_stream, s->ev_hpack, 0));
+  return FSG_OK;
+}
+
+int fsg_halo_end(fsg_session* s, void* comm_stream, int have_lo, int have_hi) {
+  if (!s->g.zpad) return set_err(FSG_EINPUT, "not a z-slab session");
+  CU(cudaSetDevice(s->cfg.device));
+  CU(cudaEventRecord(s->ev_hrecv, (cudaStream_t)comm_stream));
+  CU(cudaStreamWaitEvent(s->stream, s->ev_hrecv, 0));
+  if (have_lo || have_hi) {
+    s->L->halo_unpack(s->g, s->A(), have_lo ? s->d_hrecv[0] : nullptr,
+                      have_hi ? s->d_hrecv[1] : nullptr, s->stream);
+    CU_LAUNCH();
+  }
   return FSG_OK;
 }
 

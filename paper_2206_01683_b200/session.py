@@ -329,3 +329,17 @@ class CoupledSession:
 
     def halo_unpack(self, d_recv_lo: int | None, d_recv_hi: int | None) -> None:
         check(_abi.lib().fsg_halo_unpack(self._h, d_recv_lo, d_recv_hi))
+
+    def halo_buffers(self):
+        """-> device pointers (send_lo, send_hi, recv_lo, recv_hi), halo_bytes() each."""
+        p = [C.c_void_p() for _ in range(4)]
+        check(_abi.lib().fsg_halo_buffers(self._h, *(C.byref(x) for x in p)))
+        return tuple(int(x.value or 0) for x in p)
+
+    def halo_begin(self, comm_stream: int) -> None:
+        """comm_stream waits until this step's boundary planes are packed."""
+        check(_abi.lib().fsg_halo_begin(self._h, comm_stream))
+
+    def halo_end(self, comm_stream: int, have_lo: bool, have_hi: bool) -> None:
+        """The session waits for comm_stream, then unpacks the received planes."""
+        check(_abi.lib().fsg_halo_end(self._h, comm_stream, int(have_lo), int(have_hi)))
