@@ -22,8 +22,11 @@ time.
 
 Workloads (BASELINE.json configs): c1 64^3 sphere, c2 128x64x64 koi in an
 accelerating frame (default, configs[1]), c3 256x128x128 two-koi school,
-c5 96x48x48 env.  Under torchrun every rank runs an independent replica
-(weak scaling, no data-path collective).
+c4 512^3 pure LBM z-slab-decomposed over the ranks (NCCL halo exchange of the
+boundary planes overlapped with the interior update; weak scaling: 512^3 per
+rank, or --c4-scaling strong), c5 96x48x48 env.  Under torchrun the other
+workloads run one independent replica per rank (weak scaling, no data-path
+collective).
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
                   [--workload c2] [--no-cpu-baseline]
@@ -51,7 +54,9 @@ def parse_args():
     ap.add_argument("--steps", type=int, default=1000)
     ap.add_argument("--warmup", type=int, default=20)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="c2", choices=["c1", "c2", "c3", "c5"])
+    ap.add_argument("--workload", default="c2", choices=["c1", "c2", "c3", "c4", "c5"])
+    ap.add_argument("--c4-scaling", default="weak", choices=["weak", "strong"],
+                    help="c4: each rank owns 512^3 (weak) or one 512^3 grid is split (strong)")
     ap.add_argument("--e2e-steps", type=int, default=100)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
@@ -190,6 +195,100 @@ def cpu_reference_mlups(scene, seconds: float, max_steps: int = 400):
     cores = int(os.environ.get("OMP_NUM_THREADS", os.cpu_count() or 1))
     return {"value": scene.n_cells * n / dt / 1e6, "unit": "MLUPS", "cores": cores, "kind": kind,
             "sample": f"{n} coupled steps of {scene.name} ({dt:.1f} s wall, fp64, OpenMP)"}
+
+
+# --------------------------------------------------- ours: z-slab (c4) ---
+def run_slab(args, scene, rank, local, world):
+    """c4: pure LBM on a 512^2 x NZ grid split into z-slabs, one per rank, with
+    the boundary-plane halo exchange over NCCL overlapped with the interior
+    update (paper_2206_01683_b200/slab.py).  Fluid at rest (the per-cell work
+    does not depend on the state); the 20 GB per rank exceed L2 by ~160x."""
+    import torch
+    from paper_2206_01683_b200.slab import SlabLayout, SlabRunner
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    nx, ny, nz = scene.dims
+    NZ = nz * world if args.c4_scaling == "weak" else nz
+    L = SlabLayout(NZ, world, periodic=False)
+    run = SlabRunner(dict(dims=(nx, ny, NZ), dx=scene.dx, dt=scene.dt, rho=scene.rho, nu=scene.nu,
+                          frame_mode="none", precision="fp32", device=local, max_markers=1), L, rank)
+    s = run.session
+    stream = torch.cuda.ExternalStream(s.stream, device=dev)
+    W, K = args.warmup, args.steps
+
+    def barrier():
+        if world > 1:
+            import torch.distributed as dist
+            dist.barrier()
+
+    def max_over_ranks(v):
+        if world == 1:
+            return v
+        import torch.distributed as dist
+        t = torch.tensor([v], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    for _ in range(W):
+        run.step_async()
+    st = s.last_status()
+    torch.cuda.synchronize(dev)
+    barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        time.sleep(0.4)
+        e0.record(stream)
+        for _ in range(K):
+            run.step_async()
+        e1.record(stream)
+        torch.cuda.synchronize(dev)
+        time.sleep(0.15)
+    st = s.last_status()
+    t_total = max_over_ranks(e0.elapsed_time(e1) / 1e3)
+    total_cells = nx * ny * NZ
+    value = total_cells * K / t_total / 1e6
+    # e2e: the public per-step call with the status read back every step
+    E = min(args.e2e_steps, K)
+    barrier()
+    t0 = time.perf_counter()
+    for _ in range(E):
+        run.step_async()
+        s.last_status()
+    e2e_t = max_over_ranks(time.perf_counter() - t0)
+    run.close()
+    peak, peak_src = measured_peaks()
+    local_cells = nx * ny * run.nz
+    achieved = BYTES_PER_CELL * local_cells / (t_total / K) / 1e9
+    halo_mb = 2 * 5 * nx * ny * 4 / 1e6 if world > 1 else 0.0
+    return {
+        "metric": METRIC, "value": round(value, 1), "unit": "MLUPS", "n_gpus": world,
+        "steps": K, "warmup": W, "ms_per_step": round(t_total / K * 1e3, 4), "higher_is_better": True,
+        "scaling": args.c4_scaling, "vs_baseline": None, "dtype": "f32 (fp32 storage of f - w_i)",
+        "data": "synthetic (fluid at rest, pure LBM; SURVEY.md §8(d) C4)",
+        "config": {"workload": scene.name, "dims": [nx, ny, NZ], "markers": 0, "frame": "none",
+                   "l2": f"state {BYTES_PER_CELL * local_cells / 2 / 1e9:.1f} GB per rank >> L2 (no flush)",
+                   "parallelism": f"z-slabs x{world} ({args.c4_scaling}), NCCL halo {halo_mb:.1f} MB/step/rank"
+                   if world > 1 else "single GPU"},
+        "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                     "frac": round(achieved / peak, 4), "traffic": None,
+                     "kernel": "k_collide_fix (boundary planes + interior; per GPU)",
+                     "peak_source": peak_src},
+        "e2e": {"value": round(total_cells * E / e2e_t / 1e6, 1), "unit": "MLUPS",
+                "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 56, "steps": E},
+        "gpu_launches": K * (4 if world > 1 else 1),
+        "status": {"stable": bool(st.stable()), "min_f": st.min_f},
+        "clocks": clk.summary(),
+    }
+
+
+def cpu_sample_scene(scene):
+    """The CPU baseline's bounded sample: c4 (40 GB in fp64) is timed on a
+    128^3 stand-in with identical per-cell work."""
+    if scene.m == 0 and scene.n_cells > (1 << 22):
+        import dataclasses
+        return dataclasses.replace(scene, name=scene.name + " [CPU sample: 128^3 stand-in]",
+                                   dims=(128, 128, 128))
+    return scene
 
 
 # ------------------------------------------------------------------ ours ---
@@ -378,7 +477,7 @@ def main():
     if args.impl == "reference":
         if rank != 0:
             return
-        cb = cpu_reference_mlups(scene, seconds=max(5.0, args.cpu_seconds))
+        cb = cpu_reference_mlups(cpu_sample_scene(scene), seconds=max(5.0, args.cpu_seconds))
         out = {"metric": METRIC, "value": round(cb["value"], 3), "unit": "MLUPS", "n_gpus": world,
                "steps": args.steps, "warmup": args.warmup, "higher_is_better": True,
                "scaling": "weak", "vs_baseline": None, "dtype": "f64", "impl": "reference",
@@ -394,10 +493,13 @@ def main():
         import torch.distributed as dist
         torch.cuda.set_device(local)
         dist.init_process_group("nccl")
-    out = run_ours(args, scene, rank, local, world)
+    if args.workload == "c4":
+        out = run_slab(args, scene, rank, local, world)
+    else:
+        out = run_ours(args, scene, rank, local, world)
     if rank == 0:
         if not args.no_cpu_baseline:
-            out["cpu_baseline"] = cpu_reference_mlups(scene, seconds=args.cpu_seconds)
+            out["cpu_baseline"] = cpu_reference_mlups(cpu_sample_scene(scene), seconds=args.cpu_seconds)
         print(json.dumps(out))
     if world > 1:
         import torch.distributed as dist
