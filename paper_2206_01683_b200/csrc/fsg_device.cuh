@@ -17,6 +17,26 @@
 
 namespace fsg {
 
+// ----------------------------------------------------- dev instrumentation --
+// Built only with -DFSG_TIMING (make dbg -> libfsg_dbg.so): per-step phase
+// timestamps (%globaltimer) in a ring indexed by the step stamp, read back by
+// fsg_debug_timeline (scripts/probe_timeline.py).  Even slots take the min,
+// odd slots the max.  Compiled out of the product library.
+#ifdef FSG_TIMING
+constexpr int TL_SLOTS = 8;
+__device__ unsigned long long g_tl[64 * TL_SLOTS];  // only the fp32 TU is built with FSG_TIMING
+__device__ __forceinline__ unsigned long long tl_now() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#define FSG_TL(stamp, slot) \
+  ((slot) & 1 ? atomicMax(&fsg::g_tl[((stamp) & 63) * fsg::TL_SLOTS + (slot)], fsg::tl_now()) \
+              : atomicMin(&fsg::g_tl[((stamp) & 63) * fsg::TL_SLOTS + (slot)], fsg::tl_now()))
+#else
+#define FSG_TL(stamp, slot) ((void)0)
+#endif
+
 // ----------------------------------------------------------------- D3Q19 --
 // lattice.hpp:17-38 : 0 rest, 1-6 axes (+x,-x,+y,-y,+z,-z), 7-18 diagonals.
 __host__ __device__ __forceinline__ constexpr int ex_of(int i) {

@@ -8,10 +8,14 @@
 // is converted to 64-bit fixed point (2^-40) and added with an integer atomic.
 // Integer addition is associative, so the accumulated field is bit-identical
 // run to run whatever order the atomics land in -- deterministic without a
-// separate ordered-spread kernel.  Touched 4^3 tiles are stamped first
-// thing; K4 reads (and re-zeroes) the force only in stamped tiles.  The
-// interpolation sum uses a fixed warp butterfly (deterministic); the fp64
-// parity path keeps the reference's serial order instead (fsg_ib.cuh).
+// separate ordered-spread kernel.  Touched 4^3 tiles are stamped first thing;
+// the collide/stream pass reads (and re-zeroes) the force only in stamped
+// tiles.  The interpolation sum uses a fixed warp butterfly (deterministic);
+// the fp64 parity path keeps the reference's serial order instead
+// (fsg_ib.cuh).
+//
+// The per-marker work is split into device functions (stencil, stamp, finish)
+// so the kernel's block-level stamp / fence / trigger sequence stays visible.
 
 constexpr int FX_LANES = 32;     // one warp per marker
 constexpr int FX_PER_BLOCK = 4;  // markers per 128-thread block
@@ -21,59 +25,57 @@ __device__ __forceinline__ unsigned long long to_fix(double v) {
   return (unsigned long long)__double2ll_rn(v * FIX_SCALE);
 }
 
-template <bool PULLED>
-__global__ void __launch_bounds__(128, FSG_KM_MINB)
-    k_markers_fix(Grid g, const float* __restrict__ A, Markers mk, const SessionConsts* __restrict__ scp,
-                  const StepConsts st, MarkerStencil* __restrict__ rec_out, double* __restrict__ fworld,
-                  double* fworld_h, int* valid_h, FixBand fb, StepScratch* out) {
-  __shared__ double phs[FX_PER_BLOCK][3][5];
-  const int hl = threadIdx.x & (FX_LANES - 1);
-  const int slot = threadIdx.x / FX_LANES;
-  constexpr unsigned hmask = 0xFFFFFFFFu;
-  const int t = blockIdx.x * FX_PER_BLOCK + slot;
-  const bool live = t < mk.m;  // uniform over the warp
-  const SessionConsts& sc = *scp;
+/// Marker t in the lattice: frame position, bounds check, stencil ranges.
+struct MkStencil {
+  double xf[3];         // frame position (m)
+  double xl[3];         // lattice position
+  int lo[3], hi[3], cnt[3];
+  bool ok;              // marker_in_bounds (coupling.hpp:18-24)
+};
+
+__device__ __forceinline__ void mk_stencil(const Markers& mk, int t, const SessionConsts& sc,
+                                           const StepConsts& st, MkStencil& S) {
+  double xw[3];
+#pragma unroll
+  for (int k = 0; k < 3; ++k) xw[k] = mk.pts[3 * t + k] - st.p[k];
+  mat_t_vec(st.R, xw, S.xf);
+#pragma unroll
+  for (int k = 0; k < 3; ++k) S.xl[k] = S.xf[k] / sc.dx + sc.hd[k];
   const double half = 0.5 * (sc.kernel == 0 ? 4 : 3);
-  // marker state: broadcast loads (may be mapped pinned host memory)
-  double xw[3] = {0.0, 0.0, 0.0}, xf[3], xl[3];
-  bool ok = false;
-  int lo[3] = {0, 0, 0}, hi[3] = {0, 0, 0}, cnt[3] = {1, 1, 1};
-  if (live) {
+  S.ok = true;
 #pragma unroll
-    for (int k = 0; k < 3; ++k) {
-      xw[k] = mk.pts[3 * t + k] - st.p[k];
-    }
-    mat_t_vec(st.R, xw, xf);
-#pragma unroll
-    for (int k = 0; k < 3; ++k) xl[k] = xf[k] / sc.dx + sc.hd[k];
-    ok = true;
-#pragma unroll
-    for (int a = 0; a < 3; ++a)
-      if (xl[a] < half || xl[a] > sc.dims_g[a] - 1 - half) ok = false;  // coupling.hpp:18-24
-#pragma unroll
-    for (int a = 0; a < 3; ++a) {
-      lo[a] = (int)ceil(xl[a] - half);  // kernel.hpp:36-40
-      hi[a] = (int)floor(xl[a] + half);
-      cnt[a] = hi[a] - lo[a] + 1;
-    }
-    // stamp the touched tiles (<= 2x2x2: the stencil spans <= 5 cells)
-    if (ok && hl < 8) {
-      const int tx = ((hl & 1) ? hi[0] : lo[0]) >> 2;
-      const int ty = ((hl & 2) ? hi[1] : lo[1]) >> 2;
-      const int tz = ((hl & 4) ? hi[2] - g.z0 : lo[2] - g.z0) >> 2;
-      fb.tflag[tx + fb.tnx * (ty + fb.tny * tz)] = fb.stamp;
-    }
+  for (int a = 0; a < 3; ++a) {
+    if (S.xl[a] < half || S.xl[a] > sc.dims_g[a] - 1 - half) S.ok = false;
+    S.lo[a] = (int)ceil(S.xl[a] - half);  // kernel.hpp:36-40
+    S.hi[a] = (int)floor(S.xl[a] + half);
+    S.cnt[a] = S.hi[a] - S.lo[a] + 1;
   }
-  // every warp's stamps are visible before this block lets the banded K4
-  // (programmatic dependent) launch: K4's first phase skips stamped tiles and
-  // waits for this grid's completion before updating them
-  __syncthreads();
-  if (threadIdx.x == 0) __threadfence();
-  __syncthreads();
-  asm volatile("griddepcontrol.launch_dependents;");
-  if (!live) return;
-  if (!ok) {
-    if (hl == 0) {
+}
+
+/// Stamp the (<= 2x2x2: the stencil spans <= 5 cells) tiles the stencil touches.
+__device__ __forceinline__ void mk_stamp(const Grid& g, const FixBand& fb, const MkStencil& S,
+                                         int lane) {
+  if (S.ok && lane < 8) {
+    const int tx = ((lane & 1) ? S.hi[0] : S.lo[0]) >> 2;
+    const int ty = ((lane & 2) ? S.hi[1] : S.lo[1]) >> 2;
+    const int tz = ((lane & 4) ? S.hi[2] - g.z0 : S.lo[2] - g.z0) >> 2;
+    fb.tflag[tx + fb.tnx * (ty + fb.tny * tz)] = fb.stamp;
+  }
+}
+
+/// The rest of marker t's chain on one warp: phi, gathers + bare moments,
+/// interpolation, forcing, the diagnostic record and the fixed-point spread.
+/// phs: this warp's 15-double scratch in shared memory.
+template <bool PULLED>
+__device__ __forceinline__ void mk_finish(const Grid& g, const float* __restrict__ A, const Markers& mk,
+                                          int t, int lane, const SessionConsts& sc, const StepConsts& st,
+                                          const MkStencil& S, double (*phs)[5],
+                                          MarkerStencil* __restrict__ rec_out, double* __restrict__ fworld,
+                                          double* fworld_h, int* valid_h, const FixBand& fb,
+                                          StepScratch* out) {
+  constexpr unsigned full = 0xFFFFFFFFu;
+  if (!S.ok) {
+    if (lane == 0) {
       rec_out[t].valid = 0;
       fworld[3 * t] = fworld[3 * t + 1] = fworld[3 * t + 2] = 0.0;
       if (fworld_h) {
@@ -84,41 +86,41 @@ __global__ void __launch_bounds__(128, FSG_KM_MINB)
     }
     return;
   }
-  if (hl < 15) {
-    const int a = hl / 5, q = hl % 5;
-    const int la = a == 0 ? lo[0] : (a == 1 ? lo[1] : lo[2]);
-    const double xa = a == 0 ? xl[0] : (a == 1 ? xl[1] : xl[2]);
-    const int ca = a == 0 ? cnt[0] : (a == 1 ? cnt[1] : cnt[2]);
-    phs[slot][a][q] = q < ca ? ib_phi(sc.kernel, (la + q) - xa) : 0.0;
+  if (lane < 15) {
+    const int a = lane / 5, q = lane % 5;
+    const int la = a == 0 ? S.lo[0] : (a == 1 ? S.lo[1] : S.lo[2]);
+    const double xa = a == 0 ? S.xl[0] : (a == 1 ? S.xl[1] : S.xl[2]);
+    const int ca = a == 0 ? S.cnt[0] : (a == 1 ? S.cnt[1] : S.cnt[2]);
+    phs[a][q] = q < ca ? ib_phi(sc.kernel, (la + q) - xa) : 0.0;
   }
-  __syncwarp(hmask);
-  const int ncell = cnt[0] * cnt[1] * cnt[2];
-  const float r0 = 1.0f / (float)cnt[0], r01 = 1.0f / (float)(cnt[0] * cnt[1]);
+  __syncwarp(full);
+  const int ncell = S.cnt[0] * S.cnt[1] * S.cnt[2];
+  const float r0 = 1.0f / (float)S.cnt[0], r01 = 1.0f / (float)(S.cnt[0] * S.cnt[1]);
   double a0 = 0.0, a1 = 0.0, a2 = 0.0;
-  // this lane's cells c = hl + 32 r: FX_CPL gathered per round trip
+  // this lane's cells c = lane + 32 r: FX_CPL gathered per round trip
   for (int c0 = 0; c0 < ncell; c0 += FX_CPL * FX_LANES) {
     float sv[FX_CPL][Q];
     int cio[FX_CPL], cjo[FX_CPL], cko[FX_CPL];
 #pragma unroll
     for (int r = 0; r < FX_CPL; ++r) {
-      const int c = c0 + hl + FX_LANES * r;
+      const int c = c0 + lane + FX_LANES * r;
       const int ko = (int)(((float)c + 0.5f) * r01);
-      const int rem = c - ko * cnt[0] * cnt[1];
+      const int rem = c - ko * S.cnt[0] * S.cnt[1];
       const int jo = (int)(((float)rem + 0.5f) * r0);
-      cio[r] = rem - jo * cnt[0];
+      cio[r] = rem - jo * S.cnt[0];
       cjo[r] = jo;
       cko[r] = ko;
-      if (c < ncell) gather_cell<PULLED>(g, A, lo[0] + cio[r], lo[1] + jo, lo[2] + ko - g.z0, sv[r]);
+      if (c < ncell) gather_cell<PULLED>(g, A, S.lo[0] + cio[r], S.lo[1] + jo, S.lo[2] + ko - g.z0, sv[r]);
     }
 #pragma unroll
     for (int r = 0; r < FX_CPL; ++r) {
-      const int c = c0 + hl + FX_LANES * r;
+      const int c = c0 + lane + FX_LANES * r;
       if (c < ncell) {
         float drho, mx, my, mz;
         moments_dev(sv[r], drho, mx, my, mz);
         const float rho = 1.0f + drho;
         const float ir = rho > 0.0f ? 1.0f / rho : 0.0f;  // bare u; 0 where rho <= 0
-        const double w = (phs[slot][2][cko[r]] * phs[slot][1][cjo[r]]) * phs[slot][0][cio[r]];
+        const double w = (phs[2][cko[r]] * phs[1][cjo[r]]) * phs[0][cio[r]];
         a0 += w * (double)(mx * ir);
         a1 += w * (double)(my * ir);
         a2 += w * (double)(mz * ir);
@@ -127,9 +129,9 @@ __global__ void __launch_bounds__(128, FSG_KM_MINB)
   }
 #pragma unroll
   for (int o = FX_LANES / 2; o > 0; o >>= 1) {  // fixed butterfly: every lane gets the total
-    a0 += __shfl_xor_sync(hmask, a0, o);
-    a1 += __shfl_xor_sync(hmask, a1, o);
-    a2 += __shfl_xor_sync(hmask, a2, o);
+    a0 += __shfl_xor_sync(full, a0, o);
+    a1 += __shfl_xor_sync(full, a1, o);
+    a2 += __shfl_xor_sync(full, a2, o);
   }
   // body velocity, direct forcing, world force (identical on every lane);
   // the rest of the marker state is loaded only now (register pressure)
@@ -144,6 +146,7 @@ __global__ void __launch_bounds__(128, FSG_KM_MINB)
 #pragma unroll
   for (int k = 0; k < 3; ++k) vw[k] = vel[k] - st.pd[k];
   mat_t_vec(st.R, vw, vf);
+  const double* xf = S.xf;
   double du[3] = {vf[0] - (st.wf[1] * xf[2] - st.wf[2] * xf[1]) - uf[0],
                   vf[1] - (st.wf[2] * xf[0] - st.wf[0] * xf[2]) - uf[1],
                   vf[2] - (st.wf[0] * xf[1] - st.wf[1] * xf[0]) - uf[2]};
@@ -161,7 +164,7 @@ __global__ void __launch_bounds__(128, FSG_KM_MINB)
   mat_vec(st.R, fl, fw);
   mat_t_vec(st.R, fw, ff);
   const double fx = ff[0] * sc.f2l, fy = ff[1] * sc.f2l, fz = ff[2] * sc.f2l;
-  if (hl == 0) {
+  if (lane == 0) {
     fworld[3 * t] = fw[0];
     fworld[3 * t + 1] = fw[1];
     fworld[3 * t + 2] = fw[2];
@@ -175,9 +178,9 @@ __global__ void __launch_bounds__(128, FSG_KM_MINB)
 #pragma unroll
     for (int a = 0; a < 3; ++a) {
 #pragma unroll
-      for (int q = 0; q < 5; ++q) r.ph[a][q] = phs[slot][a][q];
-      r.lo[a] = lo[a];
-      r.hi[a] = hi[a];
+      for (int q = 0; q < 5; ++q) r.ph[a][q] = phs[a][q];
+      r.lo[a] = S.lo[a];
+      r.hi[a] = S.hi[a];
     }
     r.fl[0] = fx;
     r.fl[1] = fy;
@@ -187,17 +190,51 @@ __global__ void __launch_bounds__(128, FSG_KM_MINB)
     rec_out[t] = r;
   }
   // spread: this lane's own cells, fixed-point integer atomics
-  for (int c = hl; c < ncell; c += FX_LANES) {
+  for (int c = lane; c < ncell; c += FX_LANES) {
     const int ko = (int)(((float)c + 0.5f) * r01);
-    const int rem = c - ko * cnt[0] * cnt[1];
+    const int rem = c - ko * S.cnt[0] * S.cnt[1];
     const int jo = (int)(((float)rem + 0.5f) * r0);
-    const int io = rem - jo * cnt[0];
-    const double w = (phs[slot][2][ko] * phs[slot][1][jo]) * phs[slot][0][io];
-    const long long cell = (long long)(lo[0] + io) +
-                           (long long)g.nx * ((long long)(lo[1] + jo) + (long long)g.ny * (lo[2] + ko - g.z0));
+    const int io = rem - jo * S.cnt[0];
+    const double w = (phs[2][ko] * phs[1][jo]) * phs[0][io];
+    const long long cell = (long long)(S.lo[0] + io) +
+                           (long long)g.nx * ((long long)(S.lo[1] + jo) + (long long)g.ny * (S.lo[2] + ko - g.z0));
     unsigned long long* F = fb.F + 3 * cell;
     atomicAdd(F, to_fix(w * fx));
     atomicAdd(F + 1, to_fix(w * fy));
     atomicAdd(F + 2, to_fix(w * fz));
   }
+}
+
+/// Standalone marker kernel: a programmatic primary of the banded K4.  Every
+/// block stamps its markers' tiles, fences, and only then triggers its
+/// dependents, before the slow part.
+template <bool PULLED>
+__global__ void __launch_bounds__(128, FSG_KM_MINB)
+    k_markers_fix(Grid g, const float* __restrict__ A, Markers mk, const SessionConsts* __restrict__ scp,
+                  const StepConsts st, MarkerStencil* __restrict__ rec_out, double* __restrict__ fworld,
+                  double* fworld_h, int* valid_h, FixBand fb, StepScratch* out) {
+  __shared__ double phs[FX_PER_BLOCK][3][5];
+  const int lane = threadIdx.x & (FX_LANES - 1);
+  const int slot = threadIdx.x / FX_LANES;
+  const int t = blockIdx.x * FX_PER_BLOCK + slot;
+  const bool live = t < mk.m;  // uniform over the warp
+  const SessionConsts& sc = *scp;
+  if (threadIdx.x == 0) FSG_TL(fb.stamp, 0);  // timeline (dev build): marker kernel start
+  MkStencil S;
+  S.ok = false;
+  if (live) {
+    mk_stencil(mk, t, sc, st, S);
+    mk_stamp(g, fb, S, lane);
+  }
+  // every warp's stamps are visible before this block lets the banded K4
+  // (programmatic dependent) launch: K4's first phase skips stamped tiles and
+  // waits for this grid's completion before updating them
+  __syncthreads();
+  if (threadIdx.x == 0) __threadfence();
+  __syncthreads();
+  asm volatile("griddepcontrol.launch_dependents;");
+  if (!live) return;
+  mk_finish<PULLED>(g, A, mk, t, lane, sc, st, S, phs[slot], rec_out, fworld, fworld_h, valid_h, fb,
+                    out);
+  if (lane == 0) FSG_TL(fb.stamp, 1);  // last marker warp done
 }

@@ -165,7 +165,10 @@ __global__ void __launch_bounds__(128, FSG_K4_MINB)
   const int ncol = tx_n * ty_n, nzc = (g.nz + zc - 1) / zc;
   const int nitem = ncol * nzc;
   int nxt = 0;
-  if (tid == 0) nxt = (int)atomicAdd(&out->work, 1u);
+  if (tid == 0) {
+    nxt = (int)atomicAdd(&out->work, 1u);
+    FSG_TL(fb.stamp, 2);  // timeline (dev build): K4 start
+  }
   // ---- phase A: cells outside the stamped tiles (no IB force)
   float vmin = FLT_MAX;
   for (;;) {
@@ -180,17 +183,19 @@ __global__ void __launch_bounds__(128, FSG_K4_MINB)
     const int y = (col / tx_n) * blockDim.y + threadIdx.y;
     const int z0 = zk * zc, z1 = min(g.nz, z0 + zc);
     if (x >= g.nx || y >= g.ny) continue;
-    const int trow = (x >> 2) + fb.tnx * (y >> 2);
-    for (int z = z0; z < z1; ++z) {
-      if (__ldcg(fb.tflag + trow + fb.tnx * fb.tny * (z >> 2)) == fb.stamp) continue;  // band: phase B
+    // the item's zc (1 or 2) planes share a tile layer: one stamp load per
+    // item (stamped: the band phase's)
+    if (__ldcg(fb.tflag + (x >> 2) + fb.tnx * ((y >> 2) + fb.tny * (z0 >> 2))) == fb.stamp) continue;
+    for (int z = z0; z < z1; ++z)
       vmin = fminf(vmin, cell_update<PULLED, VF>(g, dp, A, x, y, z, 0.f, 0.f, 0.f, sc, st, out));
-    }
   }
   // ---- phase B: the stamped tiles, after the marker grid completed.  Block b
   // scans tiles b, b + G, b + 2G ... (G = gridDim.x), one per thread per
   // chunk, so a body's clustered tiles spread over all blocks; each 64
   // threads take one stamped tile per pass.
+  if (tid == 0) FSG_TL(fb.stamp, 3);  // phase A done (this block)
   pdl_wait();
+  if (tid == 0) FSG_TL(fb.stamp, 4);  // band phase start
   const int ntile = fb.tnx * fb.tny * fb.tnz;
   const int nthr = blockDim.x * blockDim.y;  // 96 or 128 (cell_block)
   const int tpp = nthr >> 6;                 // tiles per pass (64 threads each)
@@ -221,4 +226,5 @@ __global__ void __launch_bounds__(128, FSG_K4_MINB)
     __syncthreads();
   }
   report_min(out, vmin == FLT_MAX ? DBL_MAX : (double)vmin);
+  if (tid == 0) FSG_TL(fb.stamp, 5);  // K4 end
 }

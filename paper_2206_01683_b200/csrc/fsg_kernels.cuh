@@ -883,10 +883,13 @@ static void L_collide_band(const Grid& g, const void* A, int pulled, void* B, Fi
     res = std::max(res, 1);
   }
   const dim3 b = cell_block(g);
-  const int zc = 4;  // one tile layer per work item
-  const long long nitem =
-      (long long)((g.nx + b.x - 1) / b.x) * ((g.ny + b.y - 1) / b.y) * ((g.nz + zc - 1) / zc);
-  const unsigned grid = (unsigned)std::min<long long>(nitem, (long long)nsm * res);
+  // phase-A item: one block row x zc planes inside one tile layer (zc | 4);
+  // 2 planes when that still leaves >= 8 items per block, else 1
+  const long long ncol = (long long)((g.nx + b.x - 1) / b.x) * ((g.ny + b.y - 1) / b.y);
+  const long long full = (long long)nsm * res;
+  const int zc = (g.plane < (1 << 17) && ncol * ((g.nz + 1) / 2) >= 8 * full) ? 2 : 1;
+  const long long nitem = ncol * ((g.nz + zc - 1) / zc);
+  const unsigned grid = (unsigned)std::min<long long>(nitem, full);
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = b;

@@ -4,3 +4,14 @@
 namespace fsg {
 const Launchers& launchers_fp32() { return p32::kLaunchers; }
 }  // namespace fsg
+
+#ifdef FSG_TIMING
+// dev build only (libfsg_dbg.so): copy out and re-arm the phase timeline ring
+extern "C" int fsg_debug_timeline(unsigned long long* out) {
+  static unsigned long long init[64 * fsg::TL_SLOTS];
+  for (int i = 0; i < 64 * fsg::TL_SLOTS; ++i) init[i] = (i & 1) ? 0ull : ~0ull;
+  cudaDeviceSynchronize();
+  if (out) cudaMemcpyFromSymbol(out, fsg::g_tl, sizeof init);
+  return (int)cudaMemcpyToSymbol(fsg::g_tl, init, sizeof init);
+}
+#endif

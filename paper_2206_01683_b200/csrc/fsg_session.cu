@@ -492,6 +492,7 @@ int fsg_create(const fsg_config* cfg_in, fsg_session** out) {
     CUF(cudaMemsetAsync(fb.F, 0, sizeof(unsigned long long) * 3 * (size_t)g.n, s->stream));
     CUF(cudaMalloc(&fb.tflag, sizeof(unsigned) * ntile));
     CUF(cudaMemsetAsync(fb.tflag, 0, sizeof(unsigned) * ntile, s->stream));
+
   }
   if (g.zpad) {
     const size_t hb = (size_t)5 * g.plane * s->L->elem_bytes;
