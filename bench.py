@@ -270,7 +270,8 @@ def run_slab(args, scene, rank, local, world):
                    "parallelism": f"z-slabs x{world} ({args.c4_scaling}), NCCL halo {halo_mb:.1f} MB/step/rank"
                    if world > 1 else "single GPU"},
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
-                     "frac": round(achieved / peak, 4), "traffic": None,
+                     "frac": round(achieved / peak, 4),
+                     "traffic": k4_traffic("c4") if args.c4_scaling == "weak" and world == 1 else None,
                      "kernel": "k_collide_fix (boundary planes + interior; per GPU)",
                      "peak_source": peak_src},
         "e2e": {"value": round(total_cells * E / e2e_t / 1e6, 1), "unit": "MLUPS",
@@ -279,6 +280,16 @@ def run_slab(args, scene, rank, local, world):
         "status": {"stable": bool(st.stable()), "min_f": st.min_f},
         "clocks": clk.summary(),
     }
+
+
+def k4_traffic(workload):
+    """dram bytes read + written per launch of the dominant kernel, from the
+    committed ncu --set full capture of this workload (profiles/), or None."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "k4_traffic.json")) as f:
+            return json.load(f).get(workload, {}).get("dram_bytes_per_launch")
+    except Exception:
+        return None
 
 
 def cpu_sample_scene(scene):
@@ -330,7 +341,7 @@ def run_ours(args, scene, rank, local, world):
         torch.sum(fr_buf, dim=0, out=sink[0])
 
     def set_frame_only(k):
-        s.set_frame(frames[k])
+        s.set_frame(frames[k % len(frames)])
 
     def set_step(k):
         s.set_frame(frames[k])
@@ -432,14 +443,7 @@ def run_ours(args, scene, rank, local, world):
     # taken as the whole step interval on the session stream: conservative
     k4_avg_s = (prof_ms / max(nprof, 1)) / 1e3
     achieved = BYTES_PER_CELL * scene.n_cells / k4_avg_s / 1e9
-    traffic = None
-    try:
-        with open(os.path.join(ROOT, "profiles", "k4_traffic.json")) as f:
-            tr = json.load(f)
-        if tr.get("workload") == args.workload:
-            traffic = tr.get("dram_bytes_per_launch")
-    except Exception:
-        pass
+    traffic = k4_traffic(args.workload)
     out = {
         "metric": METRIC, "value": round(value, 1), "unit": "MLUPS", "n_gpus": world,
         "steps": K, "warmup": W, "ms_per_step": round(step_ms, 4), "higher_is_better": True,
