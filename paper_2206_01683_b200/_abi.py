@@ -74,12 +74,12 @@ SIGNATURES = {
     "fsg_set_frame": (C.c_int, [_vp, C.POINTER(fsg_frame_state)]),
     "fsg_get_frame": (C.c_int, [_vp, C.POINTER(fsg_frame_state)]),
     "fsg_recenter": (C.c_int, [_vp, _ip]),
-    "fsg_set_markers": (C.c_int, [_vp, C.c_int, _i64p, _dp, _dp, _dp, _dp]),
+    "fsg_set_markers": (C.c_int, [_vp, C.c_int, _vp, _vp, _vp, _vp, _vp]),
     "fsg_set_markers_device": (C.c_int, [_vp, C.c_int, _i64p, _vp, _vp, _vp, _vp]),
     "fsg_step": (C.c_int, [_vp, C.POINTER(fsg_status)]),
     "fsg_step_async": (C.c_int, [_vp]),
     "fsg_last_status": (C.c_int, [_vp, C.POINTER(fsg_status)]),
-    "fsg_get_marker_forces": (C.c_int, [_vp, _dp, _ip, _dp]),
+    "fsg_get_marker_forces": (C.c_int, [_vp, _vp, _vp, _vp]),
     "fsg_get_macro": (C.c_int, [_vp, _dp, _dp]),
     "fsg_get_force": (C.c_int, [_vp, _dp]),
     "fsg_get_stencils": (C.c_int, [_vp, _ip]),

@@ -122,7 +122,7 @@ struct fsg_session {
   StepConsts* h_st[2] = {nullptr, nullptr};     // pinned
   StepScratch* d_scr[2] = {nullptr, nullptr};
   StepScratch* h_scr[2] = {nullptr, nullptr};   // pinned
-  double* h_mk[2] = {nullptr, nullptr};         // pinned marker slots (read in place)
+  double* h_mk[2] = {nullptr, nullptr};         // pinned marker slots (copied to d_mk slots)
   double* h_fw[2] = {nullptr, nullptr};         // pinned marker forces (written in place)
   int* h_valid[2] = {nullptr, nullptr};
   cudaEvent_t ev[2] = {nullptr, nullptr};       // last graph of that parity done
@@ -134,11 +134,13 @@ struct fsg_session {
   int m = 0;
   int n_bodies = 0;
   std::vector<int64_t> offsets;
-  double* d_mk = nullptr;  // owned [pts 3cap | vel 3cap | nrm 3cap | area cap]
+  double* d_mk = nullptr;  // 2 device slots of [pts 3cap | vel 3cap | nrm 3cap | area cap]
+  cudaStream_t cstream = nullptr;                // marker upload (copy) stream
+  cudaEvent_t ev_cp[2] = {nullptr, nullptr};     // upload out of pinned slot k done
   Markers mk{};
   bool mk_host = false;
   bool mk_dirty = false;
-  std::vector<double> h_vel;  // for CouplingStats power
+  int last_mk_slot = 0;       // pinned marker slot the last step read (CouplingStats power)
   MarkerStencil* d_stencil = nullptr;
   MarkerBox* d_boxes = nullptr;
   double* d_fworld = nullptr;
@@ -170,6 +172,17 @@ struct fsg_session {
 };
 
 namespace {
+
+// Wait for the session stream with a short spin before blocking: the
+// synchronous step API waits ~10-100 us, where a blocking sync's wake-up
+// latency is a visible share of the end-to-end step.
+cudaError_t stream_wait(cudaStream_t st) {
+  for (int i = 0; i < 20000; ++i) {
+    const cudaError_t e = cudaStreamQuery(st);
+    if (e != cudaErrorNotReady) return e;
+  }
+  return cudaStreamSynchronize(st);
+}
 
 int ensure_tmp(fsg_session* s, size_t bytes) {
   if (s->tmp_bytes >= bytes) return FSG_OK;
@@ -267,7 +280,7 @@ __global__ void k_step_end(const StepScratch* __restrict__ d_scr, StepScratch* h
 void enqueue_step(fsg_session* s, int p, bool copy_mk, bool frame_on) {
   const Grid& g = s->g;
   const size_t m = (size_t)s->m;
-  (void)copy_mk;  // host markers are read in place from mapped pinned memory
+  (void)copy_mk;  // host markers: uploaded by fsg_set_markers (copy stream), waited on by the caller
   k_step_begin<<<1, 64, 0, s->stream>>>(s->h_st[p], s->d_st, s->d_scr[p]);
   if (m) {
     s->L->markers(g, s->buf[p], s->pulled, s->mk, s->d_sc, s->d_st, s->d_stencil, s->d_boxes,
@@ -468,7 +481,12 @@ int fsg_create(const fsg_config* cfg_in, fsg_session** out) {
   CUF(cudaMalloc(&s->d_st, sizeof(StepConsts)));
   CUF(cudaMemcpyAsync(s->d_sc, &s->hsc, sizeof(SessionConsts), cudaMemcpyHostToDevice, s->stream));
   s->cap = cfg.max_markers;
-  CUF(cudaMalloc(&s->d_mk, sizeof(double) * 10 * (size_t)s->cap));
+  CUF(cudaMalloc(&s->d_mk, sizeof(double) * 2 * 10 * (size_t)s->cap));
+  CUF(cudaStreamCreateWithFlags(&s->cstream, cudaStreamNonBlocking));
+  for (int k = 0; k < 2; ++k) {
+    CUF(cudaEventCreateWithFlags(&s->ev_cp[k], cudaEventDisableTiming));
+    CUF(cudaEventRecord(s->ev_cp[k], s->cstream));
+  }
   for (int k = 0; k < 2; ++k) {
     CUF(cudaMallocHost(&s->h_mk[k], sizeof(double) * 10 * (size_t)s->cap));
     CUF(cudaMallocHost(&s->h_fw[k], sizeof(double) * 3 * (size_t)s->cap));
@@ -535,6 +553,12 @@ int fsg_destroy(fsg_session* s) {
   cudaFree(s->d_sc);
   cudaFree(s->d_st);
   cudaFree(s->d_mk);
+  for (int k = 0; k < 2; ++k)
+    if (s->ev_cp[k]) cudaEventDestroy(s->ev_cp[k]);
+  if (s->cstream) {
+    cudaStreamSynchronize(s->cstream);
+    cudaStreamDestroy(s->cstream);
+  }
   cudaFree(s->d_stencil);
   cudaFree(s->d_boxes);
   cudaFree(s->d_fworld);
@@ -766,21 +790,27 @@ int fsg_set_markers(fsg_session* s, int n_bodies, const int64_t* off, const doub
   if (rc) return rc;
   const size_t m = (size_t)s->m;
   CU(cudaSetDevice(s->cfg.device));
-  // pinned slot the marker kernel reads in place (zero-copy): alternate slots so
-  // the host fills one while a queued step may still read the other
+  // two slot pairs (pinned host + device), alternated so the host fills one
+  // while a queued step may still read the other.  The pinned slot is copied
+  // to its device slot on the copy stream right away -- while the host goes
+  // on to enqueue the step -- and the marker kernel reads device memory (a
+  // zero-copy read from pinned memory would put PCIe round trips at the head
+  // of the marker kernel, which gates the collide kernel's start).
   const int p = s->mk_slot < 0 ? 0 : (s->mk_slot ^ 1);
+  double* d = s->d_mk + (size_t)p * 10 * (size_t)s->cap;
   if (m) {
     if (!pts || !vel || !nrm || !area) return set_err(FSG_EINPUT, "fsg_set_markers: null array");
-    CU(cudaEventSynchronize(s->ev_mk[p]));  // last step that read this slot is done
+    CU(cudaEventSynchronize(s->ev_cp[p]));  // the previous copy out of this pinned slot is done
     double* h = s->h_mk[p];
     std::memcpy(h, pts, sizeof(double) * 3 * m);
     std::memcpy(h + 3 * m, vel, sizeof(double) * 3 * m);
     std::memcpy(h + 6 * m, nrm, sizeof(double) * 3 * m);
     std::memcpy(h + 9 * m, area, sizeof(double) * m);
-    s->h_vel.assign(vel, vel + 3 * m);
+    CU(cudaStreamWaitEvent(s->cstream, s->ev_mk[p], 0));  // the last step that read device slot p
+    CU(cudaMemcpyAsync(d, h, sizeof(double) * 10 * m, cudaMemcpyHostToDevice, s->cstream));
+    CU(cudaEventRecord(s->ev_cp[p], s->cstream));
   }
-  double* h = s->h_mk[p];
-  s->mk = Markers{h, h + 3 * m, h + 6 * m, h + 9 * m, (int)m};
+  s->mk = Markers{d, d + 3 * m, d + 6 * m, d + 9 * m, (int)m};
   s->mk_slot = p;
   s->mk_host = true;
   s->mk_dirty = m > 0;
@@ -811,6 +841,7 @@ int fsg_step_async(fsg_session* s) {
   frame_consts(s->frame, *s->h_st[p]);
   const bool frame_on = s->cfg.frame_mode != FSG_FRAME_NONE;
   const bool copy_mk = s->mk_host && s->mk_dirty;
+  if (copy_mk) CU(cudaStreamWaitEvent(s->stream, s->ev_cp[s->mk_slot], 0));  // markers uploaded
   if (s->L->markers_fix) {
     // throughput path: frame constants by value; the status stays in the
     // device scratch until the host asks for it (fsg_last_status)
@@ -862,6 +893,7 @@ int fsg_step_async(fsg_session* s) {
   CU(cudaEventRecord(s->ev[p], s->stream));
   if (s->mk_host && s->mk_slot >= 0) CU(cudaEventRecord(s->ev_mk[s->mk_slot], s->stream));
   s->last_par = p;
+  if (s->mk_host && s->mk_slot >= 0) s->last_mk_slot = s->mk_slot;
   s->prev_pulled = s->pulled;
   s->last_frame_on = frame_on;
   s->par ^= 1;
@@ -879,7 +911,7 @@ int fsg_last_status(fsg_session* s, fsg_status* st) {
     CU(cudaMemcpyAsync(s->h_scr[s->last_par], s->d_scr[s->last_par], sizeof(StepScratch),
                        cudaMemcpyDeviceToHost, s->stream));
   }
-  CU(cudaStreamSynchronize(s->stream));
+  CU(stream_wait(s->stream));
   if (!s->stepped) {
     if (st) *st = s->last;
     return FSG_OK;
@@ -903,7 +935,7 @@ int fsg_get_marker_forces(fsg_session* s, double* fw, int* valid, double* stats)
   CU(cudaSetDevice(s->cfg.device));
   const size_t m = (size_t)s->m;
   // the marker kernel wrote the forces straight into mapped pinned memory
-  CU(cudaStreamSynchronize(s->stream));
+  CU(stream_wait(s->stream));
   if (!s->stepped) return set_err(FSG_ESTATE, "no coupled step yet");
   const double* f = s->h_fw[s->last_par];
   const int* vv = s->h_valid[s->last_par];
@@ -913,7 +945,7 @@ int fsg_get_marker_forces(fsg_session* s, double* fw, int* valid, double* stats)
     std::vector<double> vel;
     const double* v = nullptr;
     if (s->mk_host) {
-      v = s->h_vel.data();
+      v = s->h_mk[s->last_mk_slot] + 3 * m;  // the velocities the last step read
     } else if (m) {
       vel.resize(3 * m);
       CU(cudaMemcpy(vel.data(), s->mk.vel, sizeof(double) * 3 * m, cudaMemcpyDeviceToHost));

@@ -136,6 +136,8 @@ class CoupledSession:
         self._fs_c = _abi.fsg_frame_state()
         self._fs_ref = C.byref(self._fs_c)
         self._fs_view = np.frombuffer(self._fs_c, dtype=np.float64)
+        self._st = _abi.fsg_status()
+        self._st_ref = C.byref(self._st)
         self.dims = tuple(int(d) for d in cfg.dims)
         self.n_cells = int(np.prod(self.dims))
         self.m = 0
@@ -245,14 +247,13 @@ class CoupledSession:
 
     # -- coupled step ------------------------------------------------------
     def set_markers(self, body_offsets, points, velocities, normals, areas) -> None:
-        off = np.ascontiguousarray(np.asarray(body_offsets, dtype=np.int64))
-        pts = np.ascontiguousarray(points, dtype=np.float64).reshape(-1)
-        vel = np.ascontiguousarray(velocities, dtype=np.float64).reshape(-1)
-        nrm = np.ascontiguousarray(normals, dtype=np.float64).reshape(-1)
-        ar = np.ascontiguousarray(areas, dtype=np.float64).reshape(-1)
+        """Per-step marker state (world frame, SI), copied into a pinned slot."""
+        off = np.ascontiguousarray(body_offsets, dtype=np.int64)
+        arrs = [np.ascontiguousarray(a, dtype=np.float64) for a in (points, velocities, normals, areas)]
         nb = len(off) - 1
-        check(_abi.lib().fsg_set_markers(self._h, nb, off.ctypes.data_as(_abi._i64p), dptr(pts),
-                                         dptr(vel), dptr(nrm), dptr(ar)))
+        rc = self._L.fsg_set_markers(self._h, nb, off.ctypes.data, *(a.ctypes.data for a in arrs))
+        if rc:
+            check(rc)
         self.m = int(off[-1]) if nb > 0 else 0
         self.n_bodies = nb
 
@@ -267,8 +268,10 @@ class CoupledSession:
 
     def step(self) -> StepStatus:
         """Fluid half of CoupledSession::step (session.hpp:94-166)."""
-        st = _abi.fsg_status()
-        check(_abi.lib().fsg_step(self._h, C.byref(st)))
+        st = self._st
+        rc = self._L.fsg_step(self._h, self._st_ref)
+        if rc:
+            check(rc)
         return StepStatus.of(st)
 
     def step_async(self) -> None:
@@ -277,16 +280,21 @@ class CoupledSession:
             check(rc)
 
     def last_status(self) -> StepStatus:
-        st = _abi.fsg_status()
-        check(_abi.lib().fsg_last_status(self._h, C.byref(st)))
+        st = self._st
+        rc = self._L.fsg_last_status(self._h, self._st_ref)
+        if rc:
+            check(rc)
         return StepStatus.of(st)
 
     def marker_forces(self):
         """-> (force_world[m,3] on the fluid, valid[m], stats[n_bodies,7])."""
-        fw = np.zeros(3 * self.m)
-        valid = np.zeros(self.m, dtype=np.int32)
+        fw = np.empty(3 * self.m)
+        valid = np.empty(self.m, dtype=np.int32)
         stats = np.zeros(7 * max(self.n_bodies, 1))
-        check(_abi.lib().fsg_get_marker_forces(self._h, dptr(fw), iptr(valid), dptr(stats)))
+        rc = self._L.fsg_get_marker_forces(self._h, fw.ctypes.data, valid.ctypes.data,
+                                           stats.ctypes.data)
+        if rc:
+            check(rc)
         return fw.reshape(-1, 3), valid, stats[: 7 * self.n_bodies].reshape(-1, 7)
 
     def macro(self):
