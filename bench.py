@@ -55,6 +55,8 @@ def parse_args():
     ap.add_argument("--warmup", type=int, default=20)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="c2", choices=["c1", "c2", "c3", "c4", "c5"])
+    ap.add_argument("--envs", type=int, default=None,
+                    help="c5: env sessions per GPU, each on its own stream (default 8: 64 envs on 8 GPUs)")
     ap.add_argument("--c4-scaling", default="weak", choices=["weak", "strong"],
                     help="c4: each rank owns 512^3 (weak) or one 512^3 grid is split (strong)")
     ap.add_argument("--e2e-steps", type=int, default=100)
@@ -302,6 +304,128 @@ def cpu_sample_scene(scene):
     return scene
 
 
+# ------------------------------------------------------ ours: envs (c5) ---
+def run_envs(args, scene, rank, local, world):
+    """c5: E independent env sessions per GPU (BASELINE: 64 envs on 8 GPUs),
+    each on its own stream so one env's latency-bound marker kernel overlaps
+    another's collide kernel.  A round = one coupled step of every env."""
+    import numpy as np
+    import torch
+    from paper_2206_01683_b200 import CoupledSession, SessionConfig
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    E = args.envs or 8
+    W, K = args.warmup, args.steps
+    m = scene.m
+    ss, mk_dev, frames = [], [], []
+    for e in range(E):
+        ss.append(CoupledSession(SessionConfig(
+            dims=scene.dims, dx=scene.dx, dt=scene.dt, rho=scene.rho, nu=scene.nu,
+            frame_mode=scene.frame_mode, precision="fp32", device=local, max_markers=max(m, 1))))
+        # env e runs the gait with its own phase (env.hpp:73-95 randomises the start)
+        P = np.zeros((16, 4, 3 * m))
+        for k in range(16):
+            pts, vel, nrm, area = scene.markers(k + 37 * e)
+            P[k, 0], P[k, 1], P[k, 2] = pts.reshape(-1), vel.reshape(-1), nrm.reshape(-1)
+            P[k, 3, :m] = area
+        mk_dev.append(torch.tensor(P, dtype=torch.float64, device=dev))
+        frames.append([scene.frame(k + 37 * e) for k in range(16)])
+    streams = [torch.cuda.ExternalStream(s.stream, device=dev) for s in ss]
+    main = torch.cuda.current_stream(dev)
+    l2 = torch.cuda.get_device_properties(dev).L2_cache_size
+    nflush = max(2 * l2, 256 << 20) // 4
+    fw_buf = torch.empty(nflush, dtype=torch.float32, device=dev)
+    fr_buf = torch.ones(nflush, dtype=torch.float32, device=dev)
+    sink = torch.zeros(1, dtype=torch.float32, device=dev)
+
+    def round_async(k):
+        for e, s in enumerate(ss):
+            s.set_frame(frames[e][k % 16])
+            r = mk_dev[e][k % 16]
+            s.set_markers_device(scene.offsets, r[0].data_ptr(), r[1].data_ptr(), r[2].data_ptr(),
+                                 r[3].data_ptr())
+            s.step_async()
+
+    for k in range(W):
+        round_async(k)
+    for s in ss:
+        s.last_status()
+    torch.cuda.synchronize(dev)
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
+    with ClockSampler(local) as clk:
+        time.sleep(0.4)
+        for k in range(K):
+            fw_buf.fill_(1.0)
+            torch.sum(fr_buf, dim=0, out=sink[0])
+            ev[k][0].record(main)
+            for st_ in streams:
+                st_.wait_event(ev[k][0])
+            round_async(W + k)
+            for st_ in streams:
+                j = torch.cuda.Event()
+                j.record(st_)
+                main.wait_event(j)
+            ev[k][1].record(main)
+        torch.cuda.synchronize(dev)
+        time.sleep(0.15)
+    sts = [s.last_status() for s in ss]
+    round_ms = sum(a.elapsed_time(b) for a, b in ev) / K
+    t_total = round_ms * K / 1e3
+    if world > 1:
+        import torch.distributed as dist
+        t = torch.tensor([t_total], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        t_total = float(t.item())
+    value = E * scene.n_cells * K * world / t_total / 1e6
+    # e2e: every env through the host API, overlapped across envs with step_async
+    Ee = min(args.e2e_steps, K)
+    mk_host = [[scene.markers(k + 37 * e) for k in range(4)] for e in range(E)]
+    torch.cuda.synchronize(dev)
+    e2e_t = 0.0
+    for k in range(Ee):
+        t0 = time.perf_counter()
+        for e, s in enumerate(ss):
+            s.set_frame(frames[e][k % 16])
+            s.set_markers(scene.offsets, *mk_host[e][k % 4])
+            s.step_async()
+        for s in ss:
+            s.last_status()
+            s.marker_forces()
+        e2e_t += time.perf_counter() - t0
+    if world > 1:
+        import torch.distributed as dist
+        t = torch.tensor([e2e_t], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_t = float(t.item())
+    for s in ss:
+        s.close()
+    peak, peak_src = measured_peaks()
+    achieved = BYTES_PER_CELL * E * scene.n_cells / (round_ms / 1e3) / 1e9
+    return {
+        "metric": METRIC, "value": round(value, 1), "unit": "MLUPS", "n_gpus": world,
+        "steps": K, "warmup": W, "ms_per_step": round(round_ms, 4), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f32 (fp32 storage of f - w_i)",
+        "data": "synthetic (prescribed-kinematics koi per env, own gait phase; SURVEY.md §8(d) C5)",
+        "config": {"workload": scene.name, "dims": list(scene.dims), "markers": m,
+                   "envs_per_gpu": E, "frame": scene.frame_mode, "l2": "flushed between rounds",
+                   "parallelism": f"{E} env sessions per GPU on {E} streams"
+                                  + (f", replicas x{world}" if world > 1 else "")},
+        "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                     "frac": round(achieved / peak, 4), "traffic": None,
+                     "kernel": "k_markers_fix + k_collide_band of all envs, one round interval",
+                     "peak_source": peak_src},
+        "e2e": {"value": round(E * scene.n_cells * Ee * world / e2e_t / 1e6, 1), "unit": "MLUPS",
+                "h2d_bytes_per_step": E * (80 * m + 232), "d2h_bytes_per_step": E * (28 * m + 64),
+                "steps": Ee},
+        "gpu_launches": K * E * 2,
+        "status": {"stable": all(st.stable() for st in sts), "min_f": min(st.min_f for st in sts)},
+        "clocks": clk.summary(),
+    }
+
+
 # ------------------------------------------------------------------ ours ---
 def run_ours(args, scene, rank, local, world):
     import numpy as np
@@ -499,6 +623,8 @@ def main():
         dist.init_process_group("nccl")
     if args.workload == "c4":
         out = run_slab(args, scene, rank, local, world)
+    elif args.workload == "c5" and (args.envs or 8) > 1:
+        out = run_envs(args, scene, rank, local, world)
     else:
         out = run_ours(args, scene, rank, local, world)
     if rank == 0:
