@@ -12,6 +12,7 @@
 //   lbm::macroscopic(grid, force)                macroscopic
 //   lbm::total_mass / total_momentum             total_mass / total_momentum
 //   frame::recenter(grid, frame, shift)          recenter
+//   frame::FrameFollower(mode, tc) reset/step    FrameFollower reset / step / state
 //   CoupledSession::step() fluid half            set_frame + set_markers + step
 //   (session.hpp:94-166)                          + marker_forces / stats
 //
@@ -61,6 +62,40 @@ struct FrameState {
 
 struct Config : fsg_config {
   Config() { fsg_config_default(this); }
+};
+
+/// frame::FrameFollower (frame.hpp:70-125): the critically damped tracker of
+/// the robot base; state() is what FluidSession::set_frame takes.
+class FrameFollower {
+ public:
+  explicit FrameFollower(int mode = FSG_FRAME_TRANSLATION, double time_constant = 0.2) {
+    check(fsg_follower_create(mode, time_constant, &h_));
+  }
+  ~FrameFollower() { fsg_follower_destroy(h_); }
+  FrameFollower(const FrameFollower&) = delete;
+  FrameFollower& operator=(const FrameFollower&) = delete;
+
+  void reset(const std::array<double, 3>& p, double yaw) { check(fsg_follower_reset(h_, p.data(), yaw)); }
+  void step(const std::array<double, 3>& target_p, const std::array<double, 4>& target_q, double dt) {
+    check(fsg_follower_step(h_, target_p.data(), target_q.data(), dt));
+  }
+  FrameState state() const {
+    fsg_frame_state c{};
+    check(fsg_follower_state(h_, &c));
+    FrameState f;
+    for (int k = 0; k < 3; ++k) {
+      f.p[k] = c.p[k];
+      f.pd[k] = c.pd[k];
+      f.pdd[k] = c.pdd[k];
+      f.omega[k] = c.omega[k];
+      f.alpha[k] = c.alpha[k];
+    }
+    for (int k = 0; k < 4; ++k) f.q[k] = c.q[k];
+    return f;
+  }
+
+ private:
+  fsg_follower* h_ = nullptr;
 };
 
 class FluidSession {

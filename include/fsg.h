@@ -121,6 +121,18 @@ int fsg_get_frame(fsg_session* s, fsg_frame_state* fs);
  * offset and advances the frame origin by R*shift*dx. */
 int fsg_recenter(fsg_session* s, const int shift[3]);
 
+/* frame::FrameFollower (frame.hpp:70-125): the critically damped tracker of
+ * the robot base that produces the frame state fed to fsg_set_frame.  Host
+ * code (no device), fp64, bit-identical to the reference's.  mode: FSG_FRAME_*
+ * (follow_mode), time_constant in s (wn = 1/time_constant; 0.2 s default). */
+typedef struct fsg_follower fsg_follower;
+int fsg_follower_create(int mode, double time_constant, fsg_follower** out);
+int fsg_follower_destroy(fsg_follower* f);
+int fsg_follower_reset(fsg_follower* f, const double p[3], double yaw);             /* :81-87 */
+int fsg_follower_step(fsg_follower* f, const double target_p[3], const double target_q[4],
+                      double dt);                                                     /* :90-119 */
+int fsg_follower_state(const fsg_follower* f, fsg_frame_state* out);
+
 /* ---- coupled step (session.hpp:87-198, fluid half :94-166) -------------- */
 /* Marker state for this step, world frame SI (what robot::update_samples
  * produces, sampling.hpp:307-322): n_bodies bodies, body b owns markers

@@ -85,6 +85,11 @@ SIGNATURES = {
     "fsg_get_stencils": (C.c_int, [_vp, _ip]),
     "fsg_profile_enable": (C.c_int, [_vp, C.c_int]),
     "fsg_profile_read": (C.c_int, [_vp, _dp, _ip]),
+    "fsg_follower_create": (C.c_int, [C.c_int, C.c_double, C.POINTER(_vp)]),
+    "fsg_follower_destroy": (C.c_int, [_vp]),
+    "fsg_follower_reset": (C.c_int, [_vp, _dp, C.c_double]),
+    "fsg_follower_step": (C.c_int, [_vp, _dp, _dp, C.c_double]),
+    "fsg_follower_state": (C.c_int, [_vp, C.POINTER(fsg_frame_state)]),
     "fsg_halo_bytes": (C.c_size_t, [_vp]),
     "fsg_halo_pack": (C.c_int, [_vp, _vp, _vp]),
     "fsg_halo_unpack": (C.c_int, [_vp, _vp, _vp]),

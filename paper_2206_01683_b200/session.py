@@ -123,6 +123,48 @@ class FrameState:
         return cls(*(np.array(list(getattr(c, n))) for n in ("p", "pd", "pdd", "q", "omega", "alpha")))
 
 
+class FrameFollower:
+    """frame::FrameFollower (frame.hpp:70-125): critically damped tracker of
+    the robot base producing the local frame's state (host code, fp64,
+    bit-identical to the reference).  mode: none | translation |
+    translation_yaw | full; time_constant in seconds (frame.hpp:75-76)."""
+
+    def __init__(self, mode: str = "translation", time_constant: float = 0.2):
+        if mode not in FRAME:
+            raise ValueError(f"unknown frame mode '{mode}'")  # parse_follow_mode (frame.hpp:57-63)
+        self.mode = mode
+        h = C.c_void_p()
+        check(_abi.lib().fsg_follower_create(FRAME[mode], float(time_constant), C.byref(h)))
+        self._h = h
+
+    def reset(self, p, yaw: float = 0.0) -> None:
+        """Snap to a target with zero derivatives (episode reset, frame.hpp:81-87)."""
+        pa = np.ascontiguousarray(p, dtype=np.float64).reshape(3)
+        check(_abi.lib().fsg_follower_reset(self._h, dptr(pa), float(yaw)))
+
+    def step(self, target_p, target_q, dt: float) -> None:
+        """One filter step toward the base pose (position, quaternion w,x,y,z)."""
+        tp = np.ascontiguousarray(target_p, dtype=np.float64).reshape(3)
+        tq = np.ascontiguousarray(target_q, dtype=np.float64).reshape(4)
+        check(_abi.lib().fsg_follower_step(self._h, dptr(tp), dptr(tq), float(dt)))
+
+    def state(self) -> FrameState:
+        c = _abi.fsg_frame_state()
+        check(_abi.lib().fsg_follower_state(self._h, C.byref(c)))
+        return FrameState.of(c)
+
+    def close(self) -> None:
+        if getattr(self, "_h", None):
+            _abi.lib().fsg_follower_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
 class CoupledSession:
     """One device-resident IB-LBM domain (sim::CoupledSession, session.hpp:29-224)."""
 

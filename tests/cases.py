@@ -409,3 +409,59 @@ def rel_l2(a, b):
     a = np.asarray(a, dtype=np.float64).reshape(-1)
     b = np.asarray(b, dtype=np.float64).reshape(-1)
     return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300))
+
+
+# ----------------------------------------------------------------------------
+# FrameFollower (frame.hpp:70-125): a robot-base target trajectory with
+# translation, yaw, pitch and roll, two resets, 240 steps of dt = 0.004
+FOLLOW_MODES = ("none", "translation", "translation_yaw", "full")
+
+
+def follower_script():
+    ops = [("reset", (0.01, -0.02, 0.005), 0.3)]
+    for k in range(240):
+        t = 0.004 * k
+        yaw = 0.3 + 1.9 * math.sin(2.1 * t) + (3.0 if k > 150 else 0.0)  # crosses +-pi
+        pitch, roll = 0.25 * math.sin(3.3 * t), 0.2 * math.cos(2.7 * t)
+        cy, sy = math.cos(0.5 * yaw), math.sin(0.5 * yaw)
+        cp, sp = math.cos(0.5 * pitch), math.sin(0.5 * pitch)
+        cr, sr = math.cos(0.5 * roll), math.sin(0.5 * roll)
+        q = (cy * cp * cr + sy * sp * sr, cy * cp * sr - sy * sp * cr,
+             cy * sp * cr + sy * cp * sr, sy * cp * cr - cy * sp * sr)  # ZYX
+        p = (0.1 * t + 0.02 * math.sin(7 * t), 0.03 * math.cos(5 * t), 0.01 * math.sin(3 * t))
+        ops.append(("step", p, q))
+        if k == 120:
+            ops.append(("reset", (0.2, 0.0, -0.01), -2.5))
+    return ops
+
+
+def run_ref_follower(mode, ops, tc=0.2):
+    """-> [n_states, 19] (p, pd, pdd, q(w,x,y,z), omega, alpha) after every op."""
+    R = B.ref()
+    h = R.ref_follower_create(FOLLOW_MODES.index(mode), tc)
+    out, buf = [], np.zeros(22)
+    for op in ops:
+        if op[0] == "reset":
+            R.ref_follower_reset(h, B.dptr(np.array(op[1], dtype=np.float64)), op[2])
+        else:
+            R.ref_follower_step(h, B.dptr(np.array(op[1], dtype=np.float64)),
+                                B.dptr(np.array(op[2], dtype=np.float64)), 0.004)
+        R.ref_follower_state(h, B.dptr(buf))
+        out.append(buf[:19].copy())
+    R.ref_follower_destroy(h)
+    return np.array(out)
+
+
+def run_product_follower(mode, ops, tc=0.2):
+    from paper_2206_01683_b200 import FrameFollower
+    f = FrameFollower(mode, tc)
+    out = []
+    for op in ops:
+        if op[0] == "reset":
+            f.reset(op[1], op[2])
+        else:
+            f.step(op[1], op[2], 0.004)
+        s = f.state()
+        out.append(np.concatenate([s.p, s.pd, s.pdd, s.q, s.omega, s.alpha]))
+    f.close()
+    return np.array(out)

@@ -25,6 +25,18 @@ int main(int argc, char** argv) {
       if (std::string(e.what()).find("tau") == std::string::npos) return 1;
     }
   }
+  // FrameFollower (frame.hpp:70-125): a step toward a target 1 cm ahead starts
+  // with pdd = wn^2 * 0.01 (wn = 5/s) and the yaw pinned in TranslationYaw
+  {
+    FrameFollower f(FSG_FRAME_TRANSLATION_YAW, 0.2);
+    f.reset({0.0, 0.0, 0.0}, 0.5);
+    f.step({0.01, 0.0, 0.0}, {1.0, 0.0, 0.0, 0.0}, 0.004);
+    const FrameState st = f.state();
+    if (std::fabs(st.pdd[0] - 25.0 * 0.01) > 1e-15 || st.omega[0] != 0.0 || st.q[1] != 0.0) {
+      std::printf("FAIL: follower\n");
+      return 4;
+    }
+  }
   Config c;
   c.dims[0] = c.dims[1] = c.dims[2] = 8;
   c.dx = c.dt = c.rho = 1.0;

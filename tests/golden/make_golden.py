@@ -36,6 +36,11 @@ def _flat(d, prefix):
 
 def main():
     assert B.have_ref(), "oracle/_ref/libfishref.so missing: run make -C oracle with /root/reference"
+    # FrameFollower (frame.hpp:70-125), every mode
+    ops = K.follower_script()
+    np.savez_compressed(os.path.join(HERE, "follower.npz"),
+                        **{"out_" + m: K.run_ref_follower(m, ops) for m in K.FOLLOW_MODES})
+    print("follower ok")
     for mk in (K.case_lbm_open, K.case_lbm_periodic):
         c = mk()
         res = K.run_ref_lbm(c)
