@@ -56,7 +56,9 @@ def parse_args():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="c2", choices=["c1", "c2", "c3", "c4", "c5"])
     ap.add_argument("--envs", type=int, default=None,
-                    help="c5: env sessions per GPU, each on its own stream (default 8: 64 envs on 8 GPUs)")
+                    help="c5: envs per GPU (default 8: 64 envs on 8 GPUs)")
+    ap.add_argument("--c5-mode", default="batch", choices=["batch", "streams"],
+                    help="c5: one batched launch per kernel (EnvBatch) or one session per stream")
     ap.add_argument("--c4-scaling", default="weak", choices=["weak", "strong"],
                     help="c4: each rank owns 512^3 (weak) or one 512^3 grid is split (strong)")
     ap.add_argument("--e2e-steps", type=int, default=100)
@@ -306,22 +308,25 @@ def cpu_sample_scene(scene):
 
 # ------------------------------------------------------ ours: envs (c5) ---
 def run_envs(args, scene, rank, local, world):
-    """c5: E independent env sessions per GPU (BASELINE: 64 envs on 8 GPUs),
-    each on its own stream so one env's latency-bound marker kernel overlaps
-    another's collide kernel.  A round = one coupled step of every env."""
+    """c5: E independent envs per GPU (BASELINE: 64 envs on 8 GPUs).  batch
+    mode: an EnvBatch steps every env with one marker launch and one
+    collide/stream launch; streams mode: one session per
+    stream.  A round = one coupled step of every env."""
     import numpy as np
     import torch
-    from paper_2206_01683_b200 import CoupledSession, SessionConfig
+    from paper_2206_01683_b200 import CoupledSession, EnvBatch, SessionConfig
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     E = args.envs or 8
     W, K = args.warmup, args.steps
     m = scene.m
-    ss, mk_dev, frames = [], [], []
+    cfg = SessionConfig(dims=scene.dims, dx=scene.dx, dt=scene.dt, rho=scene.rho, nu=scene.nu,
+                        frame_mode=scene.frame_mode, precision="fp32", device=local,
+                        max_markers=max(m, 1))
+    batch = EnvBatch(cfg, E) if args.c5_mode == "batch" else None
+    ss = batch.envs if batch else [CoupledSession(cfg) for _ in range(E)]
+    mk_dev, frames = [], []
     for e in range(E):
-        ss.append(CoupledSession(SessionConfig(
-            dims=scene.dims, dx=scene.dx, dt=scene.dt, rho=scene.rho, nu=scene.nu,
-            frame_mode=scene.frame_mode, precision="fp32", device=local, max_markers=max(m, 1))))
         # env e runs the gait with its own phase (env.hpp:73-95 randomises the start)
         P = np.zeros((16, 4, 3 * m))
         for k in range(16):
@@ -330,7 +335,7 @@ def run_envs(args, scene, rank, local, world):
             P[k, 3, :m] = area
         mk_dev.append(torch.tensor(P, dtype=torch.float64, device=dev))
         frames.append([scene.frame(k + 37 * e) for k in range(16)])
-    streams = [torch.cuda.ExternalStream(s.stream, device=dev) for s in ss]
+    streams = [torch.cuda.ExternalStream(s.stream, device=dev) for s in (ss[:1] if batch else ss)]
     main = torch.cuda.current_stream(dev)
     l2 = torch.cuda.get_device_properties(dev).L2_cache_size
     nflush = max(2 * l2, 256 << 20) // 4
@@ -344,7 +349,10 @@ def run_envs(args, scene, rank, local, world):
             r = mk_dev[e][k % 16]
             s.set_markers_device(scene.offsets, r[0].data_ptr(), r[1].data_ptr(), r[2].data_ptr(),
                                  r[3].data_ptr())
-            s.step_async()
+            if not batch:
+                s.step_async()
+        if batch:
+            batch.step_async()
 
     for k in range(W):
         round_async(k)
@@ -390,7 +398,10 @@ def run_envs(args, scene, rank, local, world):
         for e, s in enumerate(ss):
             s.set_frame(frames[e][k % 16])
             s.set_markers(scene.offsets, *mk_host[e][k % 4])
-            s.step_async()
+            if not batch:
+                s.step_async()
+        if batch:
+            batch.step_async()
         for s in ss:
             s.last_status()
             s.marker_forces()
@@ -400,8 +411,11 @@ def run_envs(args, scene, rank, local, world):
         t = torch.tensor([e2e_t], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_t = float(t.item())
-    for s in ss:
-        s.close()
+    if batch:
+        batch.close()
+    else:
+        for s in ss:
+            s.close()
     peak, peak_src = measured_peaks()
     achieved = BYTES_PER_CELL * E * scene.n_cells / (round_ms / 1e3) / 1e9
     return {
@@ -411,16 +425,18 @@ def run_envs(args, scene, rank, local, world):
         "data": "synthetic (prescribed-kinematics koi per env, own gait phase; SURVEY.md §8(d) C5)",
         "config": {"workload": scene.name, "dims": list(scene.dims), "markers": m,
                    "envs_per_gpu": E, "frame": scene.frame_mode, "l2": "flushed between rounds",
-                   "parallelism": f"{E} env sessions per GPU on {E} streams"
+                   "parallelism": (f"{E} envs per GPU batched: one marker + one collide launch per round"
+                                   if batch else f"{E} env sessions per GPU on {E} streams")
                                   + (f", replicas x{world}" if world > 1 else "")},
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                      "frac": round(achieved / peak, 4), "traffic": None,
-                     "kernel": "k_markers_fix + k_collide_band of all envs, one round interval",
+                     "kernel": ("k_markers_batch + k_collide_band_batch, one round interval" if batch
+                                else "k_markers_fix + k_collide_band of all envs, one round interval"),
                      "peak_source": peak_src},
         "e2e": {"value": round(E * scene.n_cells * Ee * world / e2e_t / 1e6, 1), "unit": "MLUPS",
                 "h2d_bytes_per_step": E * (80 * m + 232), "d2h_bytes_per_step": E * (28 * m + 64),
                 "steps": Ee},
-        "gpu_launches": K * E * 2,
+        "gpu_launches": K * (2 if batch else E * 2),
         "status": {"stable": all(st.stable() for st in sts), "min_f": min(st.min_f for st in sts)},
         "clocks": clk.summary(),
     }

@@ -172,6 +172,19 @@ int fsg_get_stencils(fsg_session* s, int* lo_hi);
 int fsg_profile_enable(fsg_session* s, int enable);
 int fsg_profile_read(fsg_session* s, double* step_ms, int* steps);
 
+/* ---- batched envs (BASELINE config 5) ------------------
+ * n_envs (<= 64) independent sessions of one fp32 configuration sharing one
+ * stream; fsg_batch_step_async steps every env with ONE marker launch and ONE
+ * collide/stream launch.  Env e is an ordinary session handle
+ * (fsg_batch_session): set its frame and markers and read it back with the
+ * per-session calls; it is destroyed with the batch. */
+typedef struct fsg_batch fsg_batch;
+int fsg_batch_create(const fsg_config* cfg, int n_envs, fsg_batch** out);
+int fsg_batch_destroy(fsg_batch* b);
+fsg_session* fsg_batch_session(fsg_batch* b, int env);
+int fsg_batch_step_async(fsg_batch* b);
+int fsg_batch_step(fsg_batch* b, fsg_status* statuses /* n_envs, nullable */);
+
 /* ---- z-slab halo exchange ------------------------------
  * A slab session (cfg.z_offset / cfg.nz_global) owns planes [z_offset,
  * z_offset + dims[2]) of a global grid plus one halo plane per side.  Per

@@ -6,8 +6,8 @@ for benchmarking.  There is no CPU fallback: without the built library or a
 CUDA device every call raises.
 """
 from ._abi import FsgError, InputError, LIB_PATH, lib
-from .session import (CoupledSession, FrameFollower, FrameState, SessionConfig, StepStatus,
-                      tau_of)
+from .session import (CoupledSession, EnvBatch, FrameFollower, FrameState, SessionConfig,
+                      StepStatus, tau_of)
 
-__all__ = ["CoupledSession", "FrameFollower", "FrameState", "SessionConfig", "StepStatus", "tau_of",
-           "FsgError", "InputError", "LIB_PATH", "lib"]
+__all__ = ["CoupledSession", "EnvBatch", "FrameFollower", "FrameState", "SessionConfig",
+           "StepStatus", "tau_of", "FsgError", "InputError", "LIB_PATH", "lib"]

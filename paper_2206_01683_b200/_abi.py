@@ -90,6 +90,11 @@ SIGNATURES = {
     "fsg_follower_reset": (C.c_int, [_vp, _dp, C.c_double]),
     "fsg_follower_step": (C.c_int, [_vp, _dp, _dp, C.c_double]),
     "fsg_follower_state": (C.c_int, [_vp, C.POINTER(fsg_frame_state)]),
+    "fsg_batch_create": (C.c_int, [C.POINTER(fsg_config), C.c_int, C.POINTER(_vp)]),
+    "fsg_batch_destroy": (C.c_int, [_vp]),
+    "fsg_batch_session": (_vp, [_vp, C.c_int]),
+    "fsg_batch_step_async": (C.c_int, [_vp]),
+    "fsg_batch_step": (C.c_int, [_vp, C.POINTER(fsg_status)]),
     "fsg_halo_bytes": (C.c_size_t, [_vp]),
     "fsg_halo_pack": (C.c_int, [_vp, _vp, _vp]),
     "fsg_halo_unpack": (C.c_int, [_vp, _vp, _vp]),

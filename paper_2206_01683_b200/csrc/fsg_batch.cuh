@@ -1,0 +1,218 @@
+// fsg_batch.cuh -- batched throughput coupled step: E independent env
+// sessions of one configuration stepped by ONE marker launch and ONE banded
+// K4 launch (BASELINE config 5: 64 envs, 8 per GPU).
+// Included inside namespace fsg::p32 after fsg_ib_fix.cuh.
+//
+// The envs share one configuration, so the grid (dims and the pull/own
+// offsets, in the constant bank) and the session constants are common
+// kernel parameters; each env contributes an EnvPack (state pointers, frame
+// constants, tile stamp, markers, outputs) uploaded by the host per step and
+// staged in shared memory when a block moves to that env.  Work is flattened
+// across envs -- markers, phase-A items and band tiles by prefix offsets --
+// so the small per-env grids fill the GPU together and the launch overhead is
+// paid once per batch.  Arithmetic per cell and per marker is exactly the
+// single-session kernels' (bit-identical results, tests/test_batch_gpu.py).
+
+/// env of global index v given the prefix field of each pack (linear scan in
+/// shared memory; E <= 64)
+__device__ __forceinline__ int env_of(const int* pref, int E, int v) {
+  int e = 0;
+  while (e + 1 < E && pref[e + 1] <= v) ++e;
+  return e;
+}
+
+/// cell_update addressed from the env's state base pointers: the 19 source
+/// and destination offsets are the common grid's (constant bank).
+template <bool PULLED, bool VF>
+__device__ __forceinline__ float cell_update_ab(const Grid& g, const float* __restrict__ A,
+                                                float* __restrict__ B, int x, int y, int z,
+                                                float Fx, float Fy, float Fz,
+                                                const SessionConsts& sc, const StepConsts& st,
+                                                StepScratch* out) {
+  const int m = (int)mem_index(g, x, y, z);
+  const int zg = g.z0 + z;
+  float s[Q];
+  if (!PULLED) {
+#pragma unroll
+    for (int i = 0; i < Q; ++i) s[i] = __ldg(A + (m + (int)g.own[i]));
+  } else if (y > 0 && y < g.ny - 1 && zg > 0 && zg < g.nzg - 1) {
+    const int cxp = x == 0 ? (g.periodic ? g.nx : 1) : 0;
+    const int cxm = x == g.nx - 1 ? (g.periodic ? -g.nx : -1) : 0;
+#pragma unroll
+    for (int i = 0; i < Q; ++i) {
+      const int cx = ex_of(i) > 0 ? cxp : (ex_of(i) < 0 ? cxm : 0);
+      s[i] = __ldg(A + (m + (int)g.pull[i] + cx));
+    }
+  } else {
+    gather<true>(g, A, x, y, z, s);
+  }
+  Band none{nullptr, 0};
+  const float v = collide_cell32<3, VF>(s, x, y, z, g, Fx, Fy, Fz, false, 0, none, sc, st, out);
+#pragma unroll
+  for (int i = 0; i < Q; ++i) B[m + (int)g.own[i]] = s[i];
+  return v;
+}
+
+/// PMODE: 1 every env pulled, 0 none (first step after set/init/recenter),
+/// 2 mixed (runtime flag per env).  The frame mode is the batch's (VF).
+template <int PMODE, bool VF>
+__device__ __forceinline__ float cell_update_env(const Grid& g, const SessionConsts& sc,
+                                                 const EnvPack& P, int x, int y, int z, float Fx,
+                                                 float Fy, float Fz) {
+  if (PMODE == 1 || (PMODE == 2 && P.pulled))
+    return cell_update_ab<true, VF>(g, P.A, P.B, x, y, z, Fx, Fy, Fz, sc, P.st, P.out);
+  return cell_update_ab<false, VF>(g, P.A, P.B, x, y, z, Fx, Fy, Fz, sc, P.st, P.out);
+}
+
+/// Per-env status minimum: warp min, then a fire-and-forget atomic by lane 0
+/// (a block's consecutive items usually belong to different envs).  All 32
+/// lanes must call it.
+__device__ __forceinline__ void report_min_red(StepScratch* out, float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fminf(v, __shfl_xor_sync(0xffffffffu, v, o));
+  if ((threadIdx.x & 31) == 0 && v < FLT_MAX) atomicMax(&out->neg_min_key, ~ordered_key((double)v));
+}
+
+/// Stage pack e into shared memory (block-uniform e; all threads call).
+__device__ __forceinline__ void stage_pack(EnvPack& dst, const EnvPack* __restrict__ packs, int e,
+                                           int tid, int nthr) {
+  constexpr int NW = (int)(sizeof(EnvPack) / 4);
+  const int* src = reinterpret_cast<const int*>(packs + e);
+  int* d = reinterpret_cast<int*>(&dst);
+  for (int k = tid; k < NW; k += nthr) d[k] = __ldg(src + k);
+}
+
+__global__ void __launch_bounds__(128, FSG_KM_MINB)
+    k_markers_batch(Grid g, const SessionConsts* __restrict__ scp, const EnvPack* __restrict__ packs,
+                    BatchHead h) {
+  __shared__ double phs[FX_PER_BLOCK][3][5];
+  __shared__ int mkb[BATCH_MAX];
+  for (int e = threadIdx.x; e < h.E; e += blockDim.x) mkb[e] = packs[e].mk_begin;
+  __syncthreads();
+  const int lane = threadIdx.x & (FX_LANES - 1);
+  const int slot = threadIdx.x / FX_LANES;
+  const int tg = blockIdx.x * FX_PER_BLOCK + slot;
+  const bool live = tg < h.m_total;
+  const EnvPack& P = packs[live ? env_of(mkb, h.E, tg) : 0];
+  const int t = tg - P.mk_begin;
+  const SessionConsts& sc = *scp;
+  FixBand fb{P.F, P.tflag, h.tnx, h.tny, h.tnz, P.stamp};
+  MkStencil S;
+  S.ok = false;
+  if (live) {
+    mk_stencil(P.mk, t, sc, P.st, S);
+    mk_stamp(g, fb, S, lane);
+  }
+  __syncthreads();  // all stamps of the block before the K4 trigger (k_markers_fix)
+  if (threadIdx.x == 0) __threadfence();
+  __syncthreads();
+  asm volatile("griddepcontrol.launch_dependents;");
+  if (!live) return;
+  if (P.pulled)
+    mk_finish<true>(g, P.A, P.mk, t, lane, sc, P.st, S, phs[slot], P.rec, P.fworld, P.fworld_h,
+                    P.valid_h, fb, P.out);
+  else
+    mk_finish<false>(g, P.A, P.mk, t, lane, sc, P.st, S, phs[slot], P.rec, P.fworld, P.fworld_h,
+                     P.valid_h, fb, P.out);
+}
+
+/// Banded K4 over every env (see k_collide_band); a programmatic dependent
+/// of k_markers_batch.  The status minimum is reported per env.
+template <int PMODE, bool VF>
+__global__ void __launch_bounds__(128, FSG_K4_MINB)
+    k_collide_band_batch(Grid g, const SessionConsts* __restrict__ scp,
+                         const EnvPack* __restrict__ packs, BatchHead h, unsigned* work) {
+  __shared__ int item;
+  __shared__ int tl[128];
+  __shared__ int ntl;
+  __shared__ int ib[BATCH_MAX], tb[BATCH_MAX];
+  __shared__ __align__(16) EnvPack P;  // the env of the current item
+  const int tid = threadIdx.x + blockDim.x * threadIdx.y;
+  const int nthr = blockDim.x * blockDim.y;
+  const SessionConsts& sc = *scp;
+  for (int e = tid; e < h.E; e += nthr) {
+    ib[e] = packs[e].item_begin;
+    tb[e] = packs[e].tile_begin;
+  }
+  if (blockIdx.x == 0) {  // zero every env's next-step scratch
+    constexpr int NS = (int)(sizeof(StepScratch) / 4);
+    for (int k = tid; k < h.E * NS; k += nthr) reinterpret_cast<int*>(packs[k / NS].next)[k % NS] = 0;
+  }
+  __syncthreads();
+  const int tx_n = (g.nx + blockDim.x - 1) / blockDim.x;
+  const int ty_n = (g.ny + blockDim.y - 1) / blockDim.y;
+  const int ncol = tx_n * ty_n;
+  int cur = -1;
+  // ---- phase A: every env's cells outside its stamped tiles.  A fetch takes
+  // CH consecutive items (CH = 4 kept blocks within one env longer but left
+  // too few work units for small batches: E = 8 unchanged, E = 1 slower)
+  constexpr int CH = 1;
+  int nxt = 0;
+  if (tid == 0) nxt = (int)atomicAdd(work, 1u) * CH;
+  int itg = h.item_total, iend = 0;
+  for (;;) {
+    if (itg >= iend) {  // block-uniform: next chunk
+      if (tid == 0) item = nxt;
+      __syncthreads();
+      itg = item;
+      iend = min(itg + CH, h.item_total);
+      if (itg >= h.item_total) break;
+      if (tid == 0) nxt = (int)atomicAdd(work, 1u) * CH;
+    }
+    const int e = env_of(ib, h.E, itg);
+    if (e != cur) {  // block-uniform
+      __syncthreads();  // nobody still reads the previous pack
+      stage_pack(P, packs, e, tid, nthr);
+      cur = e;
+      __syncthreads();
+    }
+    const int it = itg - P.item_begin;
+    const int col = it % ncol, zk = it / ncol;
+    const int x = (col % tx_n) * blockDim.x + threadIdx.x;
+    const int y = (col / tx_n) * blockDim.y + threadIdx.y;
+    const int z0 = zk * h.zc, z1 = min(g.nz, z0 + h.zc);
+    float vmin = FLT_MAX;
+    // stamped tiles are the band phase's (one stamp load per tile-aligned item)
+    if (x < g.nx && y < g.ny &&
+        __ldcg(P.tflag + (x >> 2) + h.tnx * ((y >> 2) + h.tny * (z0 >> 2))) != P.stamp)
+      for (int z = z0; z < z1; ++z)
+        vmin = fminf(vmin, cell_update_env<PMODE, VF>(g, sc, P, x, y, z, 0.f, 0.f, 0.f));
+    report_min_red(P.out, vmin);
+    ++itg;
+    if (itg >= iend) __syncthreads();  // `item` is rewritten for the next chunk
+  }
+  // ---- phase B: every env's stamped tiles, after the marker grid completed
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  const int tpp = nthr >> 6;
+  const int half = tid >> 6, lt = tid & 63;
+  for (int base = 0; (long long)base * gridDim.x < h.tile_total; base += nthr) {
+    if (tid == 0) ntl = 0;
+    __syncthreads();
+    const long long T0 = (long long)blockIdx.x + (long long)gridDim.x * (base + tid);
+    if (T0 < h.tile_total) {
+      const EnvPack& Q0 = packs[env_of(tb, h.E, (int)T0)];
+      if (Q0.tflag[T0 - Q0.tile_begin] == Q0.stamp) tl[atomicAdd(&ntl, 1)] = (int)T0;
+    }
+    __syncthreads();
+    const int n = half < tpp ? ntl : 0;
+    for (int k = half; k < n; k += tpp) {
+      const int Tg = tl[k];
+      const EnvPack& R = packs[env_of(tb, h.E, Tg)];
+      const int T = Tg - R.tile_begin;
+      const int tx = T % h.tnx, ty = (T / h.tnx) % h.tny, tz = T / (h.tnx * h.tny);
+      const int x = 4 * tx + (lt & 3), y = 4 * ty + ((lt >> 2) & 3), z = 4 * tz + (lt >> 4);
+      float v = FLT_MAX;
+      if (x < g.nx && y < g.ny && z < g.nz) {
+        unsigned long long* F = R.F + 3 * ((long long)x + (long long)g.nx * ((long long)y + (long long)g.ny * z));
+        const long long f0 = (long long)F[0], f1 = (long long)F[1], f2 = (long long)F[2];
+        F[0] = 0ull;
+        F[1] = 0ull;
+        F[2] = 0ull;
+        v = cell_update_env<PMODE, VF>(g, sc, R, x, y, z, (float)((double)f0 * FIX_INV),
+                                       (float)((double)f1 * FIX_INV), (float)((double)f2 * FIX_INV));
+      }
+      report_min_red(R.out, v);
+    }
+    __syncthreads();
+  }
+}

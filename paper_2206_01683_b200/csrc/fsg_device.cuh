@@ -199,6 +199,54 @@ struct Band {
   long long cap;     // capacity in cells
 };
 
+// Cell-kernel block shape: up to 128 threads along x, the rest along y.
+inline dim3 cell_block_dims(const Grid& g) {
+  int bx = g.nx >= 128 ? 128 : ((g.nx + 31) / 32) * 32;
+  if (bx > 128) bx = 128;
+  return dim3(bx, 128 / bx, 1);
+}
+
+// Throughput kernels address the 19 pull sources / destinations through
+// per-direction base pointers passed as kernel parameters.
+struct DirPtrs {
+  const float* a[Q];  // A + pull[i]  (interior pull source of direction i)
+  float* b[Q];        // B + own[i]   (destination plane of direction i)
+};
+
+// Batched throughput step (fsg_batch.cuh): the envs share one configuration,
+// so the grid geometry (with its pull/own offsets) and the session constants
+// are common kernel parameters; each env contributes one small pack per step.
+struct EnvPack {
+  StepConsts st;           // this env's frame constants
+  const float* A;          // state read this step
+  float* B;                // state written this step
+  unsigned long long* F;   // fixed-point IB force
+  unsigned* tflag;         // tile stamps
+  Markers mk;
+  MarkerStencil* rec;
+  double* fworld;
+  double* fworld_h;
+  int* valid_h;
+  StepScratch* out;
+  StepScratch* next;
+  unsigned stamp;
+  int pulled, frame_on;
+  int mk_begin;            // first global marker index of this env
+  int item_begin;          // first global phase-A item
+  int tile_begin;          // first global band tile
+};
+
+constexpr int BATCH_MAX = 64;
+
+struct BatchHead {
+  int E;
+  int m_total, item_total, tile_total;
+  int tnx, tny, tnz;       // tile grid (every env)
+  int zc;                  // phase-A planes per item
+  int frame_on;            // the batch's frame mode is not None
+  int pmode;               // 1 every env pulled, 0 none, 2 mixed
+};
+
 // ---------------------------------------------------------- kernel table --
 // Launchers exported by each precision translation unit.
 struct Launchers {
@@ -242,6 +290,10 @@ struct Launchers {
   void (*collide_band)(const Grid&, const void* A, int pulled, void* B, FixBand,
                        const SessionConsts*, const StepConsts& st, int frame_on,
                        StepScratch* scr, StepScratch* scr_next, int pdl, cudaStream_t);
+  // batched coupled step over E env sessions (fp32): markers + banded K4 of
+  // every env in one launch each; d_packs: E EnvPacks in device memory
+  void (*step_batch)(const Grid&, const SessionConsts*, const EnvPack* d_packs, BatchHead h,
+                     dim3 block, unsigned* work, cudaStream_t);
   // halo planes (z-slab): pack owned boundary planes / unpack into halo planes
   void (*halo_pack)(const Grid&, const void* B, void* send_lo, void* send_hi, cudaStream_t);
   void (*halo_unpack)(const Grid&, void* B, const void* recv_lo, const void* recv_hi,

@@ -6,10 +6,7 @@
 // offsets folded into those pointers; boundary cells take the generic
 // clamped/periodic gather (solver.hpp:59-97 re-expressed as a pull).
 
-struct DirPtrs {
-  const float* a[Q];  // A + pull[i]  (interior pull source of direction i)
-  float* b[Q];        // B + own[i]   (destination plane of direction i)
-};
+// DirPtrs (fsg_device.cuh): per-direction base pointers A + pull[i] / B + own[i]
 
 template <int FMODE, bool VF>
 __global__ void __launch_bounds__(128)

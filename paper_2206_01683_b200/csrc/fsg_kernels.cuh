@@ -661,6 +661,7 @@ __global__ void k_recenter(Grid g, const Store* __restrict__ A, Store* __restric
 #include "fsg_ib.cuh"
 #if FSG_PREC == 32
 #include "fsg_ib_fix.cuh"
+#include "fsg_batch.cuh"
 #endif
 
 // ======================================================= halo (slabs) ====
@@ -692,11 +693,7 @@ __global__ void k_halo_unpack(Grid g, Store* B, const Store* __restrict__ recv_l
 }
 
 // ======================================================== launchers =====
-inline dim3 cell_block(const Grid& g) {
-  int bx = g.nx >= 128 ? 128 : ((g.nx + 31) / 32) * 32;
-  if (bx > 128) bx = 128;
-  return dim3(bx, 128 / bx, 1);
-}
+inline dim3 cell_block(const Grid& g) { return cell_block_dims(g); }
 inline dim3 cell_grid(const Grid& g, dim3 b) {
   return dim3((g.nx + b.x - 1) / b.x, (g.ny + b.y - 1) / b.y, g.nz);
 }
@@ -891,6 +888,42 @@ static void L_collide_fix(const Grid& g, const void* A, int pulled, void* B,
 #undef FSG_LF
 }
 
+// Batched step: markers of every env, then the batched banded K4 as their
+// programmatic dependent.  work: this step's phase-A counter (zeroed).
+static void L_step_batch(const Grid& g, const SessionConsts* sc, const EnvPack* d_packs,
+                         BatchHead h, dim3 block, unsigned* work, cudaStream_t s) {
+  static int nsm = 0, res = 0;
+  if (!nsm) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&res, k_collide_band_batch<2, true>, 128, 0);
+    res = std::max(res, 1);
+  }
+  if (h.m_total > 0)
+    k_markers_batch<<<(h.m_total + FX_PER_BLOCK - 1) / FX_PER_BLOCK, 128, 0, s>>>(g, sc, d_packs, h);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)std::min<long long>(h.item_total, (long long)nsm * res));
+  cfg.blockDim = block;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = h.m_total > 0 ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+#define FSG_BB(PM, V) cudaLaunchKernelEx(&cfg, k_collide_band_batch<PM, V>, g, sc, d_packs, h, work)
+  if (h.frame_on) {
+    if (h.pmode == 1) FSG_BB(1, true);
+    else if (h.pmode == 0) FSG_BB(0, true);
+    else FSG_BB(2, true);
+  } else {
+    if (h.pmode == 1) FSG_BB(1, false);
+    else if (h.pmode == 0) FSG_BB(0, false);
+    else FSG_BB(2, false);
+  }
+#undef FSG_BB
+}
+
 // Banded K4 as a programmatic dependent of the marker kernel just launched on
 // the same stream (see k_collide_band).
 static void L_collide_band(const Grid& g, const void* A, int pulled, void* B, FixBand fb,
@@ -945,9 +978,9 @@ static const Launchers kLaunchers = {
     L_fill_rest,    L_set_f,          L_init_eq,      L_get_f,         L_macroscopic,
     L_collide,      L_session_force,  L_recenter,     L_markers,       L_spread,
 #if FSG_PREC == 32
-    L_markers_fix,  L_collide_fix,    L_collide_band,
+    L_markers_fix,  L_collide_fix,    L_collide_band, L_step_batch,
 #else
-    nullptr,        nullptr,          nullptr,
+    nullptr,        nullptr,          nullptr,        nullptr,
 #endif
     L_halo_pack,    L_halo_unpack,    (int)sizeof(Store)};
 

@@ -46,6 +46,8 @@ using fsg::StepScratch;
 namespace {
 
 thread_local char g_err[1024] = "";
+// fsg_batch_create: sessions created while this is set adopt the batch's stream
+thread_local cudaStream_t g_shared_stream = nullptr;
 
 int set_err(int code, const char* fmt, ...) {
   va_list ap;
@@ -105,6 +107,7 @@ struct fsg_session {
   const Launchers* L = nullptr;
   Grid g{};
   cudaStream_t stream = nullptr;
+  bool own_stream = true;  // false: a batch's shared stream
   void* buf[2] = {nullptr, nullptr};
   int par = 0;     // A = buf[par], B = buf[par ^ 1]
   int pulled = 0;  // A holds post-collision P (1) or post-stream S (0)
@@ -464,7 +467,12 @@ int fsg_create(const fsg_config* cfg_in, fsg_session** out) {
     if (e_ != cudaSuccess)                                                             \
       return fail(set_err(FSG_ECUDA, "%s failed: %s", #call, cudaGetErrorString(e_))); \
   } while (0)
-  CUF(cudaStreamCreateWithFlags(&s->stream, cudaStreamNonBlocking));
+  if (g_shared_stream) {
+    s->stream = g_shared_stream;
+    s->own_stream = false;
+  } else {
+    CUF(cudaStreamCreateWithFlags(&s->stream, cudaStreamNonBlocking));
+  }
   const size_t fbytes = (size_t)s->L->elem_bytes * 19 * (size_t)g.stride;
   for (int k = 0; k < 2; ++k) {
     CUF(cudaMalloc(&s->buf[k], fbytes));
@@ -574,7 +582,7 @@ int fsg_destroy(fsg_session* s) {
   cudaFree(s->d_diag);
   cudaFree(s->d_tmp);
   cudaFree(s->d_red);
-  if (s->stream) cudaStreamDestroy(s->stream);
+  if (s->stream && s->own_stream) cudaStreamDestroy(s->stream);
   delete s;
   return FSG_OK;
 }
@@ -1131,6 +1139,177 @@ int fsg_halo_end(fsg_session* s, void* comm_stream, int have_lo, int have_hi) {
     s->L->halo_unpack(s->g, s->A(), have_lo ? s->d_hrecv[0] : nullptr,
                       have_hi ? s->d_hrecv[1] : nullptr, s->stream);
     CU_LAUNCH();
+  }
+  return FSG_OK;
+}
+
+
+// ---------------------------------------------------------------- batch --
+// E env sessions of one configuration sharing one stream, stepped together
+// by ONE marker launch and ONE banded K4 launch (fsg_batch.cuh; SURVEY.md
+// §8(e): the batched-RL config, 8 envs per GPU).  Env e is an ordinary
+// fsg_session (fsg_batch_session): frames, markers and every readback use
+// the per-session calls.
+struct fsg_batch {
+  int E = 0;
+  cudaStream_t stream = nullptr;
+  std::vector<fsg_session*> envs;
+  fsg::EnvPack* h_packs[2] = {nullptr, nullptr};  // pinned, by batch step parity
+  fsg::EnvPack* d_packs[2] = {nullptr, nullptr};
+  unsigned* d_work = nullptr;                      // [2] phase-A counters by parity
+  cudaEvent_t ev[2] = {nullptr, nullptr};
+  int par = 0;
+  dim3 block;
+};
+
+int fsg_batch_destroy(fsg_batch* b) {
+  if (!b) return FSG_OK;
+  if (b->stream) cudaStreamSynchronize(b->stream);
+  for (auto* s : b->envs) fsg_destroy(s);
+  for (int k = 0; k < 2; ++k) {
+    if (b->h_packs[k]) cudaFreeHost(b->h_packs[k]);
+    cudaFree(b->d_packs[k]);
+    if (b->ev[k]) cudaEventDestroy(b->ev[k]);
+  }
+  cudaFree(b->d_work);
+  if (b->stream) cudaStreamDestroy(b->stream);
+  delete b;
+  return FSG_OK;
+}
+
+int fsg_batch_create(const fsg_config* cfg, int n_envs, fsg_batch** out) {
+  if (!cfg || !out) return set_err(FSG_EINPUT, "fsg_batch_create: null argument");
+  *out = nullptr;
+  if (n_envs < 1 || n_envs > fsg::BATCH_MAX)
+    return set_err(FSG_EINPUT, "a batch holds 1..%d envs (got %d)", fsg::BATCH_MAX, n_envs);
+  if (cfg->precision != FSG_PRECISION_FP32)
+    return set_err(FSG_EINPUT, "batches run the throughput (fp32) step");
+  if (cfg->z_offset != 0 || (cfg->nz_global > 0 && cfg->nz_global != cfg->dims[2]))
+    return set_err(FSG_EINPUT, "batch envs are whole grids, not z-slabs");
+  CU(cudaSetDevice(cfg->device));
+  fsg_batch* b = new fsg_batch();
+  b->E = n_envs;
+  auto fail = [&](int code) {
+    g_shared_stream = nullptr;
+    fsg_batch_destroy(b);
+    return code;
+  };
+#define CUB(call)                                                                      \
+  do {                                                                                 \
+    cudaError_t e_ = (call);                                                           \
+    if (e_ != cudaSuccess)                                                             \
+      return fail(set_err(FSG_ECUDA, "%s failed: %s", #call, cudaGetErrorString(e_))); \
+  } while (0)
+  CUB(cudaStreamCreateWithFlags(&b->stream, cudaStreamNonBlocking));
+  g_shared_stream = b->stream;
+  for (int e = 0; e < n_envs; ++e) {
+    fsg_session* s = nullptr;
+    const int rc = fsg_create(cfg, &s);
+    if (rc) return fail(rc);
+    b->envs.push_back(s);
+  }
+  g_shared_stream = nullptr;
+  for (int k = 0; k < 2; ++k) {
+    CUB(cudaMallocHost(&b->h_packs[k], sizeof(fsg::EnvPack) * n_envs));
+    CUB(cudaMalloc(&b->d_packs[k], sizeof(fsg::EnvPack) * n_envs));
+    CUB(cudaEventCreateWithFlags(&b->ev[k], cudaEventDisableTiming));
+    CUB(cudaEventRecord(b->ev[k], b->stream));
+  }
+  CUB(cudaMalloc(&b->d_work, sizeof(unsigned) * 2));
+  CUB(cudaMemsetAsync(b->d_work, 0, sizeof(unsigned) * 2, b->stream));
+  b->block = fsg::cell_block_dims(b->envs[0]->g);
+#undef CUB
+  *out = b;
+  return FSG_OK;
+}
+
+fsg_session* fsg_batch_session(fsg_batch* b, int e) {
+  return (b && e >= 0 && e < b->E) ? b->envs[e] : nullptr;
+}
+
+int fsg_batch_step_async(fsg_batch* b) {
+  CU(cudaSetDevice(b->envs[0]->cfg.device));
+  const int q = b->par;
+  CU(cudaEventSynchronize(b->ev[q]));  // pinned packs of parity q are free again
+  fsg::EnvPack* packs = b->h_packs[q];
+  const fsg::Grid& g0 = b->envs[0]->g;
+  const fsg::FixBand& fb0 = b->envs[0]->fix;
+  fsg::BatchHead h{b->E, 0, 0, 0, fb0.tnx, fb0.tny, fb0.tnz, 1,
+                   b->envs[0]->cfg.frame_mode != FSG_FRAME_NONE ? 1 : 0, 0};
+  int npulled = 0;
+  const int tx_n = (g0.nx + (int)b->block.x - 1) / (int)b->block.x;
+  const int ty_n = (g0.ny + (int)b->block.y - 1) / (int)b->block.y;
+  // phase-A items: 2 planes when that still leaves >= 8 per resident block
+  const long long per_env2 = (long long)tx_n * ty_n * ((g0.nz + 1) / 2);
+  const int zc = (g0.plane < (1 << 17) && per_env2 * b->E >= 8ll * 148 * 6) ? 2 : 1;
+  h.zc = zc;
+  for (int e = 0; e < b->E; ++e) {
+    fsg_session* s = b->envs[e];
+    const int p = s->par;
+    frame_consts(s->frame, *s->h_st[p]);
+    const StepConsts st = *s->h_st[p];
+    s->last_st = st;
+    if (s->mk_host && s->mk_dirty) CU(cudaStreamWaitEvent(b->stream, s->ev_cp[s->mk_slot], 0));
+    if (s->scr_dirty[p]) CU(cudaMemsetAsync(s->d_scr[p], 0, sizeof(StepScratch), b->stream));
+    fsg::EnvPack& P = packs[e];
+    P.st = st;
+    P.A = (const float*)s->buf[p];
+    P.B = (float*)s->buf[p ^ 1];
+    P.F = s->fix.F;
+    P.tflag = s->fix.tflag;
+    P.stamp = ++s->stamp;  // fresh: with no markers no tile carries it
+    P.mk = s->mk;
+    P.rec = s->d_stencil;
+    P.fworld = s->d_fworld;
+    P.fworld_h = s->h_fw[p];
+    P.valid_h = s->h_valid[p];
+    P.out = s->d_scr[p];
+    P.next = s->d_scr[p ^ 1];
+    P.pulled = s->pulled;
+    P.frame_on = s->cfg.frame_mode != FSG_FRAME_NONE;
+    P.mk_begin = h.m_total;
+    P.item_begin = h.item_total;
+    P.tile_begin = h.tile_total;
+    h.m_total += s->m;  // (device or host markers; host ones were uploaded on the copy stream)
+    npulled += s->pulled ? 1 : 0;
+    h.item_total += tx_n * ty_n * ((s->g.nz + zc - 1) / zc);
+    h.tile_total += s->fix.tnx * s->fix.tny * s->fix.tnz;
+  }
+  h.pmode = npulled == b->E ? 1 : (npulled == 0 ? 0 : 2);
+  CU(cudaMemcpyAsync(b->d_packs[q], packs, sizeof(fsg::EnvPack) * b->E, cudaMemcpyHostToDevice,
+                     b->stream));
+  CU(cudaMemsetAsync(b->d_work + q, 0, sizeof(unsigned), b->stream));
+  b->envs[0]->L->step_batch(g0, b->envs[0]->d_sc, b->d_packs[q], h, b->block, b->d_work + q,
+                            b->stream);
+  CU_LAUNCH();
+  CU(cudaEventRecord(b->ev[q], b->stream));
+  for (fsg_session* s : b->envs) {
+    const int p = s->par;
+    if (s->mk_host && s->mk_slot >= 0) {
+      CU(cudaEventRecord(s->ev_mk[s->mk_slot], b->stream));
+      s->last_mk_slot = s->mk_slot;
+    }
+    s->scr_dirty[p] = true;
+    s->scr_dirty[p ^ 1] = false;
+    s->last_par = p;
+    s->prev_pulled = s->pulled;
+    s->last_frame_on = s->cfg.frame_mode != FSG_FRAME_NONE;
+    s->par ^= 1;
+    s->pulled = 1;
+    s->last_valid = true;
+    s->stepped = true;
+    s->mk_dirty = false;
+  }
+  b->par ^= 1;
+  return FSG_OK;
+}
+
+int fsg_batch_step(fsg_batch* b, fsg_status* statuses) {
+  int rc = fsg_batch_step_async(b);
+  if (rc) return rc;
+  for (int e = 0; e < b->E; ++e) {
+    rc = fsg_last_status(b->envs[e], statuses ? &statuses[e] : nullptr);
+    if (rc) return rc;
   }
   return FSG_OK;
 }

@@ -168,11 +168,15 @@ class FrameFollower:
 class CoupledSession:
     """One device-resident IB-LBM domain (sim::CoupledSession, session.hpp:29-224)."""
 
-    def __init__(self, cfg: SessionConfig):
+    def __init__(self, cfg: SessionConfig, _borrowed=None):
         self.cfg = cfg
         L = _abi.lib()
-        h = C.c_void_p()
-        check(L.fsg_create(C.byref(cfg.to_c()), C.byref(h)))
+        if _borrowed is None:
+            h = C.c_void_p()
+            check(L.fsg_create(C.byref(cfg.to_c()), C.byref(h)))
+        else:
+            h = C.c_void_p(_borrowed)  # an env of an EnvBatch: the batch owns it
+        self._owned = _borrowed is None
         self._h = h
         self._L = L
         self._fs_c = _abi.fsg_frame_state()
@@ -188,7 +192,8 @@ class CoupledSession:
     # -- lifetime --------------------------------------------------------
     def close(self) -> None:
         if getattr(self, "_h", None):
-            _abi.lib().fsg_destroy(self._h)
+            if getattr(self, "_owned", True):
+                _abi.lib().fsg_destroy(self._h)
             self._h = None
 
     def __del__(self):
@@ -393,3 +398,42 @@ class CoupledSession:
     def halo_end(self, comm_stream: int, have_lo: bool, have_hi: bool) -> None:
         """The session waits for comm_stream, then unpacks the received planes."""
         check(_abi.lib().fsg_halo_end(self._h, comm_stream, int(have_lo), int(have_hi)))
+
+
+class EnvBatch:
+    """n_envs independent env sessions of one fp32 configuration stepped
+    together by one marker launch and one collide/stream launch
+    (fsg_batch_*; BASELINE config 5).  ``envs[e]`` is an ordinary
+    CoupledSession: set its frame and markers, read its status, forces and
+    fields as usual; the batch owns it."""
+
+    def __init__(self, cfg: SessionConfig, n_envs: int):
+        L = _abi.lib()
+        h = C.c_void_p()
+        check(L.fsg_batch_create(C.byref(cfg.to_c()), int(n_envs), C.byref(h)))
+        self._h, self._L = h, L
+        self.envs = [CoupledSession(cfg, _borrowed=L.fsg_batch_session(h, e)) for e in range(n_envs)]
+
+    def step_async(self) -> None:
+        rc = self._L.fsg_batch_step_async(self._h)
+        if rc:
+            check(rc)
+
+    def step(self) -> list:
+        """One coupled step of every env -> per-env StepStatus."""
+        sts = (_abi.fsg_status * len(self.envs))()
+        check(self._L.fsg_batch_step(self._h, sts))
+        return [StepStatus.of(x) for x in sts]
+
+    def close(self) -> None:
+        if getattr(self, "_h", None):
+            for s in self.envs:
+                s.close()
+            self._L.fsg_batch_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
