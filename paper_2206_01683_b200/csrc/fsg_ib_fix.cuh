@@ -17,8 +17,16 @@
 // The per-marker work is split into device functions (stencil, stamp, finish)
 // so the kernel's block-level stamp / fence / trigger sequence stays visible.
 
-constexpr int FX_LANES = 32;     // one warp per marker
-constexpr int FX_PER_BLOCK = 4;  // markers per 128-thread block
+#ifndef FSG_FX_LANES
+#define FSG_FX_LANES 32
+#endif
+constexpr int FX_LANES = FSG_FX_LANES;     // lanes per marker (a warp or half a warp)
+constexpr int FX_PER_BLOCK = 128 / FX_LANES;  // markers per 128-thread block
+
+/// shuffle mask of this thread's marker group
+__device__ __forceinline__ unsigned fx_mask() {
+  return FX_LANES == 32 ? 0xFFFFFFFFu : (0xFFFFu << (threadIdx.x & 16));
+}
 constexpr int FX_CPL = 1;        // stencil cells per lane per round trip (register pressure)
 
 __device__ __forceinline__ unsigned long long to_fix(double v) {
@@ -73,7 +81,7 @@ __device__ __forceinline__ void mk_finish(const Grid& g, const float* __restrict
                                           MarkerStencil* __restrict__ rec_out, double* __restrict__ fworld,
                                           double* fworld_h, int* valid_h, const FixBand& fb,
                                           StepScratch* out) {
-  constexpr unsigned full = 0xFFFFFFFFu;
+  const unsigned full = fx_mask();
   if (!S.ok) {
     if (lane == 0) {
       rec_out[t].valid = 0;
