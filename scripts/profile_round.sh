@@ -9,6 +9,7 @@ mkdir -p $out
 C2="python bench.py --workload c2 --steps 30 --warmup 5 --e2e-steps 5 --no-cpu-baseline"
 C3="python bench.py --workload c3 --steps 12 --warmup 4 --e2e-steps 2 --no-cpu-baseline"
 C4="python bench.py --workload c4 --steps 6 --warmup 3 --e2e-steps 2 --no-cpu-baseline"
+C5="python bench.py --workload c5 --steps 10 --warmup 3 --e2e-steps 2 --no-cpu-baseline"
 # launch list of the headline workload (cold-cache, serialised)
 $C2 > $out/${tag}_c2_plain.log 2>&1 &&
 ncu --metrics gpu__time_duration.sum --clock-control none -c 800 --csv \
@@ -24,4 +25,8 @@ ncu --set full --clock-control none --import-source on -k regex:"k_collide_band|
 $C4 > $out/${tag}_c4_plain.log 2>&1 &&
 ncu --set full --clock-control none --import-source on -k regex:"k_collide_fix" \
     -s 3 -c 1 -o $out/${tag}_c4_full $C4 > $out/${tag}_c4_ncu_full.log 2>&1
+# c5: the batched env kernels (8 envs)
+$C5 > $out/${tag}_c5_plain.log 2>&1 &&
+ncu --set full --clock-control none --import-source on -k regex:"batch" \
+    -s 6 -c 2 -o $out/${tag}_c5_full $C5 > $out/${tag}_c5_ncu_full.log 2>&1
 ls -la $out/${tag}_*
