@@ -73,15 +73,12 @@ __device__ __forceinline__ void report_min_red(StepScratch* out, float v) {
   if ((threadIdx.x & 31) == 0 && v < FLT_MAX) atomicMax(&out->neg_min_key, ~ordered_key((double)v));
 }
 
-/// Stage pack e into shared memory (block-uniform e; all threads call).
-__device__ __forceinline__ void stage_pack(EnvPack& dst, const EnvPack* __restrict__ packs, int e,
-                                           int tid, int nthr) {
-  constexpr int NW = (int)(sizeof(EnvPack) / 4);
-  const int* src = reinterpret_cast<const int*>(packs + e);
-  int* d = reinterpret_cast<int*>(&dst);
-  for (int k = tid; k < NW; k += nthr) d[k] = __ldg(src + k);
-}
-
+/// Persistent over the markers of every env (the grid is capped at a few
+/// blocks per SM: a batch's markers would otherwise take several waves, and
+/// the dependent K4 launches only once every marker block has triggered).
+/// Each group first stamps the tiles of ALL its markers, the block fences
+/// and triggers K4, then the groups do the heavy per-marker work (the cheap
+/// stencil is recomputed rather than kept).
 __global__ void __launch_bounds__(128, FSG_KM_MINB)
     k_markers_batch(Grid g, const SessionConsts* __restrict__ scp, const EnvPack* __restrict__ packs,
                     BatchHead h) {
@@ -91,29 +88,33 @@ __global__ void __launch_bounds__(128, FSG_KM_MINB)
   __syncthreads();
   const int lane = threadIdx.x & (FX_LANES - 1);
   const int slot = threadIdx.x / FX_LANES;
-  const int tg = blockIdx.x * FX_PER_BLOCK + slot;
-  const bool live = tg < h.m_total;
-  const EnvPack& P = packs[live ? env_of(mkb, h.E, tg) : 0];
-  const int t = tg - P.mk_begin;
+  const int stride = gridDim.x * FX_PER_BLOCK;
   const SessionConsts& sc = *scp;
-  FixBand fb{P.F, P.tflag, h.tnx, h.tny, h.tnz, P.stamp};
-  MkStencil S;
-  S.ok = false;
-  if (live) {
-    mk_stencil(P.mk, t, sc, P.st, S);
+  for (int tg = blockIdx.x * FX_PER_BLOCK + slot; tg < h.m_total; tg += stride) {
+    const EnvPack& P = packs[env_of(mkb, h.E, tg)];
+    const FixBand fb{P.F, P.tflag, h.tnx, h.tny, h.tnz, P.stamp};
+    MkStencil S;
+    mk_stencil(P.mk, tg - P.mk_begin, sc, P.st, S);
     mk_stamp(g, fb, S, lane);
   }
   __syncthreads();  // all stamps of the block before the K4 trigger (k_markers_fix)
   if (threadIdx.x == 0) __threadfence();
   __syncthreads();
   asm volatile("griddepcontrol.launch_dependents;");
-  if (!live) return;
-  if (P.pulled)
-    mk_finish<true>(g, P.A, P.mk, t, lane, sc, P.st, S, phs[slot], P.rec, P.fworld, P.fworld_h,
-                    P.valid_h, fb, P.out);
-  else
-    mk_finish<false>(g, P.A, P.mk, t, lane, sc, P.st, S, phs[slot], P.rec, P.fworld, P.fworld_h,
-                     P.valid_h, fb, P.out);
+  for (int tg = blockIdx.x * FX_PER_BLOCK + slot; tg < h.m_total; tg += stride) {
+    const EnvPack& P = packs[env_of(mkb, h.E, tg)];
+    const FixBand fb{P.F, P.tflag, h.tnx, h.tny, h.tnz, P.stamp};
+    const int t = tg - P.mk_begin;
+    MkStencil S;
+    mk_stencil(P.mk, t, sc, P.st, S);
+    if (P.pulled)
+      mk_finish<true>(g, P.A, P.mk, t, lane, sc, P.st, S, phs[slot], P.rec, P.fworld, P.fworld_h,
+                      P.valid_h, fb, P.out);
+    else
+      mk_finish<false>(g, P.A, P.mk, t, lane, sc, P.st, S, phs[slot], P.rec, P.fworld, P.fworld_h,
+                       P.valid_h, fb, P.out);
+    __syncwarp(fx_mask());  // phs[slot] is reused by the group's next marker
+  }
 }
 
 /// Banded K4 over every env (see k_collide_band); a programmatic dependent
@@ -126,7 +127,6 @@ __global__ void __launch_bounds__(128, FSG_K4_MINB)
   __shared__ int tl[128];
   __shared__ int ntl;
   __shared__ int ib[BATCH_MAX], tb[BATCH_MAX];
-  __shared__ __align__(16) EnvPack P;  // the env of the current item
   const int tid = threadIdx.x + blockDim.x * threadIdx.y;
   const int nthr = blockDim.x * blockDim.y;
   const SessionConsts& sc = *scp;
@@ -142,7 +142,6 @@ __global__ void __launch_bounds__(128, FSG_K4_MINB)
   const int tx_n = (g.nx + blockDim.x - 1) / blockDim.x;
   const int ty_n = (g.ny + blockDim.y - 1) / blockDim.y;
   const int ncol = tx_n * ty_n;
-  int cur = -1;
   // ---- phase A: every env's cells outside its stamped tiles.  A fetch takes
   // CH consecutive items (CH = 4 kept blocks within one env longer but left
   // too few work units for small batches: E = 8 unchanged, E = 1 slower)
@@ -159,13 +158,11 @@ __global__ void __launch_bounds__(128, FSG_K4_MINB)
       if (itg >= h.item_total) break;
       if (tid == 0) nxt = (int)atomicAdd(work, 1u) * CH;
     }
-    const int e = env_of(ib, h.E, itg);
-    if (e != cur) {  // block-uniform
-      __syncthreads();  // nobody still reads the previous pack
-      stage_pack(P, packs, e, tid, nthr);
-      cur = e;
-      __syncthreads();
-    }
+    // the env's few per-item fields come straight from the (L1-resident)
+    // pack array: restaging a pack in shared memory on nearly every item (a
+    // block's successive items usually belong to different envs) costs an
+    // L2 round trip and two barriers
+    const EnvPack& P = packs[env_of(ib, h.E, itg)];
     const int it = itg - P.item_begin;
     const int col = it % ncol, zk = it / ncol;
     const int x = (col % tx_n) * blockDim.x + threadIdx.x;

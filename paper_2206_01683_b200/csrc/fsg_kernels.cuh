@@ -900,8 +900,10 @@ static void L_step_batch(const Grid& g, const SessionConsts* sc, const EnvPack* 
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&res, k_collide_band_batch<2, true>, 128, 0);
     res = std::max(res, 1);
   }
-  if (h.m_total > 0)
-    k_markers_batch<<<(h.m_total + FX_PER_BLOCK - 1) / FX_PER_BLOCK, 128, 0, s>>>(g, sc, d_packs, h);
+  if (h.m_total > 0) {
+    const int need = (h.m_total + FX_PER_BLOCK - 1) / FX_PER_BLOCK;
+    k_markers_batch<<<std::min(need, nsm * 4), 128, 0, s>>>(g, sc, d_packs, h);
+  }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)std::min<long long>(h.item_total, (long long)nsm * res));
   cfg.blockDim = block;
