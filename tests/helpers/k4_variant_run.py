@@ -10,7 +10,8 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspa
 from paper_2206_01683_b200 import CoupledSession, FrameState, SessionConfig  # noqa: E402
 out = {}
 for name, dims, bnd, fm in (("open", (64, 48, 40), "open", "translation_yaw"), ("per", (96, 32, 24), "periodic", "none"),
-                            ("wide", (256, 20, 12), "open", "full")):
+                            ("wide", (256, 20, 12), "open", "full"),
+                            ("per128", (128, 24, 20), "periodic", "translation_yaw")):
     s = CoupledSession(SessionConfig(dims=dims, dx=0.01, dt=0.004, boundary=bnd, frame_mode=fm, precision="fp32", max_markers=1))
     n = int(np.prod(dims)); r = np.random.default_rng(3)
     s.initialize(1.0 + 0.01 * (r.random(n) - 0.5), 0.03 * (r.random(3 * n) - 0.5))
