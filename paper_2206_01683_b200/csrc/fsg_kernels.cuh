@@ -434,7 +434,6 @@ __global__ void __launch_bounds__(128) k_collide(Grid g, const Store* __restrict
 #if FSG_PREC == 32
 #include "fsg_k4v4.cuh"
 #include "fsg_k4_tma.cuh"
-#include "fsg_k4_vec.cuh"
 #endif
 
 // ====================================================== small kernels =====
@@ -856,28 +855,6 @@ static void L_collide_fix(const Grid& g, const void* A, int pulled, void* B,
   if (planes == 2) zr = ZRange{1, g.nz - 1, 1};
   const int nq = (zr.hi - zr.lo + zr.step - 1) / zr.step;
   if (nq <= 0) return;
-  // 128-bit variant (fsg_k4_vec.cuh): rows of whole 128-cell segments
-  static const bool use_vec = [] {
-    const char* e = getenv("FSG_K4_VEC");
-    return e && e[0] == '1';
-  }();
-  if (use_vec && pulled && g.nx % 128 == 0) {
-    static int nsm_v = 0, res_v = 0;
-    if (!nsm_v) {
-      int dev = 0;
-      cudaGetDevice(&dev);
-      cudaDeviceGetAttribute(&nsm_v, cudaDevAttrMultiProcessorCount, dev);
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&res_v, k_collide_vec4<true>, 128, 0);
-      res_v = std::max(res_v, 1);
-    }
-    const long long warps = (long long)(g.nx / 128) * g.ny * nq;
-    const unsigned grid = (unsigned)std::min<long long>((warps + 3) / 4, (long long)nsm_v * res_v);
-    if (frame_on)
-      k_collide_vec4<true><<<grid, 128, 0, s>>>(g, dp, (const float*)A, sc, st, scr, scr_next, zr);
-    else
-      k_collide_vec4<false><<<grid, 128, 0, s>>>(g, dp, (const float*)A, sc, st, scr, scr_next, zr);
-    return;
-  }
   const dim3 b = cell_block(g), g3 = cell_grid(g, b);
   const long long ntile = (long long)g3.x * g3.y * nq;
   static int resident = 0;  // blocks of k_collide_fix resident per SM (same for all variants)
