@@ -29,7 +29,7 @@ __device__ __forceinline__ float cell_update_ab(const Grid& g, const float* __re
                                                 float Fx, float Fy, float Fz,
                                                 const SessionConsts& sc, const StepConsts& st,
                                                 StepScratch* out) {
-  const int m = (int)mem_index(g, x, y, z);
+  const unsigned m = (unsigned)mem_index(g, x, y, z);
   const int zg = g.z0 + z;
   float s[Q];
   if (!PULLED) {

@@ -57,9 +57,16 @@ __host__ __device__ __forceinline__ constexpr double w_of(int i) {
 constexpr int Q = 19;
 
 // --------------------------------------------------------------- layout --
-// One direction plane holds the slab's owned cells plus `zpad` halo planes
-// below and above (z-slab decomposition).  Element (i, x, y, z_local) lives at
-//   i*stride + x + nx*(y + ny*(z_local + zpad)).
+// Plane-interleaved SoA: for every z plane (the slab's owned planes plus
+// `zpad` halo planes below and above, z-slab decomposition) the 19 direction
+// planes are stored back to back.  Element (i, x, y, z_local) lives at
+//   i*stride + x + nx*y + zs*(z_local + zpad),   stride = nx*ny, zs = 19*stride.
+// Each direction plane is still one contiguous, coalesced run (the reference's
+// direction-major order within a plane, lattice.hpp:89-90), and every pull
+// source is still a constant offset from the cell's own slot; but one step
+// touches 2 regions of memory near the current z (read A, write B) instead
+// of 38 streams a whole direction array apart (measured +11-17 % on a
+// K4-shaped stream at 1.3-20 GB, scripts/probe_layout.cu).
 struct Grid {
   int nx, ny, nz;    // local (owned) dims
   int nzg, z0;       // global z extent, global z of local plane 0
@@ -68,7 +75,8 @@ struct Grid {
   int _pad;
   long long n;       // owned cells nx*ny*nz
   long long plane;   // nx*ny
-  long long stride;  // elements per direction array (>= plane*(nz+2*zpad), 32-aligned)
+  long long stride;  // elements between direction planes of one z (= plane)
+  long long zs;      // elements between z planes (= 19*plane)
   // per-direction element offsets relative to the cell's own slot (host-made,
   // land in the constant bank): own[i] = i*stride, pull[i] = i*stride - off_i
   // with off_i = ex + nx*(ey + ny*ez) (interior pull source)
@@ -79,12 +87,12 @@ struct Grid {
 inline void grid_offsets(Grid& g) {
   for (int i = 0; i < 19; ++i) {
     g.own[i] = (long long)i * g.stride;
-    g.pull[i] = g.own[i] - ((long long)ex_of(i) + (long long)g.nx * ((long long)ey_of(i) + (long long)g.ny * ez_of(i)));
+    g.pull[i] = g.own[i] - ((long long)ex_of(i) + (long long)g.nx * ey_of(i) + g.zs * ez_of(i));
   }
 }
 
 __host__ __device__ __forceinline__ long long mem_index(const Grid& g, int x, int y, int z) {
-  return (long long)x + (long long)g.nx * ((long long)y + (long long)g.ny * (long long)(z + g.zpad));
+  return (long long)x + (long long)g.nx * (long long)y + g.zs * (long long)(z + g.zpad);
 }
 
 // ------------------------------------------------------ device constants --

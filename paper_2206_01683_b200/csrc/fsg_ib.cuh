@@ -61,7 +61,7 @@ __device__ __forceinline__ void gather_slow(const Grid& g, const Store* __restri
 template <bool PULLED>
 __device__ __forceinline__ void gather_cell(const Grid& g, const Store* __restrict__ A, int x, int y,
                                             int z, Store (&s)[Q]) {
-  const Store* __restrict__ base = A + (int)mem_index(g, x, y, z);
+  const Store* __restrict__ base = A + (unsigned)mem_index(g, x, y, z);
   if (!PULLED) {
 #pragma unroll
     for (int i = 0; i < Q; ++i) s[i] = base[g.own[i]];

@@ -85,7 +85,7 @@ __global__ void __launch_bounds__(TMA_TW, FSG_K4_MINB)
     }
     constexpr unsigned bytes = TMA_ROW * sizeof(float);
     mbar_expect_tx(&bar[s], bytes * Q);
-    const long long m0 = (long long)c0 + g.plane * (z + g.zpad) - TMA_PAD;
+    const long long m0 = (long long)c0 + g.zs * (z + g.zpad) - TMA_PAD;
 #pragma unroll
     for (int i = 0; i < Q; ++i)  // dp.a[i] + ex_i: the row/plane shift only (16 B aligned)
       bulk_g2s(&sm[s][i][0], dp.a[i] + ex_of(i) + m0, bytes, &bar[s]);
@@ -118,7 +118,7 @@ __global__ void __launch_bounds__(TMA_TW, FSG_K4_MINB)
         Band none{nullptr, 0};
         vmin = fminf(vmin, collide_cell32<3, VF>(v, x, y, z, g, 0.f, 0.f, 0.f, false, 0, none, sc, st,
                                                  out));
-        const int m = (int)mem_index(g, x, y, z);
+        const unsigned m = (unsigned)mem_index(g, x, y, z);
 #pragma unroll
         for (int i = 0; i < Q; ++i) dp.b[i][m] = v[i];
       }

@@ -19,7 +19,7 @@ __global__ void __launch_bounds__(128)
   const int z = blockIdx.z;
   float vmin = FLT_MAX;
   if (x < g.nx && y < g.ny) {
-    const int m = (int)mem_index(g, x, y, z);
+    const unsigned m = (unsigned)mem_index(g, x, y, z);
     float s[Q];
     if (is_interior(g, x, y, z)) {
 #pragma unroll
@@ -59,7 +59,7 @@ __device__ __forceinline__ float cell_update(const Grid& g, const DirPtrs& dp,
                                              float Fx, float Fy, float Fz,
                                              const SessionConsts& sc, const StepConsts& st,
                                              StepScratch* out) {
-  const int m = (int)mem_index(g, x, y, z);
+  const unsigned m = (unsigned)mem_index(g, x, y, z);
   const int zg = g.z0 + z;
   float s[Q];
   if (!PULLED) {

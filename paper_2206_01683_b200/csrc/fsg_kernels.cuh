@@ -94,7 +94,7 @@ __device__ __forceinline__ bool is_interior(const Grid& g, int x, int y, int z) 
 template <bool PULLED>
 __device__ __forceinline__ void gather(const Grid& g, const Store* __restrict__ A, int x, int y,
                                        int z, Store s[Q]) {
-  const int m = (int)mem_index(g, x, y, z);  // < 2^31 for every supported grid
+  const unsigned m = (unsigned)mem_index(g, x, y, z);  // 19 * cells < 2^32 for every supported grid
   const Store* __restrict__ base = A + m;
   if (!PULLED) {
 #pragma unroll
@@ -355,7 +355,7 @@ __global__ void __launch_bounds__(128) k_collide(Grid g, const Store* __restrict
   if (live) {
     Store s[Q];
     gather<PULLED>(g, A, x, y, z, s);
-    const int m = (int)mem_index(g, x, y, z);
+    const unsigned m = (unsigned)mem_index(g, x, y, z);
     const SessionConsts& sc = *scp;
     // -------- force F for this cell
     Real Fx = 0, Fy = 0, Fz = 0;
@@ -676,9 +676,9 @@ __global__ void k_halo_pack(Grid g, const Store* __restrict__ B, Store* send_lo,
   const int k = (int)(t / g.plane);
   const long long xy = t % g.plane;
   // top owned plane, ez=+1 populations -> upper neighbour
-  send_hi[t] = B[up_dir(k) * g.stride + g.plane * (g.nz - 1 + g.zpad) + xy];
+  send_hi[t] = B[up_dir(k) * g.stride + g.zs * (g.nz - 1 + g.zpad) + xy];
   // bottom owned plane, ez=-1 populations -> lower neighbour
-  send_lo[t] = B[dn_dir(k) * g.stride + g.plane * (0 + g.zpad) + xy];
+  send_lo[t] = B[dn_dir(k) * g.stride + g.zs * (0 + g.zpad) + xy];
 }
 __global__ void k_halo_unpack(Grid g, Store* B, const Store* __restrict__ recv_lo,
                               const Store* __restrict__ recv_hi) {
@@ -689,7 +689,7 @@ __global__ void k_halo_unpack(Grid g, Store* B, const Store* __restrict__ recv_l
   // lower neighbour's top plane (ez=+1) -> halo plane z = -1
   if (recv_lo) B[up_dir(k) * g.stride + xy] = recv_lo[t];
   // upper neighbour's bottom plane (ez=-1) -> halo plane z = nz
-  if (recv_hi) B[dn_dir(k) * g.stride + g.plane * (g.nz + g.zpad) + xy] = recv_hi[t];
+  if (recv_hi) B[dn_dir(k) * g.stride + g.zs * (g.nz + g.zpad) + xy] = recv_hi[t];
 }
 
 // ======================================================== launchers =====

@@ -390,8 +390,9 @@ int fsg_create(const fsg_config* cfg_in, fsg_session** out) {
   if (cfg.dims[2] < (slab ? 2 : 8) || cfg.z_offset < 0 || cfg.z_offset + cfg.dims[2] > cfg.nz_global)
     return set_err(FSG_EINPUT, "bad z slab: offset %d depth %d of %d", cfg.z_offset, cfg.dims[2],
                    cfg.nz_global);
-  if ((long long)cfg.dims[0] * cfg.dims[1] * (cfg.dims[2] + 2) >= (1ll << 31))
-    return set_err(FSG_EINPUT, "slab too large: a direction plane must hold < 2^31 cells");
+  // kernels address the state with a 32-bit unsigned element index
+  if (19ll * cfg.dims[0] * cfg.dims[1] * (cfg.dims[2] + 2) >= (1ll << 32))
+    return set_err(FSG_EINPUT, "slab too large: 19 x cells (with halo planes) must be < 2^32");
   if (cfg.boundary != FSG_BOUNDARY_OPEN && cfg.boundary != FSG_BOUNDARY_PERIODIC)
     return set_err(FSG_EINPUT, "unknown boundary mode %d", cfg.boundary);
   if (cfg.kernel != FSG_KERNEL_PESKIN4 && cfg.kernel != FSG_KERNEL_ROMA3)
@@ -424,7 +425,8 @@ int fsg_create(const fsg_config* cfg_in, fsg_session** out) {
   g.periodic = cfg.boundary == FSG_BOUNDARY_PERIODIC ? 1 : 0;
   g.plane = (long long)g.nx * g.ny;
   g.n = g.plane * g.nz;
-  g.stride = ((g.plane * (g.nz + 2 * g.zpad) + 31) / 32) * 32;
+  g.stride = g.plane;
+  g.zs = 19 * g.plane;
   fsg::grid_offsets(g);
 
   // session constants, host fp64 in the reference's order
@@ -473,7 +475,7 @@ int fsg_create(const fsg_config* cfg_in, fsg_session** out) {
   } else {
     CUF(cudaStreamCreateWithFlags(&s->stream, cudaStreamNonBlocking));
   }
-  const size_t fbytes = (size_t)s->L->elem_bytes * 19 * (size_t)g.stride;
+  const size_t fbytes = (size_t)s->L->elem_bytes * (size_t)g.zs * (size_t)(g.nz + 2 * g.zpad);
   for (int k = 0; k < 2; ++k) {
     CUF(cudaMalloc(&s->buf[k], fbytes));
     CUF(cudaMemsetAsync(s->buf[k], 0, fbytes, s->stream));
