@@ -11,6 +11,9 @@
 #ifndef FSG_K4_MINB
 #define FSG_K4_MINB 6
 #endif
+#ifndef FSG_KM_PER_SM_DEFAULT
+#define FSG_KM_PER_SM_DEFAULT 0.0
+#endif
 #ifndef FSG_KM_MINB
 #define FSG_KM_MINB 6
 #endif

@@ -213,9 +213,12 @@ __device__ __forceinline__ void mk_finish(const Grid& g, const float* __restrict
   }
 }
 
-/// Standalone marker kernel: a programmatic primary of the banded K4.  Every
-/// block stamps its markers' tiles, fences, and only then triggers its
-/// dependents, before the slow part.
+/// Standalone marker kernel: a programmatic primary of the banded K4.
+/// Persistent over the markers (grid capped by the host, L_markers_fix): each
+/// warp first stamps the tiles of ALL its markers, the block fences and only
+/// then triggers its dependents, before the slow part.  Fewer marker blocks
+/// leave more of every SM to the concurrent phase A of K4 (the marker chain is
+/// off the critical path while phase A runs).
 template <bool PULLED>
 __global__ void __launch_bounds__(128, FSG_KM_MINB)
     k_markers_fix(Grid g, const float* __restrict__ A, Markers mk, const SessionConsts* __restrict__ scp,
@@ -224,13 +227,11 @@ __global__ void __launch_bounds__(128, FSG_KM_MINB)
   __shared__ double phs[FX_PER_BLOCK][3][5];
   const int lane = threadIdx.x & (FX_LANES - 1);
   const int slot = threadIdx.x / FX_LANES;
-  const int t = blockIdx.x * FX_PER_BLOCK + slot;
-  const bool live = t < mk.m;  // uniform over the warp
+  const int stride = gridDim.x * FX_PER_BLOCK;
   const SessionConsts& sc = *scp;
   if (threadIdx.x == 0) FSG_TL(fb.stamp, 0);  // timeline (dev build): marker kernel start
-  MkStencil S;
-  S.ok = false;
-  if (live) {
+  for (int t = blockIdx.x * FX_PER_BLOCK + slot; t < mk.m; t += stride) {
+    MkStencil S;
     mk_stencil(mk, t, sc, st, S);
     mk_stamp(g, fb, S, lane);
   }
@@ -241,8 +242,12 @@ __global__ void __launch_bounds__(128, FSG_KM_MINB)
   if (threadIdx.x == 0) __threadfence();
   __syncthreads();
   asm volatile("griddepcontrol.launch_dependents;");
-  if (!live) return;
-  mk_finish<PULLED>(g, A, mk, t, lane, sc, st, S, phs[slot], rec_out, fworld, fworld_h, valid_h, fb,
-                    out);
+  for (int t = blockIdx.x * FX_PER_BLOCK + slot; t < mk.m; t += stride) {
+    MkStencil S;
+    mk_stencil(mk, t, sc, st, S);  // cheap; recomputed rather than kept in registers
+    mk_finish<PULLED>(g, A, mk, t, lane, sc, st, S, phs[slot], rec_out, fworld, fworld_h, valid_h, fb,
+                      out);
+    __syncwarp(fx_mask());  // phs[slot] is reused by the group's next marker
+  }
   if (lane == 0) FSG_TL(fb.stamp, 1);  // last marker warp done
 }

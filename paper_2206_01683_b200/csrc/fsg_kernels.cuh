@@ -807,7 +807,19 @@ static void L_markers_fix(const Grid& g, const void* A, int pulled, Markers mk,
                           double* fworld, double* fworld_h, int* valid_h, FixBand fb,
                           StepScratch* out, cudaStream_t s) {
   if (mk.m == 0) return;
-  const unsigned nb = (unsigned)((mk.m + FX_PER_BLOCK - 1) / FX_PER_BLOCK);
+  // marker blocks per SM (FSG_KM_PER_SM, default below; 0 = one marker per
+  // warp, a single wave of up to m/4 blocks)
+  static int cap = -1;
+  if (cap < 0) {
+    int dev = 0, nsm = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    const char* e = getenv("FSG_KM_PER_SM");
+    const double per = e ? atof(e) : FSG_KM_PER_SM_DEFAULT;
+    cap = per > 0 ? std::max(1, (int)(per * nsm)) : 0;
+  }
+  unsigned nb = (unsigned)((mk.m + FX_PER_BLOCK - 1) / FX_PER_BLOCK);
+  if (cap > 0) nb = std::min(nb, (unsigned)cap);
   if (pulled)
     k_markers_fix<true><<<nb, 128, 0, s>>>(g, (const float*)A, mk, sc, st, rec, fworld, fworld_h,
                                            valid_h, fb, out);

@@ -1,4 +1,4 @@
-"""Dev probe: device phase timeline of the coupled throughput step (steady state).
+"""Dev probe: device phase timeline of the coupled throughput step (steady state;\n--flush: L2 flushed between steps as in bench.py).
 
 Needs the instrumented build (make -C paper_2206_01683_b200/csrc dbg ->
 libfsg_dbg.so, -DFSG_TIMING).  Slots: 0 marker kernel start, 1 last marker
@@ -15,6 +15,12 @@ from paper_2206_01683_b200 import CoupledSession, SessionConfig, _abi
 from paper_2206_01683_b200.scenes import make_scene
 
 lib = ctypes.CDLL(_abi.LIB_PATH)
+FLUSH = "--flush" in sys.argv
+if FLUSH:
+    sys.argv.remove("--flush")
+    fw_buf = torch.empty(64 << 20, dtype=torch.float32, device="cuda")
+    fr_buf = torch.ones(64 << 20, dtype=torch.float32, device="cuda")
+    sink = torch.zeros(1, dtype=torch.float32, device="cuda")
 S = 8
 buf = (ctypes.c_ulonglong * (64 * S))()
 for name in sys.argv[1:] or ["c2"]:
@@ -28,10 +34,14 @@ for name in sys.argv[1:] or ["c2"]:
         s.set_frame(sc.frame(k)); s.step_async()
     s.last_status(); lib.fsg_debug_timeline(None)
     frames = [sc.frame(k) for k in range(30, 60)]
-    with torch.cuda.stream(torch.cuda.ExternalStream(s.stream)):
+    ss = torch.cuda.ExternalStream(s.stream)
+    with torch.cuda.stream(ss):
         torch.cuda._sleep(int(2e6))  # queue every step before the GPU starts
-    for f in frames:
-        s.set_frame(f); s.step_async()
+        for f in frames:
+            if FLUSH:  # as bench.py: write + read 2x L2 between steps
+                fw_buf.fill_(1.0)
+                torch.sum(fr_buf, dim=0, out=sink[0])
+            s.set_frame(f); s.step_async()
     s.last_status(); lib.fsg_debug_timeline(buf)
     t = list(buf)
     rows = sorted([t[S * j: S * j + S] for j in range(64) if t[S * j + 5] not in (0, ~0 & (2**64 - 1))],
@@ -40,7 +50,7 @@ for name in sys.argv[1:] or ["c2"]:
     for r in rows[5:13]:
         b = r[0]
         f = lambda v: (v - b) / 1e3
-        gap = f"{(b - prev) / 1e3:5.1f}" if prev else "  -  "
+        gap = f"{(b - prev) / 1e3:5.1f}" if prev and not FLUSH else "  -  "
         print(f"{name} gap {gap} | markers -> {f(r[1]):6.1f} | K4 {f(r[2]):6.1f} | phaseA out "
               f"{f(r[3]):6.1f} | band {f(r[4]):6.1f} -> {f(r[5]):6.1f}")
         prev = r[5]
