@@ -164,6 +164,61 @@ int fsg_get_force(fsg_session* s, double* F);
 /* Integer stencil sets of the last step, per marker: lo[3], hi[3] (kernel.hpp:36-40). */
 int fsg_get_stencils(fsg_session* s, int* lo_hi);
 
+/* ---- skinned bodies on the device -------------------
+ * Per-step marker refresh and Jacobian-transpose force reduction of the
+ * robot side of CoupledSession::step (session.hpp:103-144), so only the
+ * per-link pose goes up and only tau_ext + CouplingStats come back:
+ *   robot::update_samples        (sampling.hpp:307-322): LBS of points,
+ *       skin_point / skin_point_velocity (skinning.hpp:105-126) and normals;
+ *   robot::accumulate_skinned_force (skinning.hpp:147-156) ->
+ *       accumulate_point_force (dynamics.hpp:216-233), called with -f_world
+ *       per valid marker in ascending order (session.hpp:129-140);
+ *   CouplingStats (coupling.hpp:88-93, session.hpp:141-143).
+ * Forward kinematics and BoneTransforms::of stay with the caller (host, per
+ * link); fsg_set_pose takes their results. */
+#define FSG_SKIN_MAX_LINKS 8
+#define FSG_SKIN_MAX_BODIES 4
+#define FSG_SKIN_MAX_WEIGHTS 4 /* nonzero blend weights per marker */
+
+/* Skeleton topology (skeleton.hpp:16-93). */
+typedef struct {
+  int n_links;                          /* <= FSG_SKIN_MAX_LINKS                     */
+  int floating_base;                    /* links[0].joint == Free (skeleton.hpp:72)  */
+  int n_dofs;                           /* Skeleton::n_dofs()                        */
+  int parent[FSG_SKIN_MAX_LINKS];       /* links[i].parent (-1 for the root)         */
+  int dof_index[FSG_SKIN_MAX_LINKS];    /* Skeleton::dof_index(i), -1: no revolute dof */
+  double axis[FSG_SKIN_MAX_LINKS][3];   /* links[i].axis.normalized() (revolute)     */
+} fsg_skeleton;
+
+/* Per-step pose of one body: BoneTransforms::of (skinning.hpp:85-102) and the
+ * KinematicsCache fields the path reads (dynamics.hpp:14-21); row-major. */
+typedef struct {
+  double bone_R[FSG_SKIN_MAX_LINKS][9];
+  double bone_t[FSG_SKIN_MAX_LINKS][3];
+  double R_world[FSG_SKIN_MAX_LINKS][9];
+  double p_world[FSG_SKIN_MAX_LINKS][3];
+  double v_origin_world[FSG_SKIN_MAX_LINKS][3];
+  double omega_world[FSG_SKIN_MAX_LINKS][3];
+} fsg_body_pose;
+
+/* Register skinned bodies (SurfaceSamples, sampling.hpp): body b owns
+ * markers [body_offsets[b], body_offsets[b+1]); rest_points/rest_normals
+ * [3m] (base at identity), areas [m], weights: for each marker, n_links(b)
+ * blend weights (rows sum to 1; at most FSG_SKIN_MAX_WEIGHTS nonzero).
+ * Replaces fsg_set_markers: every later step skins the markers on the device
+ * from the pose set by fsg_set_pose (until fsg_set_markers* is called). */
+int fsg_set_skin(fsg_session* s, int n_bodies, const int64_t* body_offsets,
+                 const fsg_skeleton* skeletons, const double* rest_points,
+                 const double* rest_normals, const double* weights, const double* areas);
+/* This step's pose of every skinned body (n_bodies entries). */
+int fsg_set_pose(fsg_session* s, const fsg_body_pose* poses);
+/* Of the last step: tau_ext of every body (concatenated, n_dofs(b) each;
+ * session.hpp:107, :139-140) and CouplingStats stats[7*b] as in
+ * fsg_get_marker_forces.  Either pointer may be NULL. */
+int fsg_get_body_wrench(fsg_session* s, double* tau_ext, double* stats);
+/* Marker state the last step used (world frame; skinned or uploaded). */
+int fsg_get_markers(fsg_session* s, double* points, double* velocities, double* normals);
+
 /* ---- measurement ---------------------------------------------------------
  * When enabled, every step is bracketed with CUDA events on the session
  * stream (the marker kernel and the banded collide/stream kernel overlap, so

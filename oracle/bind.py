@@ -87,6 +87,50 @@ class FrameConsts(C.Structure):
                 ("alpha_f", C.c_double * 3)]
 
 
+class OrcSkeleton(C.Structure):
+    """orc_skeleton (same layout as fsg_skeleton)."""
+
+    _fields_ = [("n_links", C.c_int), ("floating_base", C.c_int), ("n_dofs", C.c_int),
+                ("parent", C.c_int * 8), ("dof_index", C.c_int * 8), ("axis", (C.c_double * 3) * 8)]
+
+    @classmethod
+    def of(cls, sk):
+        """From any object with parent, dof_index, axis, floating_base, n_dofs."""
+        c = cls()
+        c.n_links = len(sk.parent)
+        c.floating_base = 1 if sk.floating_base else 0
+        c.n_dofs = int(sk.n_dofs)
+        ax = np.asarray(sk.axis, dtype=np.float64).reshape(-1, 3)
+        for j in range(len(sk.parent)):
+            c.parent[j] = int(sk.parent[j])
+            c.dof_index[j] = int(sk.dof_index[j])
+            for k in range(3):
+                c.axis[j][k] = float(ax[j, k])
+        return c
+
+
+def skin_update(sk, pose_packed, rest, nrest, weights):
+    """update_samples restated (sampling.hpp:307-322) -> (pts, vel, nrm) [m,3]."""
+    O = oracle()
+    m = int(np.asarray(rest).reshape(-1, 3).shape[0])
+    out = [np.empty(3 * m) for _ in range(3)]
+    O.orc_update_samples(OrcSkeleton.of(sk), dptr(d3(pose_packed)), m, dptr(d3(rest)), dptr(d3(nrest)),
+                         dptr(d3(weights)), *(dptr(a) for a in out))
+    return tuple(a.reshape(-1, 3) for a in out)
+
+
+def skin_tau(sk, pose_packed, rest, weights, fworld, valid, vel):
+    """session.hpp:129-143 for one body -> (tau[n_dofs], stats[7])."""
+    O = oracle()
+    m = int(np.asarray(rest).reshape(-1, 3).shape[0])
+    tau = np.empty(max(int(sk.n_dofs), 1))
+    stats = np.empty(7)
+    O.orc_skin_tau(OrcSkeleton.of(sk), dptr(d3(pose_packed)), m, dptr(d3(rest)), dptr(d3(weights)),
+                   dptr(d3(fworld)), iptr(np.ascontiguousarray(valid, dtype=np.int32)), dptr(d3(vel)),
+                   dptr(tau), dptr(stats))
+    return tau[: int(sk.n_dofs)], stats
+
+
 _oracle = None
 _ref = None
 
@@ -128,6 +172,10 @@ def oracle() -> C.CDLL:
             "orc_session_step": (C.c_int, [C.c_void_p, C.c_int, _i64p, _dp, _dp, _dp, _dp, _dp,
                                            _ip, _dp, _ip, _dp]),
             "orc_session_recenter": (None, [C.c_void_p, _ip]),
+            "orc_update_samples": (None, [C.POINTER(OrcSkeleton), _dp, C.c_int, _dp, _dp, _dp,
+                                          _dp, _dp, _dp]),
+            "orc_skin_tau": (None, [C.POINTER(OrcSkeleton), _dp, C.c_int, _dp, _dp, _dp, _ip,
+                                    _dp, _dp, _dp]),
         }
         for name, (res, args) in sig.items():
             fn = getattr(lib, name)

@@ -495,3 +495,121 @@ void orc_session_recenter(orc_session* s, const int shift[3]) {
   s->fa = s->fb;
   s->fb = t;
 }
+
+/* ======================================================= skinned bodies ==
+ * TEST INFRASTRUCTURE: restatement of the robot-side marker refresh and
+ * force reduction of CoupledSession::step.  Eigen 3.4 coefficient order as
+ * in the rest of this file: mat*vec and dot ((a0 b0 + a1 b1) + a2 b2),
+ * cross3, normalized() = v / sqrt(|v|^2) when |v|^2 > 0. */
+static void sk_mv(const double* R, const double* v, double* r) {
+  for (int i = 0; i < 3; ++i) r[i] = (R[3 * i] * v[0] + R[3 * i + 1] * v[1]) + R[3 * i + 2] * v[2];
+}
+static void sk_mtv(const double* R, const double* v, double* r) {
+  for (int i = 0; i < 3; ++i) r[i] = (R[i] * v[0] + R[3 + i] * v[1]) + R[6 + i] * v[2];
+}
+static void sk_cross(const double* a, const double* b, double* r) {
+  r[0] = a[1] * b[2] - a[2] * b[1];
+  r[1] = a[2] * b[0] - a[0] * b[2];
+  r[2] = a[0] * b[1] - a[1] * b[0];
+}
+static double sk_dot(const double* a, const double* b) { return (a[0] * b[0] + a[1] * b[1]) + a[2] * b[2]; }
+
+/* BoneTransforms::apply (skinning.hpp:101) */
+static void sk_apply(const orc_body_pose* P, int b, const double* x, double* xb) {
+  sk_mv(P->bone_R[b], x, xb);
+  for (int c = 0; c < 3; ++c) xb[c] = xb[c] + P->bone_t[b][c];
+}
+
+void orc_update_samples(const orc_skeleton* sk, const orc_body_pose* P, int m, const double* rest,
+                        const double* nrest, const double* weights, double* pts, double* vel,
+                        double* nrm) {
+  const int L = sk->n_links;
+  for (int i = 0; i < m; ++i) {
+    const double* w = weights + (size_t)i * L;
+    const double* x = rest + 3 * i;
+    double out[3] = {0, 0, 0}, vo[3] = {0, 0, 0}, nn[3] = {0, 0, 0};
+    /* skin_point (skinning.hpp:105-112) */
+    for (int b = 0; b < L; ++b) {
+      if (w[b] == 0.0) continue;
+      double xb[3];
+      sk_apply(P, b, x, xb);
+      for (int c = 0; c < 3; ++c) out[c] = out[c] + w[b] * xb[c];
+    }
+    /* skin_point_velocity (skinning.hpp:116-126) */
+    for (int b = 0; b < L; ++b) {
+      if (w[b] == 0.0) continue;
+      double xb[3], d[3], cr[3];
+      sk_apply(P, b, x, xb);
+      for (int c = 0; c < 3; ++c) d[c] = xb[c] - P->p_world[b][c];
+      sk_cross(P->omega_world[b], d, cr);
+      for (int c = 0; c < 3; ++c) vo[c] = vo[c] + w[b] * (P->v_origin_world[b][c] + cr[c]);
+    }
+    /* normals (sampling.hpp:316-319) */
+    for (int b = 0; b < L; ++b) {
+      if (w[b] == 0.0) continue;
+      double rn[3];
+      sk_mv(P->bone_R[b], nrest + 3 * i, rn);
+      for (int c = 0; c < 3; ++c) nn[c] = nn[c] + w[b] * rn[c];
+    }
+    const double z = sk_dot(nn, nn);
+    if (z > 0.0) {
+      const double s = sqrt(z);
+      for (int c = 0; c < 3; ++c) nn[c] = nn[c] / s;
+    }
+    for (int c = 0; c < 3; ++c) {
+      pts[3 * i + c] = out[c];
+      vel[3 * i + c] = vo[c];
+      nrm[3 * i + c] = nn[c];
+    }
+  }
+}
+
+/* accumulate_point_force (dynamics.hpp:216-233) */
+static void sk_point_force(const orc_skeleton* sk, const orc_body_pose* P, int link, const double* p,
+                           const double* f, double* tau) {
+  if (sk->floating_base) {
+    double d[3], cr[3], h[3], g[3];
+    for (int c = 0; c < 3; ++c) d[c] = p[c] - P->p_world[0][c];
+    sk_cross(d, f, cr);
+    sk_mtv(P->R_world[0], cr, h);
+    for (int c = 0; c < 3; ++c) tau[c] = tau[c] + h[c];
+    sk_mtv(P->R_world[0], f, g);
+    for (int c = 0; c < 3; ++c) tau[3 + c] = tau[3 + c] + g[c];
+  }
+  for (int j = link; j > 0; j = sk->parent[j]) {
+    if (sk->dof_index[j] < 0) continue; /* not revolute */
+    double aw[3], d[3], cr[3];
+    sk_mv(P->R_world[j], sk->axis[j], aw);
+    for (int c = 0; c < 3; ++c) d[c] = p[c] - P->p_world[j][c];
+    sk_cross(aw, d, cr);
+    tau[sk->dof_index[j]] = tau[sk->dof_index[j]] + sk_dot(cr, f);
+  }
+}
+
+void orc_skin_tau(const orc_skeleton* sk, const orc_body_pose* P, int m, const double* rest,
+                  const double* weights, const double* fworld, const int* valid, const double* vel,
+                  double* tau, double* stats) {
+  const int L = sk->n_links;
+  for (int d = 0; d < sk->n_dofs; ++d) tau[d] = 0.0;
+  for (int k = 0; k < 7; ++k) stats[k] = 0.0;
+  for (int i = 0; i < m; ++i) {
+    if (!valid[i]) continue;
+    const double* f = fworld + 3 * i;
+    const double fneg[3] = {-f[0], -f[1], -f[2]};
+    const double* w = weights + (size_t)i * L;
+    /* accumulate_skinned_force (skinning.hpp:147-156), called with -f_world */
+    for (int b = 0; b < L; ++b) {
+      if (w[b] == 0.0) continue;
+      double p[3], fv[3];
+      sk_apply(P, b, rest + 3 * i, p);
+      for (int c = 0; c < 3; ++c) fv[c] = w[b] * fneg[c];
+      sk_point_force(sk, P, b, p, fv, tau);
+    }
+    /* CouplingStats (session.hpp:141-143) */
+    for (int c = 0; c < 3; ++c) {
+      stats[c] = stats[c] + f[c];
+      stats[3 + c] = stats[3 + c] - f[c];
+    }
+    stats[6] = stats[6] + sk_dot(fneg, vel + 3 * i);
+  }
+}

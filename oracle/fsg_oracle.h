@@ -96,6 +96,35 @@ int orc_session_step(orc_session* s, int n_bodies, const int64_t* body_offsets,
                      int* finite, double* min_f);
 void orc_session_recenter(orc_session* s, const int shift[3]);
 
+/* ---- skinned bodies ---------------------------------
+ * Restated from skinning.hpp / sampling.hpp / dynamics.hpp, which need
+ * dynamic-size Eigen (VectorXd/MatrixXd blocks, Ref, LLT) and so do not
+ * compile against the fixed-size stand-in: parity of this restatement is
+ * pinned by the reference's own property tests for these functions
+ * (test_sampling.cpp:45-193, test_ib.cpp:215-249), restated in
+ * tests/test_skin_oracle.py.  Layouts match fsg_skeleton / fsg_body_pose. */
+typedef struct {
+  int n_links, floating_base, n_dofs;
+  int parent[8], dof_index[8];
+  double axis[8][3];
+} orc_skeleton;
+typedef struct {
+  double bone_R[8][9], bone_t[8][3], R_world[8][9], p_world[8][3], v_origin_world[8][3],
+      omega_world[8][3];
+} orc_body_pose;
+/* update_samples (sampling.hpp:307-322): points, velocities, normals [3m];
+ * weights [m][n_links] dense */
+void orc_update_samples(const orc_skeleton* sk, const orc_body_pose* pose, int m,
+                        const double* rest, const double* nrest, const double* weights,
+                        double* pts, double* vel, double* nrm);
+/* session.hpp:129-143 for one body: for every valid marker in ascending
+ * order, accumulate_skinned_force(..., -f_world, tau) (skinning.hpp:147-156 ->
+ * dynamics.hpp:216-233) and the CouplingStats sums.  tau [n_dofs] and
+ * stats[7] are zeroed first (session.hpp:106-107). */
+void orc_skin_tau(const orc_skeleton* sk, const orc_body_pose* pose, int m, const double* rest,
+                  const double* weights, const double* fworld, const int* valid,
+                  const double* vel, double* tau, double* stats);
+
 #ifdef __cplusplus
 }
 #endif

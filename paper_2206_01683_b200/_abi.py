@@ -48,6 +48,22 @@ class fsg_frame_state(C.Structure):
                 ("q", C.c_double * 4), ("omega", C.c_double * 3), ("alpha", C.c_double * 3)]
 
 
+SKIN_MAX_LINKS, SKIN_MAX_BODIES, SKIN_MAX_WEIGHTS = 8, 4, 4
+_L = SKIN_MAX_LINKS
+
+
+class fsg_skeleton(C.Structure):
+    _fields_ = [("n_links", C.c_int), ("floating_base", C.c_int), ("n_dofs", C.c_int),
+                ("parent", C.c_int * _L), ("dof_index", C.c_int * _L),
+                ("axis", (C.c_double * 3) * _L)]
+
+
+class fsg_body_pose(C.Structure):
+    _fields_ = [("bone_R", (C.c_double * 9) * _L), ("bone_t", (C.c_double * 3) * _L),
+                ("R_world", (C.c_double * 9) * _L), ("p_world", (C.c_double * 3) * _L),
+                ("v_origin_world", (C.c_double * 3) * _L), ("omega_world", (C.c_double * 3) * _L)]
+
+
 _dp = C.POINTER(C.c_double)
 _ip = C.POINTER(C.c_int)
 _i64p = C.POINTER(C.c_int64)
@@ -83,6 +99,10 @@ SIGNATURES = {
     "fsg_get_macro": (C.c_int, [_vp, _dp, _dp]),
     "fsg_get_force": (C.c_int, [_vp, _dp]),
     "fsg_get_stencils": (C.c_int, [_vp, _ip]),
+    "fsg_set_skin": (C.c_int, [_vp, C.c_int, _i64p, C.POINTER(fsg_skeleton), _dp, _dp, _dp, _dp]),
+    "fsg_set_pose": (C.c_int, [_vp, C.POINTER(fsg_body_pose)]),
+    "fsg_get_body_wrench": (C.c_int, [_vp, _dp, _dp]),
+    "fsg_get_markers": (C.c_int, [_vp, _dp, _dp, _dp]),
     "fsg_profile_enable": (C.c_int, [_vp, C.c_int]),
     "fsg_profile_read": (C.c_int, [_vp, _dp, _ip]),
     "fsg_follower_create": (C.c_int, [C.c_int, C.c_double, C.POINTER(_vp)]),

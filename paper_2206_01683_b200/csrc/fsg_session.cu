@@ -32,6 +32,7 @@
 
 #include "../../include/fsg.h"
 #include "fsg_device.cuh"
+#include "fsg_skin.cuh"
 
 using fsg::Band;
 using fsg::Grid;
@@ -166,6 +167,14 @@ struct fsg_session {
   StepScratch* d_diag = nullptr;
   // measurement: an event pair around every step
   static constexpr int PROF_CAP = 4096;
+  // skinned bodies (fsg_set_skin / fsg_set_pose)
+  bool skin = false;
+  bool pose_set = false;
+  fsg::SkinParams skp{};              // topology + the next step's pose (launch parameter)
+  int n_tau = 0;                      // sum of n_dofs over the skinned bodies
+  double* d_skin = nullptr;           // rest [3m] | nrest [3m] | ww [KW m] | pts | vel | nrm [3m] | area [m]
+  int* d_skin_wb = nullptr;           // [KW m]
+  double* h_wrench[2] = {nullptr, nullptr};  // pinned: tau + stats written by the step of parity p
   bool prof = false;
   std::vector<cudaEvent_t> prof_ev;
   int prof_n = 0;
@@ -285,9 +294,15 @@ void enqueue_step(fsg_session* s, int p, bool copy_mk, bool frame_on) {
   const size_t m = (size_t)s->m;
   (void)copy_mk;  // host markers: uploaded by fsg_set_markers (copy stream), waited on by the caller
   k_step_begin<<<1, 64, 0, s->stream>>>(s->h_st[p], s->d_st, s->d_scr[p]);
+  if (m && s->skin)
+    fsg::skin_update_launch(s->skp, (double*)s->mk.pts, (double*)s->mk.vel, (double*)s->mk.nrm,
+                            s->stream);
   if (m) {
     s->L->markers(g, s->buf[p], s->pulled, s->mk, s->d_sc, s->d_st, s->d_stencil, s->d_boxes,
                   s->d_fworld, s->h_fw[p], s->h_valid[p], s->d_scr[p], s->stream);
+    if (s->skin)  // parity: the reference's serial order (session.hpp:129-143)
+      fsg::skin_tau_launch(s->skp, s->d_fworld, s->d_stencil, s->mk.vel, s->h_wrench[p], 1,
+                           s->stream);
     s->L->spread(g, s->m, s->d_stencil, s->d_boxes, s->band, s->d_scr[p], s->stream);
   }
   s->L->collide(g, s->buf[p], s->pulled, s->buf[p ^ 1], nullptr, &s->band, s->d_scr[p], s->d_sc,
@@ -310,7 +325,7 @@ void clear_graphs(fsg_session* s) {
 }
 
 int launch_step(fsg_session* s, int p, bool copy_mk, bool frame_on) {
-  if (!use_graphs()) {
+  if (!use_graphs() || s->skin) {  // skinned: the pose is a launch parameter (not graphable)
     enqueue_step(s, p, copy_mk, frame_on);
     CU_LAUNCH();
     return FSG_OK;
@@ -582,6 +597,10 @@ int fsg_destroy(fsg_session* s) {
   if (s->ev_hpack) cudaEventDestroy(s->ev_hpack);
   if (s->ev_hrecv) cudaEventDestroy(s->ev_hrecv);
   cudaFree(s->d_diag);
+  cudaFree(s->d_skin);
+  cudaFree(s->d_skin_wb);
+  for (int k = 0; k < 2; ++k)
+    if (s->h_wrench[k]) cudaFreeHost(s->h_wrench[k]);
   cudaFree(s->d_tmp);
   cudaFree(s->d_red);
   if (s->stream && s->own_stream) cudaStreamDestroy(s->stream);
@@ -821,6 +840,7 @@ int fsg_set_markers(fsg_session* s, int n_bodies, const int64_t* off, const doub
     CU(cudaEventRecord(s->ev_cp[p], s->cstream));
   }
   s->mk = Markers{d, d + 3 * m, d + 6 * m, d + 9 * m, (int)m};
+  s->skin = false;
   s->mk_slot = p;
   s->mk_host = true;
   s->mk_dirty = m > 0;
@@ -832,15 +852,142 @@ int fsg_set_markers_device(fsg_session* s, int n_bodies, const int64_t* off, con
   int rc = set_markers_common(s, n_bodies, off);
   if (rc) return rc;
   s->mk = Markers{pts, vel, nrm, area, s->m};
+  s->skin = false;
   s->mk_host = false;
   s->mk_slot = -1;
   s->mk_dirty = false;
   return FSG_OK;
 }
 
+// -------------------------------------------------------- skinned bodies --
+int fsg_set_skin(fsg_session* s, int n_bodies, const int64_t* off, const fsg_skeleton* sk,
+                 const double* rest, const double* nrest, const double* weights,
+                 const double* areas) {
+  if (n_bodies < 1 || n_bodies > FSG_SKIN_MAX_BODIES)
+    return set_err(FSG_EINPUT, "fsg_set_skin: 1..%d bodies", FSG_SKIN_MAX_BODIES);
+  if (!sk || !rest || !nrest || !weights || !areas) return set_err(FSG_EINPUT, "fsg_set_skin: null array");
+  int rc = set_markers_common(s, n_bodies, off);
+  if (rc) return rc;
+  const int m = s->m;
+  fsg::SkinParams& P = s->skp;
+  P = fsg::SkinParams{};
+  P.nb = n_bodies;
+  P.m = m;
+  std::vector<int> wb((size_t)fsg::SKIN_KW * m, -1);
+  std::vector<double> ww((size_t)fsg::SKIN_KW * m, 0.0);
+  size_t wpos = 0;  // weights: per body, n_links columns per marker
+  int nt = 0;
+  for (int b = 0; b < n_bodies; ++b) {
+    const fsg_skeleton& k = sk[b];
+    if (k.n_links < 1 || k.n_links > FSG_SKIN_MAX_LINKS)
+      return set_err(FSG_EINPUT, "body %d: n_links must be 1..%d", b, FSG_SKIN_MAX_LINKS);
+    if (k.n_dofs < 0 || k.n_dofs > 6 + FSG_SKIN_MAX_LINKS)
+      return set_err(FSG_EINPUT, "body %d: bad n_dofs %d", b, k.n_dofs);
+    if (k.floating_base && k.n_dofs < 6) return set_err(FSG_EINPUT, "body %d: floating base needs 6 dofs", b);
+    for (int j = 1; j < k.n_links; ++j) {
+      if (k.parent[j] < 0 || k.parent[j] >= j)
+        return set_err(FSG_EINPUT, "body %d: link %d parent must precede it", b, j);
+      if (k.dof_index[j] >= k.n_dofs) return set_err(FSG_EINPUT, "body %d: dof index out of range", b);
+    }
+    fsg::SkinBody& B = P.body[b];
+    B.m0 = (int)off[b];
+    B.m1 = (int)off[b + 1];
+    B.n_links = k.n_links;
+    B.floating = k.floating_base ? 1 : 0;
+    B.n_dofs = k.n_dofs;
+    B.tau_off = nt;
+    nt += k.n_dofs;
+    for (int j = 0; j < FSG_SKIN_MAX_LINKS; ++j) {
+      B.parent[j] = j < k.n_links ? k.parent[j] : -1;
+      B.dof[j] = (j > 0 && j < k.n_links) ? k.dof_index[j] : -1;
+      for (int c = 0; c < 3; ++c) B.axis[j][c] = j < k.n_links ? k.axis[j][c] : 0.0;
+    }
+    for (int i = B.m0; i < B.m1; ++i) {
+      int nz = 0;
+      for (int j = 0; j < k.n_links; ++j) {
+        const double w = weights[wpos + (size_t)(i - B.m0) * k.n_links + j];
+        if (w == 0.0) continue;  // skin_point skips zero weights (skinning.hpp:108)
+        if (nz == fsg::SKIN_KW)
+          return set_err(FSG_EINPUT, "marker %d has more than %d nonzero skin weights", i, fsg::SKIN_KW);
+        wb[(size_t)fsg::SKIN_KW * i + nz] = j;
+        ww[(size_t)fsg::SKIN_KW * i + nz] = w;
+        ++nz;
+      }
+    }
+    wpos += (size_t)(B.m1 - B.m0) * k.n_links;
+  }
+  s->n_tau = nt;
+  CU(cudaSetDevice(s->cfg.device));
+  CU(cudaStreamSynchronize(s->stream));  // a queued step may still read the old arrays
+  cudaFree(s->d_skin);
+  cudaFree(s->d_skin_wb);
+  s->d_skin = nullptr;
+  s->d_skin_wb = nullptr;
+  const size_t M = (size_t)std::max(m, 1);
+  CU(cudaMalloc(&s->d_skin, sizeof(double) * (3 + 3 + fsg::SKIN_KW + 9 + 1) * M));
+  CU(cudaMalloc(&s->d_skin_wb, sizeof(int) * fsg::SKIN_KW * M));
+  double* d = s->d_skin;
+  CU(cudaMemcpy(d, rest, sizeof(double) * 3 * m, cudaMemcpyHostToDevice));
+  CU(cudaMemcpy(d + 3 * M, nrest, sizeof(double) * 3 * m, cudaMemcpyHostToDevice));
+  CU(cudaMemcpy(d + 6 * M, ww.data(), sizeof(double) * ww.size(), cudaMemcpyHostToDevice));
+  CU(cudaMemcpy(d + (6 + fsg::SKIN_KW + 9) * M, areas, sizeof(double) * m, cudaMemcpyHostToDevice));
+  CU(cudaMemcpy(s->d_skin_wb, wb.data(), sizeof(int) * wb.size(), cudaMemcpyHostToDevice));
+  P.rest = d;
+  P.nrest = d + 3 * M;
+  P.ww = d + 6 * M;
+  P.wb = s->d_skin_wb;
+  double* mk = d + (6 + fsg::SKIN_KW) * M;
+  s->mk = Markers{mk, mk + 3 * M, mk + 6 * M, mk + 9 * M, m};
+  for (int k = 0; k < 2; ++k)
+    if (!s->h_wrench[k]) {
+      CU(cudaMallocHost(&s->h_wrench[k], sizeof(double) * (6 + FSG_SKIN_MAX_LINKS + fsg::SKIN_NSTAT) *
+                                             FSG_SKIN_MAX_BODIES));
+      std::memset(s->h_wrench[k], 0, sizeof(double) * (6 + FSG_SKIN_MAX_LINKS + fsg::SKIN_NSTAT) *
+                                         FSG_SKIN_MAX_BODIES);
+    }
+  s->mk_host = false;
+  s->mk_slot = -1;
+  s->mk_dirty = false;
+  s->skin = true;
+  s->pose_set = false;
+  return FSG_OK;
+}
+
+int fsg_set_pose(fsg_session* s, const fsg_body_pose* poses) {
+  if (!s->skin) return set_err(FSG_ESTATE, "fsg_set_pose: no skinned bodies (fsg_set_skin)");
+  if (!poses) return set_err(FSG_EINPUT, "fsg_set_pose: null poses");
+  for (int b = 0; b < s->skp.nb; ++b) s->skp.body[b].pose = poses[b];
+  s->pose_set = true;
+  return FSG_OK;
+}
+
+int fsg_get_body_wrench(fsg_session* s, double* tau, double* stats) {
+  CU(cudaSetDevice(s->cfg.device));
+  if (!s->skin) return set_err(FSG_ESTATE, "fsg_get_body_wrench: no skinned bodies");
+  CU(stream_wait(s->stream));
+  if (!s->stepped) return set_err(FSG_ESTATE, "no coupled step yet");
+  const double* w = s->h_wrench[s->last_par];
+  if (tau) std::memcpy(tau, w, sizeof(double) * s->n_tau);
+  if (stats) std::memcpy(stats, w + s->n_tau, sizeof(double) * fsg::SKIN_NSTAT * s->skp.nb);
+  return FSG_OK;
+}
+
+int fsg_get_markers(fsg_session* s, double* pts, double* vel, double* nrm) {
+  CU(cudaSetDevice(s->cfg.device));
+  CU(stream_wait(s->stream));
+  const size_t m = (size_t)s->m;
+  if (!m) return FSG_OK;
+  if (pts) CU(cudaMemcpy(pts, s->mk.pts, sizeof(double) * 3 * m, cudaMemcpyDefault));
+  if (vel) CU(cudaMemcpy(vel, s->mk.vel, sizeof(double) * 3 * m, cudaMemcpyDefault));
+  if (nrm) CU(cudaMemcpy(nrm, s->mk.nrm, sizeof(double) * 3 * m, cudaMemcpyDefault));
+  return FSG_OK;
+}
+
 // ----------------------------------------------------------------- step --
 int fsg_step_async(fsg_session* s) {
   CU(cudaSetDevice(s->cfg.device));
+  if (s->skin && s->m && !s->pose_set)
+    return set_err(FSG_ESTATE, "skinned bodies: fsg_set_pose has not been called");
   const int p = s->par;
   // the fp64 graph reads its frame constants from pinned slot p: wait until
   // the step that last used it is done.  The throughput path passes them by
@@ -868,10 +1015,16 @@ int fsg_step_async(fsg_session* s) {
       // without markers is the plain fluid K4 below.
       fsg::FixBand fb = s->fix;
       fb.stamp = ++s->stamp;
+      if (s->skin)
+        fsg::skin_update_launch(s->skp, (double*)s->mk.pts, (double*)s->mk.vel,
+                                (double*)s->mk.nrm, s->stream);
       s->L->markers_fix(s->g, s->buf[p], s->pulled, s->mk, s->d_sc, st, s->d_stencil,
                         s->d_fworld, s->h_fw[p], s->h_valid[p], fb, s->d_scr[p], s->stream);
       s->L->collide_band(s->g, s->buf[p], s->pulled, s->buf[p ^ 1], fb, s->d_sc, st,
                          frame_on ? 1 : 0, s->d_scr[p], s->d_scr[p ^ 1], 1, s->stream);
+      if (s->skin)  // deterministic tree order; tau + stats straight into pinned memory
+        fsg::skin_tau_launch(s->skp, s->d_fworld, s->d_stencil, s->mk.vel, s->h_wrench[p], 0,
+                             s->stream);
     } else if (s->g.zpad) {
       // z-slab: the two boundary planes first, packed for the neighbours
       // (fsg_halo_begin lets a comm stream start on them), then the interior

@@ -72,6 +72,112 @@ def koi_body(spacing: float, length: float = 0.4) -> Body:
     return Body(np.concatenate(pts), np.concatenate(nrms), np.concatenate(areas), length)
 
 
+# ------------------------------------------------------- articulated koi --
+# A skinned koi for the device-side marker refresh: a
+# floating base and N_SPINE revolute z joints down the spine (koi_design's 5
+# spine joints, model_builder.hpp), every marker blended between the two
+# nearest bones.  Forward kinematics is the caller's (host) work in the
+# reference -- dynamics.hpp:23-61, restated here with numpy to produce the
+# per-link pose the path consumes; the joint angles follow a kinematic
+# travelling wave at the SineGait frequency and phase step (gait.hpp:13-44).
+N_SPINE = 5
+
+
+@dataclass
+class Articulation:
+    parent: list
+    dof_index: list
+    axis: np.ndarray          # [L,3] normalized
+    joint_origin: np.ndarray  # [L,3] in parent coordinates
+    weights: np.ndarray       # [m, L]
+    floating_base: bool = True
+
+    @property
+    def n_links(self) -> int:
+        return len(self.parent)
+
+    @property
+    def n_dofs(self) -> int:
+        return (6 if self.floating_base else 0) + sum(1 for d in self.dof_index[1:] if d >= 0)
+
+
+def koi_articulation(body: Body, n_spine: int = N_SPINE) -> Articulation:
+    L = body.length
+    nb = n_spine + 1
+    seg = L / nb
+    xj = [0.5 * L - j * seg for j in range(1, nb)]  # joint j between bone j-1 and j
+    origin = np.zeros((nb, 3))
+    origin[1] = (xj[0], 0.0, 0.0)
+    for j in range(2, nb):
+        origin[j] = (xj[j - 1] - xj[j - 2], 0.0, 0.0)
+    axis = np.zeros((nb, 3))
+    axis[1:, 2] = 1.0
+    u = (0.5 * L - body.rest[:, 0]) / seg - 0.5  # bone centres at integer u
+    W = np.zeros((body.m, nb))
+    k0 = np.clip(np.floor(u).astype(int), 0, nb - 1)
+    f = u - k0
+    for i in range(body.m):
+        if u[i] <= 0.0:
+            W[i, 0] = 1.0
+        elif k0[i] >= nb - 1:
+            W[i, nb - 1] = 1.0
+        else:
+            W[i, k0[i]] = 1.0 - f[i]
+            W[i, k0[i] + 1] = f[i]
+    return Articulation(list(range(-1, nb - 1)), [0] + [6 + j for j in range(nb - 1)], axis,
+                        origin, W)
+
+
+def _angle_axis(theta: float, a: np.ndarray) -> np.ndarray:
+    """Eigen::AngleAxisd(theta, a).toRotationMatrix() (unit a)."""
+    c, s_ = math.cos(theta), math.sin(theta)
+    x, y, z = a
+    C = 1.0 - c
+    return np.array([[c + x * x * C, x * y * C - z * s_, x * z * C + y * s_],
+                     [y * x * C + z * s_, c + y * y * C, y * z * C - x * s_],
+                     [z * x * C - y * s_, z * y * C + x * s_, c + z * z * C]])
+
+
+def forward_kinematics(art: Articulation, base_R, base_p, v_gen, q):
+    """KinematicsCache of dynamics.hpp:23-61 (joint_rotation = identity):
+    -> R_world[L,3,3], p_world[L,3], omega_world[L,3], v_origin_world[L,3]."""
+    L = art.n_links
+    R = np.zeros((L, 3, 3))
+    p = np.zeros((L, 3))
+    vb = np.zeros((L, 6))
+    R[0], p[0] = base_R, base_p
+    vb[0] = v_gen[:6] if art.floating_base else 0.0
+    for i in range(1, L):
+        pa = art.parent[i]
+        d = art.dof_index[i]
+        rel = _angle_axis(q[d - 6], art.axis[i]) if d >= 0 else np.eye(3)
+        R[i] = R[pa] @ rel
+        p[i] = p[pa] + R[pa] @ art.joint_origin[i]
+        w_pa, v_pa = vb[pa, :3], vb[pa, 3:]
+        w = rel.T @ w_pa
+        v = rel.T @ (v_pa - np.cross(art.joint_origin[i], w_pa))  # apply_motion (spatial.hpp:21-26)
+        if d >= 0:
+            w = w + art.axis[i] * v_gen[d]
+        vb[i, :3], vb[i, 3:] = w, v
+    om = np.einsum("lij,lj->li", R, vb[:, :3])
+    vo = np.einsum("lij,lj->li", R, vb[:, 3:])
+    return R, p, om, vo
+
+
+def pack_pose(R, p, om, vo, rest_R, rest_p) -> np.ndarray:
+    """fsg_body_pose layout (240 doubles): BoneTransforms::of (skinning.hpp:90-99)
+    + the KinematicsCache fields."""
+    L = R.shape[0]
+    bR = np.einsum("lij,lkj->lik", R, rest_R)        # R_world * rest.R^T
+    bt = p - np.einsum("lij,lj->li", bR, rest_p)      # p_world - R_b * rest.p
+    out = np.zeros(240)
+    o = 0
+    for a, w in ((bR, 9), (bt, 3), (R, 9), (p, 3), (vo, 3), (om, 3)):
+        out[o:o + L * w] = a.reshape(-1)
+        o += 8 * w
+    return out
+
+
 def _rotz(yaw: float) -> np.ndarray:
     c, s = math.cos(yaw), math.sin(yaw)
     return np.array([[c, -s, 0.0], [s, c, 0.0], [0.0, 0.0, 1.0]])
@@ -151,6 +257,57 @@ class Scene:
             q=np.array([math.cos(0.5 * yaw), 0.0, 0.0, math.sin(0.5 * yaw)]),
             omega=np.array([0.0, 0.0, ya * w * math.cos(w * t)]),
             alpha=np.array([0.0, 0.0, -ya * w * w * math.sin(w * t)]))
+
+    # -- skinned bodies (device-side LBS + tau_ext) -------
+    def articulations(self) -> list:
+        if not hasattr(self, "_arts"):
+            self._arts = [koi_articulation(b) if self.motion == "swim" else
+                          Articulation([-1], [0], np.zeros((1, 3)), np.zeros((1, 3)),
+                                       np.ones((b.m, 1))) for b in self.bodies]
+            self._rest = []
+            for a in self._arts:
+                R, p, _, _ = forward_kinematics(a, np.eye(3), np.zeros(3), np.zeros(a.n_dofs),
+                                                np.zeros(max(a.n_links - 1, 0)))
+                self._rest.append((R, p))
+        return self._arts
+
+    def skin(self):
+        """-> (body_offsets, skeleton specs, rest_points, rest_normals, weights list, areas)."""
+        arts = self.articulations()
+        from .session import Skeleton
+        sks = [Skeleton(a.parent, a.dof_index, a.axis, a.floating_base, a.n_dofs) for a in arts]
+        return (self.offsets, sks, np.concatenate([b.rest for b in self.bodies]),
+                np.concatenate([b.normals for b in self.bodies]), [a.weights for a in arts],
+                np.concatenate([b.areas for b in self.bodies]))
+
+    def joint_state(self, k: int, step: int):
+        """(base_R, base_p, v_gen, q) of body k: the base motion of base_pose and
+        a travelling wave q_j = A_j sin(w t - j phase_step) down the spine."""
+        a = self.articulations()[k]
+        pose = self.base_pose(k, step)
+        R0 = _rotz(pose.yaw)
+        v = np.zeros(a.n_dofs)
+        v[:3] = (0.0, 0.0, pose.yaw_rate)        # base omega, body coordinates
+        v[3:6] = R0.T @ pose.v                   # base velocity, body coordinates
+        nj = a.n_links - 1
+        q = np.zeros(nj)
+        w = 2.0 * math.pi * self.gait_hz
+        t = step * self.dt
+        for j in range(nj):
+            A = 0.15 * (j + 1) / nj
+            q[j] = A * math.sin(w * t - 0.8 * j)
+            v[6 + j] = A * w * math.cos(w * t - 0.8 * j)
+        return R0, pose.p, v, q
+
+    def poses(self, step: int) -> np.ndarray:
+        """[n_bodies, 240] packed fsg_body_pose of every body at `step`."""
+        arts = self.articulations()
+        out = np.zeros((len(arts), 240))
+        for k, a in enumerate(arts):
+            R0, p0, v, q = self.joint_state(k, step)
+            R, p, om, vo = forward_kinematics(a, R0, p0, v, q)
+            out[k] = pack_pose(R, p, om, vo, *self._rest[k])
+        return out
 
     def markers(self, step: int):
         """World-frame (points, velocities, normals, areas) of all bodies at `step`."""

@@ -165,6 +165,63 @@ class FrameFollower:
             pass
 
 
+POSE_DOUBLES = 240  # sizeof(fsg_body_pose) / 8
+
+
+@dataclass
+class Skeleton:
+    """Topology of a robot (skeleton.hpp:16-93) as the skinning path needs it:
+    parent of each link, velocity-space index of its revolute dof (-1: none)
+    and the normalized joint axis (links[i].axis.normalized())."""
+
+    parent: list
+    dof_index: list
+    axis: np.ndarray
+    floating_base: bool = True
+    n_dofs: int = 0
+
+    @property
+    def n_links(self) -> int:
+        return len(self.parent)
+
+    def to_c(self) -> _abi.fsg_skeleton:
+        c = _abi.fsg_skeleton()
+        c.n_links = self.n_links
+        c.floating_base = 1 if self.floating_base else 0
+        c.n_dofs = int(self.n_dofs)
+        ax = np.asarray(self.axis, dtype=np.float64).reshape(-1, 3)
+        for j in range(self.n_links):
+            c.parent[j] = int(self.parent[j])
+            c.dof_index[j] = int(self.dof_index[j])
+            for k in range(3):
+                c.axis[j][k] = float(ax[j, k])
+        return c
+
+
+@dataclass
+class BodyPose:
+    """One body's pose for a step: BoneTransforms::of (skinning.hpp:85-102)
+    and the KinematicsCache fields (dynamics.hpp:14-21), per link."""
+
+    bone_R: np.ndarray          # [L,3,3]
+    bone_t: np.ndarray          # [L,3]
+    R_world: np.ndarray         # [L,3,3]
+    p_world: np.ndarray         # [L,3]
+    v_origin_world: np.ndarray  # [L,3]
+    omega_world: np.ndarray     # [L,3]
+
+    def packed(self) -> np.ndarray:
+        L = _abi.SKIN_MAX_LINKS
+        out = np.zeros(POSE_DOUBLES)
+        o = 0
+        for a, w in ((self.bone_R, 9), (self.bone_t, 3), (self.R_world, 9), (self.p_world, 3),
+                     (self.v_origin_world, 3), (self.omega_world, 3)):
+            a = np.asarray(a, dtype=np.float64).reshape(-1, w)
+            out[o:o + a.shape[0] * w] = a.reshape(-1)
+            o += L * w
+        return out
+
+
 class CoupledSession:
     """One device-resident IB-LBM domain (sim::CoupledSession, session.hpp:29-224)."""
 
@@ -312,6 +369,63 @@ class CoupledSession:
                                                 d_points, d_velocities, d_normals, d_areas))
         self.m = int(off[-1]) if nb > 0 else 0
         self.n_bodies = nb
+
+    # -- skinned bodies on the device -------------------
+    def set_skin(self, body_offsets, skeletons, rest_points, rest_normals, weights, areas) -> None:
+        """Register skinned bodies (SurfaceSamples of each robot, sampling.hpp):
+        every later step refreshes the markers on the device from the pose
+        (update_samples, sampling.hpp:307-322) and reduces tau_ext and the
+        CouplingStats there (session.hpp:129-143).  weights: per body an
+        [m_b, n_links_b] array (or all of them concatenated, flattened)."""
+        off = np.ascontiguousarray(body_offsets, dtype=np.int64)
+        nb = len(off) - 1
+        sk = (_abi.fsg_skeleton * max(nb, 1))()
+        for b, k in enumerate(skeletons):
+            sk[b] = k.to_c()
+        if isinstance(weights, (list, tuple)):
+            weights = np.concatenate([np.asarray(w, dtype=np.float64).reshape(-1) for w in weights])
+        arrs = [np.ascontiguousarray(a, dtype=np.float64).reshape(-1)
+                for a in (rest_points, rest_normals, weights, areas)]
+        check(self._L.fsg_set_skin(self._h, nb, off.ctypes.data_as(_abi._i64p), sk,
+                                   *(dptr(a) for a in arrs)))
+        self.m = int(off[-1])
+        self.n_bodies = nb
+        self._ndofs = [int(k.n_dofs) for k in skeletons]
+        self._pose = (_abi.fsg_body_pose * nb)()
+        self._pose_np = np.frombuffer(self._pose, dtype=np.float64).reshape(nb, POSE_DOUBLES)
+
+    def set_pose(self, poses) -> None:
+        """This step's pose of every skinned body: a list of BodyPose, or an
+        [n_bodies, 240] array already packed in fsg_body_pose order."""
+        if getattr(self, "_pose", None) is None:  # no skinned bodies: the ABI reports it
+            check(self._L.fsg_set_pose(self._h, None))
+        if isinstance(poses, np.ndarray):
+            self._pose_np[...] = poses.reshape(self._pose_np.shape)
+        else:
+            for b, p in enumerate(poses):
+                self._pose_np[b] = p.packed()
+        rc = self._L.fsg_set_pose(self._h, self._pose)
+        if rc:
+            check(rc)
+
+    def body_wrench(self):
+        """-> (tau_ext per body [list of n_dofs arrays], stats[n_bodies, 7]) of the last step."""
+        tau = np.empty(max(sum(self._ndofs), 1))
+        stats = np.empty(7 * self.n_bodies)
+        rc = self._L.fsg_get_body_wrench(self._h, dptr(tau), dptr(stats))
+        if rc:
+            check(rc)
+        out, k = [], 0
+        for n in self._ndofs:
+            out.append(tau[k:k + n].copy())
+            k += n
+        return out, stats.reshape(-1, 7)
+
+    def markers(self):
+        """-> (points, velocities, normals) [m, 3] the last step used."""
+        a = [np.empty(3 * self.m) for _ in range(3)]
+        check(self._L.fsg_get_markers(self._h, *(dptr(x) for x in a)))
+        return tuple(x.reshape(-1, 3) for x in a)
 
     def step(self) -> StepStatus:
         """Fluid half of CoupledSession::step (session.hpp:94-166)."""

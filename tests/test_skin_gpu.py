@@ -1,0 +1,104 @@
+"""GPU: skinned bodies on the device against the oracle.
+
+fp64 (parity mode): the device-skinned markers (update_samples), the marker
+forces, tau_ext and CouplingStats (session.hpp:129-143) and the fluid state
+are bit-identical to the oracle driving the same steps.  fp32 (throughput):
+the skinned markers and stencil sets are identical to fp64 (the skinning is
+fp64 in both modes), tau_ext and the stats within rel-L2 1e-5 of fp64, and
+bit-identical run to run (fixed reduction order)."""
+import numpy as np
+import pytest
+
+from cases import rel_l2
+from skin_cases import run_gpu_skin, run_oracle_skin, skin_scene
+
+pytestmark = pytest.mark.gpu
+
+STEPS = [0, 1, 2, 3]
+
+
+@pytest.fixture(scope="module")
+def one_fish():
+    sc = skin_scene()
+    return sc, run_oracle_skin(sc, STEPS)
+
+
+def test_fp64_skinned_step_bit_exact(one_fish):
+    sc, (o, fo) = one_fish
+    g, fg = run_gpu_skin(sc, STEPS, "fp64")
+    for a, b in zip(g, o):
+        for k in ("pts", "vel", "nrm", "fw", "tau", "stats"):
+            assert np.array_equal(np.asarray(a[k]), np.asarray(b[k])), k
+        assert np.array_equal(a["valid"], b["valid"])
+        assert np.array_equal(a["stats_session"], b["stats_session"])
+        assert a["min_f"] == b["min_f"]
+    assert np.array_equal(fg, fo)
+
+
+def test_fp64_two_bodies_frame_none():
+    sc = skin_scene(dims=(64, 28, 28), frame_mode="none", bodies=2)
+    o, fo = run_oracle_skin(sc, [0, 1, 2])
+    g, fg = run_gpu_skin(sc, [0, 1, 2], "fp64")
+    for a, b in zip(g, o):
+        for k in ("pts", "vel", "nrm", "fw", "tau", "stats"):
+            assert np.array_equal(np.asarray(a[k]), np.asarray(b[k])), k
+    assert np.array_equal(fg, fo)
+
+
+def test_fp32_skinned_step_within_tolerance(one_fish):
+    sc, (o, _) = one_fish
+    g64, _ = run_gpu_skin(sc, STEPS, "fp64")
+    g, _ = run_gpu_skin(sc, STEPS, "fp32")
+    for a, b, c in zip(g, o, g64):
+        for k in ("pts", "vel", "nrm"):
+            assert np.array_equal(a[k], b[k]), k  # fp64 skinning in both modes
+        assert np.array_equal(a["valid"], b["valid"])
+        assert np.array_equal(a["stencils"], c["stencils"])
+        assert rel_l2(a["fw"], b["fw"]) <= 1e-5
+        assert rel_l2(a["tau"], b["tau"]) <= 1e-5
+        assert rel_l2(a["stats"], b["stats"]) <= 1e-5
+
+
+def test_fp32_tau_run_to_run_identical():
+    sc = skin_scene()
+    a, _ = run_gpu_skin(sc, [0, 1, 2], "fp32")
+    b, _ = run_gpu_skin(sc, [0, 1, 2], "fp32")
+    for x, y in zip(a, b):
+        assert np.array_equal(x["tau"], y["tau"]) and np.array_equal(x["stats"], y["stats"])
+
+
+def test_fp32_virtual_work_identity():
+    """test_ib.cpp:215-249 on the device's outputs: tau_ext . v = power_on_body."""
+    sc = skin_scene()
+    g, _ = run_gpu_skin(sc, [0, 1, 2], "fp32")
+    for k, r in zip([0, 1, 2], g):
+        _, _, v, _ = sc.joint_state(0, k)
+        p = r["stats"][0, 6]
+        assert abs(r["tau"] @ v - p) < 1e-9 * max(1.0, abs(p))
+
+
+def test_skin_api_contract():
+    from paper_2206_01683_b200 import CoupledSession, SessionConfig
+    from paper_2206_01683_b200._abi import FsgError, InputError
+    sc = skin_scene()
+    s = CoupledSession(SessionConfig(dims=sc.dims, dx=sc.dx, dt=sc.dt, rho=sc.rho, nu=sc.nu,
+                                     frame_mode=sc.frame_mode, precision="fp32", max_markers=sc.m))
+    off, sks, rest, nrest, W, areas = sc.skin()
+    with pytest.raises(FsgError):
+        s.set_pose(sc.poses(0))  # no skinned bodies yet
+    s.set_skin(off, sks, rest, nrest, W, areas)
+    with pytest.raises(FsgError):
+        s.step()  # no pose yet
+    bad = [np.full_like(W[0], 1.0 / W[0].shape[1])]  # 6 nonzero weights per marker
+    with pytest.raises(InputError):
+        s.set_skin(off, sks, rest, nrest, bad, areas)
+    s.set_skin(off, sks, rest, nrest, W, areas)
+    s.set_frame(sc.frame(0))
+    s.set_pose(sc.poses(0))
+    assert s.step().stable()
+    # back to host markers: the skinned path is off again
+    s.set_markers(off, *sc.markers(1))
+    s.step()
+    with pytest.raises(FsgError):
+        s.body_wrench()
+    s.close()
