@@ -62,6 +62,9 @@ def parse_args():
     ap.add_argument("--c4-scaling", default="weak", choices=["weak", "strong"],
                     help="c4: each rank owns 512^3 (weak) or one 512^3 grid is split (strong)")
     ap.add_argument("--e2e-steps", type=int, default=100)
+    ap.add_argument("--markers", default="skinned", choices=["skinned", "host"],
+                    help="c1-c3: bodies skinned on the device from a per-link pose each step "
+                         "(fsg_set_pose; tau_ext read back) or marker arrays set each step")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     return ap.parse_args()
@@ -458,9 +461,15 @@ def run_ours(args, scene, rank, local, world):
     W, K = args.warmup, args.steps
     nsteps = W + K
     m = scene.m
-    # marker state of every step, resident in HBM before timing
+    skinned = bool(m) and args.markers == "skinned"
+    # marker state of every step, resident in HBM before timing (skinned:
+    # the per-link poses, passed as launch parameters)
     mk_dev = None
-    if m:
+    poses = None
+    if skinned:
+        s.set_skin(*scene.skin())
+        poses = [scene.poses(k) for k in range(nsteps)]
+    elif m:
         P = np.zeros((nsteps, 4, 3 * m))
         for k in range(nsteps):
             pts, vel, nrm, area = scene.markers(k)
@@ -485,7 +494,9 @@ def run_ours(args, scene, rank, local, world):
 
     def set_step(k):
         s.set_frame(frames[k])
-        if m:
+        if skinned:
+            s.set_pose(poses[k])
+        elif m:
             r = mk_dev[k]
             s.set_markers_device(off, r[0].data_ptr(), r[1].data_ptr(), r[2].data_ptr(),
                                  r[3].data_ptr())
@@ -538,6 +549,8 @@ def run_ours(args, scene, rank, local, world):
             fl_ms, fl_n = s.profile_read()
             s.profile(False)
             fluid_ms = fl_ms / max(fl_n, 1)
+            if skinned:
+                s.set_skin(*scene.skin())
     t_total = step_ms * K / 1e3
     if world > 1:
         import torch.distributed as dist
@@ -548,27 +561,32 @@ def run_ours(args, scene, rank, local, world):
 
     # ---- end to end through the public API with host buffers
     E = min(args.e2e_steps, K)
-    mk_host = [scene.markers(k) for k in range(8)] if m else None
+    mk_host = [scene.markers(k) for k in range(8)] if (m and not skinned) else None
     e2e_t = 0.0
+
+    def e2e_step(k):
+        # the robot side's per-step exchange: pose up, tau_ext + stats down
+        # (skinned), or the whole marker state up and per-marker forces down
+        s.set_frame(frames[k % nsteps])
+        if skinned:
+            s.set_pose(poses[k % nsteps])
+        elif m:
+            s.set_markers(off, *mk_host[k % 8])
+        s.step()
+        if skinned:
+            s.body_wrench()
+        elif m:
+            s.marker_forces()
+
     with torch.cuda.stream(stream):
         s.reset_to_rest()
         for k in range(3):
-            s.set_frame(frames[k])
-            if m:
-                s.set_markers(off, *mk_host[k % 8])
-            s.step()
-            if m:
-                s.marker_forces()
+            e2e_step(k)
         for k in range(E):
             flush()
             torch.cuda.synchronize(dev)
             t0 = time.perf_counter()
-            s.set_frame(frames[k % nsteps])
-            if m:
-                s.set_markers(off, *mk_host[k % 8])
-            st_e = s.step()
-            if m:
-                s.marker_forces()
+            e2e_step(k)
             e2e_t += time.perf_counter() - t0
     e2e_val = scene.n_cells * E / e2e_t / 1e6
     if world > 1:
@@ -576,8 +594,14 @@ def run_ours(args, scene, rank, local, world):
         t = torch.tensor([e2e_t], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_val = scene.n_cells * E * world / float(t.item()) / 1e6
-    h2d = 80 * m + 232          # marker state (pts, vel, nrm 3x8 B, area 8 B) + frame consts
-    d2h = 28 * m + 64           # marker forces (3x8 B) + validity (4 B) + step status
+    nb = len(scene.bodies)
+    if skinned:
+        ndof = sum(sk.n_dofs for sk in scene.skin()[1])
+        h2d = 1920 * nb + 232   # fsg_body_pose per body (240 doubles) + frame consts
+        d2h = 8 * (ndof + 7 * nb) + 64  # tau_ext + CouplingStats + step status
+    else:
+        h2d = 80 * m + 232      # marker state (pts, vel, nrm 3x8 B, area 8 B) + frame consts
+        d2h = 28 * m + 64       # marker forces (3x8 B) + validity (4 B) + step status
     s.close()
 
     peak, peak_src = measured_peaks()
@@ -591,14 +615,18 @@ def run_ours(args, scene, rank, local, world):
         "metric": METRIC, "value": round(value, 1), "unit": "MLUPS", "n_gpus": world,
         "steps": K, "warmup": W, "ms_per_step": round(step_ms, 4), "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f32 (fp32 storage of f - w_i)",
-        "data": "synthetic (prescribed-kinematics bodies, fluid at rest; SURVEY.md §8(d))",
+        "data": ("synthetic (articulated bodies skinned on the device from a prescribed "
+                 "per-link pose each step, fluid at rest; SURVEY.md §8(d))" if skinned else
+                 "synthetic (prescribed-kinematics bodies, fluid at rest; SURVEY.md §8(d))"),
         "config": {"workload": scene.name, "dims": list(scene.dims), "markers": m,
+                   "marker_source": "skinned on device" if skinned else ("host arrays" if m else None),
                    "frame": scene.frame_mode, "l2": "flushed between timed steps",
                    "parallelism": f"replicas x{world}" if world > 1 else "single GPU"},
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                      "frac": round(achieved / peak, 4), "traffic": traffic,
                      "kernel": ("k_collide_band (collide+stream+open BC+VF+IB band) with the "
-                                "overlapped k_markers_fix: timed as the whole step interval"
+                                "overlapped k_markers_fix" + (" (+ k_skin_update, k_skin_tau)" if skinned else "")
+                                + ": timed as the whole step interval"
                                 if m else "k_collide_fix (collide+stream+open BC+VF)"),
                      "peak_source": peak_src,
                      "step_ms": round(k4_avg_s * 1e3, 4),
@@ -609,7 +637,7 @@ def run_ours(args, scene, rank, local, world):
                          "frac": round(BYTES_PER_CELL * scene.n_cells / (fluid_ms / 1e3) / 1e9 / peak, 4)}},
         "e2e": {"value": round(e2e_val, 1), "unit": "MLUPS", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h, "steps": E},
-        "gpu_launches": K * (2 if m else 1),
+        "gpu_launches": K * (4 if skinned else (2 if m else 1)),
         "status": {"stable": bool(st.stable()), "min_f": st.min_f},
         "clocks": clk.summary(),
     }

@@ -6,6 +6,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include "../../include/fsg.h"
+
 // minimum resident 128-thread blocks per SM asked of ptxas for the
 // throughput K4 and marker kernels (register caps: 65536 / (128 * MINB))
 #ifndef FSG_K4_MINB
@@ -151,6 +153,20 @@ constexpr int LO_BIAS = 0x40000000;
 // deterministic whatever the order -- over 4x4x4 tiles flagged per step.
 constexpr double FIX_SCALE = 1099511627776.0;        // 2^40
 constexpr double FIX_INV = 1.0 / 1099511627776.0;   // 2^-40
+// Skinned bodies, fused path: the marker kernel adds every block's tau_ext /
+// CouplingStats sums to 64-bit fixed-point accumulators (integer atomics:
+// order-independent, deterministic); the banded K4, after it has waited for
+// the marker grid, converts them into the output (pinned host memory) and
+// re-zeroes them.  acc = nullptr: no skinned bodies.
+constexpr double SKIN_FIX_SCALE = 17592186044416.0;      // 2^44
+constexpr double SKIN_FIX_INV = 1.0 / 17592186044416.0;  // 2^-44
+struct SkinOut {
+  unsigned long long* acc;  // [nb][32]: dof c (< 14) and stat 14 + k
+  double* out;              // tau (concatenated) then 7 stats per body
+  int nb, nt;               // bodies, total dofs
+  int ndof[2], off[2];      // per body: n_dofs, first tau entry
+};
+
 struct FixBand {
   unsigned long long* F;     // 3 per owned cell (x + nx*(y + ny*z))
   unsigned* tflag;           // per 4^3 tile: stamp of the last step a stencil touched it
@@ -259,6 +275,9 @@ struct BatchHead {
 };
 
 // ---------------------------------------------------------- kernel table --
+template <int NB>
+struct SkinParamsN;
+
 // Launchers exported by each precision translation unit.
 struct Launchers {
   void (*fill_rest)(const Grid&, void* A, cudaStream_t);
@@ -288,9 +307,17 @@ struct Launchers {
   // throughput path (fp32 only; nullptr in the fp64 table): markers scatter
   // fixed-point forces; K4 consumes them.  Both K4 variants reset the next
   // step's scratch from block 0; the host copies the status out on demand.
-  void (*markers_fix)(const Grid&, const void* A, int pulled, Markers, const SessionConsts*,
-                      const StepConsts& st, MarkerStencil*, double* fworld, double* fworld_host,
-                      int* valid_host, FixBand, StepScratch*, cudaStream_t);
+  // km_done (nullable): every block adds 1 when its markers are complete (a
+  // concurrent consumer spins on it); pdl: launched as a programmatic
+  // dependent of the kernel before it (which must trigger early).  Returns
+  // the grid size.
+  // skin (nullable, <= 2 bodies): skinned bodies fused into the marker kernel
+  // (fsg_skin_fused.cuh), tau + stats added to the fixed-point skin_acc.
+  int (*markers_fix)(const Grid&, const void* A, int pulled, Markers, const SessionConsts*,
+                     const StepConsts& st, MarkerStencil*, double* fworld, double* fworld_host,
+                     int* valid_host, FixBand, StepScratch*, unsigned* km_done, int pdl,
+                     const SkinParamsN<FSG_SKIN_MAX_BODIES>* skin, unsigned long long* skin_acc,
+                     cudaStream_t);
   // pure-fluid step (no IB band); planes: 0 all, 1 the two z-boundary planes,
   // 2 the interior planes (z-slab step: boundary first, halo send, interior)
   void (*collide_fix)(const Grid&, const void* A, int pulled, void* B, const SessionConsts*,
@@ -300,7 +327,8 @@ struct Launchers {
   // of the marker kernel launched just before it on the same stream
   void (*collide_band)(const Grid&, const void* A, int pulled, void* B, FixBand,
                        const SessionConsts*, const StepConsts& st, int frame_on,
-                       StepScratch* scr, StepScratch* scr_next, int pdl, cudaStream_t);
+                       StepScratch* scr, StepScratch* scr_next, int pdl, const SkinOut& so,
+                       cudaStream_t);
   // batched coupled step over E env sessions (fp32): markers + banded K4 of
   // every env in one launch each; d_packs: E EnvPacks in device memory
   void (*step_batch)(const Grid&, const SessionConsts*, const EnvPack* d_packs, BatchHead h,

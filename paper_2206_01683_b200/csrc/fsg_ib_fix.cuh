@@ -41,11 +41,12 @@ struct MkStencil {
   bool ok;              // marker_in_bounds (coupling.hpp:18-24)
 };
 
-__device__ __forceinline__ void mk_stencil(const Markers& mk, int t, const SessionConsts& sc,
-                                           const StepConsts& st, MkStencil& S) {
+/// From the world position x (SI).
+__device__ __forceinline__ void mk_stencil_x(const double* x, const SessionConsts& sc,
+                                             const StepConsts& st, MkStencil& S) {
   double xw[3];
 #pragma unroll
-  for (int k = 0; k < 3; ++k) xw[k] = mk.pts[3 * t + k] - st.p[k];
+  for (int k = 0; k < 3; ++k) xw[k] = x[k] - st.p[k];
   mat_t_vec(st.R, xw, S.xf);
 #pragma unroll
   for (int k = 0; k < 3; ++k) S.xl[k] = S.xf[k] / sc.dx + sc.hd[k];
@@ -58,6 +59,12 @@ __device__ __forceinline__ void mk_stencil(const Markers& mk, int t, const Sessi
     S.hi[a] = (int)floor(S.xl[a] + half);
     S.cnt[a] = S.hi[a] - S.lo[a] + 1;
   }
+}
+
+__device__ __forceinline__ void mk_stencil(const Markers& mk, int t, const SessionConsts& sc,
+                                           const StepConsts& st, MkStencil& S) {
+  const double x[3] = {mk.pts[3 * t], mk.pts[3 * t + 1], mk.pts[3 * t + 2]};
+  mk_stencil_x(x, sc, st, S);
 }
 
 /// Stamp the (<= 2x2x2: the stencil spans <= 5 cells) tiles the stencil touches.
@@ -80,7 +87,8 @@ __device__ __forceinline__ void mk_finish(const Grid& g, const float* __restrict
                                           const MkStencil& S, double (*phs)[5],
                                           MarkerStencil* __restrict__ rec_out, double* __restrict__ fworld,
                                           double* fworld_h, int* valid_h, const FixBand& fb,
-                                          StepScratch* out) {
+                                          StepScratch* out, const double* vel_in = nullptr,
+                                          const double* nrm_in = nullptr, double* fw_out = nullptr) {
   const unsigned full = fx_mask();
   if (!S.ok) {
     if (lane == 0) {
@@ -147,8 +155,8 @@ __device__ __forceinline__ void mk_finish(const Grid& g, const float* __restrict
   double vel[3], nrm[3], vw[3], vf[3], nf[3], fl[3], fw[3], ff[3];
 #pragma unroll
   for (int k = 0; k < 3; ++k) {
-    vel[k] = mk.vel[3 * t + k];
-    nrm[k] = mk.nrm[3 * t + k];
+    vel[k] = vel_in ? vel_in[k] : mk.vel[3 * t + k];
+    nrm[k] = nrm_in ? nrm_in[k] : mk.nrm[3 * t + k];
   }
   const double area = mk.area[t];
 #pragma unroll
@@ -172,6 +180,11 @@ __device__ __forceinline__ void mk_finish(const Grid& g, const float* __restrict
   mat_vec(st.R, fl, fw);
   mat_t_vec(st.R, fw, ff);
   const double fx = ff[0] * sc.f2l, fy = ff[1] * sc.f2l, fz = ff[2] * sc.f2l;
+  if (fw_out) {
+    fw_out[0] = fw[0];
+    fw_out[1] = fw[1];
+    fw_out[2] = fw[2];
+  }
   if (lane == 0) {
     fworld[3 * t] = fw[0];
     fworld[3 * t + 1] = fw[1];
@@ -223,12 +236,16 @@ template <bool PULLED>
 __global__ void __launch_bounds__(128, FSG_KM_MINB)
     k_markers_fix(Grid g, const float* __restrict__ A, Markers mk, const SessionConsts* __restrict__ scp,
                   const StepConsts st, MarkerStencil* __restrict__ rec_out, double* __restrict__ fworld,
-                  double* fworld_h, int* valid_h, FixBand fb, StepScratch* out) {
+                  double* fworld_h, int* valid_h, FixBand fb, StepScratch* out, unsigned* km_done) {
   __shared__ double phs[FX_PER_BLOCK][3][5];
   const int lane = threadIdx.x & (FX_LANES - 1);
   const int slot = threadIdx.x / FX_LANES;
   const int stride = gridDim.x * FX_PER_BLOCK;
   const SessionConsts& sc = *scp;
+  // skinned bodies: launched as a programmatic dependent of the skinning
+  // kernel (its launch latency overlaps it); wait for the marker state.  A
+  // no-op for an ordinary launch.
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   if (threadIdx.x == 0) FSG_TL(fb.stamp, 0);  // timeline (dev build): marker kernel start
   for (int t = blockIdx.x * FX_PER_BLOCK + slot; t < mk.m; t += stride) {
     MkStencil S;
@@ -250,4 +267,88 @@ __global__ void __launch_bounds__(128, FSG_KM_MINB)
     __syncwarp(fx_mask());  // phs[slot] is reused by the group's next marker
   }
   if (lane == 0) FSG_TL(fb.stamp, 1);  // last marker warp done
+  if (km_done) {  // this block's forces and validity flags are complete
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      __threadfence();
+      atomicAdd(km_done, 1u);
+    }
+  }
+}
+
+#include "fsg_skin_fused.cuh"
+
+/// The marker kernel for skinned bodies (fsg_set_skin, up to two): each warp
+/// skins its marker from the pose (launch parameter) before stamping, skins
+/// velocity and normal before the forcing, and adds the marker's tau_ext
+/// terms and stats to the warp's running sums; the block tail reduces them
+/// (fsg_skin_fused.cuh).  Same stamp / fence / trigger protocol as
+/// k_markers_fix.
+template <bool PULLED, int NB>
+__global__ void __launch_bounds__(128, FSG_KM_MINB)
+    k_markers_skin(Grid g, const float* __restrict__ A, Markers mk, const SessionConsts* __restrict__ scp,
+                   const StepConsts st, MarkerStencil* __restrict__ rec_out, double* __restrict__ fworld,
+                   double* fworld_h, int* valid_h, FixBand fb, StepScratch* out,
+                   const __grid_constant__ SkinParamsN<NB> P, unsigned long long* fixacc) {
+  __shared__ double phs[FX_PER_BLOCK][3][5];
+  const int lane = threadIdx.x & (FX_LANES - 1);
+  const int slot = threadIdx.x / FX_LANES;
+  const int stride = gridDim.x * FX_PER_BLOCK;
+  const SessionConsts& sc = *scp;
+  if (threadIdx.x == 0) FSG_TL(fb.stamp, 0);
+  for (int t = blockIdx.x * FX_PER_BLOCK + slot; t < mk.m; t += stride) {
+    const SkinBody& B = P.body[skin_body_of(P, t)];
+    const SkinSlot sl = skin_slot(P, t, lane);
+    double xw[3];
+    skin_point_warp(P, B.pose, t, sl, xw);
+    if (lane == 0) {
+      double* pts = const_cast<double*>(mk.pts);
+      pts[3 * t] = xw[0];
+      pts[3 * t + 1] = xw[1];
+      pts[3 * t + 2] = xw[2];
+    }
+    MkStencil S;
+    mk_stencil_x(xw, sc, st, S);
+    mk_stamp(g, fb, S, lane);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) __threadfence();
+  __syncthreads();
+  asm volatile("griddepcontrol.launch_dependents;");
+  double acc[NB];
+#pragma unroll
+  for (int b = 0; b < NB; ++b) acc[b] = 0.0;
+  for (int t = blockIdx.x * FX_PER_BLOCK + slot; t < mk.m; t += stride) {
+    const int bi = skin_body_of(P, t);
+    const SkinBody& B = P.body[bi];
+    const SkinSlot sl = skin_slot(P, t, lane);
+    double xw[3], vel[3], nrm[3], fw[3];
+    skin_point_warp(P, B.pose, t, sl, xw);  // recomputed: cheaper than keeping it live
+    skin_vel_nrm_warp(P, B.pose, t, sl, vel, nrm);
+    if (lane == 0) {
+      double* v = const_cast<double*>(mk.vel);
+      double* n = const_cast<double*>(mk.nrm);
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        v[3 * t + c] = vel[c];
+        n[3 * t + c] = nrm[c];
+      }
+    }
+    MkStencil S;
+    mk_stencil_x(xw, sc, st, S);
+    mk_finish<PULLED>(g, A, mk, t, lane, sc, st, S, phs[slot], rec_out, fworld, fworld_h, valid_h, fb,
+                      out, vel, nrm, fw);
+    __syncwarp(fx_mask());
+#ifndef FSG_SKIN_NO_TAU
+    if (S.ok) {
+#pragma unroll
+      for (int b = 0; b < NB; ++b)
+        if (b == bi) skin_tau_warp(P, B, t, lane, fw, vel, acc[b]);
+    }
+#endif
+  }
+  if (lane == 0) FSG_TL(fb.stamp, 1);
+#ifndef FSG_SKIN_NO_TAIL
+  skin_block_red(acc, fixacc);
+#endif
 }

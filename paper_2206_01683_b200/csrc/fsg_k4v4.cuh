@@ -150,11 +150,15 @@ template <bool PULLED, bool VF>
 __global__ void __launch_bounds__(128, FSG_K4_MINB)
     k_collide_band(Grid g, DirPtrs dp, const float* __restrict__ A, FixBand fb,
                    const SessionConsts* __restrict__ scp, const StepConsts st,
-                   StepScratch* __restrict__ out, StepScratch* __restrict__ next, int zc) {
+                   StepScratch* __restrict__ out, StepScratch* __restrict__ next, int zc,
+                   SkinOut so) {
   __shared__ int item;
   __shared__ int tl[128];
   __shared__ int ntl;
   const int tid = threadIdx.x + blockDim.x * threadIdx.y;
+  // a programmatic dependent (the skinned bodies' tau reduction) may start now:
+  // it waits on the marker kernel, not on this one
+  asm volatile("griddepcontrol.launch_dependents;");
   reset_next(next, tid);
   const SessionConsts& sc = *scp;
   const int tx_n = (g.nx + blockDim.x - 1) / blockDim.x;
@@ -193,6 +197,16 @@ __global__ void __launch_bounds__(128, FSG_K4_MINB)
   if (tid == 0) FSG_TL(fb.stamp, 3);  // phase A done (this block)
   pdl_wait();
   if (tid == 0) FSG_TL(fb.stamp, 4);  // band phase start
+  // skinned bodies: the marker grid's tau_ext / stats sums are complete
+  if (so.acc && blockIdx.x == gridDim.x - 1 && tid < so.nb * 32) {
+    const int b = tid >> 5, c = tid & 31;
+    const long long v = (long long)__ldcg(so.acc + tid);
+    so.acc[tid] = 0ull;
+    const double d = (double)v * SKIN_FIX_INV;
+    if (c < so.ndof[b]) so.out[so.off[b] + c] = d;
+    if (c >= SKIN_TAU_MAX && c < SKIN_TAU_MAX + SKIN_NSTAT)
+      so.out[so.nt + SKIN_NSTAT * b + (c - SKIN_TAU_MAX)] = d;
+  }
   const int ntile = fb.tnx * fb.tny * fb.tnz;
   const int nthr = blockDim.x * blockDim.y;  // 96 or 128 (cell_block)
   const int tpp = nthr >> 6;                 // tiles per pass (64 threads each)

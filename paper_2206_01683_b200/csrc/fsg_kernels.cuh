@@ -26,6 +26,7 @@
 #include <math.h>
 
 #include "fsg_device.cuh"
+#include "fsg_skin.cuh"
 
 #ifndef FSG_PREC
 #error "define FSG_PREC to 32 or 64"
@@ -802,11 +803,27 @@ static void L_halo_unpack(const Grid& g, void* B, const void* lo, const void* hi
 }
 
 #if FSG_PREC == 32
-static void L_markers_fix(const Grid& g, const void* A, int pulled, Markers mk,
-                          const SessionConsts* sc, const StepConsts& st, MarkerStencil* rec,
-                          double* fworld, double* fworld_h, int* valid_h, FixBand fb,
-                          StepScratch* out, cudaStream_t s) {
-  if (mk.m == 0) return;
+template <int NB>
+static SkinParamsN<NB> skin_narrow(const SkinParams& P) {
+  SkinParamsN<NB> q;
+  q.nb = P.nb;
+  q.m = P.m;
+  q.rest = P.rest;
+  q.nrest = P.nrest;
+  q.wb = P.wb;
+  q.ww = P.ww;
+  q.part = P.part;
+  q.ticket = P.ticket;
+  for (int b = 0; b < NB; ++b) q.body[b] = P.body[b];
+  return q;
+}
+
+static int L_markers_fix(const Grid& g, const void* A, int pulled, Markers mk,
+                         const SessionConsts* sc, const StepConsts& st, MarkerStencil* rec,
+                         double* fworld, double* fworld_h, int* valid_h, FixBand fb,
+                         StepScratch* out, unsigned* km_done, int pdl, const SkinParams* skin,
+                         unsigned long long* skin_acc, cudaStream_t s) {
+  if (mk.m == 0) return 0;
   // marker blocks per SM (FSG_KM_PER_SM, default below; 0 = one marker per
   // warp, a single wave of up to m/4 blocks)
   static int cap = -1;
@@ -820,12 +837,36 @@ static void L_markers_fix(const Grid& g, const void* A, int pulled, Markers mk,
   }
   unsigned nb = (unsigned)((mk.m + FX_PER_BLOCK - 1) / FX_PER_BLOCK);
   if (cap > 0) nb = std::min(nb, (unsigned)cap);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(nb);
+  cfg.blockDim = dim3(128);
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = pdl ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  if (skin) {  // skinned bodies fused into the marker kernel (fsg_skin_fused.cuh)
+#define FSG_KS(P, NB)                                                                        \
+  cudaLaunchKernelEx(&cfg, k_markers_skin<P, NB>, g, (const float*)A, mk, sc, st, rec, fworld, \
+                     fworld_h, valid_h, fb, out, skin_narrow<NB>(*skin), skin_acc)
+    if (skin->nb <= 1) {
+      if (pulled) FSG_KS(true, 1);
+      else FSG_KS(false, 1);
+    } else {
+      if (pulled) FSG_KS(true, 2);
+      else FSG_KS(false, 2);
+    }
+#undef FSG_KS
+    return (int)nb;
+  }
   if (pulled)
-    k_markers_fix<true><<<nb, 128, 0, s>>>(g, (const float*)A, mk, sc, st, rec, fworld, fworld_h,
-                                           valid_h, fb, out);
+    cudaLaunchKernelEx(&cfg, k_markers_fix<true>, g, (const float*)A, mk, sc, st, rec, fworld,
+                       fworld_h, valid_h, fb, out, km_done);
   else
-    k_markers_fix<false><<<nb, 128, 0, s>>>(g, (const float*)A, mk, sc, st, rec, fworld, fworld_h,
-                                            valid_h, fb, out);
+    cudaLaunchKernelEx(&cfg, k_markers_fix<false>, g, (const float*)A, mk, sc, st, rec, fworld,
+                       fworld_h, valid_h, fb, out, km_done);
+  return (int)nb;
 }
 static void L_collide_fix(const Grid& g, const void* A, int pulled, void* B,
                           const SessionConsts* sc, const StepConsts& st, int frame_on,
@@ -942,7 +983,8 @@ static void L_step_batch(const Grid& g, const SessionConsts* sc, const EnvPack* 
 // the same stream (see k_collide_band).
 static void L_collide_band(const Grid& g, const void* A, int pulled, void* B, FixBand fb,
                            const SessionConsts* sc, const StepConsts& st, int frame_on,
-                           StepScratch* scr, StepScratch* scr_next, int pdl, cudaStream_t s) {
+                           StepScratch* scr, StepScratch* scr_next, int pdl, const SkinOut& so,
+                           cudaStream_t s) {
   DirPtrs dp;
   for (int i = 0; i < Q; ++i) {
     dp.a[i] = (const float*)A + (pulled ? g.pull[i] : g.own[i]);
@@ -976,7 +1018,7 @@ static void L_collide_band(const Grid& g, const void* A, int pulled, void* B, Fi
   cfg.numAttrs = 1;
 #define FSG_PB(P, V)                                                                     \
   cudaLaunchKernelEx(&cfg, k_collide_band<P, V>, g, dp, (const float*)A, fb, sc, st, scr, \
-                     scr_next, zc)
+                     scr_next, zc, so)
   if (pulled) {
     if (frame_on) FSG_PB(true, true);
     else FSG_PB(true, false);

@@ -174,6 +174,9 @@ struct fsg_session {
   int n_tau = 0;                      // sum of n_dofs over the skinned bodies
   double* d_skin = nullptr;           // rest [3m] | nrest [3m] | ww [KW m] | pts | vel | nrm [3m] | area [m]
   int* d_skin_wb = nullptr;           // [KW m]
+  double* d_skin_part = nullptr;      // tau block partials (split path)
+  unsigned long long* d_skin_fix = nullptr;  // fused path: fixed-point sums [2][32]
+  unsigned* d_skin_ticket = nullptr;
   double* h_wrench[2] = {nullptr, nullptr};  // pinned: tau + stats written by the step of parity p
   bool prof = false;
   std::vector<cudaEvent_t> prof_ev;
@@ -302,7 +305,7 @@ void enqueue_step(fsg_session* s, int p, bool copy_mk, bool frame_on) {
                   s->d_fworld, s->h_fw[p], s->h_valid[p], s->d_scr[p], s->stream);
     if (s->skin)  // parity: the reference's serial order (session.hpp:129-143)
       fsg::skin_tau_launch(s->skp, s->d_fworld, s->d_stencil, s->mk.vel, s->h_wrench[p], 1,
-                           s->stream);
+                           nullptr, 0, s->stream);
     s->L->spread(g, s->m, s->d_stencil, s->d_boxes, s->band, s->d_scr[p], s->stream);
   }
   s->L->collide(g, s->buf[p], s->pulled, s->buf[p ^ 1], nullptr, &s->band, s->d_scr[p], s->d_sc,
@@ -599,6 +602,9 @@ int fsg_destroy(fsg_session* s) {
   cudaFree(s->d_diag);
   cudaFree(s->d_skin);
   cudaFree(s->d_skin_wb);
+  cudaFree(s->d_skin_part);
+  cudaFree(s->d_skin_fix);
+  cudaFree(s->d_skin_ticket);
   for (int k = 0; k < 2; ++k)
     if (s->h_wrench[k]) cudaFreeHost(s->h_wrench[k]);
   cudaFree(s->d_tmp);
@@ -898,6 +904,11 @@ int fsg_set_skin(fsg_session* s, int n_bodies, const int64_t* off, const fsg_ske
     B.tau_off = nt;
     nt += k.n_dofs;
     for (int j = 0; j < FSG_SKIN_MAX_LINKS; ++j) {
+      int a = j < k.n_links ? j : -1;  // chain table for the fused marker kernel
+      for (int l = 0; l < FSG_SKIN_MAX_LINKS; ++l) {
+        B.anc[j][l] = (signed char)(a > 0 ? a : -1);
+        a = a > 0 ? k.parent[a] : -1;
+      }
       B.parent[j] = j < k.n_links ? k.parent[j] : -1;
       B.dof[j] = (j > 0 && j < k.n_links) ? k.dof_index[j] : -1;
       for (int c = 0; c < 3; ++c) B.axis[j][c] = j < k.n_links ? k.axis[j][c] : 0.0;
@@ -932,6 +943,25 @@ int fsg_set_skin(fsg_session* s, int n_bodies, const int64_t* off, const fsg_ske
   CU(cudaMemcpy(d + 6 * M, ww.data(), sizeof(double) * ww.size(), cudaMemcpyHostToDevice));
   CU(cudaMemcpy(d + (6 + fsg::SKIN_KW + 9) * M, areas, sizeof(double) * m, cudaMemcpyHostToDevice));
   CU(cudaMemcpy(s->d_skin_wb, wb.data(), sizeof(int) * wb.size(), cudaMemcpyHostToDevice));
+  {
+    int mmax = 1;
+    for (int b = 0; b < n_bodies; ++b) mmax = std::max(mmax, (int)(off[b + 1] - off[b]));
+    const size_t bpb = (size_t)(mmax + fsg::SKIN_TAU_THREADS - 1) / fsg::SKIN_TAU_THREADS;
+    // block partials of the split tau kernel [bodies][blocks][ACC_N]
+    cudaFree(s->d_skin_part);
+    s->d_skin_part = nullptr;
+    CU(cudaMalloc(&s->d_skin_part, sizeof(double) * fsg::SKIN_ACC_N * bpb * n_bodies));
+    if (!s->d_skin_ticket) {  // [0] tau ticket, [1] marker blocks done (split path)
+      CU(cudaMalloc(&s->d_skin_ticket, 2 * sizeof(unsigned)));
+      CU(cudaMemset(s->d_skin_ticket, 0, 2 * sizeof(unsigned)));
+    }
+  }
+  if (!s->d_skin_fix) {
+    CU(cudaMalloc(&s->d_skin_fix, sizeof(unsigned long long) * 64));
+    CU(cudaMemset(s->d_skin_fix, 0, sizeof(unsigned long long) * 64));
+  }
+  P.part = s->d_skin_part;
+  P.ticket = s->d_skin_ticket;
   P.rest = d;
   P.nrest = d + 3 * M;
   P.ww = d + 6 * M;
@@ -1015,16 +1045,34 @@ int fsg_step_async(fsg_session* s) {
       // without markers is the plain fluid K4 below.
       fsg::FixBand fb = s->fix;
       fb.stamp = ++s->stamp;
-      if (s->skin)
+      // skinned bodies: up to two are skinned and reduced inside the marker
+      // kernel; more take the separate skin kernels around it
+      const bool fused = s->skin && s->skp.nb <= 2;
+      const bool split = s->skin && !fused;
+      if (split)
         fsg::skin_update_launch(s->skp, (double*)s->mk.pts, (double*)s->mk.vel,
                                 (double*)s->mk.nrm, s->stream);
-      s->L->markers_fix(s->g, s->buf[p], s->pulled, s->mk, s->d_sc, st, s->d_stencil,
-                        s->d_fworld, s->h_fw[p], s->h_valid[p], fb, s->d_scr[p], s->stream);
+      const int km_blocks =
+          s->L->markers_fix(s->g, s->buf[p], s->pulled, s->mk, s->d_sc, st, s->d_stencil, s->d_fworld,
+                            s->h_fw[p], s->h_valid[p], fb, s->d_scr[p],
+                            split ? s->d_skin_ticket + 1 : nullptr, split ? 1 : 0,
+                            fused ? &s->skp : nullptr, fused ? s->d_skin_fix : nullptr, s->stream);
+      fsg::SkinOut so{};
+      if (fused) {
+        so.acc = s->d_skin_fix;
+        so.out = s->h_wrench[p];
+        so.nb = s->skp.nb;
+        so.nt = s->n_tau;
+        for (int b = 0; b < s->skp.nb; ++b) {
+          so.ndof[b] = s->skp.body[b].n_dofs;
+          so.off[b] = s->skp.body[b].tau_off;
+        }
+      }
       s->L->collide_band(s->g, s->buf[p], s->pulled, s->buf[p ^ 1], fb, s->d_sc, st,
-                         frame_on ? 1 : 0, s->d_scr[p], s->d_scr[p ^ 1], 1, s->stream);
-      if (s->skin)  // deterministic tree order; tau + stats straight into pinned memory
+                         frame_on ? 1 : 0, s->d_scr[p], s->d_scr[p ^ 1], 1, so, s->stream);
+      if (split)  // beside K4's first phase; fixed tree order; tau + stats into pinned memory
         fsg::skin_tau_launch(s->skp, s->d_fworld, s->d_stencil, s->mk.vel, s->h_wrench[p], 0,
-                             s->stream);
+                             s->d_skin_ticket + 1, (unsigned)km_blocks, s->stream);
     } else if (s->g.zpad) {
       // z-slab: the two boundary planes first, packed for the neighbours
       // (fsg_halo_begin lets a comm stream start on them), then the interior

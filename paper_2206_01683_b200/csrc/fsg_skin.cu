@@ -38,10 +38,29 @@ __device__ __forceinline__ double dot3(const double* a, const double* b) {
   return (a[0] * b[0] + a[1] * b[1]) + a[2] * b[2];
 }
 
-__device__ __forceinline__ int body_of(const SkinParams& P, int i) {
+template <int NB>
+__device__ __forceinline__ int body_of(const SkinParamsN<NB>& P, int i) {
   int b = 0;
-  while (b + 1 < P.nb && i >= P.body[b].m1) ++b;
+#pragma unroll
+  for (int k = 1; k < NB; ++k)
+    if (k < P.nb && i >= P.body[k].m0) b = k;
   return b;
+}
+
+/// Copy bodies [b0, b1) of the parameter block into shared memory: the
+/// kernels index the pose by runtime bone / link numbers, and dependent
+/// constant-bank loads at runtime offsets (cold constant cache, one unique
+/// address at a time) cost far more than one staged copy per block.
+template <int NB>
+__device__ __forceinline__ void stage_bodies(const SkinParamsN<NB>& P, SkinBody* dst, int b0, int b1) {
+  static_assert(sizeof(SkinBody) % 8 == 0, "SkinBody is copied as doubles");
+  constexpr int NW = (int)(sizeof(SkinBody) / 8);
+  for (int b = b0; b < b1; ++b) {
+    const double* src = reinterpret_cast<const double*>(&P.body[b]);
+    double* d = reinterpret_cast<double*>(dst + (b - b0));
+    for (int w = threadIdx.x; w < NW; w += blockDim.x) d[w] = src[w];
+  }
+  __syncthreads();
 }
 
 /// BoneTransforms::apply (skinning.hpp:101): R[b] * x + t[b]
@@ -51,11 +70,18 @@ __device__ __forceinline__ void bone_apply(const fsg_body_pose& Q, int b, const 
   for (int c = 0; c < 3; ++c) xb[c] = xb[c] + Q.bone_t[b][c];
 }
 
-__global__ void k_skin_update(const __grid_constant__ SkinParams P, double* __restrict__ pts,
-                              double* __restrict__ vel, double* __restrict__ nrm) {
+template <int NB>
+__global__ void __launch_bounds__(64)
+    k_skin_update(const __grid_constant__ SkinParamsN<NB> P, double* __restrict__ pts,
+                  double* __restrict__ vel, double* __restrict__ nrm) {
+  // the marker kernel is this kernel's programmatic dependent: let it launch
+  // (it waits for this grid's completion before reading the markers)
+  asm volatile("griddepcontrol.launch_dependents;");
+  __shared__ SkinBody sb[NB];
+  stage_bodies(P, sb, 0, P.nb);
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= P.m) return;
-  const fsg_body_pose& Q = P.body[body_of(P, i)].pose;
+  const fsg_body_pose& Q = sb[body_of(P, i)].pose;
   const double x[3] = {P.rest[3 * i], P.rest[3 * i + 1], P.rest[3 * i + 2]};
   const double n0[3] = {P.nrest[3 * i], P.nrest[3 * i + 1], P.nrest[3 * i + 2]};
   double out[3] = {0.0, 0.0, 0.0}, vout[3] = {0.0, 0.0, 0.0}, nn[3] = {0.0, 0.0, 0.0};
@@ -92,16 +118,25 @@ __global__ void k_skin_update(const __grid_constant__ SkinParams P, double* __re
   }
 }
 
-constexpr int TAU_MAX = 6 + SKIN_L;      // dofs per body
-constexpr int ACC_N = TAU_MAX + SKIN_NSTAT;
+constexpr int TAU_MAX = SKIN_TAU_MAX;
+constexpr int ACC_N = SKIN_ACC_N;
+
+/// acc[d] += v for a runtime d, with acc kept in registers (every slot is a
+/// compile-time index; the others are left untouched, not added to).
+__device__ __forceinline__ void acc_add(double* acc, int d, double v) {
+#pragma unroll
+  for (int k = 0; k < TAU_MAX; ++k)
+    if (k == d) acc[k] = acc[k] + v;
+}
 
 /// One marker's contribution (reference order) into acc[0..n_dofs) and the
 /// stats into acc[TAU_MAX..TAU_MAX+7).
-__device__ __forceinline__ void marker_contrib(const SkinParams& P, const SkinBody& B, int i,
+template <int NB>
+__device__ __forceinline__ void marker_contrib(const SkinParamsN<NB>& P, const SkinBody& B, int i,
                                                const double* __restrict__ fworld,
                                                const double* __restrict__ vel, double* acc) {
   const fsg_body_pose& Q = B.pose;
-  const double f[3] = {fworld[3 * i], fworld[3 * i + 1], fworld[3 * i + 2]};
+  const double f[3] = {__ldcg(fworld + 3 * i), __ldcg(fworld + 3 * i + 1), __ldcg(fworld + 3 * i + 2)};
   const double fneg[3] = {-f[0], -f[1], -f[2]};
   const double x[3] = {P.rest[3 * i], P.rest[3 * i + 1], P.rest[3 * i + 2]};
   for (int k = 0; k < SKIN_KW; ++k) {
@@ -133,7 +168,7 @@ __device__ __forceinline__ void marker_contrib(const SkinParams& P, const SkinBo
 #pragma unroll
       for (int c = 0; c < 3; ++c) d[c] = p[c] - Q.p_world[j][c];
       cross3(aw, d, cr);
-      acc[dof] = acc[dof] + dot3(cr, fv);
+      acc_add(acc, dof, dot3(cr, fv));
     }
   }
   double* st = acc + TAU_MAX;  // CouplingStats
@@ -146,14 +181,17 @@ __device__ __forceinline__ void marker_contrib(const SkinParams& P, const SkinBo
   st[6] = st[6] + dot3(fneg, v);
 }
 
-__device__ __forceinline__ int tau_total(const SkinParams& P) {
+template <int NB>
+__device__ __forceinline__ int tau_total(const SkinParamsN<NB>& P) {
   int n = 0;
   for (int b = 0; b < P.nb; ++b) n += P.body[b].n_dofs;
   return n;
 }
 
 /// Parity: one thread, bodies and markers in the reference's order.
-__global__ void k_skin_tau_serial(const __grid_constant__ SkinParams P, const double* __restrict__ fworld,
+template <int NB>
+__global__ void k_skin_tau_serial(const __grid_constant__ SkinParamsN<NB> P,
+                                  const double* __restrict__ fworld,
                                   const MarkerStencil* __restrict__ ms, const double* __restrict__ vel,
                                   double* out) {
   if (threadIdx.x != 0 || blockIdx.x != 0) return;
@@ -169,21 +207,37 @@ __global__ void k_skin_tau_serial(const __grid_constant__ SkinParams P, const do
   }
 }
 
-/// Throughput: one block per body; thread t sums markers t, t + T, ... in
-/// ascending order, then a fixed warp butterfly and a fixed in-order sum of
-/// the warp partials.  Deterministic run to run.
-constexpr int TAU_THREADS = 256;
+/// Throughput: grid (blocks per body, bodies) of one-warp blocks, launched as
+/// a programmatic dependent of K4 so it runs beside K4's first phase: spin
+/// until the marker kernel has counted all its blocks done, then one marker
+/// per thread, a fixed warp butterfly per block, and the last block to finish
+/// (ticket) sums the block partials of every body in block order.
+/// Deterministic run to run.
+constexpr int TAU_THREADS = SKIN_TAU_THREADS;
+constexpr int TAU_STAGE = 2016;  // doubles of block partials staged per pass (96 blocks)
+template <int NB>
 __global__ void __launch_bounds__(TAU_THREADS)
-    k_skin_tau(const __grid_constant__ SkinParams P, const double* __restrict__ fworld,
-               const MarkerStencil* __restrict__ ms, const double* __restrict__ vel, double* out) {
+    k_skin_tau(const __grid_constant__ SkinParamsN<NB> P, const double* __restrict__ fworld,
+               const MarkerStencil* __restrict__ ms, const double* __restrict__ vel, double* out,
+               unsigned* km_done, unsigned km_blocks) {
   __shared__ double part[TAU_THREADS / 32][ACC_N];
-  const int b = blockIdx.x;
-  const SkinBody& B = P.body[b];
+  __shared__ double stage[TAU_STAGE];
+  __shared__ bool last;
+  if (km_done) {
+    if (threadIdx.x == 0)
+      while (*(volatile unsigned*)km_done < km_blocks) __nanosleep(64);
+    __syncthreads();
+    __threadfence();
+  }
+  const int b = blockIdx.y;
+  __shared__ SkinBody sb[1];
+  stage_bodies(P, sb, b, b + 1);
+  const SkinBody& B = sb[0];
   double acc[ACC_N];
 #pragma unroll
   for (int k = 0; k < ACC_N; ++k) acc[k] = 0.0;
-  for (int i = B.m0 + threadIdx.x; i < B.m1; i += TAU_THREADS)
-    if (ms[i].valid) marker_contrib(P, B, i, fworld, vel, acc);
+  const int i = B.m0 + blockIdx.x * TAU_THREADS + threadIdx.x;
+  if (i < B.m1 && __ldcg(&ms[i].valid)) marker_contrib(P, B, i, fworld, vel, acc);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 #pragma unroll
   for (int k = 0; k < ACC_N; ++k) {
@@ -193,30 +247,103 @@ __global__ void __launch_bounds__(TAU_THREADS)
     if (lane == 0) part[warp][k] = v;
   }
   __syncthreads();
+  const int bpb = gridDim.x;
   if (threadIdx.x < ACC_N) {
     const int k = threadIdx.x;
     double v = part[0][k];
     for (int w = 1; w < TAU_THREADS / 32; ++w) v = v + part[w][k];
-    const int nt = tau_total(P);
-    if (k < B.n_dofs) out[B.tau_off + k] = v;
-    if (k >= TAU_MAX) out[nt + SKIN_NSTAT * b + (k - TAU_MAX)] = v;
+    P.part[((size_t)b * bpb + blockIdx.x) * ACC_N + k] = v;
   }
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) last = atomicAdd(P.ticket, 1u) == gridDim.x * gridDim.y - 1;
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  // every body's block partials: staged into shared memory with independent
+  // loads (one L2 round trip per chunk), then summed in block order
+  const int nt = tau_total(P);
+  constexpr int CH = TAU_STAGE / ACC_N;  // blocks per chunk
+  for (int bb = 0; bb < P.nb; ++bb) {
+    double v = 0.0;  // lane k < ACC_N owns component k
+    for (int j0 = 0; j0 < bpb; j0 += CH) {
+      const int nj = min(CH, bpb - j0);
+      const double* src = P.part + ((size_t)bb * bpb + j0) * ACC_N;
+      __syncwarp();
+      for (int t = threadIdx.x; t < nj * ACC_N; t += TAU_THREADS) stage[t] = __ldcg(src + t);
+      __syncwarp();
+      if (threadIdx.x < ACC_N)
+        for (int j = 0; j < nj; ++j) v = (j0 + j == 0) ? stage[threadIdx.x] : v + stage[j * ACC_N + threadIdx.x];
+    }
+    const int k = threadIdx.x;
+    if (k < ACC_N) {
+      if (k < P.body[bb].n_dofs) out[P.body[bb].tau_off + k] = v;
+      if (k >= TAU_MAX) out[nt + SKIN_NSTAT * bb + (k - TAU_MAX)] = v;
+    }
+  }
+  if (threadIdx.x == 0) {
+    *P.ticket = 0u;
+    if (km_done) *km_done = 0u;
+  }
+}
+
+template <int NB>
+SkinParamsN<NB> narrow(const SkinParams& P) {
+  SkinParamsN<NB> q;
+  q.nb = P.nb;
+  q.m = P.m;
+  q.rest = P.rest;
+  q.nrest = P.nrest;
+  q.wb = P.wb;
+  q.ww = P.ww;
+  q.part = P.part;
+  q.ticket = P.ticket;
+  for (int b = 0; b < NB; ++b) q.body[b] = P.body[b];
+  return q;
+}
+
+template <int NB>
+void update_nb(const SkinParams& P, double* pts, double* vel, double* nrm, cudaStream_t s) {
+  k_skin_update<NB><<<(P.m + 63) / 64, 64, 0, s>>>(narrow<NB>(P), pts, vel, nrm);
+}
+
+template <int NB>
+void tau_nb(const SkinParams& P, const double* fworld, const MarkerStencil* ms, const double* vel,
+            double* out, int serial, unsigned* km_done, unsigned km_blocks, cudaStream_t s) {
+  if (serial) {
+    k_skin_tau_serial<NB><<<1, 32, 0, s>>>(narrow<NB>(P), fworld, ms, vel, out);
+    return;
+  }
+  int mmax = 1;
+  for (int b = 0; b < P.nb; ++b) mmax = mmax > P.body[b].m1 - P.body[b].m0 ? mmax : P.body[b].m1 - P.body[b].m0;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)((mmax + TAU_THREADS - 1) / TAU_THREADS), (unsigned)P.nb);
+  cfg.blockDim = dim3(TAU_THREADS);
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = km_done ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, k_skin_tau<NB>, narrow<NB>(P), fworld, ms, vel, out, km_done, km_blocks);
 }
 
 }  // namespace
 
 void skin_update_launch(const SkinParams& P, double* pts, double* vel, double* nrm, cudaStream_t s) {
   if (P.m <= 0) return;
-  k_skin_update<<<(P.m + 127) / 128, 128, 0, s>>>(P, pts, vel, nrm);
+  if (P.nb <= 1) update_nb<1>(P, pts, vel, nrm, s);
+  else if (P.nb <= 2) update_nb<2>(P, pts, vel, nrm, s);
+  else update_nb<4>(P, pts, vel, nrm, s);
 }
 
 void skin_tau_launch(const SkinParams& P, const double* fworld, const MarkerStencil* ms,
-                     const double* vel, double* out, int serial, cudaStream_t s) {
+                     const double* vel, double* out, int serial, unsigned* km_done,
+                     unsigned km_blocks, cudaStream_t s) {
   if (P.nb <= 0) return;
-  if (serial)
-    k_skin_tau_serial<<<1, 32, 0, s>>>(P, fworld, ms, vel, out);
-  else
-    k_skin_tau<<<P.nb, TAU_THREADS, 0, s>>>(P, fworld, ms, vel, out);
+  if (P.nb <= 1) tau_nb<1>(P, fworld, ms, vel, out, serial, km_done, km_blocks, s);
+  else if (P.nb <= 2) tau_nb<2>(P, fworld, ms, vel, out, serial, km_done, km_blocks, s);
+  else tau_nb<4>(P, fworld, ms, vel, out, serial, km_done, km_blocks, s);
 }
 
 }  // namespace fsg

@@ -1,0 +1,214 @@
+// fsg_skin_fused.cuh -- skinned bodies fused into the throughput marker
+// kernel, included inside namespace fsg::p32 by
+// fsg_ib_fix.cuh.  For up to two skinned bodies the coupled fp32 step stays
+// two launches: the marker kernel skins its own markers from the pose it
+// receives as a __grid_constant__ parameter and reduces tau_ext and the
+// CouplingStats in its tail (off the critical path: the banded K4's first
+// phase runs meanwhile).
+//
+// * LBS (update_samples, sampling.hpp:307-322; skin_point /
+//   skin_point_velocity, skinning.hpp:105-126): lane l < SKIN_KW evaluates
+//   bone slot l, the warp adds the slots in ascending bone order.  Explicit
+//   round-to-nearest intrinsics keep this TU's FMA contraction out, so the
+//   marker state is bit-identical to the fp64 parity path's.
+// * tau_ext (accumulate_skinned_force -> accumulate_point_force,
+//   skinning.hpp:147-156, dynamics.hpp:216-233): lane k*8 + l evaluates, for
+//   bone slot k, the floating-base wrench (l = 0) or the l-th joint up the
+//   chain; a fixed butterfly sums a marker's terms, lane c keeps dof c's
+//   running sum over the warp's markers; the block sums its warps in order
+//   and adds the total to 64-bit fixed-point accumulators (2^-44) with integer
+//   atomics, which the banded K4 converts once the marker grid is complete:
+//   deterministic run to run (throughput mode; parity mode keeps the
+//   reference's serial order).
+
+__device__ __forceinline__ double rn_mul(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ double rn_add(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ double rn_sub(double a, double b) { return __dsub_rn(a, b); }
+
+__device__ __forceinline__ void rn_mv(const double* R, const double* v, double* r) {
+#pragma unroll
+  for (int i = 0; i < 3; ++i)
+    r[i] = rn_add(rn_add(rn_mul(R[3 * i], v[0]), rn_mul(R[3 * i + 1], v[1])), rn_mul(R[3 * i + 2], v[2]));
+}
+__device__ __forceinline__ void rn_mtv(const double* R, const double* v, double* r) {
+#pragma unroll
+  for (int i = 0; i < 3; ++i)
+    r[i] = rn_add(rn_add(rn_mul(R[i], v[0]), rn_mul(R[3 + i], v[1])), rn_mul(R[6 + i], v[2]));
+}
+__device__ __forceinline__ void rn_cross(const double* a, const double* b, double* r) {
+  r[0] = rn_sub(rn_mul(a[1], b[2]), rn_mul(a[2], b[1]));
+  r[1] = rn_sub(rn_mul(a[2], b[0]), rn_mul(a[0], b[2]));
+  r[2] = rn_sub(rn_mul(a[0], b[1]), rn_mul(a[1], b[0]));
+}
+__device__ __forceinline__ double rn_dot(const double* a, const double* b) {
+  return rn_add(rn_add(rn_mul(a[0], b[0]), rn_mul(a[1], b[1])), rn_mul(a[2], b[2]));
+}
+/// BoneTransforms::apply (skinning.hpp:101)
+__device__ __forceinline__ void rn_apply(const fsg_body_pose& Q, int b, const double* x, double* xb) {
+  rn_mv(Q.bone_R[b], x, xb);
+#pragma unroll
+  for (int c = 0; c < 3; ++c) xb[c] = rn_add(xb[c], Q.bone_t[b][c]);
+}
+
+/// This lane's bone slot of marker t (lanes >= SKIN_KW: none).
+struct SkinSlot {
+  int b;     // bone (-1: none)
+  double w;  // its weight
+};
+
+template <int NB>
+__device__ __forceinline__ int skin_body_of(const SkinParamsN<NB>& P, int t) {
+  int b = 0;
+#pragma unroll
+  for (int k = 1; k < NB; ++k)
+    if (k < P.nb && t >= P.body[k].m0) b = k;
+  return b;
+}
+
+template <int NB>
+__device__ __forceinline__ SkinSlot skin_slot(const SkinParamsN<NB>& P, int t, int lane) {
+  SkinSlot s{-1, 0.0};
+  if (lane < SKIN_KW) {
+    s.b = __ldg(P.wb + SKIN_KW * t + lane);
+    if (s.b >= 0) s.w = __ldg(P.ww + SKIN_KW * t + lane);
+  }
+  return s;
+}
+
+/// Warp sum of the per-slot vectors in ascending slot order, starting from 0
+/// (out += w[b] * term_b for the nonzero weights, skinning.hpp:108-110).
+__device__ __forceinline__ void slot_sum(const SkinSlot& s, const double* term, double* out) {
+#pragma unroll
+  for (int c = 0; c < 3; ++c) out[c] = 0.0;
+#pragma unroll
+  for (int l = 0; l < SKIN_KW; ++l) {
+    const int bl = __shfl_sync(0xffffffffu, s.b, l);
+    double v[3];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) v[c] = __shfl_sync(0xffffffffu, term[c], l);
+    if (bl < 0) break;  // slots are packed: the first empty one ends the list
+#pragma unroll
+    for (int c = 0; c < 3; ++c) out[c] = rn_add(out[c], v[c]);
+  }
+}
+
+/// skin_point: world position of marker t (all lanes).
+template <int NB>
+__device__ __forceinline__ void skin_point_warp(const SkinParamsN<NB>& P, const fsg_body_pose& Q, int t,
+                                                const SkinSlot& s, double* xw) {
+  const double x[3] = {__ldg(P.rest + 3 * t), __ldg(P.rest + 3 * t + 1), __ldg(P.rest + 3 * t + 2)};
+  double term[3] = {0.0, 0.0, 0.0};
+  if (s.b >= 0) {
+    double xb[3];
+    rn_apply(Q, s.b, x, xb);
+#pragma unroll
+    for (int c = 0; c < 3; ++c) term[c] = rn_mul(s.w, xb[c]);
+  }
+  slot_sum(s, term, xw);
+}
+
+/// skin_point_velocity and the blended normal, normalized() (all lanes).
+template <int NB>
+__device__ __forceinline__ void skin_vel_nrm_warp(const SkinParamsN<NB>& P, const fsg_body_pose& Q, int t,
+                                                  const SkinSlot& s, double* vel, double* nrm) {
+  double tv[3] = {0.0, 0.0, 0.0}, tn[3] = {0.0, 0.0, 0.0};
+  if (s.b >= 0) {
+    const double x[3] = {__ldg(P.rest + 3 * t), __ldg(P.rest + 3 * t + 1), __ldg(P.rest + 3 * t + 2)};
+    const double n0[3] = {__ldg(P.nrest + 3 * t), __ldg(P.nrest + 3 * t + 1), __ldg(P.nrest + 3 * t + 2)};
+    double xb[3], d[3], cr[3], rn[3];
+    rn_apply(Q, s.b, x, xb);
+#pragma unroll
+    for (int c = 0; c < 3; ++c) d[c] = rn_sub(xb[c], Q.p_world[s.b][c]);
+    rn_cross(Q.omega_world[s.b], d, cr);
+    rn_mv(Q.bone_R[s.b], n0, rn);
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      tv[c] = rn_mul(s.w, rn_add(Q.v_origin_world[s.b][c], cr[c]));
+      tn[c] = rn_mul(s.w, rn[c]);
+    }
+  }
+  slot_sum(s, tv, vel);
+  slot_sum(s, tn, nrm);
+  const double z = rn_dot(nrm, nrm);
+  if (z > 0.0) {
+    const double sz = __dsqrt_rn(z);
+#pragma unroll
+    for (int c = 0; c < 3; ++c) nrm[c] = __ddiv_rn(nrm[c], sz);
+  }
+}
+
+/// Add marker t's J^T(-f) terms and CouplingStats to the warp's running sums:
+/// lane c (< SKIN_TAU_MAX) holds dof c, lane SKIN_TAU_MAX + k stat k.
+template <int NB>
+__device__ __forceinline__ void skin_tau_warp(const SkinParamsN<NB>& P, const SkinBody& B, int t, int lane,
+                                              const double* fw, const double* vel, double& acc) {
+  const fsg_body_pose& Q = B.pose;
+  const int k = lane >> 3, l = lane & 7;  // bone slot, level (0: base wrench, l: l-th joint up)
+  int b = -1;
+  double w = 0.0;
+  if (k < SKIN_KW) {
+    b = __ldg(P.wb + SKIN_KW * t + k);
+    if (b >= 0) w = __ldg(P.ww + SKIN_KW * t + k);
+  }
+  double term[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+  int comp = -1;  // l > 0: the dof this lane's term goes to
+  if (b >= 0) {
+    const double x[3] = {__ldg(P.rest + 3 * t), __ldg(P.rest + 3 * t + 1), __ldg(P.rest + 3 * t + 2)};
+    double p[3], fv[3];
+    rn_apply(Q, b, x, p);
+#pragma unroll
+    for (int c = 0; c < 3; ++c) fv[c] = rn_mul(w, -fw[c]);
+    if (l == 0) {
+      if (B.floating) {
+        double d[3], cr[3];
+#pragma unroll
+        for (int c = 0; c < 3; ++c) d[c] = rn_sub(p[c], Q.p_world[0][c]);
+        rn_cross(d, fv, cr);
+        rn_mtv(Q.R_world[0], cr, term);
+        rn_mtv(Q.R_world[0], fv, term + 3);
+      }
+    } else {
+      const int j = B.anc[b][l - 1];
+      if (j > 0 && B.dof[j] >= 0) {
+        double aw[3], d[3], cr[3];
+        rn_mv(Q.R_world[j], B.axis[j], aw);
+#pragma unroll
+        for (int c = 0; c < 3; ++c) d[c] = rn_sub(p[c], Q.p_world[j][c]);
+        rn_cross(aw, d, cr);
+        term[0] = rn_dot(cr, fv);
+        comp = B.dof[j];
+      }
+    }
+  }
+  // marker total of every dof: fixed butterfly, then lane c keeps dof c
+#pragma unroll
+  for (int c = 0; c < SKIN_TAU_MAX; ++c) {
+    double v = (l == 0) ? (c < 6 ? term[c] : 0.0) : (comp == c ? term[0] : 0.0);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (lane == c && c < B.n_dofs) acc += v;
+  }
+  // CouplingStats (session.hpp:141-143)
+  const int sidx = lane - SKIN_TAU_MAX;
+  if (sidx >= 0 && sidx < 3) acc += fw[sidx];
+  else if (sidx >= 3 && sidx < 6) acc -= fw[sidx - 3];
+  else if (sidx == 6) acc += (-fw[0]) * vel[0] + (-fw[1]) * vel[1] + (-fw[2]) * vel[2];
+}
+
+/// Block tail: sum the warps' running sums in warp order and add the block's
+/// total to the fixed-point accumulators (integer atomics: the accumulated
+/// value does not depend on the order the blocks land in).
+template <int NB>
+__device__ __forceinline__ void skin_block_red(const double (&acc)[NB], unsigned long long* fixacc) {
+  __shared__ double wsum[FX_PER_BLOCK][NB * 32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int b = 0; b < NB; ++b) wsum[warp][b * 32 + lane] = acc[b];
+  __syncthreads();
+  if (threadIdx.x < NB * 32 && (threadIdx.x & 31) < SKIN_TAU_MAX + SKIN_NSTAT) {
+    double v = wsum[0][threadIdx.x];
+#pragma unroll
+    for (int w = 1; w < FX_PER_BLOCK; ++w) v = v + wsum[w][threadIdx.x];
+    if (v != 0.0) atomicAdd(fixacc + threadIdx.x, (unsigned long long)__double2ll_rn(v * SKIN_FIX_SCALE));
+  }
+}

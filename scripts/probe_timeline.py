@@ -16,6 +16,9 @@ from paper_2206_01683_b200.scenes import make_scene
 
 lib = ctypes.CDLL(_abi.LIB_PATH)
 FLUSH = "--flush" in sys.argv
+SKIN = "--skin" in sys.argv
+if SKIN:
+    sys.argv.remove("--skin")
 if FLUSH:
     sys.argv.remove("--flush")
     fw_buf = torch.empty(64 << 20, dtype=torch.float32, device="cuda")
@@ -28,10 +31,17 @@ for name in sys.argv[1:] or ["c2"]:
     cfg = SessionConfig(dims=sc.dims, dx=sc.dx, dt=sc.dt, rho=sc.rho, nu=sc.nu,
                         frame_mode=sc.frame_mode, precision="fp32", max_markers=sc.m)
     s = CoupledSession(cfg)
-    dm = [torch.tensor(np.ascontiguousarray(a).reshape(-1), device="cuda") for a in sc.markers(0)]
-    s.set_markers_device(sc.offsets, *(t.data_ptr() for t in dm))
+    if SKIN:  # skinned on the device (fsg_set_skin / fsg_set_pose)
+        s.set_skin(*sc.skin())
+        poses = [sc.poses(k) for k in range(60)]
+    else:
+        dm = [torch.tensor(np.ascontiguousarray(a).reshape(-1), device="cuda") for a in sc.markers(0)]
+        s.set_markers_device(sc.offsets, *(t.data_ptr() for t in dm))
     for k in range(30):
-        s.set_frame(sc.frame(k)); s.step_async()
+        s.set_frame(sc.frame(k))
+        if SKIN:
+            s.set_pose(poses[k])
+        s.step_async()
     s.last_status(); lib.fsg_debug_timeline(None)
     frames = [sc.frame(k) for k in range(30, 60)]
     ss = torch.cuda.ExternalStream(s.stream)
@@ -41,7 +51,10 @@ for name in sys.argv[1:] or ["c2"]:
             if FLUSH:  # as bench.py: write + read 2x L2 between steps
                 fw_buf.fill_(1.0)
                 torch.sum(fr_buf, dim=0, out=sink[0])
-            s.set_frame(f); s.step_async()
+            s.set_frame(f)
+            if SKIN:
+                s.set_pose(poses[30])
+            s.step_async()
     s.last_status(); lib.fsg_debug_timeline(buf)
     t = list(buf)
     rows = sorted([t[S * j: S * j + S] for j in range(64) if t[S * j + 5] not in (0, ~0 & (2**64 - 1))],

@@ -14,8 +14,9 @@ from paper_2206_01683_b200.scenes import Scene, koi_body
 
 
 def skin_scene(dims=(48, 28, 28), dx=0.012, frame_mode="translation_yaw", bodies=1):
-    origins = [np.zeros(3)] if bodies == 1 else [np.array([-0.27, 0.0, 0.0]),
-                                                 np.array([0.27, 0.0, 0.0])]
+    origins = {1: [np.zeros(3)],
+               2: [np.array([-0.27, 0.0, 0.0]), np.array([0.27, 0.0, 0.0])],
+               3: [np.array([-0.5, 0.0, 0.0]), np.zeros(3), np.array([0.5, 0.0, 0.0])]}[bodies]
     return Scene("skin", dims, dx, frame_mode, [koi_body(dx) for _ in range(bodies)], 4,
                  origins=origins, motion="swim")
 

@@ -59,6 +59,30 @@ def test_fp32_skinned_step_within_tolerance(one_fish):
         assert rel_l2(a["stats"], b["stats"]) <= 1e-5
 
 
+def test_fp32_three_bodies_split_kernels():
+    """More than two skinned bodies take the separate skin kernels (k_skin_update,
+    k_skin_tau beside K4) instead of the fused marker kernel: same contract."""
+    sc = skin_scene(dims=(120, 28, 28), frame_mode="none", bodies=3)
+    o, _ = run_oracle_skin(sc, [0, 1, 2])
+    g, _ = run_gpu_skin(sc, [0, 1, 2], "fp32")
+    g2, _ = run_gpu_skin(sc, [0, 1, 2], "fp32")
+    for a, b, c in zip(g, o, g2):
+        for k in ("pts", "vel", "nrm"):
+            assert np.array_equal(a[k], b[k]), k
+        assert rel_l2(a["tau"], b["tau"]) <= 1e-5 and rel_l2(a["stats"], b["stats"]) <= 1e-5
+        assert np.array_equal(a["tau"], c["tau"]) and np.array_equal(a["stats"], c["stats"])
+
+
+def test_fp32_two_bodies_fused():
+    sc = skin_scene(dims=(64, 28, 28), frame_mode="none", bodies=2)
+    o, _ = run_oracle_skin(sc, [0, 1, 2])
+    g, _ = run_gpu_skin(sc, [0, 1, 2], "fp32")
+    for a, b in zip(g, o):
+        for k in ("pts", "vel", "nrm"):
+            assert np.array_equal(a[k], b[k]), k
+        assert rel_l2(a["tau"], b["tau"]) <= 1e-5 and rel_l2(a["stats"], b["stats"]) <= 1e-5
+
+
 def test_fp32_tau_run_to_run_identical():
     sc = skin_scene()
     a, _ = run_gpu_skin(sc, [0, 1, 2], "fp32")
