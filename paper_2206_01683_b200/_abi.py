@@ -101,7 +101,7 @@ SIGNATURES = {
     "fsg_get_stencils": (C.c_int, [_vp, _ip]),
     "fsg_set_skin": (C.c_int, [_vp, C.c_int, _i64p, C.POINTER(fsg_skeleton), _dp, _dp, _dp, _dp]),
     "fsg_set_pose": (C.c_int, [_vp, C.POINTER(fsg_body_pose)]),
-    "fsg_get_body_wrench": (C.c_int, [_vp, _dp, _dp]),
+    "fsg_get_body_wrench": (C.c_int, [_vp, _vp, _vp]),
     "fsg_get_markers": (C.c_int, [_vp, _dp, _dp, _dp]),
     "fsg_profile_enable": (C.c_int, [_vp, C.c_int]),
     "fsg_profile_read": (C.c_int, [_vp, _dp, _ip]),

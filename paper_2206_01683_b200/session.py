@@ -391,6 +391,11 @@ class CoupledSession:
         self.m = int(off[-1])
         self.n_bodies = nb
         self._ndofs = [int(k.n_dofs) for k in skeletons]
+        self._nt = sum(self._ndofs)
+        self._wbuf = np.empty(self._nt + 7 * nb)  # readback staging (pointer cached)
+        self._wptr = self._wbuf.ctypes.data
+        ends = np.cumsum(self._ndofs).tolist()
+        self._tau_ranges = list(zip([0] + ends[:-1], ends))
         self._pose = (_abi.fsg_body_pose * nb)()
         self._pose_np = np.frombuffer(self._pose, dtype=np.float64).reshape(nb, POSE_DOUBLES)
 
@@ -410,16 +415,11 @@ class CoupledSession:
 
     def body_wrench(self):
         """-> (tau_ext per body [list of n_dofs arrays], stats[n_bodies, 7]) of the last step."""
-        tau = np.empty(max(sum(self._ndofs), 1))
-        stats = np.empty(7 * self.n_bodies)
-        rc = self._L.fsg_get_body_wrench(self._h, dptr(tau), dptr(stats))
+        rc = self._L.fsg_get_body_wrench(self._h, self._wptr, self._wptr + 8 * self._nt)
         if rc:
             check(rc)
-        out, k = [], 0
-        for n in self._ndofs:
-            out.append(tau[k:k + n].copy())
-            k += n
-        return out, stats.reshape(-1, 7)
+        buf = self._wbuf.copy()
+        return [buf[a:b] for a, b in self._tau_ranges], buf[self._nt:].reshape(-1, 7)
 
     def markers(self):
         """-> (points, velocities, normals) [m, 3] the last step used."""
