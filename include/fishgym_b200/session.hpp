@@ -186,6 +186,33 @@ class FluidSession {
     check(fsg_get_marker_forces(h_, force_world.data(), valid.data(), stats.data()));
   }
 
+  // ---- skinned bodies on the device ---------------------
+  /// Register the robots' SurfaceSamples (sampling.hpp): rest points/normals
+  /// (base at identity), blend weights (n_links(b) per marker, concatenated
+  /// over bodies), areas, and each robot's topology.  From then on every
+  /// step() skins the markers on the device (update_samples,
+  /// sampling.hpp:307-322) from the pose given to set_pose().
+  void set_skin(const std::vector<int64_t>& offsets, const std::vector<fsg_skeleton>& skeletons,
+                const std::vector<double>& rest_points, const std::vector<double>& rest_normals,
+                const std::vector<double>& weights, const std::vector<double>& areas) {
+    m_ = offsets.empty() ? 0 : static_cast<size_t>(offsets.back());
+    nb_ = offsets.empty() ? 0 : static_cast<int>(offsets.size()) - 1;
+    check(fsg_set_skin(h_, nb_, offsets.data(), skeletons.data(), rest_points.data(),
+                       rest_normals.data(), weights.data(), areas.data()));
+    nt_ = 0;
+    for (const auto& k : skeletons) nt_ += static_cast<size_t>(k.n_dofs);
+  }
+  /// This step's pose of every robot: BoneTransforms::of (skinning.hpp:85-102)
+  /// and the KinematicsCache fields of forward_kinematics (dynamics.hpp:23-61).
+  void set_pose(const std::vector<fsg_body_pose>& poses) { check(fsg_set_pose(h_, poses.data())); }
+  /// tau_ext of every robot (concatenated; session.hpp:139-140) and the
+  /// CouplingStats (7 per body) of the last step.
+  void body_wrench(std::vector<double>& tau_ext, std::vector<double>& stats) const {
+    tau_ext.resize(nt_);
+    stats.resize(7 * static_cast<size_t>(nb_ > 0 ? nb_ : 1));
+    check(fsg_get_body_wrench(h_, tau_ext.data(), stats.data()));
+  }
+
   fsg_session* handle() const { return h_; }
 
  private:
@@ -208,6 +235,7 @@ class FluidSession {
   std::array<int, 3> dims_{};
   size_t n_ = 0;
   size_t m_ = 0;
+  size_t nt_ = 0;
   int nb_ = 0;
 };
 

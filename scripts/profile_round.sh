@@ -15,11 +15,11 @@ $C2 > $out/${tag}_c2_plain.log 2>&1 &&
 ncu --metrics gpu__time_duration.sum --clock-control none -c 800 --csv \
     --log-file $out/${tag}_c2_launches.csv $C2 > $out/${tag}_c2_ncu_list.log 2>&1
 # full sections: the coupled pair at c2
-ncu --set full --clock-control none --import-source on -k regex:"k_collide_band|k_markers_fix" \
+ncu --set full --clock-control none --import-source on -k regex:"k_collide_band|k_markers_fix|k_markers_skin" \
     -s 20 -c 4 -o $out/${tag}_c2_full $C2 > $out/${tag}_c2_ncu_full.log 2>&1
 # c3: the coupled pair on a grid larger than L2
 $C3 > $out/${tag}_c3_plain.log 2>&1 &&
-ncu --set full --clock-control none --import-source on -k regex:"k_collide_band|k_markers_fix" \
+ncu --set full --clock-control none --import-source on -k regex:"k_collide_band|k_markers_fix|k_markers_skin" \
     -s 8 -c 2 -o $out/${tag}_c3_full $C3 > $out/${tag}_c3_ncu_full.log 2>&1
 # c4: the pure-fluid K4 at 512^3
 $C4 > $out/${tag}_c4_plain.log 2>&1 &&
