@@ -79,6 +79,7 @@ __device__ __forceinline__ void report_min_red(StepScratch* out, float v) {
 /// Each group first stamps the tiles of ALL its markers, the block fences
 /// and triggers K4, then the groups do the heavy per-marker work (the cheap
 /// stencil is recomputed rather than kept).
+template <bool SKIN>  // SKIN: some env has a skinned body (P.skb)
 __global__ void __launch_bounds__(128, FSG_KM_MINB)
     k_markers_batch(Grid g, const SessionConsts* __restrict__ scp, const EnvPack* __restrict__ packs,
                     BatchHead h) {
@@ -93,8 +94,23 @@ __global__ void __launch_bounds__(128, FSG_KM_MINB)
   for (int tg = blockIdx.x * FX_PER_BLOCK + slot; tg < h.m_total; tg += stride) {
     const EnvPack& P = packs[env_of(mkb, h.E, tg)];
     const FixBand fb{P.F, P.tflag, h.tnx, h.tny, h.tnz, P.stamp};
+    const int t = tg - P.mk_begin;
     MkStencil S;
-    mk_stencil(P.mk, tg - P.mk_begin, sc, P.st, S);
+    if (SKIN && P.skb) {  // skinned env (fsg_skin_fused.cuh): LBS of the marker first
+      const SkinView V{P.sk_rest, P.sk_nrest, P.sk_wb, P.sk_ww};
+      const SkinSlot sl = skin_slot(V, t, lane);
+      double xw[3];
+      skin_point_warp(V, P.skb->pose, t, sl, xw);
+      if (lane == 0) {
+        double* pts = const_cast<double*>(P.mk.pts);
+        pts[3 * t] = xw[0];
+        pts[3 * t + 1] = xw[1];
+        pts[3 * t + 2] = xw[2];
+      }
+      mk_stencil_x(xw, sc, P.st, S);
+    } else {
+      mk_stencil(P.mk, t, sc, P.st, S);
+    }
     mk_stamp(g, fb, S, lane);
   }
   __syncthreads();  // all stamps of the block before the K4 trigger (k_markers_fix)
@@ -106,6 +122,37 @@ __global__ void __launch_bounds__(128, FSG_KM_MINB)
     const FixBand fb{P.F, P.tflag, h.tnx, h.tny, h.tnz, P.stamp};
     const int t = tg - P.mk_begin;
     MkStencil S;
+    if (SKIN && P.skb) {
+      const SkinView V{P.sk_rest, P.sk_nrest, P.sk_wb, P.sk_ww};
+      const SkinBody& B = *P.skb;
+      const SkinSlot sl = skin_slot(V, t, lane);
+      double xw[3], vel[3], nrm[3], fw[3];
+      skin_point_warp(V, B.pose, t, sl, xw);
+      skin_vel_nrm_warp(V, B.pose, t, sl, vel, nrm);
+      if (lane == 0) {
+        double* v = const_cast<double*>(P.mk.vel);
+        double* n = const_cast<double*>(P.mk.nrm);
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+          v[3 * t + c] = vel[c];
+          n[3 * t + c] = nrm[c];
+        }
+      }
+      mk_stencil_x(xw, sc, P.st, S);
+      if (P.pulled)
+        mk_finish<true>(g, P.A, P.mk, t, lane, sc, P.st, S, phs[slot], P.rec, P.fworld, P.fworld_h,
+                        P.valid_h, fb, P.out, vel, nrm, fw);
+      else
+        mk_finish<false>(g, P.A, P.mk, t, lane, sc, P.st, S, phs[slot], P.rec, P.fworld, P.fworld_h,
+                         P.valid_h, fb, P.out, vel, nrm, fw);
+      __syncwarp(fx_mask());
+      if (S.ok) {
+        double acc = 0.0;
+        skin_tau_warp(V, B, t, lane, fw, vel, acc);
+        skin_red_marker(acc, lane, P.sk_acc);
+      }
+      continue;
+    }
     mk_stencil(P.mk, t, sc, P.st, S);
     if (P.pulled)
       mk_finish<true>(g, P.A, P.mk, t, lane, sc, P.st, S, phs[slot], P.rec, P.fworld, P.fworld_h,
@@ -180,6 +227,16 @@ __global__ void __launch_bounds__(128, FSG_K4_MINB)
   }
   // ---- phase B: every env's stamped tiles, after the marker grid completed
   asm volatile("griddepcontrol.wait;" ::: "memory");
+  if (blockIdx.x == gridDim.x - 1)  // skinned envs: tau_ext / stats sums are complete
+    for (int k = tid; k < h.E * 32; k += nthr) {
+      const EnvPack& Q0 = packs[k >> 5];
+      const int c = k & 31;
+      if (!Q0.skb) continue;
+      const double d = (double)(long long)__ldcg(Q0.sk_acc + c) * SKIN_FIX_INV;
+      Q0.sk_acc[c] = 0ull;
+      if (c < Q0.sk_ndof) Q0.sk_out[c] = d;
+      if (c >= SKIN_TAU_MAX && c < SKIN_TAU_MAX + SKIN_NSTAT) Q0.sk_out[Q0.sk_ndof + (c - SKIN_TAU_MAX)] = d;
+    }
   const int tpp = nthr >> 6;
   const int half = tid >> 6, lt = tid & 63;
   for (int base = 0; (long long)base * gridDim.x < h.tile_total; base += nthr) {

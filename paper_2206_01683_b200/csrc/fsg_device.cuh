@@ -243,6 +243,7 @@ struct DirPtrs {
 // Batched throughput step (fsg_batch.cuh): the envs share one configuration,
 // so the grid geometry (with its pull/own offsets) and the session constants
 // are common kernel parameters; each env contributes one small pack per step.
+struct SkinBody;  // fsg_skin.cuh
 struct EnvPack {
   StepConsts st;           // this env's frame constants
   const float* A;          // state read this step
@@ -258,6 +259,15 @@ struct EnvPack {
   StepScratch* next;
   unsigned stamp;
   int pulled, frame_on;
+  // skinned body (fsg_set_skin, one per env), nullptr: plain markers
+  const SkinBody* skb;           // topology + this step's pose (device copy)
+  const double* sk_rest;
+  const double* sk_nrest;
+  const int* sk_wb;
+  const double* sk_ww;
+  unsigned long long* sk_acc;    // fixed-point tau/stat sums [32]
+  double* sk_out;                // tau then 7 stats (pinned)
+  int sk_ndof;
   int mk_begin;            // first global marker index of this env
   int item_begin;          // first global phase-A item
   int tile_begin;          // first global band tile
@@ -272,6 +282,7 @@ struct BatchHead {
   int zc;                  // phase-A planes per item
   int frame_on;            // the batch's frame mode is not None
   int pmode;               // 1 every env pulled, 0 none, 2 mixed
+  int skin;                // some env has a skinned body
 };
 
 // ---------------------------------------------------------- kernel table --

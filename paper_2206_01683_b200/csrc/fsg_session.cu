@@ -1360,6 +1360,8 @@ struct fsg_batch {
   fsg::EnvPack* h_packs[2] = {nullptr, nullptr};  // pinned, by batch step parity
   fsg::EnvPack* d_packs[2] = {nullptr, nullptr};
   unsigned* d_work = nullptr;                      // [2] phase-A counters by parity
+  fsg::SkinBody* h_skb[2] = {nullptr, nullptr};    // pinned: skinned envs' topology + pose
+  fsg::SkinBody* d_skb[2] = {nullptr, nullptr};
   cudaEvent_t ev[2] = {nullptr, nullptr};
   int par = 0;
   dim3 block;
@@ -1372,6 +1374,8 @@ int fsg_batch_destroy(fsg_batch* b) {
   for (int k = 0; k < 2; ++k) {
     if (b->h_packs[k]) cudaFreeHost(b->h_packs[k]);
     cudaFree(b->d_packs[k]);
+    if (b->h_skb[k]) cudaFreeHost(b->h_skb[k]);
+    cudaFree(b->d_skb[k]);
     if (b->ev[k]) cudaEventDestroy(b->ev[k]);
   }
   cudaFree(b->d_work);
@@ -1415,6 +1419,8 @@ int fsg_batch_create(const fsg_config* cfg, int n_envs, fsg_batch** out) {
   for (int k = 0; k < 2; ++k) {
     CUB(cudaMallocHost(&b->h_packs[k], sizeof(fsg::EnvPack) * n_envs));
     CUB(cudaMalloc(&b->d_packs[k], sizeof(fsg::EnvPack) * n_envs));
+    CUB(cudaMallocHost(&b->h_skb[k], sizeof(fsg::SkinBody) * n_envs));
+    CUB(cudaMalloc(&b->d_skb[k], sizeof(fsg::SkinBody) * n_envs));
     CUB(cudaEventCreateWithFlags(&b->ev[k], cudaEventDisableTiming));
     CUB(cudaEventRecord(b->ev[k], b->stream));
   }
@@ -1438,8 +1444,8 @@ int fsg_batch_step_async(fsg_batch* b) {
   const fsg::Grid& g0 = b->envs[0]->g;
   const fsg::FixBand& fb0 = b->envs[0]->fix;
   fsg::BatchHead h{b->E, 0, 0, 0, fb0.tnx, fb0.tny, fb0.tnz, 1,
-                   b->envs[0]->cfg.frame_mode != FSG_FRAME_NONE ? 1 : 0, 0};
-  int npulled = 0;
+                   b->envs[0]->cfg.frame_mode != FSG_FRAME_NONE ? 1 : 0, 0, 0};
+  int npulled = 0, nskin = 0;
   const int tx_n = (g0.nx + (int)b->block.x - 1) / (int)b->block.x;
   const int ty_n = (g0.ny + (int)b->block.y - 1) / (int)b->block.y;
   // phase-A items: 2 planes when that still leaves >= 8 per resident block
@@ -1470,6 +1476,22 @@ int fsg_batch_step_async(fsg_batch* b) {
     P.next = s->d_scr[p ^ 1];
     P.pulled = s->pulled;
     P.frame_on = s->cfg.frame_mode != FSG_FRAME_NONE;
+    P.skb = nullptr;
+    if (s->skin && s->m) {  // skinned env: its topology + pose go up with the packs
+      if (s->skp.nb != 1)
+        return set_err(FSG_EINPUT, "batched envs: one skinned body per env (env %d has %d)", e, s->skp.nb);
+      if (!s->pose_set) return set_err(FSG_ESTATE, "env %d: fsg_set_pose has not been called", e);
+      b->h_skb[q][e] = s->skp.body[0];
+      P.skb = b->d_skb[q] + e;
+      P.sk_rest = s->skp.rest;
+      P.sk_nrest = s->skp.nrest;
+      P.sk_wb = s->skp.wb;
+      P.sk_ww = s->skp.ww;
+      P.sk_acc = s->d_skin_fix;
+      P.sk_out = s->h_wrench[p];
+      P.sk_ndof = s->skp.body[0].n_dofs;
+      ++nskin;
+    }
     P.mk_begin = h.m_total;
     P.item_begin = h.item_total;
     P.tile_begin = h.tile_total;
@@ -1479,8 +1501,12 @@ int fsg_batch_step_async(fsg_batch* b) {
     h.tile_total += s->fix.tnx * s->fix.tny * s->fix.tnz;
   }
   h.pmode = npulled == b->E ? 1 : (npulled == 0 ? 0 : 2);
+  h.skin = nskin > 0 ? 1 : 0;
   CU(cudaMemcpyAsync(b->d_packs[q], packs, sizeof(fsg::EnvPack) * b->E, cudaMemcpyHostToDevice,
                      b->stream));
+  if (nskin)
+    CU(cudaMemcpyAsync(b->d_skb[q], b->h_skb[q], sizeof(fsg::SkinBody) * b->E, cudaMemcpyHostToDevice,
+                       b->stream));
   CU(cudaMemsetAsync(b->d_work + q, 0, sizeof(unsigned), b->stream));
   b->envs[0]->L->step_batch(g0, b->envs[0]->d_sc, b->d_packs[q], h, b->block, b->d_work + q,
                             b->stream);

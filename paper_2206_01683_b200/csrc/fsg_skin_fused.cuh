@@ -50,6 +50,14 @@ __device__ __forceinline__ void rn_apply(const fsg_body_pose& Q, int b, const do
   for (int c = 0; c < 3; ++c) xb[c] = rn_add(xb[c], Q.bone_t[b][c]);
 }
 
+/// The per-marker skin arrays (SkinParamsN, or one env's in a batch).
+struct SkinView {
+  const double* rest;   // [3m]
+  const double* nrest;  // [3m]
+  const int* wb;        // [m][SKIN_KW]
+  const double* ww;     // [m][SKIN_KW]
+};
+
 /// This lane's bone slot of marker t (lanes >= SKIN_KW: none).
 struct SkinSlot {
   int b;     // bone (-1: none)
@@ -65,8 +73,8 @@ __device__ __forceinline__ int skin_body_of(const SkinParamsN<NB>& P, int t) {
   return b;
 }
 
-template <int NB>
-__device__ __forceinline__ SkinSlot skin_slot(const SkinParamsN<NB>& P, int t, int lane) {
+template <class SP>
+__device__ __forceinline__ SkinSlot skin_slot(const SP& P, int t, int lane) {
   SkinSlot s{-1, 0.0};
   if (lane < SKIN_KW) {
     s.b = __ldg(P.wb + SKIN_KW * t + lane);
@@ -93,8 +101,8 @@ __device__ __forceinline__ void slot_sum(const SkinSlot& s, const double* term, 
 }
 
 /// skin_point: world position of marker t (all lanes).
-template <int NB>
-__device__ __forceinline__ void skin_point_warp(const SkinParamsN<NB>& P, const fsg_body_pose& Q, int t,
+template <class SP>
+__device__ __forceinline__ void skin_point_warp(const SP& P, const fsg_body_pose& Q, int t,
                                                 const SkinSlot& s, double* xw) {
   const double x[3] = {__ldg(P.rest + 3 * t), __ldg(P.rest + 3 * t + 1), __ldg(P.rest + 3 * t + 2)};
   double term[3] = {0.0, 0.0, 0.0};
@@ -108,8 +116,8 @@ __device__ __forceinline__ void skin_point_warp(const SkinParamsN<NB>& P, const 
 }
 
 /// skin_point_velocity and the blended normal, normalized() (all lanes).
-template <int NB>
-__device__ __forceinline__ void skin_vel_nrm_warp(const SkinParamsN<NB>& P, const fsg_body_pose& Q, int t,
+template <class SP>
+__device__ __forceinline__ void skin_vel_nrm_warp(const SP& P, const fsg_body_pose& Q, int t,
                                                   const SkinSlot& s, double* vel, double* nrm) {
   double tv[3] = {0.0, 0.0, 0.0}, tn[3] = {0.0, 0.0, 0.0};
   if (s.b >= 0) {
@@ -139,8 +147,8 @@ __device__ __forceinline__ void skin_vel_nrm_warp(const SkinParamsN<NB>& P, cons
 
 /// Add marker t's J^T(-f) terms and CouplingStats to the warp's running sums:
 /// lane c (< SKIN_TAU_MAX) holds dof c, lane SKIN_TAU_MAX + k stat k.
-template <int NB>
-__device__ __forceinline__ void skin_tau_warp(const SkinParamsN<NB>& P, const SkinBody& B, int t, int lane,
+template <class SP>
+__device__ __forceinline__ void skin_tau_warp(const SP& P, const SkinBody& B, int t, int lane,
                                               const double* fw, const double* vel, double& acc) {
   const fsg_body_pose& Q = B.pose;
   const int k = lane >> 3, l = lane & 7;  // bone slot, level (0: base wrench, l: l-th joint up)
@@ -211,4 +219,10 @@ __device__ __forceinline__ void skin_block_red(const double (&acc)[NB], unsigned
     for (int w = 1; w < FX_PER_BLOCK; ++w) v = v + wsum[w][threadIdx.x];
     if (v != 0.0) atomicAdd(fixacc + threadIdx.x, (unsigned long long)__double2ll_rn(v * SKIN_FIX_SCALE));
   }
+}
+
+/// Batched envs: one marker's terms straight into its env's fixed-point sums.
+__device__ __forceinline__ void skin_red_marker(double v, int lane, unsigned long long* fixacc) {
+  if (lane < SKIN_TAU_MAX + SKIN_NSTAT && v != 0.0)
+    atomicAdd(fixacc + lane, (unsigned long long)__double2ll_rn(v * SKIN_FIX_SCALE));
 }

@@ -10,7 +10,7 @@ import numpy as np
 import pytest
 
 from cases import rel_l2
-from skin_cases import run_gpu_skin, run_oracle_skin, skin_scene
+from skin_cases import init_fluid, run_gpu_skin, run_oracle_skin, skin_scene
 
 pytestmark = pytest.mark.gpu
 
@@ -126,3 +126,56 @@ def test_skin_api_contract():
     with pytest.raises(FsgError):
         s.body_wrench()
     s.close()
+
+
+def test_batched_skinned_envs_match_single_sessions():
+    """EnvBatch with skinned envs (one fish per env, each its own gait phase)
+    plus one env with host markers: distributions, skinned markers and marker
+    forces bit-identical to the envs stepped one by one; tau_ext / stats within
+    1e-9 (the batch sums each marker's fixed-point terms, a session its warps'
+    sums)."""
+    from paper_2206_01683_b200 import CoupledSession, EnvBatch, SessionConfig
+    sc = skin_scene()
+    E = 4
+    cfg = SessionConfig(dims=sc.dims, dx=sc.dx, dt=sc.dt, rho=sc.rho, nu=sc.nu,
+                        frame_mode=sc.frame_mode, precision="fp32", max_markers=sc.m)
+    rho, u = init_fluid(sc)
+
+    def drive(sessions, step_all):
+        for s in sessions:
+            s.initialize(rho, u)
+        for e, s in enumerate(sessions):
+            if e == 2:
+                continue
+            s.set_skin(*sc.skin())
+        out = []
+        for k in range(4):
+            for e, s in enumerate(sessions):
+                s.set_frame(sc.frame(k + 5 * e))
+                if e == 2:
+                    s.set_markers(sc.offsets, *sc.markers(k))
+                else:
+                    s.set_pose(sc.poses(k + 5 * e))
+            step_all()
+        for e, s in enumerate(sessions):
+            r = dict(f=s.get_f(), fw=s.marker_forces()[0], st=s.last_status())
+            if e != 2:
+                r["mk"] = s.markers()
+                r["tau"], r["stats"] = s.body_wrench()
+            out.append(r)
+        return out
+
+    singles = [CoupledSession(cfg) for _ in range(E)]
+    a = drive(singles, lambda: [s.step() for s in singles])
+    batch = EnvBatch(cfg, E)
+    b = drive(batch.envs, batch.step)
+    for x, y in zip(a, b):
+        assert np.array_equal(x["f"], y["f"]) and np.array_equal(x["fw"], y["fw"])
+        if "mk" in x:
+            for p, q in zip(x["mk"], y["mk"]):
+                assert np.array_equal(p, q)
+            assert rel_l2(np.concatenate(y["tau"]), np.concatenate(x["tau"])) <= 1e-9
+            assert rel_l2(y["stats"], x["stats"]) <= 1e-9
+    for s in singles:
+        s.close()
+    batch.close()
