@@ -328,16 +328,23 @@ def run_envs(args, scene, rank, local, world):
                         max_markers=max(m, 1))
     batch = EnvBatch(cfg, E) if args.c5_mode == "batch" else None
     ss = batch.envs if batch else [CoupledSession(cfg) for _ in range(E)]
-    mk_dev, frames = [], []
+    skinned = bool(m) and args.markers == "skinned"
+    nsteps = W + K
+    # every env runs the gait with its own phase (env.hpp:73-95 randomises the
+    # start); continuous motion over all W + K rounds
+    mk_dev, frames, poses = [], [], []
     for e in range(E):
-        # env e runs the gait with its own phase (env.hpp:73-95 randomises the start)
-        P = np.zeros((16, 4, 3 * m))
-        for k in range(16):
+        frames.append([scene.frame(k + 37 * e) for k in range(nsteps)])
+        if skinned:  # the per-link pose of each round (device-side skinning)
+            ss[e].set_skin(*scene.skin())
+            poses.append([scene.poses(k + 37 * e) for k in range(nsteps)])
+            continue
+        P = np.zeros((nsteps, 4, 3 * m))
+        for k in range(nsteps):
             pts, vel, nrm, area = scene.markers(k + 37 * e)
             P[k, 0], P[k, 1], P[k, 2] = pts.reshape(-1), vel.reshape(-1), nrm.reshape(-1)
             P[k, 3, :m] = area
         mk_dev.append(torch.tensor(P, dtype=torch.float64, device=dev))
-        frames.append([scene.frame(k + 37 * e) for k in range(16)])
     streams = [torch.cuda.ExternalStream(s.stream, device=dev) for s in (ss[:1] if batch else ss)]
     main = torch.cuda.current_stream(dev)
     l2 = torch.cuda.get_device_properties(dev).L2_cache_size
@@ -348,10 +355,13 @@ def run_envs(args, scene, rank, local, world):
 
     def round_async(k):
         for e, s in enumerate(ss):
-            s.set_frame(frames[e][k % 16])
-            r = mk_dev[e][k % 16]
-            s.set_markers_device(scene.offsets, r[0].data_ptr(), r[1].data_ptr(), r[2].data_ptr(),
-                                 r[3].data_ptr())
+            s.set_frame(frames[e][k % nsteps])
+            if skinned:
+                s.set_pose(poses[e][k % nsteps])
+            else:
+                r = mk_dev[e][k % nsteps]
+                s.set_markers_device(scene.offsets, r[0].data_ptr(), r[1].data_ptr(),
+                                     r[2].data_ptr(), r[3].data_ptr())
             if not batch:
                 s.step_async()
         if batch:
@@ -393,21 +403,31 @@ def run_envs(args, scene, rank, local, world):
     value = E * scene.n_cells * K * world / t_total / 1e6
     # e2e: every env through the host API, overlapped across envs with step_async
     Ee = min(args.e2e_steps, K)
-    mk_host = [[scene.markers(k + 37 * e) for k in range(4)] for e in range(E)]
-    torch.cuda.synchronize(dev)
+    kk = W + K  # continue the motion where the timed rounds stopped
+    mk_host = None if skinned else [[scene.markers(kk + k + 37 * e) for k in range(Ee)]
+                                    for e in range(E)]
     e2e_t = 0.0
     for k in range(Ee):
+        fw_buf.fill_(1.0)
+        torch.sum(fr_buf, dim=0, out=sink[0])
+        torch.cuda.synchronize(dev)
         t0 = time.perf_counter()
         for e, s in enumerate(ss):
-            s.set_frame(frames[e][k % 16])
-            s.set_markers(scene.offsets, *mk_host[e][k % 4])
+            s.set_frame(scene.frame(kk + k + 37 * e) if k == 0 else frames[e][(kk + k) % nsteps])
+            if skinned:
+                s.set_pose(poses[e][(kk + k) % nsteps])
+            else:
+                s.set_markers(scene.offsets, *mk_host[e][k])
             if not batch:
                 s.step_async()
         if batch:
             batch.step_async()
         for s in ss:
             s.last_status()
-            s.marker_forces()
+            if skinned:
+                s.body_wrench()
+            else:
+                s.marker_forces()
         e2e_t += time.perf_counter() - t0
     if world > 1:
         import torch.distributed as dist
@@ -425,7 +445,9 @@ def run_envs(args, scene, rank, local, world):
         "metric": METRIC, "value": round(value, 1), "unit": "MLUPS", "n_gpus": world,
         "steps": K, "warmup": W, "ms_per_step": round(round_ms, 4), "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f32 (fp32 storage of f - w_i)",
-        "data": "synthetic (prescribed-kinematics koi per env, own gait phase; SURVEY.md §8(d) C5)",
+        "data": ("synthetic (articulated koi per env skinned on the device from a per-link pose, "
+                 "own gait phase; SURVEY.md §8(d) C5)" if skinned else
+                 "synthetic (prescribed-kinematics koi per env, own gait phase; SURVEY.md §8(d) C5)"),
         "config": {"workload": scene.name, "dims": list(scene.dims), "markers": m,
                    "envs_per_gpu": E, "frame": scene.frame_mode, "l2": "flushed between rounds",
                    "parallelism": (f"{E} envs per GPU batched: one marker + one collide launch per round"
@@ -437,7 +459,8 @@ def run_envs(args, scene, rank, local, world):
                                 else "k_markers_fix + k_collide_band of all envs, one round interval"),
                      "peak_source": peak_src},
         "e2e": {"value": round(E * scene.n_cells * Ee * world / e2e_t / 1e6, 1), "unit": "MLUPS",
-                "h2d_bytes_per_step": E * (80 * m + 232), "d2h_bytes_per_step": E * (28 * m + 64),
+                "h2d_bytes_per_step": E * ((1920 if skinned else 80 * m) + 232),
+                "d2h_bytes_per_step": E * ((8 * (scene.skin()[1][0].n_dofs + 7) if skinned else 28 * m) + 64),
                 "steps": Ee},
         "gpu_launches": K * (2 if batch else E * 2),
         "status": {"stable": all(st.stable() for st in sts), "min_f": min(st.min_f for st in sts)},
