@@ -1,0 +1,84 @@
+"""Summarise a profile round (scripts/profile_round.sh <tag>) into profiles/:
+<tag>_ncu_summary.json (launch list means + the key `--set full` metrics of
+every captured kernel) and k4_traffic.json (DRAM bytes per launch of each
+workload's dominant kernel, read by bench.py's roofline `traffic`).
+
+  python scripts/summarize_profiles.py r1e
+"""
+import csv
+import io
+import json
+import os
+import subprocess
+import sys
+from collections import defaultdict
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+OUT = os.path.join(ROOT, "gpurun_out")
+KEYS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
+        "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed",
+        "sm__warps_active.avg.pct_of_peak_sustained_active", "launch__registers_per_thread",
+        "lts__t_sector_hit_rate.pct", "launch__grid_size", "launch__block_size",
+        "sm__throughput.avg.pct_of_peak_sustained_elapsed", "smsp__inst_executed.sum"]
+DOMINANT = {"c2": "k_collide_band", "c3": "k_collide_band", "c4": "k_collide_fix",
+            "c5": "k_collide_band_batch"}
+
+
+def raw(rep):
+    txt = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True,
+                         text=True).stdout
+    rows = list(csv.reader(io.StringIO(txt)))
+    h, u = rows[0], rows[1]
+    out = []
+    for r in rows[2:]:
+        d = {"kernel": r[h.index("Kernel Name")].split("(")[0]}
+        for k in KEYS:
+            if k in h:
+                d[k] = f"{r[h.index(k)]} {u[h.index(k)]}".strip()
+        out.append(d)
+    return out
+
+
+def to_bytes(v):
+    x, unit = v.split()
+    x = float(x.replace(",", ""))
+    return x * {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}[unit]
+
+
+def main(tag):
+    summ = {"round": tag, "commands": {"script": f"scripts/profile_round.sh {tag}"},
+            "note": "Launch times are cold-cache and serialised by ncu: live, the marker kernel "
+                    "and the banded K4 overlap (K4 is its programmatic dependent).  c2's 80 MB "
+                    "state fits the 126 MB L2; c3 (640 MB) and c4 (20 GB) show full traffic."}
+    lst = os.path.join(OUT, f"{tag}_c2_launches.csv")
+    if os.path.exists(lst):
+        rows = [r for r in csv.reader(open(lst)) if len(r) > 10]
+        h = rows[0]
+        agg = defaultdict(list)
+        for r in rows[1:]:
+            name = r[h.index("Kernel Name")].split("(")[0] + " grid" + r[h.index("Grid Size")]
+            agg[name].append(float(r[h.index("Metric Value")].replace(",", "")) / 1e3)
+        summ["c2_launch_list"] = {k: {"n": len(v), "mean_us": round(sum(v) / len(v), 2)}
+                                  for k, v in agg.items()}
+    traffic = {}
+    for w in ("c2", "c3", "c4", "c5"):
+        rep = os.path.join(OUT, f"{tag}_{w}_full.ncu-rep")
+        if not os.path.exists(rep):
+            continue
+        ks = raw(rep)
+        summ[f"{w}_full"] = ks
+        dom = [k for k in ks if k["kernel"].split("<")[0].endswith(DOMINANT[w])]
+        if dom:
+            b = [to_bytes(k["dram__bytes_read.sum"]) + to_bytes(k["dram__bytes_write.sum"]) for k in dom]
+            traffic[w] = {"kernel": DOMINANT[w], "dram_bytes_per_launch": int(sum(b) / len(b)),
+                          "source": f"profiles/{tag}_ncu_summary.json"}
+    with open(os.path.join(ROOT, "profiles", f"{tag}_ncu_summary.json"), "w") as f:
+        json.dump(summ, f, indent=1)
+    if traffic:
+        with open(os.path.join(ROOT, "profiles", "k4_traffic.json"), "w") as f:
+            json.dump(traffic, f, indent=1)
+    print(json.dumps(traffic, indent=1))
+
+
+if __name__ == "__main__":
+    main(sys.argv[1] if len(sys.argv) > 1 else "r1e")
