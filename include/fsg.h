@@ -219,6 +219,28 @@ int fsg_get_body_wrench(fsg_session* s, double* tau_ext, double* stats);
 /* Marker state the last step used (world frame; skinned or uploaded). */
 int fsg_get_markers(fsg_session* s, double* points, double* velocities, double* normals);
 
+/* ---- empirical drag backend, batched ----------------
+ * EmpiricalBackend::step (empirical.hpp:74-100) for n_envs envs of one robot
+ * each, up to the robot integration: device-side skinning of the samples
+ * (update_samples), surface_force F = -k (n.v) n A on advancing patches
+ * (empirical.hpp:25-30), tau_ext += J^T F (accumulate_skinned_force) and
+ * CouplingStats (force on body, power).  precision FSG_PRECISION_FP64: the
+ * reference's serial order, bit-identical; FSG_PRECISION_FP32: fp64
+ * arithmetic with a deterministic fixed-point (2^-44) reduction.  Errors:
+ * fsg_drag_last_error(). */
+typedef struct fsg_drag fsg_drag;
+const char* fsg_drag_last_error(void);
+int fsg_drag_create(int n_envs, double k, int precision, int device, fsg_drag** out);
+int fsg_drag_destroy(fsg_drag* d);
+/* env's robot: SurfaceSamples (rest points/normals [3m], weights [m][n_links], areas [m]) */
+int fsg_drag_set_skin(fsg_drag* d, int env, const fsg_skeleton* skeleton, int m,
+                      const double* rest_points, const double* rest_normals,
+                      const double* weights, const double* areas);
+int fsg_drag_set_pose(fsg_drag* d, int env, const fsg_body_pose* pose);
+/* one step of every env: tau_ext (concatenated n_dofs per env) and
+ * stats[7*env] = {force_on_fluid[3] (0), force_on_body[3], power_on_body} */
+int fsg_drag_step(fsg_drag* d, double* tau_ext, double* stats);
+
 /* ---- measurement ---------------------------------------------------------
  * When enabled, every step is bracketed with CUDA events on the session
  * stream (the marker kernel and the banded collide/stream kernel overlap, so

@@ -131,6 +131,17 @@ def skin_tau(sk, pose_packed, rest, weights, fworld, valid, vel):
     return tau[: int(sk.n_dofs)], stats
 
 
+def empirical_step(sk, pose_packed, rest, nrest, weights, areas, k):
+    """EmpiricalBackend::step surface work restated -> (tau[n_dofs], stats[7])."""
+    O = oracle()
+    m = int(np.asarray(rest).reshape(-1, 3).shape[0])
+    tau = np.empty(max(int(sk.n_dofs), 1))
+    stats = np.empty(7)
+    O.orc_empirical_step(OrcSkeleton.of(sk), dptr(d3(pose_packed)), m, dptr(d3(rest)), dptr(d3(nrest)),
+                         dptr(d3(weights)), dptr(d3(areas)), float(k), dptr(tau), dptr(stats))
+    return tau[: int(sk.n_dofs)], stats
+
+
 _oracle = None
 _ref = None
 
@@ -176,6 +187,8 @@ def oracle() -> C.CDLL:
                                           _dp, _dp, _dp]),
             "orc_skin_tau": (None, [C.POINTER(OrcSkeleton), _dp, C.c_int, _dp, _dp, _dp, _ip,
                                     _dp, _dp, _dp]),
+            "orc_empirical_step": (None, [C.POINTER(OrcSkeleton), _dp, C.c_int, _dp, _dp, _dp, _dp,
+                                          C.c_double, _dp, _dp]),
         }
         for name, (res, args) in sig.items():
             fn = getattr(lib, name)

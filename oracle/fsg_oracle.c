@@ -613,3 +613,44 @@ void orc_skin_tau(const orc_skeleton* sk, const orc_body_pose* P, int m, const d
     stats[6] = stats[6] + sk_dot(fneg, vel + 3 * i);
   }
 }
+
+/* surface_force (empirical.hpp:25-30): -k (n.v) n A on advancing patches */
+static void orc_surface_force(const double* n, const double* v, double area, double k, double* f) {
+  const double vn = sk_dot(n, v);
+  if (vn <= 0.0) {
+    f[0] = f[1] = f[2] = 0.0;
+    return;
+  }
+  const double s = ((-k) * vn) * area;
+  for (int c = 0; c < 3; ++c) f[c] = s * n[c];
+}
+
+void orc_empirical_step(const orc_skeleton* sk, const orc_body_pose* P, int m, const double* rest,
+                        const double* nrest, const double* weights, const double* areas, double k,
+                        double* tau, double* stats) {
+  const int L = sk->n_links;
+  double* pts = (double*)malloc(sizeof(double) * 3 * (size_t)(m > 0 ? m : 1));
+  double* vel = (double*)malloc(sizeof(double) * 3 * (size_t)(m > 0 ? m : 1));
+  double* nrm = (double*)malloc(sizeof(double) * 3 * (size_t)(m > 0 ? m : 1));
+  orc_update_samples(sk, P, m, rest, nrest, weights, pts, vel, nrm);
+  for (int d = 0; d < sk->n_dofs; ++d) tau[d] = 0.0;
+  for (int q = 0; q < 7; ++q) stats[q] = 0.0;
+  for (int i = 0; i < m; ++i) {
+    double f[3];
+    orc_surface_force(nrm + 3 * i, vel + 3 * i, areas[i], k, f);
+    if (fabs(f[0]) <= 1e-12 && fabs(f[1]) <= 1e-12 && fabs(f[2]) <= 1e-12) continue; /* isZero */
+    const double* w = weights + (size_t)i * L;
+    for (int b = 0; b < L; ++b) { /* accumulate_skinned_force(..., f, tau) */
+      if (w[b] == 0.0) continue;
+      double p[3], fv[3];
+      sk_apply(P, b, rest + 3 * i, p);
+      for (int c = 0; c < 3; ++c) fv[c] = w[b] * f[c];
+      sk_point_force(sk, P, b, p, fv, tau);
+    }
+    for (int c = 0; c < 3; ++c) stats[3 + c] = stats[3 + c] + f[c];
+    stats[6] = stats[6] + sk_dot(f, vel + 3 * i);
+  }
+  free(pts);
+  free(vel);
+  free(nrm);
+}

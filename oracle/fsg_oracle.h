@@ -125,6 +125,14 @@ void orc_skin_tau(const orc_skeleton* sk, const orc_body_pose* pose, int m, cons
                   const double* weights, const double* fworld, const int* valid,
                   const double* vel, double* tau, double* stats);
 
+/* EmpiricalBackend::step surface work for one robot (empirical.hpp:74-100):
+ * update_samples, surface_force (empirical.hpp:25-30, skipped when
+ * f.isZero(): every |f_c| <= 1e-12), accumulate_skinned_force with +f,
+ * force on body and power; stats[0..2] (force on fluid) stay 0. */
+void orc_empirical_step(const orc_skeleton* sk, const orc_body_pose* pose, int m,
+                        const double* rest, const double* nrest, const double* weights,
+                        const double* areas, double k, double* tau, double* stats);
+
 #ifdef __cplusplus
 }
 #endif

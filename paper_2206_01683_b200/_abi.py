@@ -103,6 +103,12 @@ SIGNATURES = {
     "fsg_set_pose": (C.c_int, [_vp, C.POINTER(fsg_body_pose)]),
     "fsg_get_body_wrench": (C.c_int, [_vp, _vp, _vp]),
     "fsg_get_markers": (C.c_int, [_vp, _dp, _dp, _dp]),
+    "fsg_drag_last_error": (C.c_char_p, []),
+    "fsg_drag_create": (C.c_int, [C.c_int, C.c_double, C.c_int, C.c_int, C.POINTER(_vp)]),
+    "fsg_drag_destroy": (C.c_int, [_vp]),
+    "fsg_drag_set_skin": (C.c_int, [_vp, C.c_int, C.POINTER(fsg_skeleton), C.c_int, _dp, _dp, _dp, _dp]),
+    "fsg_drag_set_pose": (C.c_int, [_vp, C.c_int, _vp]),
+    "fsg_drag_step": (C.c_int, [_vp, _dp, _dp]),
     "fsg_profile_enable": (C.c_int, [_vp, C.c_int]),
     "fsg_profile_read": (C.c_int, [_vp, _dp, _ip]),
     "fsg_follower_create": (C.c_int, [C.c_int, C.c_double, C.POINTER(_vp)]),
@@ -143,9 +149,10 @@ def lib() -> C.CDLL:
     return _lib
 
 
-def check(rc: int) -> None:
+def check(rc: int, drag: bool = False) -> None:
     if rc != FSG_OK:
-        msg = lib().fsg_last_error().decode(errors="replace")
+        L = lib()
+        msg = (L.fsg_drag_last_error() if drag else L.fsg_last_error()).decode(errors="replace")
         if rc == FSG_EINPUT:
             raise InputError(rc, msg)
         raise FsgError(rc, msg)

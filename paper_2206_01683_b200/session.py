@@ -551,3 +551,58 @@ class EnvBatch:
             self.close()
         except Exception:
             pass
+
+
+class DragBatch:
+    """The empirical-drag backend's per-step surface work for n_envs robots
+    on the device (fsg_drag_*; EmpiricalBackend::step, empirical.hpp:74-100,
+    up to the robot integration): skinning, surface_force, tau_ext and the
+    CouplingStats of every env in one launch."""
+
+    def __init__(self, n_envs: int, k: float = 40.0, precision: str = "fp32", device: int = 0):
+        L = _abi.lib()
+        h = C.c_void_p()
+        prec = {"fp32": 0, "fp64": 1}[precision]  # FSG_PRECISION_*
+        _abi.check(L.fsg_drag_create(int(n_envs), float(k), prec, int(device), C.byref(h)), drag=True)
+        self._h, self._L, self.n_envs = h, L, int(n_envs)
+        self._ndofs = [0] * self.n_envs
+        self._poses = (_abi.fsg_body_pose * self.n_envs)()
+        self._pose_np = np.frombuffer(self._poses, dtype=np.float64).reshape(self.n_envs, POSE_DOUBLES)
+
+    def set_skin(self, env: int, skeleton: "Skeleton", rest_points, rest_normals, weights, areas):
+        arrs = [np.ascontiguousarray(a, dtype=np.float64).reshape(-1)
+                for a in (rest_points, rest_normals, weights, areas)]
+        m = arrs[3].shape[0]
+        sk = skeleton.to_c()
+        _abi.check(self._L.fsg_drag_set_skin(self._h, int(env), C.byref(sk), m,
+                                             *(dptr(a) for a in arrs)), drag=True)
+        self._ndofs[env] = int(skeleton.n_dofs)
+
+    def set_pose(self, env: int, pose) -> None:
+        """pose: a BodyPose or a packed [240] array (fsg_body_pose order)."""
+        self._pose_np[env] = pose if isinstance(pose, np.ndarray) else pose.packed()
+        addr = C.addressof(self._poses) + env * C.sizeof(_abi.fsg_body_pose)
+        _abi.check(self._L.fsg_drag_set_pose(self._h, int(env), addr), drag=True)
+
+    def step(self):
+        """-> (tau_ext per env [list], stats[n_envs, 7])."""
+        nt = sum(self._ndofs)
+        tau = np.empty(max(nt, 1))
+        stats = np.empty(7 * self.n_envs)
+        _abi.check(self._L.fsg_drag_step(self._h, dptr(tau), dptr(stats)), drag=True)
+        out, k = [], 0
+        for n in self._ndofs:
+            out.append(tau[k:k + n].copy())
+            k += n
+        return out, stats.reshape(-1, 7)
+
+    def close(self) -> None:
+        if getattr(self, "_h", None):
+            self._L.fsg_drag_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
