@@ -237,6 +237,8 @@ int fsg_drag_set_skin(fsg_drag* d, int env, const fsg_skeleton* skeleton, int m,
                       const double* rest_points, const double* rest_normals,
                       const double* weights, const double* areas);
 int fsg_drag_set_pose(fsg_drag* d, int env, const fsg_body_pose* pose);
+/* every env's pose at once (n_envs entries) */
+int fsg_drag_set_poses(fsg_drag* d, const fsg_body_pose* poses);
 /* one step of every env: tau_ext (concatenated n_dofs per env) and
  * stats[7*env] = {force_on_fluid[3] (0), force_on_body[3], power_on_body} */
 int fsg_drag_step(fsg_drag* d, double* tau_ext, double* stats);

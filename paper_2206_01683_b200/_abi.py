@@ -108,6 +108,7 @@ SIGNATURES = {
     "fsg_drag_destroy": (C.c_int, [_vp]),
     "fsg_drag_set_skin": (C.c_int, [_vp, C.c_int, C.POINTER(fsg_skeleton), C.c_int, _dp, _dp, _dp, _dp]),
     "fsg_drag_set_pose": (C.c_int, [_vp, C.c_int, _vp]),
+    "fsg_drag_set_poses": (C.c_int, [_vp, _vp]),
     "fsg_drag_step": (C.c_int, [_vp, _dp, _dp]),
     "fsg_profile_enable": (C.c_int, [_vp, C.c_int]),
     "fsg_profile_read": (C.c_int, [_vp, _dp, _ip]),

@@ -410,6 +410,16 @@ int fsg_drag_set_pose(fsg_drag* d, int env, const fsg_body_pose* pose) {
   return FSG_OK;
 }
 
+int fsg_drag_set_poses(fsg_drag* d, const fsg_body_pose* poses) {
+  if (!poses) return fsg::drag_err(FSG_EINPUT, "fsg_drag_set_poses: null poses");
+  DCU(cudaStreamSynchronize(d->stream));
+  for (int e = 0; e < d->E; ++e) {
+    d->h_bodies[e].pose = poses[e];
+    d->posed[e] = 1;
+  }
+  return FSG_OK;
+}
+
 int fsg_drag_step(fsg_drag* d, double* tau_ext, double* stats) {
   DCU(cudaSetDevice(d->device));
   for (int e = 0; e < d->E; ++e)

@@ -584,6 +584,11 @@ class DragBatch:
         addr = C.addressof(self._poses) + env * C.sizeof(_abi.fsg_body_pose)
         _abi.check(self._L.fsg_drag_set_pose(self._h, int(env), addr), drag=True)
 
+    def set_poses(self, poses: np.ndarray) -> None:
+        """Every env's pose: [n_envs, 240] packed fsg_body_pose rows."""
+        self._pose_np[...] = np.asarray(poses, dtype=np.float64).reshape(self._pose_np.shape)
+        _abi.check(self._L.fsg_drag_set_poses(self._h, C.addressof(self._poses)), drag=True)
+
     def step(self):
         """-> (tau_ext per env [list], stats[n_envs, 7])."""
         nt = sum(self._ndofs)

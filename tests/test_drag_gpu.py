@@ -79,4 +79,7 @@ def test_drag_api_contract():
     d.set_pose(1, sc.poses(1)[0])
     taus, stats = d.step()
     assert len(taus) == 2 and stats.shape == (2, 7)
+    d.set_poses(np.stack([sc.poses(0)[0], sc.poses(1)[0]]))  # bulk form, same poses
+    taus2, stats2 = d.step()
+    assert np.array_equal(np.concatenate(taus), np.concatenate(taus2)) and np.array_equal(stats, stats2)
     d.close()
