@@ -243,6 +243,28 @@ int fsg_drag_set_poses(fsg_drag* d, const fsg_body_pose* poses);
  * stats[7*env] = {force_on_fluid[3] (0), force_on_body[3], power_on_body} */
 int fsg_drag_step(fsg_drag* d, double* tau_ext, double* stats);
 
+/* ---- output formats -----------------------------------
+ * fsg_snapshot_begin enqueues the bare moments of the state the last step
+ * read (CoupledSession::macro(), session.hpp:95-96) into a snapshot buffer and
+ * copies it to pinned host memory on the copy stream: later steps proceed
+ * while it travels.  fsg_snapshot_wait returns it (rho [n], u [3n], lattice
+ * units, cell order).  fsg_write_vtk writes the latest snapshot as
+ * lbm::write_vtk (vtk.hpp:15-38) does, byte for byte; fsg_write_vtk_fields
+ * writes given fields.  fsg_csv_* is CsvWriter (csv.hpp:27-66) with
+ * format_full's %.17g round-trip formatting (csv.hpp:18-22).  Errors of the
+ * host-only writers: fsg_io_last_error(). */
+int fsg_snapshot_begin(fsg_session* s);
+int fsg_snapshot_wait(fsg_session* s, double* rho, double* u);
+int fsg_write_vtk(fsg_session* s, const char* path, const double origin[3]);
+const char* fsg_io_last_error(void);
+int fsg_write_vtk_fields(const char* path, const int dims[3], const double* rho, const double* u,
+                         double dx, double dt, double rho_phys, const double origin[3]);
+int fsg_format_full(double v, char* buf, int size);
+typedef struct fsg_csv fsg_csv;
+int fsg_csv_open(const char* path, int n_cols, const char* const* columns, fsg_csv** out);
+int fsg_csv_write_row(fsg_csv* h, int n, const double* values);
+int fsg_csv_close(fsg_csv* h);
+
 /* ---- measurement ---------------------------------------------------------
  * When enabled, every step is bracketed with CUDA events on the session
  * stream (the marker kernel and the banded collide/stream kernel overlap, so

@@ -209,6 +209,10 @@ def ref() -> C.CDLL:
         vp = C.c_void_p
         sig = {
             "ref_last_error": (C.c_char_p, []),
+            "ref_write_vtk": (C.c_int, [C.c_char_p, C.c_int, C.c_int, C.c_int, _dp, _dp, C.c_double,
+                                        C.c_double, C.c_double, C.c_double, _dp]),
+            "ref_csv_write": (C.c_int, [C.c_char_p, C.c_int, C.POINTER(C.c_char_p), C.c_int, _dp]),
+            "ref_csv_read": (C.c_int, [C.c_char_p, C.c_int, _dp, _ip]),
             "ref_units_tau": (C.c_double, [C.c_double] * 4),
             "ref_units_validate": (C.c_int, [C.c_double] * 4),
             "ref_rng_uniform": (None, [C.c_uint64, C.c_int64, _dp]),

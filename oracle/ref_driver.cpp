@@ -30,6 +30,8 @@
 #include "fishsim/ib/kernel.hpp"
 #include "fishsim/lbm/lattice.hpp"
 #include "fishsim/lbm/solver.hpp"
+#include "fishsim/lbm/vtk.hpp"
+#include "fishsim/core/csv.hpp"
 
 using namespace fishsim;
 
@@ -79,6 +81,57 @@ thread_local char g_err[512];
 }  // namespace
 
 extern "C" {
+
+// lbm::write_vtk (vtk.hpp:15-38) on caller fields; 0 ok, 1 InputError
+int ref_write_vtk(const char* path, int nx, int ny, int nz, const double* rho, const double* u,
+                  double dx, double dt, double rho_phys, double nu, const double* origin) {
+  try {
+    lbm::FluidMacro m;
+    m.resize(Index3{nx, ny, nz});
+    for (size_t c = 0; c < m.rho.size(); ++c) {
+      m.rho[c] = rho[c];
+      m.u[c] = Vec3(u[3 * c], u[3 * c + 1], u[3 * c + 2]);
+    }
+    UnitMap un;
+    un.dx = dx;
+    un.dt_phys = dt;
+    un.rho_phys = rho_phys;
+    un.nu_phys = nu;
+    lbm::write_vtk(path, m, un, Vec3(origin[0], origin[1], origin[2]));
+    return 0;
+  } catch (const std::exception&) {
+    return 1;
+  }
+}
+
+// CsvWriter (csv.hpp:27-66): header + nrows rows of ncols values
+int ref_csv_write(const char* path, int ncols, const char* const* names, int nrows,
+                  const double* values) {
+  try {
+    std::vector<std::string> cols(names, names + ncols);
+    CsvWriter w(path, cols);
+    for (int r = 0; r < nrows; ++r)
+      w.write_row(std::vector<double>(values + (size_t)r * ncols, values + (size_t)(r + 1) * ncols));
+    return 0;
+  } catch (const std::exception&) {
+    return 1;
+  }
+}
+
+// read_csv (csv.hpp:88-112): rows x cols values, returns rows or -1
+int ref_csv_read(const char* path, int max_values, double* values, int* ncols) {
+  try {
+    const CsvTable t = read_csv(path);
+    *ncols = (int)t.columns.size();
+    int k = 0;
+    for (const auto& r : t.rows)
+      for (double v : r)
+        if (k < max_values) values[k++] = v;
+    return (int)t.rows.size();
+  } catch (const std::exception&) {
+    return -1;
+  }
+}
 
 const char* ref_last_error() { return g_err; }
 

@@ -110,6 +110,16 @@ SIGNATURES = {
     "fsg_drag_set_pose": (C.c_int, [_vp, C.c_int, _vp]),
     "fsg_drag_set_poses": (C.c_int, [_vp, _vp]),
     "fsg_drag_step": (C.c_int, [_vp, _dp, _dp]),
+    "fsg_snapshot_begin": (C.c_int, [_vp]),
+    "fsg_snapshot_wait": (C.c_int, [_vp, _dp, _dp]),
+    "fsg_write_vtk": (C.c_int, [_vp, C.c_char_p, _dp]),
+    "fsg_io_last_error": (C.c_char_p, []),
+    "fsg_write_vtk_fields": (C.c_int, [C.c_char_p, _ip, _dp, _dp, C.c_double, C.c_double, C.c_double,
+                                       _dp]),
+    "fsg_format_full": (C.c_int, [C.c_double, C.c_char_p, C.c_int]),
+    "fsg_csv_open": (C.c_int, [C.c_char_p, C.c_int, C.POINTER(C.c_char_p), C.POINTER(_vp)]),
+    "fsg_csv_write_row": (C.c_int, [_vp, C.c_int, _dp]),
+    "fsg_csv_close": (C.c_int, [_vp]),
     "fsg_profile_enable": (C.c_int, [_vp, C.c_int]),
     "fsg_profile_read": (C.c_int, [_vp, _dp, _ip]),
     "fsg_follower_create": (C.c_int, [C.c_int, C.c_double, C.POINTER(_vp)]),
@@ -150,10 +160,11 @@ def lib() -> C.CDLL:
     return _lib
 
 
-def check(rc: int, drag: bool = False) -> None:
+def check(rc: int, drag: bool = False, io: bool = False) -> None:
     if rc != FSG_OK:
         L = lib()
-        msg = (L.fsg_drag_last_error() if drag else L.fsg_last_error()).decode(errors="replace")
+        err = L.fsg_drag_last_error if drag else (L.fsg_io_last_error if io else L.fsg_last_error)
+        msg = err().decode(errors="replace")
         if rc == FSG_EINPUT:
             raise InputError(rc, msg)
         raise FsgError(rc, msg)

@@ -178,6 +178,12 @@ struct fsg_session {
   unsigned long long* d_skin_fix = nullptr;  // fused path: fixed-point sums [2][32]
   unsigned* d_skin_ticket = nullptr;
   double* h_wrench[2] = {nullptr, nullptr};  // pinned: tau + stats written by the step of parity p
+  // asynchronous macro snapshot (fsg_snapshot_begin / _wait, fsg_write_vtk)
+  double* d_snap = nullptr;           // rho [n] | u [3n] of the snapshotted step
+  double* h_snap = nullptr;           // pinned copy
+  cudaEvent_t ev_snap_k = nullptr;    // snapshot kernel done (session stream)
+  cudaEvent_t ev_snap = nullptr;      // copy to h_snap done (copy stream)
+  bool snap_pending = false;
   bool prof = false;
   std::vector<cudaEvent_t> prof_ev;
   int prof_n = 0;
@@ -600,6 +606,11 @@ int fsg_destroy(fsg_session* s) {
   if (s->ev_hpack) cudaEventDestroy(s->ev_hpack);
   if (s->ev_hrecv) cudaEventDestroy(s->ev_hrecv);
   cudaFree(s->d_diag);
+  if (s->snap_pending && s->ev_snap) cudaEventSynchronize(s->ev_snap);
+  cudaFree(s->d_snap);
+  if (s->h_snap) cudaFreeHost(s->h_snap);
+  if (s->ev_snap) cudaEventDestroy(s->ev_snap);
+  if (s->ev_snap_k) cudaEventDestroy(s->ev_snap_k);
   cudaFree(s->d_skin);
   cudaFree(s->d_skin_wb);
   cudaFree(s->d_skin_part);
@@ -1200,6 +1211,56 @@ int fsg_get_stencils(fsg_session* s, int* lo_hi) {
       lo_hi[6 * i + a] = st[i].valid ? st[i].lo[a] : 0;
       lo_hi[6 * i + 3 + a] = st[i].valid ? st[i].hi[a] : -1;
     }
+  return FSG_OK;
+}
+
+// ------------------------------------------------------- output snapshots --
+int fsg_snapshot_begin(fsg_session* s) {
+  if (!s->last_valid) return set_err(FSG_ESTATE, "no coupled step since the last state change");
+  CU(cudaSetDevice(s->cfg.device));
+  const size_t n = (size_t)s->g.n;
+  if (!s->d_snap) {
+    CU(cudaMalloc(&s->d_snap, sizeof(double) * 4 * n));
+    CU(cudaMallocHost(&s->h_snap, sizeof(double) * 4 * n));
+    CU(cudaEventCreateWithFlags(&s->ev_snap, cudaEventDisableTiming));
+    CU(cudaEventCreateWithFlags(&s->ev_snap_k, cudaEventDisableTiming));
+  }
+  if (s->snap_pending) CU(cudaEventSynchronize(s->ev_snap));  // one snapshot in flight
+  // bare moments of the state the last step read (macro(), session.hpp:95-96),
+  // in stream order, into the snapshot's own buffer; the copy to pinned host
+  // memory runs on the copy stream while later steps proceed
+  s->L->macroscopic(s->g, s->buf[s->last_par], s->prev_pulled, nullptr, s->d_snap, s->d_snap + n,
+                    s->d_diag, s->stream);
+  CU_LAUNCH();
+  CU(cudaEventRecord(s->ev_snap_k, s->stream));
+  CU(cudaStreamWaitEvent(s->cstream, s->ev_snap_k, 0));
+  CU(cudaMemcpyAsync(s->h_snap, s->d_snap, sizeof(double) * 4 * n, cudaMemcpyDeviceToHost, s->cstream));
+  CU(cudaEventRecord(s->ev_snap, s->cstream));
+  s->snap_pending = true;
+  return FSG_OK;
+}
+
+int fsg_snapshot_wait(fsg_session* s, double* rho, double* u) {
+  if (!s->snap_pending && !s->h_snap) return set_err(FSG_ESTATE, "no snapshot taken (fsg_snapshot_begin)");
+  CU(cudaSetDevice(s->cfg.device));
+  if (s->snap_pending) CU(cudaEventSynchronize(s->ev_snap));
+  s->snap_pending = false;
+  const size_t n = (size_t)s->g.n;
+  if (rho) std::memcpy(rho, s->h_snap, sizeof(double) * n);
+  if (u) std::memcpy(u, s->h_snap + n, sizeof(double) * 3 * n);
+  return FSG_OK;
+}
+
+int fsg_write_vtk(fsg_session* s, const char* path, const double origin[3]) {
+  if (!path || !origin) return set_err(FSG_EINPUT, "fsg_write_vtk: null path or origin");
+  const size_t n = (size_t)s->g.n;
+  if (s->g.zpad) return set_err(FSG_EINPUT, "fsg_write_vtk: z-slab sessions dump per slab (not supported)");
+  std::vector<double> rho(n), u(3 * n);
+  int rc = fsg_snapshot_wait(s, rho.data(), u.data());
+  if (rc) return rc;
+  rc = fsg_write_vtk_fields(path, s->cfg.dims, rho.data(), u.data(), s->cfg.dx, s->cfg.dt, s->cfg.rho,
+                            origin);
+  if (rc) return set_err(rc, "%s", fsg_io_last_error());
   return FSG_OK;
 }
 

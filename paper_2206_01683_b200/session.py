@@ -16,6 +16,7 @@ instability is reported in the returned status, never raised.
 from __future__ import annotations
 
 import ctypes as C
+import os
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -427,6 +428,24 @@ class CoupledSession:
         check(self._L.fsg_get_markers(self._h, *(dptr(x) for x in a)))
         return tuple(x.reshape(-1, 3) for x in a)
 
+    # -- output formats --------------------------------
+    def snapshot_begin(self) -> None:
+        """Start an asynchronous copy of the last step's bare macro fields
+        (later steps proceed while it travels)."""
+        check(self._L.fsg_snapshot_begin(self._h))
+
+    def snapshot_wait(self):
+        """-> (rho[n], u[n,3]) of the last snapshot (lattice units)."""
+        n = int(np.prod(self.cfg.dims))
+        rho, u = np.empty(n), np.empty(3 * n)
+        check(self._L.fsg_snapshot_wait(self._h, dptr(rho), dptr(u)))
+        return rho, u.reshape(-1, 3)
+
+    def write_vtk(self, path: str, origin=(0.0, 0.0, 0.0)) -> None:
+        """lbm::write_vtk (vtk.hpp:15-38) of the last snapshot."""
+        o = np.ascontiguousarray(origin, dtype=np.float64)
+        check(self._L.fsg_write_vtk(self._h, os.fsencode(path), dptr(o)))
+
     def step(self) -> StepStatus:
         """Fluid half of CoupledSession::step (session.hpp:94-166)."""
         st = self._st
@@ -605,6 +624,57 @@ class DragBatch:
         if getattr(self, "_h", None):
             self._L.fsg_drag_destroy(self._h)
             self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def format_full(v: float) -> str:
+    """format_full (csv.hpp:18-22): %.17g, round-trips to the same double."""
+    buf = C.create_string_buffer(40)
+    _abi.check(_abi.lib().fsg_format_full(float(v), buf, 40), io=True)
+    return buf.value.decode()
+
+
+def write_vtk_fields(path: str, dims, rho, u, dx: float, dt: float, rho_phys: float,
+                     origin=(0.0, 0.0, 0.0)) -> None:
+    """lbm::write_vtk (vtk.hpp:15-38) of given lattice-unit fields."""
+    d = np.ascontiguousarray(dims, dtype=np.int32)
+    r = np.ascontiguousarray(rho, dtype=np.float64).reshape(-1)
+    uu = np.ascontiguousarray(u, dtype=np.float64).reshape(-1)
+    o = np.ascontiguousarray(origin, dtype=np.float64)
+    _abi.check(_abi.lib().fsg_write_vtk_fields(os.fsencode(path), iptr(d), dptr(r), dptr(uu), dx, dt,
+                                               rho_phys, dptr(o)), io=True)
+
+
+class CsvWriter:
+    """CsvWriter (csv.hpp:27-66): header on construction, every row flushed
+    (a truncated file is a valid prefix), %.17g values."""
+
+    def __init__(self, path: str, columns):
+        self._L = _abi.lib()
+        names = (C.c_char_p * len(columns))(*(c.encode() for c in columns))
+        h = C.c_void_p()
+        _abi.check(self._L.fsg_csv_open(os.fsencode(path), len(columns), names, C.byref(h)), io=True)
+        self._h, self.path = h, path
+
+    def write_row(self, values) -> None:
+        v = np.ascontiguousarray(values, dtype=np.float64)
+        _abi.check(self._L.fsg_csv_write_row(self._h, int(v.size), dptr(v)), io=True)
+
+    def close(self) -> None:
+        if getattr(self, "_h", None):
+            self._L.fsg_csv_close(self._h)
+            self._h = None
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
 
     def __del__(self):
         try:
