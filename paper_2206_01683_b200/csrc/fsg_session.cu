@@ -915,15 +915,20 @@ int fsg_set_skin(fsg_session* s, int n_bodies, const int64_t* off, const fsg_ske
     B.tau_off = nt;
     nt += k.n_dofs;
     for (int j = 0; j < FSG_SKIN_MAX_LINKS; ++j) {
-      int a = j < k.n_links ? j : -1;  // chain table for the fused marker kernel
+      int a = j < k.n_links ? j : -1;  // chain tables for the fused marker kernel
+      for (int l = 0; l < FSG_SKIN_MAX_LINKS; ++l) B.lvl[j][l] = -1;
       for (int l = 0; l < FSG_SKIN_MAX_LINKS; ++l) {
         B.anc[j][l] = (signed char)(a > 0 ? a : -1);
+        if (a > 0) B.lvl[j][a] = (signed char)(l + 1);
         a = a > 0 ? k.parent[a] : -1;
       }
       B.parent[j] = j < k.n_links ? k.parent[j] : -1;
       B.dof[j] = (j > 0 && j < k.n_links) ? k.dof_index[j] : -1;
       for (int c = 0; c < 3; ++c) B.axis[j][c] = j < k.n_links ? k.axis[j][c] : 0.0;
     }
+    for (int d = 0; d < 6 + FSG_SKIN_MAX_LINKS; ++d) B.dof_link[d] = -1;
+    for (int j = 1; j < k.n_links; ++j)
+      if (k.dof_index[j] >= 0) B.dof_link[k.dof_index[j]] = (signed char)j;
     for (int i = B.m0; i < B.m1; ++i) {
       int nz = 0;
       for (int j = 0; j < k.n_links; ++j) {

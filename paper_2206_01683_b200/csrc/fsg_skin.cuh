@@ -16,13 +16,16 @@ constexpr int SKIN_KW = FSG_SKIN_MAX_WEIGHTS;
 constexpr int SKIN_NSTAT = 7;  // CouplingStats: force_on_fluid[3], force_on_body[3], power
 
 // One skinned body: its marker range, topology and this step's pose.
-struct SkinBody {
+struct SkinBody {  // (a multiple of 8 bytes: copied as doubles)
   int m0, m1;        // markers [m0, m1)
   int n_links, floating, n_dofs, tau_off;  // tau_off: first entry in the tau/stat output
   int parent[SKIN_L];
   int dof[SKIN_L];
   signed char anc[SKIN_L][SKIN_L];  // anc[b][l]: the (l+1)-th link up the chain from bone b
                                     // (anc[b][0] = b), -1 past the base (link 0)
+  signed char lvl[SKIN_L][SKIN_L];  // lvl[b][J] = l >= 1 with anc[b][l-1] == J (J > 0), else -1
+  signed char dof_link[6 + SKIN_L];  // link whose revolute dof is d (-1: base dof / none)
+  signed char _pad[2];
   double axis[SKIN_L][3];
   fsg_body_pose pose;
 };

@@ -188,14 +188,29 @@ __device__ __forceinline__ void skin_tau_warp(const SP& P, const SkinBody& B, in
       }
     }
   }
-  // marker total of every dof: fixed butterfly, then lane c keeps dof c
+  // marker total of every dof, lane c keeps dof c.  Base dofs (c < 6): the
+  // four level-0 lanes' wrenches through shared memory, in slot order.
+  // Joint dofs: lane c pulls, for each bone slot k, the term of the lane that
+  // evaluated its joint (k * 8 + lvl[b_k][J]), in slot order.
+  __shared__ double wr[FX_PER_BLOCK][SKIN_KW][6];
+  const int warp = threadIdx.x >> 5;
+  if (l == 0) {
 #pragma unroll
-  for (int c = 0; c < SKIN_TAU_MAX; ++c) {
-    double v = (l == 0) ? (c < 6 ? term[c] : 0.0) : (comp == c ? term[0] : 0.0);
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-    if (lane == c && c < B.n_dofs) acc += v;
+    for (int c = 0; c < 6; ++c) wr[warp][k][c] = term[c];
   }
+  __syncwarp();
+  const int J = (lane >= 6 && lane < SKIN_TAU_MAX) ? B.dof_link[lane] : -1;
+  double v = 0.0;
+#pragma unroll
+  for (int kk = 0; kk < SKIN_KW; ++kk) {
+    const int bk = __shfl_sync(0xffffffffu, b, kk * 8);
+    const int lv = (J > 0 && bk >= 0) ? B.lvl[bk][J] : -1;
+    const double jt = __shfl_sync(0xffffffffu, term[0], kk * 8 + (lv > 0 ? lv : 0));
+    if (lane < 6) v += wr[warp][kk][lane];
+    else if (lv > 0) v += jt;
+  }
+  __syncwarp();  // wr is rewritten by the warp's next marker
+  if (lane < SKIN_TAU_MAX && lane < B.n_dofs) acc += v;
   // CouplingStats (session.hpp:141-143)
   const int sidx = lane - SKIN_TAU_MAX;
   if (sidx >= 0 && sidx < 3) acc += fw[sidx];
