@@ -84,20 +84,26 @@ __device__ __forceinline__ SkinSlot skin_slot(const SP& P, int t, int lane) {
 }
 
 /// Warp sum of the per-slot vectors in ascending slot order, starting from 0
-/// (out += w[b] * term_b for the nonzero weights, skinning.hpp:108-110).
+/// (out += w[b] * term_b for the nonzero weights, skinning.hpp:108-110); the
+/// slot lanes' vectors go through a per-warp shared-memory buffer.
 __device__ __forceinline__ void slot_sum(const SkinSlot& s, const double* term, double* out) {
+  __shared__ double sb[FX_PER_BLOCK][SKIN_KW][4];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (lane < SKIN_KW) {
+#pragma unroll
+    for (int c = 0; c < 3; ++c) sb[warp][lane][c] = term[c];
+    sb[warp][lane][3] = s.b >= 0 ? 1.0 : 0.0;
+  }
+  __syncwarp();
 #pragma unroll
   for (int c = 0; c < 3; ++c) out[c] = 0.0;
 #pragma unroll
   for (int l = 0; l < SKIN_KW; ++l) {
-    const int bl = __shfl_sync(0xffffffffu, s.b, l);
-    double v[3];
+    if (sb[warp][l][3] == 0.0) break;  // slots are packed: the first empty one ends the list
 #pragma unroll
-    for (int c = 0; c < 3; ++c) v[c] = __shfl_sync(0xffffffffu, term[c], l);
-    if (bl < 0) break;  // slots are packed: the first empty one ends the list
-#pragma unroll
-    for (int c = 0; c < 3; ++c) out[c] = rn_add(out[c], v[c]);
+    for (int c = 0; c < 3; ++c) out[c] = rn_add(out[c], sb[warp][l][c]);
   }
+  __syncwarp();  // the buffer is rewritten by the next sum
 }
 
 /// skin_point: world position of marker t (all lanes).
