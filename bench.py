@@ -588,17 +588,17 @@ def run_ours(args, scene, rank, local, world):
     e2e_t = 0.0
 
     def e2e_step(k):
-        # the robot side's per-step exchange: pose up, tau_ext + stats down
-        # (skinned), or the whole marker state up and per-marker forces down
-        s.set_frame(frames[k % nsteps])
+        # the robot side's per-step exchange: pose up, tau_ext + stats down in
+        # one ABI call (skinned), or the whole marker state up and per-marker
+        # forces down
         if skinned:
-            s.set_pose(poses[k % nsteps])
-        elif m:
+            s.step_skinned(frames[k % nsteps], poses[k % nsteps])
+            return
+        s.set_frame(frames[k % nsteps])
+        if m:
             s.set_markers(off, *mk_host[k % 8])
         s.step()
-        if skinned:
-            s.body_wrench()
-        elif m:
+        if m:
             s.marker_forces()
 
     with torch.cuda.stream(stream):

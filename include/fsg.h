@@ -216,6 +216,11 @@ int fsg_set_pose(fsg_session* s, const fsg_body_pose* poses);
  * session.hpp:107, :139-140) and CouplingStats stats[7*b] as in
  * fsg_get_marker_forces.  Either pointer may be NULL. */
 int fsg_get_body_wrench(fsg_session* s, double* tau_ext, double* stats);
+/* The robot loop's whole per-step exchange in one call: fsg_set_frame (fs
+ * may be NULL: keep the frame), fsg_set_pose, fsg_step (synchronous status),
+ * fsg_get_body_wrench. */
+int fsg_step_skinned(fsg_session* s, const fsg_frame_state* fs, const fsg_body_pose* poses,
+                     fsg_status* st, double* tau_ext, double* stats);
 /* Marker state the last step used (world frame; skinned or uploaded). */
 int fsg_get_markers(fsg_session* s, double* points, double* velocities, double* normals);
 

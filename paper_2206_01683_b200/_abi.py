@@ -103,6 +103,7 @@ SIGNATURES = {
     "fsg_set_pose": (C.c_int, [_vp, C.POINTER(fsg_body_pose)]),
     "fsg_get_body_wrench": (C.c_int, [_vp, _vp, _vp]),
     "fsg_get_markers": (C.c_int, [_vp, _dp, _dp, _dp]),
+    "fsg_step_skinned": (C.c_int, [_vp, _vp, _vp, _vp, _vp, _vp]),
     "fsg_drag_last_error": (C.c_char_p, []),
     "fsg_drag_create": (C.c_int, [C.c_int, C.c_double, C.c_int, C.c_int, C.POINTER(_vp)]),
     "fsg_drag_destroy": (C.c_int, [_vp]),

@@ -1018,6 +1018,15 @@ int fsg_get_body_wrench(fsg_session* s, double* tau, double* stats) {
   return FSG_OK;
 }
 
+int fsg_step_skinned(fsg_session* s, const fsg_frame_state* fs, const fsg_body_pose* poses,
+                     fsg_status* st, double* tau, double* stats) {
+  int rc = FSG_OK;
+  if (fs && (rc = fsg_set_frame(s, fs))) return rc;
+  if ((rc = fsg_set_pose(s, poses))) return rc;
+  if ((rc = fsg_step(s, st))) return rc;
+  return fsg_get_body_wrench(s, tau, stats);
+}
+
 int fsg_get_markers(fsg_session* s, double* pts, double* vel, double* nrm) {
   CU(cudaSetDevice(s->cfg.device));
   CU(stream_wait(s->stream));

@@ -242,6 +242,8 @@ class CoupledSession:
         self._fs_view = np.frombuffer(self._fs_c, dtype=np.float64)
         self._st = _abi.fsg_status()
         self._st_ref = C.byref(self._st)
+        self._st_addr = C.addressof(self._st)
+        self._fs_addr = C.addressof(self._fs_c)
         self.dims = tuple(int(d) for d in cfg.dims)
         self.n_cells = int(np.prod(self.dims))
         self.m = 0
@@ -399,6 +401,7 @@ class CoupledSession:
         self._tau_ranges = list(zip([0] + ends[:-1], ends))
         self._pose = (_abi.fsg_body_pose * nb)()
         self._pose_np = np.frombuffer(self._pose, dtype=np.float64).reshape(nb, POSE_DOUBLES)
+        self._pose_addr = C.addressof(self._pose)
 
     def set_pose(self, poses) -> None:
         """This step's pose of every skinned body: a list of BodyPose, or an
@@ -421,6 +424,28 @@ class CoupledSession:
             check(rc)
         buf = self._wbuf.copy()
         return [buf[a:b] for a, b in self._tau_ranges], buf[self._nt:].reshape(-1, 7)
+
+    def step_skinned(self, frame, poses):
+        """The robot loop's per-step exchange in one ABI call (fsg_step_skinned):
+        frame (FrameState, a packed [19] array, or None to keep it), poses
+        ([n_bodies, 240] packed or a list of BodyPose) -> (StepStatus,
+        tau_ext per body, stats[n_bodies, 7])."""
+        fp = None
+        if frame is not None:
+            self._fs_view[:] = frame if isinstance(frame, np.ndarray) else frame.packed()
+            fp = self._fs_addr
+        if isinstance(poses, np.ndarray):
+            self._pose_np[...] = poses.reshape(self._pose_np.shape)
+        else:
+            for b, p in enumerate(poses):
+                self._pose_np[b] = p.packed()
+        rc = self._L.fsg_step_skinned(self._h, fp, self._pose_addr, self._st_addr, self._wptr,
+                                      self._wptr + 8 * self._nt)
+        if rc:
+            check(rc)
+        buf = self._wbuf.copy()
+        return (StepStatus.of(self._st), [buf[a:b] for a, b in self._tau_ranges],
+                buf[self._nt:].reshape(-1, 7))
 
     def markers(self):
         """-> (points, velocities, normals) [m, 3] the last step used."""

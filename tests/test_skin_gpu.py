@@ -179,3 +179,28 @@ def test_batched_skinned_envs_match_single_sessions():
     for s in singles:
         s.close()
     batch.close()
+
+
+def test_step_skinned_one_call_matches_separate_calls():
+    """fsg_step_skinned (frame + pose + step + wrench in one ABI call) gives
+    the same step as the separate calls."""
+    from paper_2206_01683_b200 import CoupledSession, SessionConfig
+    sc = skin_scene()
+    cfg = SessionConfig(dims=sc.dims, dx=sc.dx, dt=sc.dt, rho=sc.rho, nu=sc.nu,
+                        frame_mode=sc.frame_mode, precision="fp32", max_markers=sc.m)
+    rho, u = init_fluid(sc)
+    a, b = CoupledSession(cfg), CoupledSession(cfg)
+    for s in (a, b):
+        s.initialize(rho, u)
+        s.set_skin(*sc.skin())
+    for k in range(3):
+        a.set_frame(sc.frame(k))
+        a.set_pose(sc.poses(k))
+        sa = a.step()
+        ta, wa = a.body_wrench()
+        sb, tb, wb = b.step_skinned(sc.frame(k).packed(), sc.poses(k))
+        assert sa.min_f == sb.min_f and np.array_equal(np.concatenate(ta), np.concatenate(tb))
+        assert np.array_equal(wa, wb)
+    assert np.array_equal(a.get_f(), b.get_f())
+    a.close()
+    b.close()
