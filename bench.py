@@ -411,9 +411,16 @@ def run_envs(args, scene, rank, local, world):
         fw_buf.fill_(1.0)
         torch.sum(fr_buf, dim=0, out=sink[0])
         torch.cuda.synchronize(dev)
+        if skinned and batch:  # the rollout loop's exchange in one ABI call
+            fr = np.stack([frames[e][(kk + k) % nsteps].packed() for e in range(E)])
+            po = np.stack([poses[e][(kk + k) % nsteps][0] for e in range(E)])
+            t0 = time.perf_counter()
+            batch.step_skinned(fr, po)
+            e2e_t += time.perf_counter() - t0
+            continue
         t0 = time.perf_counter()
         for e, s in enumerate(ss):
-            s.set_frame(scene.frame(kk + k + 37 * e) if k == 0 else frames[e][(kk + k) % nsteps])
+            s.set_frame(frames[e][(kk + k) % nsteps])
             if skinned:
                 s.set_pose(poses[e][(kk + k) % nsteps])
             else:

@@ -290,6 +290,12 @@ int fsg_batch_destroy(fsg_batch* b);
 fsg_session* fsg_batch_session(fsg_batch* b, int env);
 int fsg_batch_step_async(fsg_batch* b);
 int fsg_batch_step(fsg_batch* b, fsg_status* statuses /* n_envs, nullable */);
+/* Every env with one skinned body (fsg_set_skin on each env): the frames
+ * (n_envs, NULL: keep) and poses (n_envs) in, one batched step, every env's
+ * status, tau_ext (concatenated) and CouplingStats (7 per env) out -- the RL
+ * rollout loop's per-step exchange in one call. */
+int fsg_batch_step_skinned(fsg_batch* b, const fsg_frame_state* frames, const fsg_body_pose* poses,
+                           fsg_status* statuses, double* tau_ext, double* stats);
 
 /* ---- z-slab halo exchange ------------------------------
  * A slab session (cfg.z_offset / cfg.nz_global) owns planes [z_offset,

@@ -133,6 +133,7 @@ SIGNATURES = {
     "fsg_batch_session": (_vp, [_vp, C.c_int]),
     "fsg_batch_step_async": (C.c_int, [_vp]),
     "fsg_batch_step": (C.c_int, [_vp, C.POINTER(fsg_status)]),
+    "fsg_batch_step_skinned": (C.c_int, [_vp, _vp, _vp, _vp, _vp, _vp]),
     "fsg_halo_bytes": (C.c_size_t, [_vp]),
     "fsg_halo_pack": (C.c_int, [_vp, _vp, _vp]),
     "fsg_halo_unpack": (C.c_int, [_vp, _vp, _vp]),

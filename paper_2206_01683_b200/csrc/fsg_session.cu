@@ -1435,6 +1435,7 @@ struct fsg_batch {
   fsg::EnvPack* h_packs[2] = {nullptr, nullptr};  // pinned, by batch step parity
   fsg::EnvPack* d_packs[2] = {nullptr, nullptr};
   unsigned* d_work = nullptr;                      // [2] phase-A counters by parity
+  StepScratch* h_stat = nullptr;                   // pinned: every env's status (one-call step)
   fsg::SkinBody* h_skb[2] = {nullptr, nullptr};    // pinned: skinned envs' topology + pose
   fsg::SkinBody* d_skb[2] = {nullptr, nullptr};
   cudaEvent_t ev[2] = {nullptr, nullptr};
@@ -1454,6 +1455,7 @@ int fsg_batch_destroy(fsg_batch* b) {
     if (b->ev[k]) cudaEventDestroy(b->ev[k]);
   }
   cudaFree(b->d_work);
+  if (b->h_stat) cudaFreeHost(b->h_stat);
   if (b->stream) cudaStreamDestroy(b->stream);
   delete b;
   return FSG_OK;
@@ -1605,6 +1607,49 @@ int fsg_batch_step_async(fsg_batch* b) {
     s->mk_dirty = false;
   }
   b->par ^= 1;
+  return FSG_OK;
+}
+
+namespace {
+// every env's step status into pinned host memory in one launch (the batched
+// K4 left each in its env's device scratch, packs[e].out)
+__global__ void k_batch_status(const fsg::EnvPack* __restrict__ packs, int E, StepScratch* dst) {
+  constexpr int NS = (int)(sizeof(StepScratch) / 4);
+  for (int k = threadIdx.x; k < E * NS; k += blockDim.x)
+    reinterpret_cast<volatile int*>(dst)[k] = reinterpret_cast<const int*>(packs[k / NS].out)[k % NS];
+}
+}  // namespace
+
+int fsg_batch_step_skinned(fsg_batch* b, const fsg_frame_state* frames, const fsg_body_pose* poses,
+                           fsg_status* statuses, double* tau, double* stats) {
+  CU(cudaSetDevice(b->envs[0]->cfg.device));
+  for (int e = 0; e < b->E; ++e) {
+    fsg_session* s = b->envs[e];
+    if (!s->skin || s->skp.nb != 1)
+      return set_err(FSG_ESTATE, "fsg_batch_step_skinned: env %d has no single skinned body", e);
+    if (frames) s->frame = frames[e];
+    s->skp.body[0].pose = poses[e];
+    s->pose_set = true;
+  }
+  const int q = b->par;  // the packs this step uploads
+  int rc = fsg_batch_step_async(b);
+  if (rc) return rc;
+  if (!b->h_stat) CU(cudaMallocHost(&b->h_stat, sizeof(StepScratch) * b->E));
+  k_batch_status<<<1, 256, 0, b->stream>>>(b->d_packs[q], b->E, b->h_stat);
+  CU_LAUNCH();
+  CU(stream_wait(b->stream));
+  int off = 0;
+  for (int e = 0; e < b->E; ++e) {
+    fsg_session* s = b->envs[e];
+    if (b->h_stat[e].band_overflow) return set_err(FSG_ESTATE, "env %d: IB band overflow", e);
+    decode_status(b->h_stat[e], &s->last, true);
+    if (statuses) statuses[e] = s->last;
+    const double* w = s->h_wrench[s->last_par];
+    const int nd = s->skp.body[0].n_dofs;
+    if (tau) std::memcpy(tau + off, w, sizeof(double) * nd);
+    if (stats) std::memcpy(stats + fsg::SKIN_NSTAT * e, w + nd, sizeof(double) * fsg::SKIN_NSTAT);
+    off += nd;
+  }
   return FSG_OK;
 }
 

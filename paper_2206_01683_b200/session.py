@@ -583,6 +583,40 @@ class EnvBatch:
         check(self._L.fsg_batch_step(self._h, sts))
         return [StepStatus.of(x) for x in sts]
 
+    def step_skinned(self, frames, poses):
+        """Every env skinned (set_skin on each): frames ([E, 19] packed, a list
+        of FrameState, or None to keep) and poses ([E, 240] packed) in, one
+        batched step -> (statuses, tau_ext per env, stats[E, 7])."""
+        E = len(self.envs)
+        if not hasattr(self, "_bpose"):
+            self._bpose = (_abi.fsg_body_pose * E)()
+            self._bpose_np = np.frombuffer(self._bpose, dtype=np.float64).reshape(E, POSE_DOUBLES)
+            self._bframe = (_abi.fsg_frame_state * E)()
+            self._bframe_np = np.frombuffer(self._bframe, dtype=np.float64).reshape(E, 19)
+            self._bst = (_abi.fsg_status * E)()
+            self._bnd = [getattr(s, "_nt", 0) for s in self.envs]
+            self._bw = np.empty(sum(self._bnd) + 7 * E)
+        fp = None
+        if frames is not None:
+            if isinstance(frames, np.ndarray):
+                self._bframe_np[...] = frames.reshape(E, 19)
+            else:
+                for e, f in enumerate(frames):
+                    self._bframe_np[e] = f.packed()
+            fp = C.addressof(self._bframe)
+        self._bpose_np[...] = np.asarray(poses, dtype=np.float64).reshape(E, POSE_DOUBLES)
+        nt = sum(self._bnd)
+        w = self._bw
+        check(self._L.fsg_batch_step_skinned(self._h, fp, C.addressof(self._bpose),
+                                             C.addressof(self._bst), w.ctypes.data,
+                                             w.ctypes.data + 8 * nt))
+        out = w.copy()
+        taus, k = [], 0
+        for n in self._bnd:
+            taus.append(out[k:k + n])
+            k += n
+        return [StepStatus.of(x) for x in self._bst], taus, out[nt:].reshape(E, 7)
+
     def close(self) -> None:
         if getattr(self, "_h", None):
             for s in self.envs:

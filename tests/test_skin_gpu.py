@@ -204,3 +204,33 @@ def test_step_skinned_one_call_matches_separate_calls():
     assert np.array_equal(a.get_f(), b.get_f())
     a.close()
     b.close()
+
+
+def test_batch_step_skinned_one_call_matches_separate_calls():
+    from paper_2206_01683_b200 import EnvBatch, SessionConfig
+    sc = skin_scene()
+    E = 3
+    cfg = SessionConfig(dims=sc.dims, dx=sc.dx, dt=sc.dt, rho=sc.rho, nu=sc.nu,
+                        frame_mode=sc.frame_mode, precision="fp32", max_markers=sc.m)
+    rho, u = init_fluid(sc)
+    A, Bt = EnvBatch(cfg, E), EnvBatch(cfg, E)
+    for bt in (A, Bt):
+        for s in bt.envs:
+            s.initialize(rho, u)
+            s.set_skin(*sc.skin())
+    for k in range(3):
+        for e, s in enumerate(A.envs):
+            s.set_frame(sc.frame(k + 5 * e))
+            s.set_pose(sc.poses(k + 5 * e))
+        sa = A.step()
+        frames = np.stack([sc.frame(k + 5 * e).packed() for e in range(E)])
+        poses = np.stack([sc.poses(k + 5 * e)[0] for e in range(E)])
+        sb, taus, stats = Bt.step_skinned(frames, poses)
+        for e in range(E):
+            ta, wa = A.envs[e].body_wrench()
+            assert sa[e].min_f == sb[e].min_f and sa[e].stable() == sb[e].stable()
+            assert np.array_equal(ta[0], taus[e]) and np.array_equal(wa[0], stats[e])
+    for e in range(E):
+        assert np.array_equal(A.envs[e].get_f(), Bt.envs[e].get_f())
+    A.close()
+    Bt.close()
