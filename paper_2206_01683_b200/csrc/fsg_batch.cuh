@@ -80,7 +80,7 @@ __device__ __forceinline__ void report_min_red(StepScratch* out, float v) {
 /// and triggers K4, then the groups do the heavy per-marker work (the cheap
 /// stencil is recomputed rather than kept).
 template <bool SKIN>  // SKIN: some env has a skinned body (P.skb)
-__global__ void __launch_bounds__(128, FSG_KM_MINB)
+__global__ void __launch_bounds__(128, FSG_KMB_MINB)
     k_markers_batch(Grid g, const SessionConsts* __restrict__ scp, const EnvPack* __restrict__ packs,
                     BatchHead h) {
   __shared__ double phs[FX_PER_BLOCK][3][5];

@@ -16,6 +16,14 @@
 #ifndef FSG_KM_PER_SM_DEFAULT
 #define FSG_KM_PER_SM_DEFAULT 0.0
 #endif
+// batched marker kernel: register budget (min resident blocks) and grid cap
+// per SM (it is persistent over every env's markers)
+#ifndef FSG_KMB_MINB
+#define FSG_KMB_MINB 6
+#endif
+#ifndef FSG_KMB_PER_SM
+#define FSG_KMB_PER_SM 4
+#endif
 #ifndef FSG_KM_MINB
 #define FSG_KM_MINB 6
 #endif

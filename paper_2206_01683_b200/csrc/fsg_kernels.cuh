@@ -955,10 +955,11 @@ static void L_step_batch(const Grid& g, const SessionConsts* sc, const EnvPack* 
   }
   if (h.m_total > 0) {
     const int need = (h.m_total + FX_PER_BLOCK - 1) / FX_PER_BLOCK;
+    const int grid = std::min(need, nsm * FSG_KMB_PER_SM);
     if (h.skin)
-      k_markers_batch<true><<<std::min(need, nsm * 4), 128, 0, s>>>(g, sc, d_packs, h);
+      k_markers_batch<true><<<grid, 128, 0, s>>>(g, sc, d_packs, h);
     else
-      k_markers_batch<false><<<std::min(need, nsm * 4), 128, 0, s>>>(g, sc, d_packs, h);
+      k_markers_batch<false><<<grid, 128, 0, s>>>(g, sc, d_packs, h);
   }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)std::min<long long>(h.item_total, (long long)nsm * res));
