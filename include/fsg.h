@@ -248,6 +248,90 @@ int fsg_drag_set_poses(fsg_drag* d, const fsg_body_pose* poses);
  * stats[7*env] = {force_on_fluid[3] (0), force_on_body[3], power_on_body} */
 int fsg_drag_step(fsg_drag* d, double* tau_ext, double* stats);
 
+/* ---- articulated robot dynamics, batched -------------
+ * The robot half of CoupledSession::step (session.hpp:169-175) for n_envs
+ * robots of one Skeleton on the device, one thread per env in fp64:
+ *   hydro = robot::buoyancy_gravity_forces(kc(state), bladder, rho, g_hydro)
+ *                                                    (dynamics.hpp:237-255)
+ *   robot::integrate(state, actuation, tau_ext + hydro, dt, substeps, gravity)
+ *                                                    (dynamics.hpp:259-289)
+ * with forward_kinematics / mass_matrix (CRBA) / bias_forces (RNEA) /
+ * internal_forces / joint_limit_forces / LLT solve (dynamics.hpp:23-212),
+ * and the new pose for device skinning (fsg_dyn_poses: forward_kinematics +
+ * BoneTransforms::of, skinning.hpp:85-102).  Results agree with the fp64
+ * restatement to rounding (libm vs device sin/cos: rel <= 1e-12 per step).
+ * Errors: fsg_dyn_last_error() (Skeleton::validate messages, InputError);
+ * a mass matrix that is not positive definite (NumericalError in the
+ * reference, dynamics.hpp:208-210) sets FSG_DYN_NOT_SPD in the env's flags
+ * and leaves that env's state unchanged. */
+#define FSG_DYN_MAX_LINKS 8
+#define FSG_DYN_MAX_DOFS (6 + FSG_DYN_MAX_LINKS)
+enum { FSG_JOINT_FREE = 0, FSG_JOINT_REVOLUTE = 1, FSG_JOINT_FIXED = 2 };
+enum { FSG_DYN_CLAMPED = 1, FSG_DYN_NOT_SPD = 2, FSG_DYN_NONFINITE = 4 };
+
+/* robot::Link (skeleton.hpp:16-36); matrices row-major */
+typedef struct {
+  int parent; /* -1 for the root */
+  int joint;  /* FSG_JOINT_* */
+  double joint_origin[3];
+  double joint_rotation[9];
+  double axis[3];
+  double mass;
+  double com[3];
+  double inertia_com[9];
+  double stiffness, damping, q_rest, limit_lo, limit_hi, torque_limit;
+  double displaced_volume;
+  double volume_centroid[3];
+} fsg_link;
+
+/* robot::Skeleton + its Bladder (skeleton.hpp:38-93) */
+typedef struct {
+  int n_links;
+  fsg_link links[FSG_DYN_MAX_LINKS];
+  double bladder_volume, bladder_volume_min, bladder_volume_max, bladder_rate_bound;
+  double bladder_centroid[3];
+} fsg_robot;
+
+/* robot::JointState (skeleton.hpp:138-150); quaternion (w, x, y, z) */
+typedef struct {
+  double base_pos[3];
+  double base_quat[4];
+  double q[FSG_DYN_MAX_LINKS];
+  double v[FSG_DYN_MAX_DOFS];
+  double qdd[FSG_DYN_MAX_DOFS];
+} fsg_joint_state;
+
+typedef struct fsg_dyn fsg_dyn;
+const char* fsg_dyn_last_error(void);
+/* validates the skeleton as Skeleton::validate; every env starts at
+ * JointState::zero with the robot's bladder */
+int fsg_dyn_create(const fsg_robot* robot, int n_envs, int device, fsg_dyn** out);
+int fsg_dyn_destroy(fsg_dyn* d);
+int fsg_dyn_n_dofs(const fsg_dyn* d);
+int fsg_dyn_n_joints(const fsg_dyn* d);
+int fsg_dyn_set_state(fsg_dyn* d, const fsg_joint_state* states); /* n_envs */
+int fsg_dyn_get_state(fsg_dyn* d, fsg_joint_state* states);
+/* Bladder::apply_change per env (skeleton.hpp:48-51, Backend::change_bladder);
+ * volumes (nullable) receives the new volumes */
+int fsg_dyn_change_bladder(fsg_dyn* d, const double* dv, double* volumes);
+/* one robot step of every env (host arrays): actuation [n_envs * n_joints],
+ * tau_ext [n_envs * n_dofs] (NULL: zero), flags [n_envs] (nullable).
+ * g_hydro: gravity of buoyancy_gravity_forces (NULL: no hydrostatics);
+ * gravity: integrate's gravity argument (NULL: zero). */
+int fsg_dyn_step(fsg_dyn* d, const double* actuation, const double* tau_ext, double rho_fluid,
+                 const double* g_hydro, double dt, int substeps, const double* gravity,
+                 int* flags);
+/* the same with device pointers, stream-ordered on the handle's stream */
+int fsg_dyn_step_device(fsg_dyn* d, const double* d_actuation, const double* d_tau_ext,
+                        double rho_fluid, const double* g_hydro, double dt, int substeps,
+                        const double* gravity, int* d_flags);
+/* parity probes: mass_matrix (row-major nd x nd per env) and bias_forces (nd)
+ * at the current state; either pointer may be NULL */
+int fsg_dyn_mass_matrix(fsg_dyn* d, const double* gravity, double* M, double* bias);
+/* the current state's pose of every env for fsg_set_pose / fsg_drag_set_poses
+ * (rest_R [n_links*9], rest_p [n_links*3]: BoneTransforms rest pose) */
+int fsg_dyn_poses(fsg_dyn* d, const double* rest_R, const double* rest_p, fsg_body_pose* poses);
+
 /* ---- output formats -----------------------------------
  * fsg_snapshot_begin enqueues the bare moments of the state the last step
  * read (CoupledSession::macro(), session.hpp:95-96) into a snapshot buffer and

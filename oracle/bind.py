@@ -189,6 +189,22 @@ def oracle() -> C.CDLL:
                                     _dp, _dp, _dp]),
             "orc_empirical_step": (None, [C.POINTER(OrcSkeleton), _dp, C.c_int, _dp, _dp, _dp, _dp,
                                           C.c_double, _dp, _dp]),
+            "orc_quat_exp": (None, [_dp, _dp]),
+            "orc_quat_to_R": (None, [_dp, _dp]),
+            "orc_forward_kinematics": (None, [C.c_void_p, C.c_void_p, C.c_void_p]),
+            "orc_mass_matrix": (None, [C.c_void_p, C.c_void_p, _dp]),
+            "orc_bias_forces": (None, [C.c_void_p, C.c_void_p, C.c_void_p, _dp, _dp]),
+            "orc_internal_forces": (C.c_int, [C.c_void_p, C.c_void_p, _dp, _dp]),
+            "orc_joint_limit_forces": (None, [C.c_void_p, C.c_void_p, _dp]),
+            "orc_llt_solve": (C.c_int, [C.c_int, _dp, _dp, _dp]),
+            "orc_forward_dynamics": (C.c_int, [C.c_void_p, C.c_void_p, _dp, _dp, _dp, _dp]),
+            "orc_buoyancy_gravity_forces": (None, [C.c_void_p, C.c_void_p, C.c_double, C.c_double,
+                                                   _dp, _dp]),
+            "orc_integrate": (C.c_int, [C.c_void_p, C.c_void_p, _dp, _dp, C.c_double, C.c_int, _dp]),
+            "orc_robot_step": (C.c_int, [C.c_void_p, C.c_void_p, C.c_double, _dp, _dp, C.c_double,
+                                         _dp, C.c_double, C.c_int, _dp]),
+            "orc_mechanical_energy": (C.c_double, [C.c_void_p, C.c_void_p, _dp]),
+            "orc_dyn_pose": (None, [C.c_void_p, C.c_void_p, _dp, _dp, C.c_void_p]),
         }
         for name, (res, args) in sig.items():
             fn = getattr(lib, name)
@@ -306,3 +322,117 @@ class Rng:
 
     def uniforms(self, n: int) -> np.ndarray:
         return np.array([self.uniform() for _ in range(n)], dtype=np.float64)
+
+
+# --------------------------------------------------------------------------
+# Articulated dynamics restated (fsg_dyn_oracle.c; dynamics.hpp).  Robots and
+# states are the product's host types (paper_2206_01683_b200.dynamics), whose
+# POD structs are the boundary's own layout.
+class DynKC(C.Structure):
+    _L = 8
+    _fields_ = [("E", (C.c_double * 9) * _L), ("r", (C.c_double * 3) * _L),
+                ("R_world", (C.c_double * 9) * _L), ("p_world", (C.c_double * 3) * _L),
+                ("v_body", (C.c_double * 6) * _L), ("omega_world", (C.c_double * 3) * _L),
+                ("v_origin_world", (C.c_double * 3) * _L)]
+
+
+class DynOracle:
+    """One robot (host types from paper_2206_01683_b200.dynamics) on the fp64
+    restatement; states are JointState objects, updated in place by step()."""
+
+    def __init__(self, robot):
+        self.robot = robot
+        self.rs = robot.to_struct()
+        self.nd, self.nj = robot.n_dofs, robot.n_joints
+        self.bladder_volume = robot.bladder.volume
+
+    def _st(self, st):
+        return st.to_struct()
+
+    def _back(self, s, st):
+        from paper_2206_01683_b200.dynamics import JointState
+        n = JointState.from_struct(s, self.nj, self.nd)
+        st.base_pos, st.base_quat, st.q, st.v, st.qdd = n.base_pos, n.base_quat, n.q, n.v, n.qdd
+
+    def kinematics(self, st):
+        kc = DynKC()
+        oracle().orc_forward_kinematics(C.byref(self.rs), C.byref(self._st(st)), C.byref(kc))
+        return kc
+
+    def mass_matrix(self, st):
+        M = np.zeros(self.nd * self.nd)
+        oracle().orc_mass_matrix(C.byref(self.rs), C.byref(self.kinematics(st)), dptr(M))
+        return M.reshape(self.nd, self.nd)
+
+    def bias_forces(self, st, g=(0.0, 0.0, 0.0)):
+        c = np.zeros(max(self.nd, 1))
+        s = self._st(st)
+        kc = DynKC()
+        oracle().orc_forward_kinematics(C.byref(self.rs), C.byref(s), C.byref(kc))
+        oracle().orc_bias_forces(C.byref(self.rs), C.byref(s), C.byref(kc), dptr(d3(g)), dptr(c))
+        return c[: self.nd]
+
+    def internal_forces(self, st, act):
+        tau = np.zeros(max(self.nd, 1))
+        cl = oracle().orc_internal_forces(C.byref(self.rs), C.byref(self._st(st)),
+                                          dptr(d3(act) if len(act) else np.zeros(1)), dptr(tau))
+        return tau[: self.nd], bool(cl)
+
+    def joint_limit_forces(self, st):
+        tau = np.zeros(max(self.nd, 1))
+        oracle().orc_joint_limit_forces(C.byref(self.rs), C.byref(self._st(st)), dptr(tau))
+        return tau[: self.nd]
+
+    def forward_dynamics(self, st, tau_int, tau_ext, g=(0.0, 0.0, 0.0)):
+        qdd = np.zeros(self.nd)
+        ok = oracle().orc_forward_dynamics(C.byref(self.rs), C.byref(self._st(st)), dptr(d3(tau_int)),
+                                           dptr(d3(tau_ext)), dptr(d3(g)), dptr(qdd))
+        if not ok:
+            raise ArithmeticError("mass matrix is not positive definite; check link inertias")
+        return qdd
+
+    def buoyancy_gravity_forces(self, st, rho, g, bladder_volume=None):
+        tau = np.zeros(max(self.nd, 1))
+        bv = self.bladder_volume if bladder_volume is None else bladder_volume
+        oracle().orc_buoyancy_gravity_forces(C.byref(self.rs), C.byref(self.kinematics(st)),
+                                             float(bv), float(rho), dptr(d3(g)), dptr(tau))
+        return tau[: self.nd]
+
+    def integrate(self, st, act, tau_ext, dt, substeps=1, g=(0.0, 0.0, 0.0)):
+        s = self._st(st)
+        a = d3(act) if len(act) else np.zeros(1)
+        fl = oracle().orc_integrate(C.byref(self.rs), C.byref(s), dptr(a), dptr(d3(tau_ext)),
+                                    float(dt), int(substeps), dptr(d3(g)))
+        self._back(s, st)
+        return fl
+
+    def robot_step(self, st, act, tau_ext, rho, g_hydro, dt, substeps=1, g=None):
+        s = self._st(st)
+        a = d3(act) if len(act) else np.zeros(1)
+        fl = oracle().orc_robot_step(C.byref(self.rs), C.byref(s), float(self.bladder_volume), dptr(a),
+                                     None if tau_ext is None else dptr(d3(tau_ext)), float(rho),
+                                     None if g_hydro is None else dptr(d3(g_hydro)), float(dt),
+                                     int(substeps), None if g is None else dptr(d3(g)))
+        self._back(s, st)
+        return fl
+
+    def mechanical_energy(self, st, g):
+        return oracle().orc_mechanical_energy(C.byref(self.rs), C.byref(self._st(st)), dptr(d3(g)))
+
+    def pose(self, st, rest_R, rest_p):
+        out = np.zeros(240)
+        oracle().orc_dyn_pose(C.byref(self.rs), C.byref(self._st(st)), dptr(d3(rest_R)), dptr(d3(rest_p)),
+                              out.ctypes.data_as(C.c_void_p))
+        return out
+
+
+def quat_exp(w):
+    q = np.zeros(4)
+    oracle().orc_quat_exp(dptr(d3(w)), dptr(q))
+    return q
+
+
+def quat_to_R(q):
+    R = np.zeros(9)
+    oracle().orc_quat_to_R(dptr(d3(q)), dptr(R))
+    return R.reshape(3, 3)

@@ -64,6 +64,34 @@ class fsg_body_pose(C.Structure):
                 ("v_origin_world", (C.c_double * 3) * _L), ("omega_world", (C.c_double * 3) * _L)]
 
 
+DYN_MAX_LINKS = 8
+DYN_MAX_DOFS = 6 + DYN_MAX_LINKS
+FSG_JOINT_FREE, FSG_JOINT_REVOLUTE, FSG_JOINT_FIXED = 0, 1, 2
+FSG_DYN_CLAMPED, FSG_DYN_NOT_SPD, FSG_DYN_NONFINITE = 1, 2, 4
+
+
+class fsg_link(C.Structure):
+    _fields_ = [("parent", C.c_int), ("joint", C.c_int), ("joint_origin", C.c_double * 3),
+                ("joint_rotation", C.c_double * 9), ("axis", C.c_double * 3), ("mass", C.c_double),
+                ("com", C.c_double * 3), ("inertia_com", C.c_double * 9), ("stiffness", C.c_double),
+                ("damping", C.c_double), ("q_rest", C.c_double), ("limit_lo", C.c_double),
+                ("limit_hi", C.c_double), ("torque_limit", C.c_double),
+                ("displaced_volume", C.c_double), ("volume_centroid", C.c_double * 3)]
+
+
+class fsg_robot(C.Structure):
+    _fields_ = [("n_links", C.c_int), ("links", fsg_link * DYN_MAX_LINKS),
+                ("bladder_volume", C.c_double), ("bladder_volume_min", C.c_double),
+                ("bladder_volume_max", C.c_double), ("bladder_rate_bound", C.c_double),
+                ("bladder_centroid", C.c_double * 3)]
+
+
+class fsg_joint_state(C.Structure):
+    _fields_ = [("base_pos", C.c_double * 3), ("base_quat", C.c_double * 4),
+                ("q", C.c_double * DYN_MAX_LINKS), ("v", C.c_double * DYN_MAX_DOFS),
+                ("qdd", C.c_double * DYN_MAX_DOFS)]
+
+
 _dp = C.POINTER(C.c_double)
 _ip = C.POINTER(C.c_int)
 _i64p = C.POINTER(C.c_int64)
@@ -111,6 +139,19 @@ SIGNATURES = {
     "fsg_drag_set_pose": (C.c_int, [_vp, C.c_int, _vp]),
     "fsg_drag_set_poses": (C.c_int, [_vp, _vp]),
     "fsg_drag_step": (C.c_int, [_vp, _dp, _dp]),
+    "fsg_dyn_last_error": (C.c_char_p, []),
+    "fsg_dyn_create": (C.c_int, [C.POINTER(fsg_robot), C.c_int, C.c_int, C.POINTER(_vp)]),
+    "fsg_dyn_destroy": (C.c_int, [_vp]),
+    "fsg_dyn_n_dofs": (C.c_int, [_vp]),
+    "fsg_dyn_n_joints": (C.c_int, [_vp]),
+    "fsg_dyn_set_state": (C.c_int, [_vp, _vp]),
+    "fsg_dyn_get_state": (C.c_int, [_vp, _vp]),
+    "fsg_dyn_change_bladder": (C.c_int, [_vp, _dp, _dp]),
+    "fsg_dyn_step": (C.c_int, [_vp, _dp, _dp, C.c_double, _dp, C.c_double, C.c_int, _dp, _ip]),
+    "fsg_dyn_step_device": (C.c_int, [_vp, _vp, _vp, C.c_double, _dp, C.c_double, C.c_int, _dp,
+                                      _vp]),
+    "fsg_dyn_mass_matrix": (C.c_int, [_vp, _dp, _dp, _dp]),
+    "fsg_dyn_poses": (C.c_int, [_vp, _dp, _dp, _vp]),
     "fsg_snapshot_begin": (C.c_int, [_vp]),
     "fsg_snapshot_wait": (C.c_int, [_vp, _dp, _dp]),
     "fsg_write_vtk": (C.c_int, [_vp, C.c_char_p, _dp]),
@@ -162,10 +203,12 @@ def lib() -> C.CDLL:
     return _lib
 
 
-def check(rc: int, drag: bool = False, io: bool = False) -> None:
+def check(rc: int, drag: bool = False, io: bool = False, dyn: bool = False) -> None:
     if rc != FSG_OK:
         L = lib()
         err = L.fsg_drag_last_error if drag else (L.fsg_io_last_error if io else L.fsg_last_error)
+        if dyn:
+            err = L.fsg_dyn_last_error
         msg = err().decode(errors="replace")
         if rc == FSG_EINPUT:
             raise InputError(rc, msg)

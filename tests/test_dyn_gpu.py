@@ -1,0 +1,195 @@
+"""Device robot dynamics (fsg_dyn_*, csrc/fsg_dyn.cu) against the fp64
+restatement (oracle/fsg_dyn_oracle.c, pinned by test_dyn_oracle.py).
+
+Tolerance: the device and the oracle run the same fp64 operations in the same
+order (no FMA contraction on either side) except sin/cos (CUDA's vs libm's,
+<= 2 ulp apart), so one step agrees to rel <= 1e-12 and a damped trajectory of
+hundreds of steps to rel <= 1e-9."""
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+from oracle import bind as B
+from paper_2206_01683_b200 import dynamics as D
+from paper_2206_01683_b200.scenes import koi_articulation, koi_body
+from dyn_cases import G, fin_tree, make_chain, skewed_chain
+
+pytestmark = pytest.mark.gpu
+
+
+def _koi():
+    body = koi_body(0.01)
+    return D.koi_robot(body, koi_articulation(body))
+
+
+def _robots():
+    return {"koi": _koi(), "skewed": skewed_chain(), "fins": fin_tree(),
+            "pendulum": make_chain(2, 0.4, 0.25, D.FIXED, False, 0.5, 0.01)}
+
+
+def _random_states(robot, E, seed):
+    rng = np.random.default_rng(seed)
+    out = []
+    for _ in range(E):
+        st = D.JointState.zero(robot)
+        st.base_pos = rng.uniform(-0.2, 0.2, 3)
+        st.base_quat = B.quat_exp(rng.uniform(-1.5, 1.5, 3)) if robot.floating_base else st.base_quat
+        st.q = rng.uniform(-0.6, 0.6, robot.n_joints)
+        st.v = rng.uniform(-1.0, 1.0, robot.n_dofs)
+        out.append(st)
+    return out
+
+
+def _copy(st):
+    return D.JointState(st.base_pos.copy(), st.base_quat.copy(), st.q.copy(), st.v.copy(), st.qdd.copy())
+
+
+def _state_vec(st):
+    return np.concatenate([st.base_pos, st.base_quat, st.q, st.v, st.qdd])
+
+
+def _rel(a, b):
+    return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300))
+
+
+@pytest.mark.parametrize("name", ["koi", "skewed", "fins", "pendulum"])
+def test_mass_matrix_and_bias_match_oracle(name):
+    robot = _robots()[name]
+    E = 37
+    rb = D.RobotBatch(robot, E)
+    sts = _random_states(robot, E, 1)
+    rb.set_states(sts)
+    M, c = rb.mass_matrix(G)
+    O = B.DynOracle(robot)
+    for e in range(E):
+        assert _rel(M[e], O.mass_matrix(sts[e])) <= 1e-12
+        assert _rel(c[e], O.bias_forces(sts[e], G)) <= 1e-12
+        # test_robot.cpp:180's symmetry bound (the CRBA sums are not exactly symmetric)
+        assert np.linalg.norm(M[e] - M[e].T) < 1e-10 * (1.0 + np.linalg.norm(M[e]))
+
+
+@pytest.mark.parametrize("name", ["koi", "skewed", "fins", "pendulum"])
+def test_one_robot_step_matches_oracle(name):
+    robot = _robots()[name]
+    E = 40
+    rng = np.random.default_rng(2)
+    rb = D.RobotBatch(robot, E)
+    sts = _random_states(robot, E, 3)
+    rb.set_states(sts)
+    act = rng.uniform(-0.5, 0.5, (E, robot.n_joints))
+    act[0, :] = 1e3  # clamped against torque_limit
+    tau = rng.uniform(-0.05, 0.05, (E, robot.n_dofs))
+    flags = rb.step(act, tau, 1000.0, G, 0.004, 4, None)
+    got = rb.states()
+    O = B.DynOracle(robot)
+    for e in range(E):
+        x = _copy(sts[e])
+        fl = O.robot_step(x, act[e], tau[e], 1000.0, G, 0.004, 4, None)
+        assert flags[e] == fl
+        assert _rel(_state_vec(got[e]), _state_vec(x)) <= 1e-12
+    if robot.n_joints:
+        assert flags[0] & D.FSG_DYN_CLAMPED
+
+
+def test_koi_trajectory_matches_oracle():
+    """300 steps of a gait-driven, buoyancy-trimmed koi with integrate's own
+    gravity (tests both gravity paths) and 4 substeps."""
+    robot = _koi()
+    E = 8
+    rb = D.RobotBatch(robot, E)
+    sts = _random_states(robot, E, 4)
+    for st in sts:
+        st.v *= 0.2
+    rb.set_states(sts)
+    O = B.DynOracle(robot)
+    ref = [_copy(s) for s in sts]
+    nj = robot.n_joints
+    for k in range(300):
+        t = k * 0.004
+        act = np.array([[0.25 * np.sin(2 * np.pi * 2.0 * t - 0.8 * j + e) for j in range(nj)]
+                        for e in range(E)])
+        flags = rb.step(act, None, 1000.0, G, 0.004, 4, 0.1 * G)
+        for e in range(E):
+            assert O.robot_step(ref[e], act[e], None, 1000.0, G, 0.004, 4, 0.1 * G) == flags[e]
+    got = rb.states()
+    for e in range(E):
+        assert _rel(_state_vec(got[e]), _state_vec(ref[e])) <= 1e-9
+
+
+def test_envs_are_independent():
+    """A batch of 64 equals each env stepped alone (bit-identical)."""
+    robot = skewed_chain()
+    E = 64
+    rng = np.random.default_rng(7)
+    sts = _random_states(robot, E, 8)
+    act = rng.uniform(-0.3, 0.3, (E, robot.n_joints))
+    rb = D.RobotBatch(robot, E)
+    rb.set_states(sts)
+    rb.step(act, None, 1000.0, G, 0.004, 2)
+    all_ = rb.states()
+    for e in (0, 17, 63):
+        one = D.RobotBatch(robot, 1)
+        one.set_states([sts[e]])
+        one.step(act[e:e + 1], None, 1000.0, G, 0.004, 2)
+        assert np.array_equal(_state_vec(one.states()[0]), _state_vec(all_[e]))
+
+
+def test_step_device_equals_host_call():
+    torch = pytest.importorskip("torch")
+    robot = _koi()
+    E = 16
+    rng = np.random.default_rng(9)
+    sts = _random_states(robot, E, 10)
+    act = rng.uniform(-0.3, 0.3, (E, robot.n_joints))
+    tau = rng.uniform(-0.02, 0.02, (E, robot.n_dofs))
+    a, b = D.RobotBatch(robot, E), D.RobotBatch(robot, E)
+    a.set_states(sts)
+    b.set_states(sts)
+    fa = a.step(act, tau, 1000.0, G, 0.004, 4)
+    ta = torch.tensor(act, dtype=torch.float64, device="cuda")
+    tt = torch.tensor(tau, dtype=torch.float64, device="cuda")
+    fl = torch.zeros(E, dtype=torch.int32, device="cuda")
+    torch.cuda.synchronize()
+    b.step_device(ta, tt, 1000.0, G, 0.004, 4, flags=fl)
+    sb = b.states()  # synchronises the handle's stream
+    for x, y in zip(a.states(), sb):
+        assert np.array_equal(_state_vec(x), _state_vec(y))
+    assert np.array_equal(fl.cpu().numpy(), fa)
+
+
+def test_nonfinite_state_is_flagged_not_raised():
+    robot = skewed_chain()
+    rb = D.RobotBatch(robot, 2)
+    sts = _random_states(robot, 2, 11)
+    sts[1].v[0] = np.nan
+    rb.set_states(sts)
+    flags = rb.step(np.zeros((2, robot.n_joints)), None, 1000.0, G, 0.004, 1)
+    assert not flags[0] & D.FSG_DYN_NONFINITE
+    assert flags[1] & D.FSG_DYN_NONFINITE
+
+
+def test_poses_match_oracle_and_feed_skinning():
+    robot = _koi()
+    E = 5
+    rb = D.RobotBatch(robot, E)
+    sts = _random_states(robot, E, 12)
+    rb.set_states(sts)
+    rR, rp = D.rest_pose(robot)
+    P = rb.poses(rR, rp)
+    O = B.DynOracle(robot)
+    for e in range(E):
+        ref = O.pose(sts[e], rR, rp)
+        assert _rel(P[e], ref) <= 1e-12
+
+
+def test_bladder_change_matches_host_mirror():
+    robot = _koi()
+    rb = D.RobotBatch(robot, 3)
+    b = [D.Bladder(**{k: getattr(robot.bladder, k) for k in
+                      ("volume", "volume_min", "volume_max", "rate_bound")}) for _ in range(3)]
+    for dv in ([5e-7, -2e-6, 1e-5], [1e-5, 1e-5, -1e-5]):
+        vol = rb.change_bladder(np.array(dv))
+        for e in range(3):
+            b[e].apply_change(dv[e])
+            assert vol[e] == b[e].volume
