@@ -23,6 +23,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -541,6 +542,360 @@ __global__ void __launch_bounds__(DYN_BLOCK)
   if (flags) flags[e] = fl;
 }
 
+// ---- warp-per-env step (latency path for small batches) -------------------
+// The same per-element arithmetic as dyn_env_step (so results are identical
+// bit for bit), with the independent work spread over the lanes of one warp:
+// per-link joint rotations, the 36 coefficients of each X^T I X product, the
+// mass-matrix columns (one lane per revolute link), the per-link RNEA forces,
+// and the rows of each Cholesky column.  The recursive chains (forward
+// kinematics, RNEA sweeps, triangular solves) stay on lane 0; everything
+// lives in shared memory.
+constexpr int DYN_WARPS = 4;
+
+struct WarpWS {
+  fsg_joint_state st;
+  double rr[NL][9];  // r_rel of each link (link -> parent)
+  double E[NL][9], r[NL][3], Rw[NL][9], pw[NL][3], vb[NL][6];
+  double ic[NL][36];
+  double X[36], T[36];
+  double H[ND * ND];
+  double a[NL][6], f[NL][6];
+  double te[ND], tsum[ND], cb[ND], rhs[ND], y[ND], qdd[ND];
+  double sig[NL];
+  int ok, fl;
+};
+
+__device__ void wk_fk(const DynConst& c, WarpWS& w, int lane) {
+  const fsg_joint_state& st = w.st;
+  if (lane == 0) {
+    quat_to_R(st.base_quat, w.Rw[0]);
+    for (int a = 0; a < 3; ++a)
+      for (int b = 0; b < 3; ++b) w.E[0][3 * a + b] = w.Rw[0][3 * b + a];
+    for (int a = 0; a < 3; ++a) w.pw[0][a] = st.base_pos[a], w.r[0][a] = st.base_pos[a];
+    for (int a = 0; a < 6; ++a) w.vb[0][a] = c.floating ? st.v[a] : 0.0;
+  } else if (lane < c.n_links) {
+    const int i = lane;
+    double rj[9] = {1, 0, 0, 0, 1, 0, 0, 0, 1};
+    if (c.joint[i] == FSG_JOINT_REVOLUTE) angle_axis_R(st.q[c.jidx[i]], c.axis[i], rj);
+    mm3(c.jrot[i], rj, w.rr[i]);
+    for (int a = 0; a < 3; ++a)
+      for (int b = 0; b < 3; ++b) w.E[i][3 * a + b] = w.rr[i][3 * b + a];
+    for (int a = 0; a < 3; ++a) w.r[i][a] = c.jorig[i][a];
+  }
+  __syncwarp();
+  if (lane == 0) {
+    for (int i = 1; i < c.n_links; ++i) {
+      const int pa = c.parent[i];
+      double t[3];
+      mm3(w.Rw[pa], w.rr[i], w.Rw[i]);
+      mv3(w.Rw[pa], c.jorig[i], t);
+      for (int a = 0; a < 3; ++a) w.pw[i][a] = w.pw[pa][a] + t[a];
+      apply_motion(w.E[i], w.r[i], w.vb[pa], w.vb[i]);
+      if (c.joint[i] == FSG_JOINT_REVOLUTE) {
+        const double qd = st.v[c.dof[i]];
+        for (int a = 0; a < 3; ++a) w.vb[i][a] = w.vb[i][a] + c.axis[i][a] * qd;
+      }
+    }
+  }
+  __syncwarp();
+}
+
+__device__ void wk_crba(const DynConst& c, WarpWS& w, int lane) {
+  const int nb = c.n_links, nd = c.nd;
+  for (int e = lane; e < nb * 36; e += 32) w.ic[e / 36][e % 36] = c.I6[e / 36][e % 36];
+  __syncwarp();
+  for (int i = nb - 1; i >= 1; --i) {
+    for (int e = lane; e < 36; e += 32) {  // X = [E 0; -E S(r) E]
+      const int a = e / 6, b = e % 6;
+      double x;
+      if (a < 3) {
+        x = b < 3 ? w.E[i][3 * a + b] : 0.0;
+      } else if (b >= 3) {
+        x = w.E[i][3 * (a - 3) + (b - 3)];
+      } else {
+        const double* r = w.r[i];
+        const double S[9] = {0.0, -r[2], r[1], r[2], 0.0, -r[0], -r[1], r[0], 0.0};
+        const double* A = w.E[i] + 3 * (a - 3);
+        x = -(A[0] * S[b] + A[1] * S[3 + b] + A[2] * S[6 + b]);
+      }
+      w.X[e] = x;
+    }
+    __syncwarp();
+    for (int e = lane; e < 36; e += 32) {
+      const int a = e / 6, b = e % 6;
+      double s = 0.0;
+#pragma unroll
+      for (int q = 0; q < 6; ++q) s += w.X[6 * q + a] * w.ic[i][6 * q + b];
+      w.T[e] = s;
+    }
+    __syncwarp();
+    double* P = w.ic[c.parent[i]];
+    for (int e = lane; e < 36; e += 32) {
+      const int a = e / 6, b = e % 6;
+      double s = 0.0;
+#pragma unroll
+      for (int q = 0; q < 6; ++q) s += w.T[6 * a + q] * w.X[6 * q + b];
+      P[e] = P[e] + s;
+    }
+    __syncwarp();
+  }
+  for (int e = lane; e < nd * nd; e += 32) w.H[e] = 0.0;
+  __syncwarp();
+  if (c.floating)
+    for (int e = lane; e < 36; e += 32) w.H[nd * (e / 6) + e % 6] = w.ic[0][e];
+  const int i = lane;
+  if (i >= 1 && i < nb && c.joint[i] == FSG_JOINT_REVOLUTE) {  // column of link i
+    const int di = c.dof[i];
+    const double s[6] = {c.axis[i][0], c.axis[i][1], c.axis[i][2], 0.0, 0.0, 0.0};
+    double f[6];
+    mv6(w.ic[i], s, f);
+    double d = 0.0;
+#pragma unroll
+    for (int q = 0; q < 6; ++q) d += s[q] * f[q];
+    w.H[nd * di + di] = d;
+    int j = i;
+    while (c.parent[j] >= 0) {
+      transpose_force(w.E[j], w.r[j], f, f);
+      j = c.parent[j];
+      if (j == 0) {
+        if (c.floating)
+          for (int q = 0; q < 6; ++q) w.H[nd * q + di] = w.H[nd * di + q] = f[q];
+      } else if (c.joint[j] == FSG_JOINT_REVOLUTE) {
+        const double sj[6] = {c.axis[j][0], c.axis[j][1], c.axis[j][2], 0.0, 0.0, 0.0};
+        double dd = 0.0;
+#pragma unroll
+        for (int q = 0; q < 6; ++q) dd += sj[q] * f[q];
+        const int dj = c.dof[j];
+        w.H[nd * dj + di] = dd;
+        w.H[nd * di + dj] = dd;
+      }
+    }
+  }
+  __syncwarp();
+}
+
+__device__ void wk_rnea(const DynConst& c, WarpWS& w, int lane, const double* g) {
+  const int nb = c.n_links;
+  if (lane == 0) {
+    double rtg[3];
+    mtv3(w.Rw[0], g, rtg);
+    w.a[0][0] = w.a[0][1] = w.a[0][2] = 0.0;
+    w.a[0][3] = -rtg[0], w.a[0][4] = -rtg[1], w.a[0][5] = -rtg[2];
+    for (int i = 1; i < nb; ++i) {
+      apply_motion(w.E[i], w.r[i], w.a[c.parent[i]], w.a[i]);
+      if (c.joint[i] == FSG_JOINT_REVOLUTE) {
+        const double qd = w.st.v[c.dof[i]];
+        const double m[6] = {c.axis[i][0] * qd, c.axis[i][1] * qd, c.axis[i][2] * qd, 0.0, 0.0, 0.0};
+        const double* v = w.vb[i];
+        double x0[3], x1[3], x2[3];
+        cross3(v, m, x0);
+        cross3(v, m + 3, x1);
+        cross3(v + 3, m, x2);
+        for (int q = 0; q < 3; ++q) w.a[i][q] = w.a[i][q] + x0[q];
+        for (int q = 0; q < 3; ++q) w.a[i][3 + q] = w.a[i][3 + q] + (x1[q] + x2[q]);
+      }
+    }
+  }
+  __syncwarp();
+  if (lane < nb) {
+    const int i = lane;
+    double ia[6], iv[6], x0[3], x1[3], x2[3];
+    mv6(c.I6[i], w.a[i], ia);
+    mv6(c.I6[i], w.vb[i], iv);
+    const double* v = w.vb[i];
+    cross3(v, iv, x0);
+    cross3(v + 3, iv + 3, x1);
+    cross3(v, iv + 3, x2);
+    for (int q = 0; q < 3; ++q) w.f[i][q] = ia[q] + (x0[q] + x1[q]), w.f[i][3 + q] = ia[3 + q] + x2[q];
+  }
+  __syncwarp();
+  if (lane == 0) {
+    for (int q = 0; q < c.nd; ++q) w.cb[q] = 0.0;
+    for (int i = nb - 1; i >= 0; --i) {
+      if (i == 0) {
+        if (c.floating)
+          for (int q = 0; q < 6; ++q) w.cb[q] = w.f[0][q];
+        continue;
+      }
+      if (c.joint[i] == FSG_JOINT_REVOLUTE) {
+        double d = 0.0;
+        for (int q = 0; q < 3; ++q) d += c.axis[i][q] * w.f[i][q];
+        for (int q = 3; q < 6; ++q) d += 0.0 * w.f[i][q];
+        w.cb[c.dof[i]] = d;
+      }
+      double t[6];
+      transpose_force(w.E[i], w.r[i], w.f[i], t);
+      double* P = w.f[c.parent[i]];
+      for (int q = 0; q < 6; ++q) P[q] = P[q] + t[q];
+    }
+  }
+  __syncwarp();
+}
+
+// Cholesky in place (as dk_llt_solve) with the rows of each column on lanes
+__device__ bool wk_llt_solve(WarpWS& w, int lane, int n) {
+  double* M = w.H;
+  for (int j = 0; j < n; ++j) {
+    if (lane == 0) {
+      double d = M[n * j + j];
+      for (int q = 0; q < j; ++q) d -= M[n * j + q] * M[n * j + q];
+      w.ok = d > 0.0;
+      if (w.ok) M[n * j + j] = sqrt(d);
+    }
+    __syncwarp();
+    if (!w.ok) return false;
+    const double ljj = M[n * j + j];
+    const int i = j + 1 + lane;
+    if (i < n) {
+      double s = M[n * i + j];
+      for (int q = 0; q < j; ++q) s -= M[n * i + q] * M[n * j + q];
+      M[n * i + j] = s / ljj;
+    }
+    __syncwarp();
+  }
+  if (lane == 0) {
+    for (int i = 0; i < n; ++i) {
+      double s = w.rhs[i];
+      for (int q = 0; q < i; ++q) s -= M[n * i + q] * w.y[q];
+      w.y[i] = s / M[n * i + i];
+    }
+    for (int i = n - 1; i >= 0; --i) {
+      double s = w.y[i];
+      for (int q = i + 1; q < n; ++q) s -= M[n * q + i] * w.qdd[q];
+      w.qdd[i] = s / M[n * i + i];
+    }
+  }
+  __syncwarp();
+  return true;
+}
+
+__global__ void __launch_bounds__(32 * DYN_WARPS)
+    k_dyn_step_warp(const DynConst* __restrict__ gc, fsg_joint_state* __restrict__ states,
+                    const double* __restrict__ bladder, const double* __restrict__ act,
+                    const double* __restrict__ tau_ext, double rho, int hydro, double3 gh,
+                    double dt, int substeps, double3 gv, int* __restrict__ flags, int E) {
+  __shared__ DynConst c;
+  __shared__ WarpWS ws[DYN_WARPS];
+  load_const(c, gc);
+  const int lane = threadIdx.x & 31, wi = threadIdx.x >> 5;
+  const int e = blockIdx.x * DYN_WARPS + wi;
+  if (e >= E) return;
+  WarpWS& w = ws[wi];
+  const int nd = c.nd, nj = c.nj;
+  {
+    const double* src = reinterpret_cast<const double*>(states + e);
+    double* dst = reinterpret_cast<double*>(&w.st);
+    for (int q = lane; q < (int)(sizeof(fsg_joint_state) / 8); q += 32) dst[q] = src[q];
+  }
+  for (int q = lane; q < nd; q += 32) w.te[q] = tau_ext ? tau_ext[(size_t)e * nd + q] : 0.0;
+  for (int q = lane; q < nj; q += 32) w.sig[q] = act[(size_t)e * nj + q];
+  if (lane == 0) w.fl = 0;
+  __syncwarp();
+  if (hydro) {
+    wk_fk(c, w, lane);
+    // buoyancy_gravity_forces on the pre-step kinematics (serial order, lane 0;
+    // dk_hydro reads a KinematicsCache, assembled from the warp's arrays)
+    if (lane == 0) {
+      KC k;
+      for (int i = 0; i < c.n_links; ++i) {
+        for (int q = 0; q < 9; ++q) k.E[i][q] = w.E[i][q], k.Rw[i][q] = w.Rw[i][q];
+        for (int q = 0; q < 3; ++q) k.r[i][q] = w.r[i][q], k.pw[i][q] = w.pw[i][q];
+        for (int q = 0; q < 6; ++q) k.vb[i][q] = w.vb[i][q];
+      }
+      const double g[3] = {gh.x, gh.y, gh.z};
+      dk_hydro(c, k, bladder[e], rho, g, w.te);
+    }
+    __syncwarp();
+  }
+  const double g[3] = {gv.x, gv.y, gv.z};
+  const double h = dt / substeps;
+  for (int s = 0; s < substeps; ++s) {
+    // internal_forces + joint_limit_forces, one lane per link
+    for (int q = lane; q < nd; q += 32) w.tsum[q] = 0.0 + 0.0;
+    __syncwarp();
+    bool clamped = false;
+    if (lane >= 1 && lane < c.n_links && c.joint[lane] == FSG_JOINT_REVOLUTE) {
+      const int i = lane, di = c.dof[i], ji = c.jidx[i];
+      double sigma = w.sig[ji];
+      if (fabs(sigma) > c.tlim[i]) {
+        sigma = fmin(fmax(sigma, -c.tlim[i]), c.tlim[i]);
+        clamped = true;
+      }
+      const double qi = w.st.q[ji], vi = w.st.v[di];
+      const double ti = sigma - c.stiff[i] * (qi - c.q_rest[i]) - c.damp[i] * vi;
+      double tl = 0.0;
+      if (qi > c.lim_hi[i])
+        tl = -50.0 * (qi - c.lim_hi[i]) - 0.5 * fmax(vi, 0.0);
+      else if (qi < c.lim_lo[i])
+        tl = -50.0 * (qi - c.lim_lo[i]) - 0.5 * fmin(vi, 0.0);
+      w.tsum[di] = ti + tl;
+    }
+    if (__any_sync(0xffffffffu, clamped) && lane == 0) w.fl |= FSG_DYN_CLAMPED;
+    wk_fk(c, w, lane);
+    wk_crba(c, w, lane);
+    wk_rnea(c, w, lane, g);
+    for (int q = lane; q < nd; q += 32) w.rhs[q] = (w.tsum[q] + w.te[q]) - w.cb[q];
+    __syncwarp();
+    if (!wk_llt_solve(w, lane, nd)) {
+      if (lane == 0) w.fl |= FSG_DYN_NOT_SPD;
+      break;
+    }
+    if (lane == 0) {
+      fsg_joint_state& st = w.st;
+      for (int q = 0; q < nd; ++q) st.qdd[q] = w.qdd[q], st.v[q] = st.v[q] + h * w.qdd[q];
+      if (c.floating) {
+        double R[9], t[3], wv[3], dq[4], qn[4];
+        quat_to_R(st.base_quat, R);
+        mv3(R, st.v + 3, t);
+        for (int q = 0; q < 3; ++q) st.base_pos[q] = st.base_pos[q] + h * t[q], wv[q] = st.v[q] * h;
+        const double angle = sqrt(dot3(wv, wv));
+        if (angle < 1e-12) {
+          dq[0] = 1.0, dq[1] = 0.5 * wv[0], dq[2] = 0.5 * wv[1], dq[3] = 0.5 * wv[2];
+          quat_normalize(dq);
+        } else {
+          const double ax[3] = {wv[0] / angle, wv[1] / angle, wv[2] / angle};
+          double sh, ch;
+          sincos(0.5 * angle, &sh, &ch);
+          dq[0] = ch, dq[1] = sh * ax[0], dq[2] = sh * ax[1], dq[3] = sh * ax[2];
+        }
+        const double* a = st.base_quat;
+        qn[0] = a[0] * dq[0] - a[1] * dq[1] - a[2] * dq[2] - a[3] * dq[3];
+        qn[1] = a[0] * dq[1] + a[1] * dq[0] + a[2] * dq[3] - a[3] * dq[2];
+        qn[2] = a[0] * dq[2] + a[2] * dq[0] + a[3] * dq[1] - a[1] * dq[3];
+        qn[3] = a[0] * dq[3] + a[3] * dq[0] + a[1] * dq[2] - a[2] * dq[1];
+        quat_normalize(qn);
+        for (int q = 0; q < 4; ++q) st.base_quat[q] = qn[q];
+      }
+      for (int i = 1; i < c.n_links; ++i) {
+        if (c.joint[i] != FSG_JOINT_REVOLUTE) continue;
+        const int di = c.dof[i], ji = c.jidx[i];
+        st.q[ji] = st.q[ji] + h * st.v[di];
+        if (st.q[ji] > c.lim_hi[i]) {
+          st.q[ji] = c.lim_hi[i];
+          st.v[di] = fmin(st.v[di], 0.0);
+        } else if (st.q[ji] < c.lim_lo[i]) {
+          st.q[ji] = c.lim_lo[i];
+          st.v[di] = fmax(st.v[di], 0.0);
+        }
+      }
+    }
+    __syncwarp();
+  }
+  if (lane == 0) {
+    bool finite = true;
+    for (int q = 0; q < nd; ++q) finite &= isfinite(w.st.v[q]);
+    for (int q = 0; q < 3; ++q) finite &= isfinite(w.st.base_pos[q]);
+    if (!finite) w.fl |= FSG_DYN_NONFINITE;
+    if (flags) flags[e] = w.fl;
+  }
+  __syncwarp();
+  {
+    const double* src = reinterpret_cast<const double*>(&w.st);
+    double* dst = reinterpret_cast<double*>(states + e);
+    for (int q = lane; q < (int)(sizeof(fsg_joint_state) / 8); q += 32) dst[q] = src[q];
+  }
+}
+
 __global__ void __launch_bounds__(DYN_BLOCK)
     k_dyn_mass(const DynConst* __restrict__ gc, const fsg_joint_state* __restrict__ states,
                double3 gv, double* __restrict__ M, double* __restrict__ bias, int E) {
@@ -710,6 +1065,9 @@ struct fsg_dyn {
   int* d_flags = nullptr;
   double* d_M = nullptr;
   fsg_body_pose* d_pose = nullptr;
+  // warp per env (latency) below FSG_DYN_WARP_MAX envs, else thread per env
+  // (throughput); both compute the same arithmetic, bit for bit
+  bool warp_kernel = true;
 };
 
 namespace {
@@ -744,6 +1102,11 @@ int fsg_dyn_create(const fsg_robot* robot, int n_envs, int device, fsg_dyn** out
   d->E = n_envs;
   d->robot = *robot;
   make_const(*robot, d->hc);
+  {
+    const char* env = std::getenv("FSG_DYN_WARP_MAX");
+    const long wmax = env ? std::atol(env) : 2048;
+    d->warp_kernel = n_envs <= wmax;
+  }
   auto cleanup = [&](int r) {
     fsg_dyn_destroy(d);
     return r;
@@ -840,10 +1203,15 @@ int fsg_dyn_step_device(fsg_dyn* d, const double* d_actuation, const double* d_t
   DevGuard g(d->dev);
   const double3 gh = g_hydro ? make_double3(g_hydro[0], g_hydro[1], g_hydro[2]) : make_double3(0, 0, 0);
   const double3 gv = gravity ? make_double3(gravity[0], gravity[1], gravity[2]) : make_double3(0, 0, 0);
-  k_dyn_step<<<blocks(d->E), DYN_BLOCK, 0, d->s>>>(d->d_c, d->d_state, d->d_bladder,
-                                                   d_actuation ? d_actuation : d->d_act, d_tau_ext,
-                                                   rho_fluid, g_hydro ? 1 : 0, gh, dt, substeps, gv,
-                                                   d_flags, d->E);
+  const double* act = d_actuation ? d_actuation : d->d_act;
+  if (d->warp_kernel)
+    k_dyn_step_warp<<<(unsigned)((d->E + DYN_WARPS - 1) / DYN_WARPS), 32 * DYN_WARPS, 0, d->s>>>(
+        d->d_c, d->d_state, d->d_bladder, act, d_tau_ext, rho_fluid, g_hydro ? 1 : 0, gh, dt,
+        substeps, gv, d_flags, d->E);
+  else
+    k_dyn_step<<<blocks(d->E), DYN_BLOCK, 0, d->s>>>(d->d_c, d->d_state, d->d_bladder, act,
+                                                     d_tau_ext, rho_fluid, g_hydro ? 1 : 0, gh, dt,
+                                                     substeps, gv, d_flags, d->E);
   CK(cudaGetLastError());
   return FSG_OK;
 }

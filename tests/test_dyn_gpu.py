@@ -193,3 +193,26 @@ def test_bladder_change_matches_host_mirror():
         for e in range(3):
             b[e].apply_change(dv[e])
             assert vol[e] == b[e].volume
+
+
+@pytest.mark.parametrize("name", ["koi", "fins"])
+def test_warp_and_thread_kernels_are_bit_identical(name, monkeypatch):
+    """The warp-per-env kernel (small batches) and the thread-per-env kernel
+    (large batches) run the same arithmetic: identical states and flags."""
+    robot = _robots()[name]
+    E = 24
+    rng = np.random.default_rng(13)
+    sts = _random_states(robot, E, 14)
+    act = rng.uniform(-0.5, 0.5, (E, robot.n_joints))
+    act[3, :] = 50.0
+    tau = rng.uniform(-0.05, 0.05, (E, robot.n_dofs))
+    out = []
+    for wmax in ("4096", "0"):
+        monkeypatch.setenv("FSG_DYN_WARP_MAX", wmax)
+        rb = D.RobotBatch(robot, E)
+        rb.set_states(sts)
+        fl = [rb.step(act, tau, 1000.0, G, 0.004, 4, 0.3 * G) for _ in range(20)]
+        out.append((np.stack([_state_vec(s) for s in rb.states()]), np.stack(fl)))
+    # (the light fins blow up under this drive: NaNs must match too)
+    assert np.array_equal(out[0][0], out[1][0], equal_nan=True)
+    assert np.array_equal(out[0][1], out[1][1])
