@@ -331,6 +331,8 @@ int fsg_dyn_mass_matrix(fsg_dyn* d, const double* gravity, double* M, double* bi
 /* the current state's pose of every env for fsg_set_pose / fsg_drag_set_poses
  * (rest_R [n_links*9], rest_p [n_links*3]: BoneTransforms rest pose) */
 int fsg_dyn_poses(fsg_dyn* d, const double* rest_R, const double* rest_p, fsg_body_pose* poses);
+/* the rest pose (RestPose::of) the device-side poses of fsg_batch_step_dynamic use */
+int fsg_dyn_set_rest(fsg_dyn* d, const double* rest_R, const double* rest_p);
 
 /* ---- output formats -----------------------------------
  * fsg_snapshot_begin enqueues the bare moments of the state the last step
@@ -380,6 +382,19 @@ int fsg_batch_step(fsg_batch* b, fsg_status* statuses /* n_envs, nullable */);
  * rollout loop's per-step exchange in one call. */
 int fsg_batch_step_skinned(fsg_batch* b, const fsg_frame_state* frames, const fsg_body_pose* poses,
                            fsg_status* statuses, double* tau_ext, double* stats);
+/* The whole CoupledSession::step (session.hpp:87-176) for every env, on the
+ * device: env e's skinned body is robot e of the dyn handle (n_envs equal;
+ * fsg_dyn_set_rest called).  Its pose comes from the robot state (forward
+ * kinematics + BoneTransforms, no host round trip), the coupled fluid step
+ * runs, and its tau_ext feeds the robot step (buoyancy_gravity_forces +
+ * integrate, session.hpp:169-175) in the same stream.  Up: frames (NULL:
+ * keep) and actuation [n_envs * n_joints]; down: statuses, robot flags and
+ * the post-step robot states (each nullable; states feed the caller's
+ * FrameFollower). */
+int fsg_batch_step_dynamic(fsg_batch* b, fsg_dyn* d, const fsg_frame_state* frames,
+                           const double* actuation, double rho_fluid, const double* g_hydro,
+                           double dt, int substeps, fsg_status* statuses, int* flags,
+                           fsg_joint_state* states);
 
 /* ---- z-slab halo exchange ------------------------------
  * A slab session (cfg.z_offset / cfg.nz_global) owns planes [z_offset,

@@ -152,6 +152,7 @@ SIGNATURES = {
                                       _vp]),
     "fsg_dyn_mass_matrix": (C.c_int, [_vp, _dp, _dp, _dp]),
     "fsg_dyn_poses": (C.c_int, [_vp, _dp, _dp, _vp]),
+    "fsg_dyn_set_rest": (C.c_int, [_vp, _dp, _dp]),
     "fsg_snapshot_begin": (C.c_int, [_vp]),
     "fsg_snapshot_wait": (C.c_int, [_vp, _dp, _dp]),
     "fsg_write_vtk": (C.c_int, [_vp, C.c_char_p, _dp]),
@@ -175,6 +176,8 @@ SIGNATURES = {
     "fsg_batch_step_async": (C.c_int, [_vp]),
     "fsg_batch_step": (C.c_int, [_vp, C.POINTER(fsg_status)]),
     "fsg_batch_step_skinned": (C.c_int, [_vp, _vp, _vp, _vp, _vp, _vp]),
+    "fsg_batch_step_dynamic": (C.c_int, [_vp, _vp, _vp, _dp, C.c_double, _dp, C.c_double, C.c_int,
+                                         _vp, _vp, _vp]),
     "fsg_halo_bytes": (C.c_size_t, [_vp]),
     "fsg_halo_pack": (C.c_int, [_vp, _vp, _vp]),
     "fsg_halo_unpack": (C.c_int, [_vp, _vp, _vp]),

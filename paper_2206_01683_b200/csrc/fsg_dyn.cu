@@ -30,6 +30,7 @@
 #include <cuda_runtime.h>
 
 #include "../../include/fsg.h"
+#include "fsg_dyn_internal.h"
 
 namespace {
 
@@ -528,15 +529,16 @@ __global__ void __launch_bounds__(DYN_BLOCK)
     k_dyn_step(const DynConst* __restrict__ gc, fsg_joint_state* __restrict__ states,
                const double* __restrict__ bladder, const double* __restrict__ act,
                const double* __restrict__ tau_ext, double rho, int hydro, double3 gh, double dt,
-               int substeps, double3 gv, int* __restrict__ flags, int E) {
+               int substeps, double3 gv, int* __restrict__ flags, int E,
+               const double* const* __restrict__ tau_ptrs) {
   __shared__ DynConst c;
   load_const(c, gc);
   const int e = blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= E) return;
   fsg_joint_state st = states[e];
   const double ghv[3] = {gh.x, gh.y, gh.z}, gvv[3] = {gv.x, gv.y, gv.z};
-  const int fl = dyn_env_step(c, st, bladder[e], act + (size_t)e * c.nj,
-                              tau_ext ? tau_ext + (size_t)e * c.nd : nullptr, rho, hydro, ghv, dt,
+  const double* te = tau_ptrs ? tau_ptrs[e] : (tau_ext ? tau_ext + (size_t)e * c.nd : nullptr);
+  const int fl = dyn_env_step(c, st, bladder[e], act + (size_t)e * c.nj, te, rho, hydro, ghv, dt,
                               substeps, gvv);
   states[e] = st;
   if (flags) flags[e] = fl;
@@ -773,7 +775,8 @@ __global__ void __launch_bounds__(32 * DYN_WARPS)
     k_dyn_step_warp(const DynConst* __restrict__ gc, fsg_joint_state* __restrict__ states,
                     const double* __restrict__ bladder, const double* __restrict__ act,
                     const double* __restrict__ tau_ext, double rho, int hydro, double3 gh,
-                    double dt, int substeps, double3 gv, int* __restrict__ flags, int E) {
+                    double dt, int substeps, double3 gv, int* __restrict__ flags, int E,
+                    const double* const* __restrict__ tau_ptrs) {
   __shared__ DynConst c;
   __shared__ WarpWS ws[DYN_WARPS];
   load_const(c, gc);
@@ -787,7 +790,10 @@ __global__ void __launch_bounds__(32 * DYN_WARPS)
     double* dst = reinterpret_cast<double*>(&w.st);
     for (int q = lane; q < (int)(sizeof(fsg_joint_state) / 8); q += 32) dst[q] = src[q];
   }
-  for (int q = lane; q < nd; q += 32) w.te[q] = tau_ext ? tau_ext[(size_t)e * nd + q] : 0.0;
+  {
+    const double* te = tau_ptrs ? tau_ptrs[e] : (tau_ext ? tau_ext + (size_t)e * nd : nullptr);
+    for (int q = lane; q < nd; q += 32) w.te[q] = te ? te[q] : 0.0;
+  }
   for (int q = lane; q < nj; q += 32) w.sig[q] = act[(size_t)e * nj + q];
   if (lane == 0) w.fl = 0;
   __syncwarp();
@@ -921,7 +927,7 @@ __global__ void __launch_bounds__(DYN_BLOCK)
 __global__ void __launch_bounds__(DYN_BLOCK)
     k_dyn_pose(const DynConst* __restrict__ gc, const fsg_joint_state* __restrict__ states,
                const double* __restrict__ restR, const double* __restrict__ restp,
-               fsg_body_pose* __restrict__ poses, int E) {
+               char* __restrict__ poses, size_t stride, int E) {
   __shared__ DynConst c;
   load_const(c, gc);
   const int e = blockIdx.x * blockDim.x + threadIdx.x;
@@ -929,7 +935,7 @@ __global__ void __launch_bounds__(DYN_BLOCK)
   const fsg_joint_state st = states[e];
   KC k;
   dk_fk(c, st, k);
-  fsg_body_pose& P = poses[e];
+  fsg_body_pose& P = *reinterpret_cast<fsg_body_pose*>(poses + (size_t)e * stride);
   for (int b = 0; b < NL; ++b) {
     if (b >= c.n_links) {
       for (int q = 0; q < 9; ++q) P.bone_R[b][q] = 0.0, P.R_world[b][q] = 0.0;
@@ -1068,7 +1074,10 @@ struct fsg_dyn {
   // warp per env (latency) below FSG_DYN_WARP_MAX envs, else thread per env
   // (throughput); both compute the same arithmetic, bit for bit
   bool warp_kernel = true;
+  bool rest_set = false;
 };
+
+
 
 namespace {
 struct DevGuard {
@@ -1081,6 +1090,64 @@ struct DevGuard {
 };
 unsigned blocks(int E) { return (unsigned)((E + DYN_BLOCK - 1) / DYN_BLOCK); }
 }  // namespace
+
+// internal entry points for the batched coupled loop (fsg_session.cu)
+namespace fsg {
+int dyn_launch_step(fsg_dyn* d, const double* d_actuation, const double* d_tau_ext,
+                    const double* const* d_tau_ptrs, double rho_fluid, const double* g_hydro,
+                    double dt, int substeps, const double* gravity, int* d_flags, cudaStream_t s) {
+  if (!d) return fail(FSG_EINPUT, "NULL handle");
+  if (!d_actuation && d->hc.nj > 0) return fail(FSG_EINPUT, "actuation is NULL");
+  if (substeps < 1) return fail(FSG_EINPUT, "substeps must be >= 1");
+  if (!(dt > 0.0)) return fail(FSG_EINPUT, "dt must be positive");
+  DevGuard g(d->dev);
+  if (!s) s = d->s;
+  const double3 gh = g_hydro ? make_double3(g_hydro[0], g_hydro[1], g_hydro[2]) : make_double3(0, 0, 0);
+  const double3 gv = gravity ? make_double3(gravity[0], gravity[1], gravity[2]) : make_double3(0, 0, 0);
+  const double* act = d_actuation ? d_actuation : d->d_act;
+  if (d->warp_kernel)
+    k_dyn_step_warp<<<(unsigned)((d->E + DYN_WARPS - 1) / DYN_WARPS), 32 * DYN_WARPS, 0, s>>>(
+        d->d_c, d->d_state, d->d_bladder, act, d_tau_ext, rho_fluid, g_hydro ? 1 : 0, gh, dt,
+        substeps, gv, d_flags, d->E, d_tau_ptrs);
+  else
+    k_dyn_step<<<blocks(d->E), DYN_BLOCK, 0, s>>>(d->d_c, d->d_state, d->d_bladder, act, d_tau_ext,
+                                                  rho_fluid, g_hydro ? 1 : 0, gh, dt, substeps, gv,
+                                                  d_flags, d->E, d_tau_ptrs);
+  CK(cudaGetLastError());
+  return FSG_OK;
+}
+
+int dyn_launch_pose(fsg_dyn* d, void* dst, size_t stride, cudaStream_t s) {
+  if (!d->rest_set) return fail(FSG_ESTATE, "fsg_dyn_set_rest has not been called");
+  DevGuard g(d->dev);
+  k_dyn_pose<<<blocks(d->E), DYN_BLOCK, 0, s>>>(d->d_c, d->d_state, d->d_rest, d->d_rest + 9 * NL,
+                                                static_cast<char*>(dst), stride, d->E);
+  CK(cudaGetLastError());
+  return FSG_OK;
+}
+
+int dyn_upload_actuation(fsg_dyn* d, const double* act, cudaStream_t s, double** d_act) {
+  DevGuard g(d->dev);
+  CK(cudaStreamSynchronize(d->s));  // earlier fsg_dyn_* work on the handle's own stream
+  if (d->hc.nj > 0)
+    CK(cudaMemcpyAsync(d->d_act, act, sizeof(double) * d->E * d->hc.nj, cudaMemcpyHostToDevice, s));
+  *d_act = d->d_act;
+  return FSG_OK;
+}
+
+int dyn_read_states(fsg_dyn* d, fsg_joint_state* out, int* flags, cudaStream_t s) {
+  DevGuard g(d->dev);
+  if (out)
+    CK(cudaMemcpyAsync(out, d->d_state, sizeof(fsg_joint_state) * d->E, cudaMemcpyDeviceToHost, s));
+  if (flags) CK(cudaMemcpyAsync(flags, d->d_flags, sizeof(int) * d->E, cudaMemcpyDeviceToHost, s));
+  return FSG_OK;
+}
+
+int* dyn_flags(fsg_dyn* d) { return d->d_flags; }
+int dyn_n_envs(const fsg_dyn* d) { return d->E; }
+int dyn_n_links(const fsg_dyn* d) { return d->hc.n_links; }
+int dyn_device(const fsg_dyn* d) { return d->dev; }
+}  // namespace fsg
 
 extern "C" {
 
@@ -1196,23 +1263,18 @@ int fsg_dyn_change_bladder(fsg_dyn* d, const double* dv, double* volumes) {
 int fsg_dyn_step_device(fsg_dyn* d, const double* d_actuation, const double* d_tau_ext,
                         double rho_fluid, const double* g_hydro, double dt, int substeps,
                         const double* gravity, int* d_flags) {
-  if (!d) return fail(FSG_EINPUT, "NULL handle");
-  if (!d_actuation && d->hc.nj > 0) return fail(FSG_EINPUT, "actuation is NULL");
-  if (substeps < 1) return fail(FSG_EINPUT, "substeps must be >= 1");
-  if (!(dt > 0.0)) return fail(FSG_EINPUT, "dt must be positive");
+  return fsg::dyn_launch_step(d, d_actuation, d_tau_ext, nullptr, rho_fluid, g_hydro, dt, substeps,
+                              gravity, d_flags, nullptr);
+}
+
+int fsg_dyn_set_rest(fsg_dyn* d, const double* rest_R, const double* rest_p) {
+  if (!d || !rest_R || !rest_p) return fail(FSG_EINPUT, "NULL argument");
   DevGuard g(d->dev);
-  const double3 gh = g_hydro ? make_double3(g_hydro[0], g_hydro[1], g_hydro[2]) : make_double3(0, 0, 0);
-  const double3 gv = gravity ? make_double3(gravity[0], gravity[1], gravity[2]) : make_double3(0, 0, 0);
-  const double* act = d_actuation ? d_actuation : d->d_act;
-  if (d->warp_kernel)
-    k_dyn_step_warp<<<(unsigned)((d->E + DYN_WARPS - 1) / DYN_WARPS), 32 * DYN_WARPS, 0, d->s>>>(
-        d->d_c, d->d_state, d->d_bladder, act, d_tau_ext, rho_fluid, g_hydro ? 1 : 0, gh, dt,
-        substeps, gv, d_flags, d->E);
-  else
-    k_dyn_step<<<blocks(d->E), DYN_BLOCK, 0, d->s>>>(d->d_c, d->d_state, d->d_bladder, act,
-                                                     d_tau_ext, rho_fluid, g_hydro ? 1 : 0, gh, dt,
-                                                     substeps, gv, d_flags, d->E);
-  CK(cudaGetLastError());
+  const int nl = d->hc.n_links;
+  CK(cudaMemcpyAsync(d->d_rest, rest_R, sizeof(double) * 9 * nl, cudaMemcpyHostToDevice, d->s));
+  CK(cudaMemcpyAsync(d->d_rest + 9 * NL, rest_p, sizeof(double) * 3 * nl, cudaMemcpyHostToDevice, d->s));
+  CK(cudaStreamSynchronize(d->s));
+  d->rest_set = true;
   return FSG_OK;
 }
 
@@ -1256,7 +1318,8 @@ int fsg_dyn_poses(fsg_dyn* d, const double* rest_R, const double* rest_p, fsg_bo
   CK(cudaMemcpyAsync(d->d_rest, rest_R, sizeof(double) * 9 * nl, cudaMemcpyHostToDevice, d->s));
   CK(cudaMemcpyAsync(d->d_rest + 9 * NL, rest_p, sizeof(double) * 3 * nl, cudaMemcpyHostToDevice, d->s));
   k_dyn_pose<<<blocks(d->E), DYN_BLOCK, 0, d->s>>>(d->d_c, d->d_state, d->d_rest, d->d_rest + 9 * NL,
-                                                   d->d_pose, d->E);
+                                                   reinterpret_cast<char*>(d->d_pose),
+                                                   sizeof(fsg_body_pose), d->E);
   CK(cudaGetLastError());
   CK(cudaMemcpyAsync(poses, d->d_pose, sizeof(fsg_body_pose) * d->E, cudaMemcpyDeviceToHost, d->s));
   CK(cudaStreamSynchronize(d->s));

@@ -33,6 +33,7 @@
 #include "../../include/fsg.h"
 #include "fsg_device.cuh"
 #include "fsg_skin.cuh"
+#include "fsg_dyn_internal.h"
 
 using fsg::Band;
 using fsg::Grid;
@@ -1441,6 +1442,9 @@ struct fsg_batch {
   cudaEvent_t ev[2] = {nullptr, nullptr};
   int par = 0;
   dim3 block;
+  fsg_dyn* dyn = nullptr;                          // set during fsg_batch_step_dynamic
+  const double** h_tauptr = nullptr;               // pinned: every env's tau_ext (mapped)
+  const double** d_tauptr = nullptr;
 };
 
 int fsg_batch_destroy(fsg_batch* b) {
@@ -1454,6 +1458,8 @@ int fsg_batch_destroy(fsg_batch* b) {
     cudaFree(b->d_skb[k]);
     if (b->ev[k]) cudaEventDestroy(b->ev[k]);
   }
+  if (b->h_tauptr) cudaFreeHost(b->h_tauptr);
+  cudaFree(b->d_tauptr);
   cudaFree(b->d_work);
   if (b->h_stat) cudaFreeHost(b->h_stat);
   if (b->stream) cudaStreamDestroy(b->stream);
@@ -1584,6 +1590,12 @@ int fsg_batch_step_async(fsg_batch* b) {
   if (nskin)
     CU(cudaMemcpyAsync(b->d_skb[q], b->h_skb[q], sizeof(fsg::SkinBody) * b->E, cudaMemcpyHostToDevice,
                        b->stream));
+  if (b->dyn) {  // this step's poses from the robot states, written over the uploaded ones
+    const int rc = fsg::dyn_launch_pose(b->dyn,
+                                        reinterpret_cast<char*>(b->d_skb[q]) + offsetof(fsg::SkinBody, pose),
+                                        sizeof(fsg::SkinBody), b->stream);
+    if (rc) return set_err(rc, "%s", fsg_dyn_last_error());
+  }
   CU(cudaMemsetAsync(b->d_work + q, 0, sizeof(unsigned), b->stream));
   b->envs[0]->L->step_batch(g0, b->envs[0]->d_sc, b->d_packs[q], h, b->block, b->d_work + q,
                             b->stream);
@@ -1649,6 +1661,60 @@ int fsg_batch_step_skinned(fsg_batch* b, const fsg_frame_state* frames, const fs
     if (tau) std::memcpy(tau + off, w, sizeof(double) * nd);
     if (stats) std::memcpy(stats + fsg::SKIN_NSTAT * e, w + nd, sizeof(double) * fsg::SKIN_NSTAT);
     off += nd;
+  }
+  return FSG_OK;
+}
+
+int fsg_batch_step_dynamic(fsg_batch* b, fsg_dyn* d, const fsg_frame_state* frames,
+                           const double* actuation, double rho_fluid, const double* g_hydro,
+                           double dt, int substeps, fsg_status* statuses, int* flags,
+                           fsg_joint_state* states) {
+  if (!b || !d) return set_err(FSG_EINPUT, "fsg_batch_step_dynamic: NULL handle");
+  if (fsg::dyn_n_envs(d) != b->E)
+    return set_err(FSG_EINPUT, "fsg_batch_step_dynamic: %d robots for %d envs", fsg::dyn_n_envs(d), b->E);
+  if (fsg::dyn_device(d) != b->envs[0]->cfg.device)
+    return set_err(FSG_EINPUT, "fsg_batch_step_dynamic: robots and envs on different devices");
+  CU(cudaSetDevice(b->envs[0]->cfg.device));
+  for (int e = 0; e < b->E; ++e) {
+    fsg_session* s = b->envs[e];
+    if (!s->skin || s->skp.nb != 1)
+      return set_err(FSG_ESTATE, "fsg_batch_step_dynamic: env %d has no single skinned body", e);
+    if (s->skp.body[0].n_dofs != fsg_dyn_n_dofs(d) || s->skp.body[0].n_links != fsg::dyn_n_links(d))
+      return set_err(FSG_EINPUT, "fsg_batch_step_dynamic: env %d's skeleton is not the robot's", e);
+    if (frames) s->frame = frames[e];
+    s->pose_set = true;  // the pose is produced on the device
+  }
+  double* d_act = nullptr;
+  int rc = fsg::dyn_upload_actuation(d, actuation, b->stream, &d_act);
+  if (rc) return set_err(rc, "%s", fsg_dyn_last_error());
+  const int q = b->par;
+  b->dyn = d;
+  rc = fsg_batch_step_async(b);
+  b->dyn = nullptr;
+  if (rc) return rc;
+  if (!b->h_tauptr) {
+    CU(cudaMallocHost(&b->h_tauptr, sizeof(double*) * b->E));
+    CU(cudaMalloc(&b->d_tauptr, sizeof(double*) * b->E));
+  }
+  for (int e = 0; e < b->E; ++e) b->h_tauptr[e] = b->envs[e]->h_wrench[b->envs[e]->last_par];
+  CU(cudaMemcpyAsync(b->d_tauptr, b->h_tauptr, sizeof(double*) * b->E, cudaMemcpyHostToDevice,
+                     b->stream));
+  // session.hpp:169-175: buoyancy on the pre-step kinematics + integrate
+  // (gravity enters through the hydrostatics only)
+  rc = fsg::dyn_launch_step(d, d_act, nullptr, b->d_tauptr, rho_fluid, g_hydro, dt, substeps, nullptr,
+                            fsg::dyn_flags(d), b->stream);
+  if (rc) return set_err(rc, "%s", fsg_dyn_last_error());
+  if (!b->h_stat) CU(cudaMallocHost(&b->h_stat, sizeof(StepScratch) * b->E));
+  k_batch_status<<<1, 256, 0, b->stream>>>(b->d_packs[q], b->E, b->h_stat);
+  CU_LAUNCH();
+  rc = fsg::dyn_read_states(d, states, flags, b->stream);
+  if (rc) return set_err(rc, "%s", fsg_dyn_last_error());
+  CU(stream_wait(b->stream));
+  for (int e = 0; e < b->E; ++e) {
+    fsg_session* s = b->envs[e];
+    if (b->h_stat[e].band_overflow) return set_err(FSG_ESTATE, "env %d: IB band overflow", e);
+    decode_status(b->h_stat[e], &s->last, true);
+    if (statuses) statuses[e] = s->last;
   }
   return FSG_OK;
 }

@@ -245,6 +245,12 @@ class RobotBatch:
                                                   float(rho_fluid), _abi.dptr(gh), float(dt),
                                                   int(substeps), _abi.dptr(gv), p(flags)), dyn=True)
 
+    def set_rest(self, rest_R, rest_p) -> None:
+        """RestPose::of the device poses of EnvBatch.step_dynamic use (fsg_dyn_set_rest)."""
+        rR = np.ascontiguousarray(np.asarray(rest_R, dtype=np.float64).reshape(-1))
+        rp = np.ascontiguousarray(np.asarray(rest_p, dtype=np.float64).reshape(-1))
+        _abi.check(_abi.lib().fsg_dyn_set_rest(self._h, _abi.dptr(rR), _abi.dptr(rp)), dyn=True)
+
     # -- probes --------------------------------------------------------------------
     def mass_matrix(self, gravity=None):
         """(mass_matrix [E, nd, nd], bias_forces [E, nd]) at the current states."""

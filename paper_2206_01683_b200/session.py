@@ -617,6 +617,37 @@ class EnvBatch:
             k += n
         return [StepStatus.of(x) for x in self._bst], taus, out[nt:].reshape(E, 7)
 
+    def step_dynamic(self, robots, actuation, frames=None, rho_fluid: float = 1000.0,
+                     g_hydro=(0.0, 0.0, -9.81), dt: float = 0.004, substeps: int = 4):
+        """The whole coupled step with the robots on the device
+        (fsg_batch_step_dynamic): ``robots`` is a dynamics.RobotBatch with one
+        robot per env (rest pose set), ``actuation`` [E, n_joints] -> (statuses,
+        robot flags [E], post-step JointStates)."""
+        from .dynamics import JointState
+        E = len(self.envs)
+        if not hasattr(self, "_dst"):
+            self._dst = (_abi.fsg_joint_state * E)()
+            self._dfl = np.zeros(E, dtype=np.int32)
+            self._dst_s = (_abi.fsg_status * E)()
+            self._dframe = (_abi.fsg_frame_state * E)()
+            self._dframe_np = np.frombuffer(self._dframe, dtype=np.float64).reshape(E, 19)
+        fp = None
+        if frames is not None:
+            if isinstance(frames, np.ndarray):
+                self._dframe_np[...] = frames.reshape(E, 19)
+            else:
+                for e, f in enumerate(frames):
+                    self._dframe_np[e] = f.packed()
+            fp = C.addressof(self._dframe)
+        act = np.ascontiguousarray(np.asarray(actuation, dtype=np.float64).reshape(E, -1))
+        gh = None if g_hydro is None else np.ascontiguousarray(np.asarray(g_hydro, dtype=np.float64))
+        check(self._L.fsg_batch_step_dynamic(self._h, robots._h, fp, dptr(act), float(rho_fluid),
+                                             dptr(gh), float(dt), int(substeps),
+                                             C.addressof(self._dst_s), self._dfl.ctypes.data,
+                                             C.addressof(self._dst)))
+        sts = [JointState.from_struct(self._dst[e], robots.n_joints, robots.n_dofs) for e in range(E)]
+        return [StepStatus.of(x) for x in self._dst_s], self._dfl.copy(), sts
+
     def close(self) -> None:
         if getattr(self, "_h", None):
             for s in self.envs:

@@ -216,3 +216,50 @@ def test_warp_and_thread_kernels_are_bit_identical(name, monkeypatch):
     # (the light fins blow up under this drive: NaNs must match too)
     assert np.array_equal(out[0][0], out[1][0], equal_nan=True)
     assert np.array_equal(out[0][1], out[1][1])
+
+
+def test_batch_step_dynamic_equals_host_loop():
+    """fsg_batch_step_dynamic (poses from the robot states on the device, the
+    coupled step, tau_ext into the robot step, one call) equals the host-driven
+    loop: RobotBatch.poses -> EnvBatch.step_skinned -> RobotBatch.step with the
+    returned tau_ext -- bit for bit (fluid, statuses, robot states)."""
+    from paper_2206_01683_b200 import EnvBatch, SessionConfig
+    from skin_cases import init_fluid, skin_scene
+    sc = skin_scene()
+    E = 3
+    robot = D.koi_robot(sc.bodies[0], sc.articulations()[0])
+    rR, rp = D.rest_pose(robot)
+    cfg = SessionConfig(dims=sc.dims, dx=sc.dx, dt=sc.dt, rho=sc.rho, nu=sc.nu,
+                        frame_mode=sc.frame_mode, precision="fp32", max_markers=sc.m)
+    rho, u = init_fluid(sc)
+    A, Bt = EnvBatch(cfg, E), EnvBatch(cfg, E)
+    RA, RB = D.RobotBatch(robot, E), D.RobotBatch(robot, E)
+    sts = _random_states(robot, E, 21)
+    for st in sts:
+        st.base_pos[:] = 0.0
+        st.v *= 0.1
+        st.q *= 0.3
+    for bt in (A, Bt):
+        for s in bt.envs:
+            s.initialize(rho, u)
+            s.set_skin(*sc.skin())
+    RA.set_states(sts)
+    RB.set_states(sts)
+    RB.set_rest(rR, rp)
+    rng = np.random.default_rng(22)
+    for k in range(6):
+        frames = np.stack([sc.frame(k + 3 * e).packed() for e in range(E)])
+        act = rng.uniform(-0.2, 0.2, (E, robot.n_joints))
+        sa, taus, _ = A.step_skinned(frames, RA.poses(rR, rp))
+        fa = RA.step(act, np.stack(taus), sc.rho, G, sc.dt, 4)
+        sb, fb, stb = Bt.step_dynamic(RB, act, frames, sc.rho, G, sc.dt, 4)
+        assert np.array_equal(fa, fb)
+        for e in range(E):
+            assert sa[e].min_f == sb[e].min_f and sa[e].stable() == sb[e].stable()
+        for x, y in zip(RA.states(), stb):
+            assert np.array_equal(_state_vec(x), _state_vec(y))
+        assert np.abs(np.stack(taus)).max() > 0.0
+    for e in range(E):
+        assert np.array_equal(A.envs[e].get_f(), Bt.envs[e].get_f())
+    A.close()
+    Bt.close()
