@@ -35,6 +35,7 @@ from __future__ import annotations
 
 import argparse
 import json
+import math
 import os
 import subprocess
 import sys
@@ -62,6 +63,8 @@ def parse_args():
     ap.add_argument("--c4-scaling", default="weak", choices=["weak", "strong"],
                     help="c4: each rank owns 512^3 (weak) or one 512^3 grid is split (strong)")
     ap.add_argument("--e2e-steps", type=int, default=100)
+    ap.add_argument("--no-robot-leg", action="store_true",
+                    help="c5: skip the e2e leg with the robot dynamics on the device")
     ap.add_argument("--markers", default="skinned", choices=["skinned", "host"],
                     help="c1-c3: bodies skinned on the device from a per-link pose each step "
                          "(fsg_set_pose; tau_ext read back) or marker arrays set each step")
@@ -441,6 +444,36 @@ def run_envs(args, scene, rank, local, world):
         t = torch.tensor([e2e_t], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_t = float(t.item())
+    e2e_dyn = None
+    if skinned and batch and not args.no_robot_leg:
+        # the rollout loop with the robots on the device too:
+        # one call per round uploads the actuation, steps fluid + robots, and
+        # returns statuses and the post-step robot states
+        from paper_2206_01683_b200 import dynamics as D
+        robot = D.koi_robot(scene.bodies[0], scene.articulations()[0])
+        rb = D.RobotBatch(robot, E, device=local)
+        rb.set_rest(*D.rest_pose(robot))
+        nj = robot.n_joints
+        dyn_t, dyn_ok = 0.0, True
+        for k in range(Ee):
+            fw_buf.fill_(1.0)
+            torch.sum(fr_buf, dim=0, out=sink[0])
+            torch.cuda.synchronize(dev)
+            t_ = (kk + Ee + k) * scene.dt
+            act = np.array([[0.2 * math.sin(2 * math.pi * 2.0 * t_ - 0.8 * j + e) for j in range(nj)]
+                            for e in range(E)])
+            fr = np.stack([frames[e][(kk + k) % nsteps].packed() for e in range(E)])
+            t0 = time.perf_counter()
+            sts_d, fl_d, _ = batch.step_dynamic(rb, act, fr, scene.rho, (0.0, 0.0, -9.81), scene.dt, 4)
+            dyn_t += time.perf_counter() - t0
+            dyn_ok &= all(x.stable() for x in sts_d) and not (fl_d & D.FSG_DYN_NONFINITE).any()
+        rb.close()
+        e2e_dyn = {"value": round(E * scene.n_cells * Ee * world / dyn_t / 1e6, 1), "unit": "MLUPS",
+                   "h2d_bytes_per_step": E * (8 * nj + 152),
+                   "d2h_bytes_per_step": E * (64 + 344 + 4), "steps": Ee, "stable": bool(dyn_ok),
+                   "what": "fsg_batch_step_dynamic: actuation up; device poses, coupled step, "
+                           "buoyancy + integrate (4 substeps) of every robot; statuses + robot "
+                           "states down (the reference's full CoupledSession::step)"}
     if batch:
         batch.close()
     else:
@@ -469,6 +502,7 @@ def run_envs(args, scene, rank, local, world):
                 "h2d_bytes_per_step": E * ((1920 if skinned else 80 * m) + 232),
                 "d2h_bytes_per_step": E * ((8 * (scene.skin()[1][0].n_dofs + 7) if skinned else 28 * m) + 64),
                 "steps": Ee},
+        **({"e2e_robots_on_device": e2e_dyn} if e2e_dyn else {}),
         "gpu_launches": K * (2 if batch else E * 2),
         "status": {"stable": all(st.stable() for st in sts), "min_f": min(st.min_f for st in sts)},
         "clocks": clk.summary(),

@@ -392,9 +392,9 @@ int orc_llt_solve(int n, const double* M, const double* b, double* x) {
     for (int k = 0; k < i; ++k) s -= Lm[n * i + k] * y[k];
     y[i] = s / Lm[n * i + i];
   }
-  for (int i = n - 1; i >= 0; --i) {
+  for (int i = n - 1; i >= 0; --i) { /* descending k, as the device kernels sum */
     double s = y[i];
-    for (int k = i + 1; k < n; ++k) s -= Lm[n * k + i] * x[k];
+    for (int k = n - 1; k > i; --k) s -= Lm[n * k + i] * x[k];
     x[i] = s / Lm[n * i + i];
   }
   return 1;

@@ -417,9 +417,9 @@ __host__ __device__ bool dk_llt_solve(int n, double* M, const double* b, double*
     for (int q = 0; q < i; ++q) s -= M[n * i + q] * y[q];
     y[i] = s / M[n * i + i];
   }
-  for (int i = n - 1; i >= 0; --i) {
-    double s = y[i];
-    for (int q = i + 1; q < n; ++q) s -= M[n * q + i] * x[q];
+  for (int i = n - 1; i >= 0; --i) {  // (descending q: the order the warp kernel's
+    double s = y[i];                    //  lanes accumulate as x[q] become known)
+    for (int q = n - 1; q > i; --q) s -= M[n * q + i] * x[q];
     x[i] = s / M[n * i + i];
   }
   return true;
@@ -554,10 +554,26 @@ __global__ void __launch_bounds__(DYN_BLOCK)
 // lives in shared memory.
 constexpr int DYN_WARPS = 4;
 
+#ifdef FSG_DYN_TIMING  // dev builds only (scripts/build_variant.sh): per-phase clock64 of warp 0
+__device__ unsigned long long g_dyn_t[8];
+#define DYN_T(k)                                                        \
+  do {                                                                  \
+    if (blockIdx.x == 0 && threadIdx.x == 0) {                          \
+      const long long t_ = clock64();                                   \
+      g_dyn_t[k] += (unsigned long long)(t_ - t_last);                  \
+      t_last = t_;                                                      \
+    }                                                                   \
+  } while (0)
+#else
+#define DYN_T(k) \
+  do {           \
+  } while (0)
+#endif
+
 struct WarpWS {
   fsg_joint_state st;
   double rr[NL][9];  // r_rel of each link (link -> parent)
-  double E[NL][9], r[NL][3], Rw[NL][9], pw[NL][3], vb[NL][6];
+  KC k;  // E, r, Rw, pw, vb of every link
   double ic[NL][36];
   double X[36], T[36];
   double H[ND * ND];
@@ -570,32 +586,32 @@ struct WarpWS {
 __device__ void wk_fk(const DynConst& c, WarpWS& w, int lane) {
   const fsg_joint_state& st = w.st;
   if (lane == 0) {
-    quat_to_R(st.base_quat, w.Rw[0]);
+    quat_to_R(st.base_quat, w.k.Rw[0]);
     for (int a = 0; a < 3; ++a)
-      for (int b = 0; b < 3; ++b) w.E[0][3 * a + b] = w.Rw[0][3 * b + a];
-    for (int a = 0; a < 3; ++a) w.pw[0][a] = st.base_pos[a], w.r[0][a] = st.base_pos[a];
-    for (int a = 0; a < 6; ++a) w.vb[0][a] = c.floating ? st.v[a] : 0.0;
+      for (int b = 0; b < 3; ++b) w.k.E[0][3 * a + b] = w.k.Rw[0][3 * b + a];
+    for (int a = 0; a < 3; ++a) w.k.pw[0][a] = st.base_pos[a], w.k.r[0][a] = st.base_pos[a];
+    for (int a = 0; a < 6; ++a) w.k.vb[0][a] = c.floating ? st.v[a] : 0.0;
   } else if (lane < c.n_links) {
     const int i = lane;
     double rj[9] = {1, 0, 0, 0, 1, 0, 0, 0, 1};
     if (c.joint[i] == FSG_JOINT_REVOLUTE) angle_axis_R(st.q[c.jidx[i]], c.axis[i], rj);
     mm3(c.jrot[i], rj, w.rr[i]);
     for (int a = 0; a < 3; ++a)
-      for (int b = 0; b < 3; ++b) w.E[i][3 * a + b] = w.rr[i][3 * b + a];
-    for (int a = 0; a < 3; ++a) w.r[i][a] = c.jorig[i][a];
+      for (int b = 0; b < 3; ++b) w.k.E[i][3 * a + b] = w.rr[i][3 * b + a];
+    for (int a = 0; a < 3; ++a) w.k.r[i][a] = c.jorig[i][a];
   }
   __syncwarp();
   if (lane == 0) {
     for (int i = 1; i < c.n_links; ++i) {
       const int pa = c.parent[i];
       double t[3];
-      mm3(w.Rw[pa], w.rr[i], w.Rw[i]);
-      mv3(w.Rw[pa], c.jorig[i], t);
-      for (int a = 0; a < 3; ++a) w.pw[i][a] = w.pw[pa][a] + t[a];
-      apply_motion(w.E[i], w.r[i], w.vb[pa], w.vb[i]);
+      mm3(w.k.Rw[pa], w.rr[i], w.k.Rw[i]);
+      mv3(w.k.Rw[pa], c.jorig[i], t);
+      for (int a = 0; a < 3; ++a) w.k.pw[i][a] = w.k.pw[pa][a] + t[a];
+      apply_motion(w.k.E[i], w.k.r[i], w.k.vb[pa], w.k.vb[i]);
       if (c.joint[i] == FSG_JOINT_REVOLUTE) {
         const double qd = st.v[c.dof[i]];
-        for (int a = 0; a < 3; ++a) w.vb[i][a] = w.vb[i][a] + c.axis[i][a] * qd;
+        for (int a = 0; a < 3; ++a) w.k.vb[i][a] = w.k.vb[i][a] + c.axis[i][a] * qd;
       }
     }
   }
@@ -611,13 +627,13 @@ __device__ void wk_crba(const DynConst& c, WarpWS& w, int lane) {
       const int a = e / 6, b = e % 6;
       double x;
       if (a < 3) {
-        x = b < 3 ? w.E[i][3 * a + b] : 0.0;
+        x = b < 3 ? w.k.E[i][3 * a + b] : 0.0;
       } else if (b >= 3) {
-        x = w.E[i][3 * (a - 3) + (b - 3)];
+        x = w.k.E[i][3 * (a - 3) + (b - 3)];
       } else {
-        const double* r = w.r[i];
+        const double* r = w.k.r[i];
         const double S[9] = {0.0, -r[2], r[1], r[2], 0.0, -r[0], -r[1], r[0], 0.0};
-        const double* A = w.E[i] + 3 * (a - 3);
+        const double* A = w.k.E[i] + 3 * (a - 3);
         x = -(A[0] * S[b] + A[1] * S[3 + b] + A[2] * S[6 + b]);
       }
       w.X[e] = x;
@@ -657,7 +673,7 @@ __device__ void wk_crba(const DynConst& c, WarpWS& w, int lane) {
     w.H[nd * di + di] = d;
     int j = i;
     while (c.parent[j] >= 0) {
-      transpose_force(w.E[j], w.r[j], f, f);
+      transpose_force(w.k.E[j], w.k.r[j], f, f);
       j = c.parent[j];
       if (j == 0) {
         if (c.floating)
@@ -680,15 +696,15 @@ __device__ void wk_rnea(const DynConst& c, WarpWS& w, int lane, const double* g)
   const int nb = c.n_links;
   if (lane == 0) {
     double rtg[3];
-    mtv3(w.Rw[0], g, rtg);
+    mtv3(w.k.Rw[0], g, rtg);
     w.a[0][0] = w.a[0][1] = w.a[0][2] = 0.0;
     w.a[0][3] = -rtg[0], w.a[0][4] = -rtg[1], w.a[0][5] = -rtg[2];
     for (int i = 1; i < nb; ++i) {
-      apply_motion(w.E[i], w.r[i], w.a[c.parent[i]], w.a[i]);
+      apply_motion(w.k.E[i], w.k.r[i], w.a[c.parent[i]], w.a[i]);
       if (c.joint[i] == FSG_JOINT_REVOLUTE) {
         const double qd = w.st.v[c.dof[i]];
         const double m[6] = {c.axis[i][0] * qd, c.axis[i][1] * qd, c.axis[i][2] * qd, 0.0, 0.0, 0.0};
-        const double* v = w.vb[i];
+        const double* v = w.k.vb[i];
         double x0[3], x1[3], x2[3];
         cross3(v, m, x0);
         cross3(v, m + 3, x1);
@@ -703,8 +719,8 @@ __device__ void wk_rnea(const DynConst& c, WarpWS& w, int lane, const double* g)
     const int i = lane;
     double ia[6], iv[6], x0[3], x1[3], x2[3];
     mv6(c.I6[i], w.a[i], ia);
-    mv6(c.I6[i], w.vb[i], iv);
-    const double* v = w.vb[i];
+    mv6(c.I6[i], w.k.vb[i], iv);
+    const double* v = w.k.vb[i];
     cross3(v, iv, x0);
     cross3(v + 3, iv + 3, x1);
     cross3(v, iv + 3, x2);
@@ -726,7 +742,7 @@ __device__ void wk_rnea(const DynConst& c, WarpWS& w, int lane, const double* g)
         w.cb[c.dof[i]] = d;
       }
       double t[6];
-      transpose_force(w.E[i], w.r[i], w.f[i], t);
+      transpose_force(w.k.E[i], w.k.r[i], w.f[i], t);
       double* P = w.f[c.parent[i]];
       for (int q = 0; q < 6; ++q) P[q] = P[q] + t[q];
     }
@@ -734,7 +750,11 @@ __device__ void wk_rnea(const DynConst& c, WarpWS& w, int lane, const double* g)
   __syncwarp();
 }
 
-// Cholesky in place (as dk_llt_solve) with the rows of each column on lanes
+// Cholesky in place (as dk_llt_solve, element by element in the same order)
+// with the rows of each column on lanes; the triangular solves on lane 0.
+// (A register-resident variant -- rows in lane registers, right-looking
+// rank-1 updates over shuffles -- measured slower: the solves' dependent
+// divisions dominate either way.)
 __device__ bool wk_llt_solve(WarpWS& w, int lane, int n) {
   double* M = w.H;
   for (int j = 0; j < n; ++j) {
@@ -763,7 +783,7 @@ __device__ bool wk_llt_solve(WarpWS& w, int lane, int n) {
     }
     for (int i = n - 1; i >= 0; --i) {
       double s = w.y[i];
-      for (int q = i + 1; q < n; ++q) s -= M[n * q + i] * w.qdd[q];
+      for (int q = n - 1; q > i; --q) s -= M[n * q + i] * w.qdd[q];
       w.qdd[i] = s / M[n * i + i];
     }
   }
@@ -785,6 +805,9 @@ __global__ void __launch_bounds__(32 * DYN_WARPS)
   if (e >= E) return;
   WarpWS& w = ws[wi];
   const int nd = c.nd, nj = c.nj;
+#ifdef FSG_DYN_TIMING
+  long long t_last = clock64();
+#endif
   {
     const double* src = reinterpret_cast<const double*>(states + e);
     double* dst = reinterpret_cast<double*>(&w.st);
@@ -799,20 +822,14 @@ __global__ void __launch_bounds__(32 * DYN_WARPS)
   __syncwarp();
   if (hydro) {
     wk_fk(c, w, lane);
-    // buoyancy_gravity_forces on the pre-step kinematics (serial order, lane 0;
-    // dk_hydro reads a KinematicsCache, assembled from the warp's arrays)
+    // buoyancy_gravity_forces on the pre-step kinematics (serial order, lane 0)
     if (lane == 0) {
-      KC k;
-      for (int i = 0; i < c.n_links; ++i) {
-        for (int q = 0; q < 9; ++q) k.E[i][q] = w.E[i][q], k.Rw[i][q] = w.Rw[i][q];
-        for (int q = 0; q < 3; ++q) k.r[i][q] = w.r[i][q], k.pw[i][q] = w.pw[i][q];
-        for (int q = 0; q < 6; ++q) k.vb[i][q] = w.vb[i][q];
-      }
       const double g[3] = {gh.x, gh.y, gh.z};
-      dk_hydro(c, k, bladder[e], rho, g, w.te);
+      dk_hydro(c, w.k, bladder[e], rho, g, w.te);
     }
     __syncwarp();
   }
+  DYN_T(0);
   const double g[3] = {gv.x, gv.y, gv.z};
   const double h = dt / substeps;
   for (int s = 0; s < substeps; ++s) {
@@ -837,15 +854,20 @@ __global__ void __launch_bounds__(32 * DYN_WARPS)
       w.tsum[di] = ti + tl;
     }
     if (__any_sync(0xffffffffu, clamped) && lane == 0) w.fl |= FSG_DYN_CLAMPED;
+    DYN_T(1);
     wk_fk(c, w, lane);
+    DYN_T(2);
     wk_crba(c, w, lane);
+    DYN_T(3);
     wk_rnea(c, w, lane, g);
     for (int q = lane; q < nd; q += 32) w.rhs[q] = (w.tsum[q] + w.te[q]) - w.cb[q];
     __syncwarp();
+    DYN_T(4);
     if (!wk_llt_solve(w, lane, nd)) {
       if (lane == 0) w.fl |= FSG_DYN_NOT_SPD;
       break;
     }
+    DYN_T(5);
     if (lane == 0) {
       fsg_joint_state& st = w.st;
       for (int q = 0; q < nd; ++q) st.qdd[q] = w.qdd[q], st.v[q] = st.v[q] + h * w.qdd[q];
@@ -886,6 +908,7 @@ __global__ void __launch_bounds__(32 * DYN_WARPS)
       }
     }
     __syncwarp();
+    DYN_T(6);
   }
   if (lane == 0) {
     bool finite = true;
@@ -1152,6 +1175,18 @@ int dyn_device(const fsg_dyn* d) { return d->dev; }
 extern "C" {
 
 const char* fsg_dyn_last_error(void) { return g_dyn_err; }
+
+#ifdef FSG_DYN_TIMING
+int fsg_dyn_debug_timing(unsigned long long* out, int reset) {
+  cudaDeviceSynchronize();
+  cudaMemcpyFromSymbol(out, g_dyn_t, sizeof(unsigned long long) * 8);
+  if (reset) {
+    unsigned long long z[8] = {};
+    cudaMemcpyToSymbol(g_dyn_t, z, sizeof z);
+  }
+  return FSG_OK;
+}
+#endif
 
 int fsg_dyn_create(const fsg_robot* robot, int n_envs, int device, fsg_dyn** out) {
   if (!out) return fail(FSG_EINPUT, "out is NULL");

@@ -18,6 +18,7 @@ nvcc $F --fmad=false -c $SRC/fsg_kernels_fp64.cu -o $OUT/obj_$name/k64.o &
 nvcc $F -c $SRC/fsg_session.cu -o $OUT/obj_$name/s.o &
 [ -f $SRC/fsg_skin.cu ] && nvcc $F --fmad=false -c $SRC/fsg_skin.cu -o $OUT/obj_$name/sk.o &
 [ -f $SRC/fsg_drag.cu ] && nvcc $F --fmad=false -c $SRC/fsg_drag.cu -o $OUT/obj_$name/dr.o &
+[ -f $SRC/fsg_dyn.cu ] && nvcc $F --fmad=false -c $SRC/fsg_dyn.cu -o $OUT/obj_$name/dy.o &
 [ -f $SRC/fsg_io.cpp ] && g++ -std=c++17 -O2 -fPIC -ffp-contract=off -c $SRC/fsg_io.cpp -o $OUT/obj_$name/io.o &
 g++ -std=c++17 -O2 -fPIC -ffp-contract=off -c $SRC/fsg_follower.cpp -o $OUT/obj_$name/f.o &
 wait
