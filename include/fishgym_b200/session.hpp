@@ -43,6 +43,13 @@ inline void check(int rc) {
   throw std::runtime_error("fsg: " + msg);
 }
 
+inline void check_dyn(int rc) {
+  if (rc == FSG_OK) return;
+  const std::string msg = fsg_dyn_last_error();
+  if (rc == FSG_EINPUT) throw InputError(msg);
+  throw std::runtime_error("fsg_dyn: " + msg);
+}
+
 /// StepStatus (solver.hpp:13-20) + StepOutcome (backend.hpp:37-40).
 struct StepStatus {
   bool finite = true;
@@ -237,6 +244,48 @@ class FluidSession {
   size_t m_ = 0;
   size_t nt_ = 0;
   int nb_ = 0;
+};
+
+/// A batch of robots of one skeleton on the device:
+/// robot::integrate / buoyancy_gravity_forces (dynamics.hpp:237-289) for
+/// every robot per call.  fsg_robot mirrors robot::Skeleton + Bladder
+/// (skeleton.hpp:16-93); an invalid skeleton throws InputError with
+/// Skeleton::validate's message.
+class RobotDynamics {
+ public:
+  RobotDynamics(const fsg_robot& robot, int n_envs, int device = 0) : n_envs_(n_envs) {
+    check_dyn(fsg_dyn_create(&robot, n_envs, device, &h_));
+    nd_ = fsg_dyn_n_dofs(h_);
+    nj_ = fsg_dyn_n_joints(h_);
+  }
+  ~RobotDynamics() { fsg_dyn_destroy(h_); }
+  RobotDynamics(const RobotDynamics&) = delete;
+  RobotDynamics& operator=(const RobotDynamics&) = delete;
+
+  int n_dofs() const { return nd_; }
+  int n_joints() const { return nj_; }
+  void set_states(const std::vector<fsg_joint_state>& st) { check_dyn(fsg_dyn_set_state(h_, st.data())); }
+  std::vector<fsg_joint_state> states() {
+    std::vector<fsg_joint_state> st(n_envs_);
+    check_dyn(fsg_dyn_get_state(h_, st.data()));
+    return st;
+  }
+  /// session.hpp:169-175 for every robot: actuation [n_envs * n_joints],
+  /// tau_ext [n_envs * n_dofs] (empty: zero); g_hydro / gravity nullable.
+  /// Returns the FSG_DYN_* flags per robot.
+  std::vector<int> step(const std::vector<double>& actuation, const std::vector<double>& tau_ext,
+                        double rho_fluid, const double* g_hydro, double dt, int substeps,
+                        const double* gravity) {
+    std::vector<int> flags(n_envs_);
+    check_dyn(fsg_dyn_step(h_, actuation.data(), tau_ext.empty() ? nullptr : tau_ext.data(), rho_fluid,
+                           g_hydro, dt, substeps, gravity, flags.data()));
+    return flags;
+  }
+  fsg_dyn* handle() { return h_; }
+
+ private:
+  fsg_dyn* h_ = nullptr;
+  int n_envs_ = 0, nd_ = 0, nj_ = 0;
 };
 
 }  // namespace fishgym_b200

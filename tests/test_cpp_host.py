@@ -10,9 +10,9 @@ SRC = os.path.join(ROOT, "tests", "cpp", "session_smoke.cpp")
 LIBDIR = os.path.join(ROOT, "paper_2206_01683_b200")
 
 
-def build(tmp_path):
-    exe = str(tmp_path / "session_smoke")
-    subprocess.run(["/usr/bin/g++", "-std=c++17", "-O1", "-I", os.path.join(ROOT, "include"), SRC,
+def build(tmp_path, src=SRC):
+    exe = str(tmp_path / os.path.splitext(os.path.basename(src))[0])
+    subprocess.run(["/usr/bin/g++", "-std=c++17", "-O1", "-I", os.path.join(ROOT, "include"), src,
                     "-L", LIBDIR, "-lfsg", f"-Wl,-rpath,{LIBDIR}", "-o", exe], check=True)
     return exe
 
@@ -28,3 +28,19 @@ def test_cpp_wrapper_runs_reference_kats(tmp_path, prec):
     r = subprocess.run([exe, str(prec)], capture_output=True, text=True, timeout=120)
     assert r.returncode == 0, r.stdout + r.stderr
     assert "guo_forcing_rel_err" in r.stdout
+
+
+DYN_SRC = os.path.join(ROOT, "tests", "cpp", "dyn_smoke.cpp")
+
+
+def test_cpp_robot_wrapper_compiles_and_links(tmp_path):
+    assert os.path.exists(build(tmp_path, DYN_SRC))
+
+
+@pytest.mark.gpu
+def test_cpp_robot_wrapper_pendulum_kat(tmp_path):
+    """test_robot.cpp:113-139 through the C++ wrapper on the device."""
+    exe = build(tmp_path, DYN_SRC)
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "pendulum_period_rel_err" in r.stdout and "joint limits inverted" in r.stdout
