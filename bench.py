@@ -454,8 +454,8 @@ def run_envs(args, scene, rank, local, world):
         rb = D.RobotBatch(robot, E, device=local)
         rb.set_rest(*D.rest_pose(robot))
         nj = robot.n_joints
-        dyn_t, dyn_ok = 0.0, True
-        for k in range(Ee):
+        dyn_t, dyn_ok, per_call = 0.0, True, []
+        for k in range(-3, Ee):  # 3 untimed warm-up rounds (lazy module load, first-call allocations)
             fw_buf.fill_(1.0)
             torch.sum(fr_buf, dim=0, out=sink[0])
             torch.cuda.synchronize(dev)
@@ -465,12 +465,17 @@ def run_envs(args, scene, rank, local, world):
             fr = np.stack([frames[e][(kk + k) % nsteps].packed() for e in range(E)])
             t0 = time.perf_counter()
             sts_d, fl_d, _ = batch.step_dynamic(rb, act, fr, scene.rho, (0.0, 0.0, -9.81), scene.dt, 4)
-            dyn_t += time.perf_counter() - t0
+            if k < 0:
+                continue
+            per_call.append(time.perf_counter() - t0)
+            dyn_t += per_call[-1]
             dyn_ok &= all(x.stable() for x in sts_d) and not (fl_d & D.FSG_DYN_NONFINITE).any()
         rb.close()
         e2e_dyn = {"value": round(E * scene.n_cells * Ee * world / dyn_t / 1e6, 1), "unit": "MLUPS",
                    "h2d_bytes_per_step": E * (8 * nj + 152),
                    "d2h_bytes_per_step": E * (64 + 344 + 4), "steps": Ee, "stable": bool(dyn_ok),
+                   "call_us": {q: round(float(np.percentile(per_call, p)) * 1e6, 1)
+                               for q, p in (("p50", 50), ("p90", 90), ("max", 100))},
                    "what": "fsg_batch_step_dynamic: actuation up; device poses, coupled step, "
                            "buoyancy + integrate (4 substeps) of every robot; statuses + robot "
                            "states down (the reference's full CoupledSession::step)"}
