@@ -760,6 +760,7 @@ __device__ bool wk_llt_solve(WarpWS& w, int lane, int n) {
   for (int j = 0; j < n; ++j) {
     if (lane == 0) {
       double d = M[n * j + j];
+#pragma unroll 4
       for (int q = 0; q < j; ++q) d -= M[n * j + q] * M[n * j + q];
       w.ok = d > 0.0;
       if (w.ok) M[n * j + j] = sqrt(d);
@@ -770,6 +771,7 @@ __device__ bool wk_llt_solve(WarpWS& w, int lane, int n) {
     const int i = j + 1 + lane;
     if (i < n) {
       double s = M[n * i + j];
+#pragma unroll 4
       for (int q = 0; q < j; ++q) s -= M[n * i + q] * M[n * j + q];
       M[n * i + j] = s / ljj;
     }
@@ -778,11 +780,13 @@ __device__ bool wk_llt_solve(WarpWS& w, int lane, int n) {
   if (lane == 0) {
     for (int i = 0; i < n; ++i) {
       double s = w.rhs[i];
+#pragma unroll 4
       for (int q = 0; q < i; ++q) s -= M[n * i + q] * w.y[q];
       w.y[i] = s / M[n * i + i];
     }
     for (int i = n - 1; i >= 0; --i) {
       double s = w.y[i];
+#pragma unroll 4
       for (int q = n - 1; q > i; --q) s -= M[n * q + i] * w.qdd[q];
       w.qdd[i] = s / M[n * i + i];
     }
