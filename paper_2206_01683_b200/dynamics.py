@@ -174,6 +174,16 @@ class JointState:
                           np.array(s.v[:nd]), np.array(s.qdd[:nd]))
 
 
+def unpack_states(packed, n_joints: int, n_dofs: int) -> list:
+    """Packed fsg_joint_state rows ([E, 43], EnvBatch.step_dynamic) -> JointStates."""
+    L, Dm = DYN_MAX_LINKS, DYN_MAX_DOFS
+    out = []
+    for r in np.asarray(packed, dtype=np.float64).reshape(-1, 7 + L + 2 * Dm):
+        out.append(JointState(r[0:3].copy(), r[3:7].copy(), r[7:7 + n_joints].copy(),
+                              r[7 + L:7 + L + n_dofs].copy(), r[7 + L + Dm:7 + L + Dm + n_dofs].copy()))
+    return out
+
+
 class RobotBatch:
     """E robots of one skeleton on one device (fsg_dyn_*)."""
 

@@ -622,11 +622,13 @@ class EnvBatch:
         """The whole coupled step with the robots on the device
         (fsg_batch_step_dynamic): ``robots`` is a dynamics.RobotBatch with one
         robot per env (rest pose set), ``actuation`` [E, n_joints] -> (statuses,
-        robot flags [E], post-step JointStates)."""
-        from .dynamics import JointState
+        robot flags [E], post-step states as packed fsg_joint_state rows
+        [E, 43]: base_pos 3, base_quat 4, q 8, v 14, qdd 14;
+        dynamics.unpack_states turns them into JointStates)."""
         E = len(self.envs)
         if not hasattr(self, "_dst"):
             self._dst = (_abi.fsg_joint_state * E)()
+            self._dst_np = np.frombuffer(self._dst, dtype=np.float64).reshape(E, -1)
             self._dfl = np.zeros(E, dtype=np.int32)
             self._dst_s = (_abi.fsg_status * E)()
             self._dframe = (_abi.fsg_frame_state * E)()
@@ -645,8 +647,7 @@ class EnvBatch:
                                              dptr(gh), float(dt), int(substeps),
                                              C.addressof(self._dst_s), self._dfl.ctypes.data,
                                              C.addressof(self._dst)))
-        sts = [JointState.from_struct(self._dst[e], robots.n_joints, robots.n_dofs) for e in range(E)]
-        return [StepStatus.of(x) for x in self._dst_s], self._dfl.copy(), sts
+        return [StepStatus.of(x) for x in self._dst_s], self._dfl.copy(), self._dst_np.copy()
 
     def close(self) -> None:
         if getattr(self, "_h", None):

@@ -252,7 +252,8 @@ def test_batch_step_dynamic_equals_host_loop():
         act = rng.uniform(-0.2, 0.2, (E, robot.n_joints))
         sa, taus, _ = A.step_skinned(frames, RA.poses(rR, rp))
         fa = RA.step(act, np.stack(taus), sc.rho, G, sc.dt, 4)
-        sb, fb, stb = Bt.step_dynamic(RB, act, frames, sc.rho, G, sc.dt, 4)
+        sb, fb, packed = Bt.step_dynamic(RB, act, frames, sc.rho, G, sc.dt, 4)
+        stb = D.unpack_states(packed, robot.n_joints, robot.n_dofs)
         assert np.array_equal(fa, fb)
         for e in range(E):
             assert sa[e].min_f == sb[e].min_f and sa[e].stable() == sb[e].stable()
