@@ -706,7 +706,9 @@ def run_ours(args, scene, rank, local, world):
                          "frac": round(BYTES_PER_CELL * scene.n_cells / (fluid_ms / 1e3) / 1e9 / peak, 4)}},
         "e2e": {"value": round(e2e_val, 1), "unit": "MLUPS", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h, "steps": E},
-        "gpu_launches": K * (4 if skinned else (2 if m else 1)),
+        # skinned bodies ride in the marker kernel (<= 2 bodies; more use the
+        # split skin kernels beside K4): K_m + K4 per step
+        "gpu_launches": K * ((2 if len(scene.bodies) <= 2 else 4) if skinned else (2 if m else 1)),
         "status": {"stable": bool(st.stable()), "min_f": st.min_f},
         "clocks": clk.summary(),
     }
