@@ -1173,6 +1173,7 @@ int dyn_read_states(fsg_dyn* d, fsg_joint_state* out, int* flags, cudaStream_t s
 int* dyn_flags(fsg_dyn* d) { return d->d_flags; }
 int dyn_n_envs(const fsg_dyn* d) { return d->E; }
 int dyn_n_links(const fsg_dyn* d) { return d->hc.n_links; }
+bool dyn_rest_set(const fsg_dyn* d) { return d->rest_set; }
 int dyn_device(const fsg_dyn* d) { return d->dev; }
 }  // namespace fsg
 

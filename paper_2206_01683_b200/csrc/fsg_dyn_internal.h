@@ -20,4 +20,5 @@ int* dyn_flags(fsg_dyn* d);
 int dyn_n_envs(const fsg_dyn* d);
 int dyn_n_links(const fsg_dyn* d);
 int dyn_device(const fsg_dyn* d);
+bool dyn_rest_set(const fsg_dyn* d);
 }  // namespace fsg

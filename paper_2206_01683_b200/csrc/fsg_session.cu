@@ -1674,6 +1674,8 @@ int fsg_batch_step_dynamic(fsg_batch* b, fsg_dyn* d, const fsg_frame_state* fram
     return set_err(FSG_EINPUT, "fsg_batch_step_dynamic: %d robots for %d envs", fsg::dyn_n_envs(d), b->E);
   if (fsg::dyn_device(d) != b->envs[0]->cfg.device)
     return set_err(FSG_EINPUT, "fsg_batch_step_dynamic: robots and envs on different devices");
+  if (!fsg::dyn_rest_set(d))
+    return set_err(FSG_ESTATE, "fsg_batch_step_dynamic: fsg_dyn_set_rest has not been called");
   CU(cudaSetDevice(b->envs[0]->cfg.device));
   for (int e = 0; e < b->E; ++e) {
     fsg_session* s = b->envs[e];

@@ -641,7 +641,10 @@ class EnvBatch:
                 for e, f in enumerate(frames):
                     self._dframe_np[e] = f.packed()
             fp = C.addressof(self._dframe)
-        act = np.ascontiguousarray(np.asarray(actuation, dtype=np.float64).reshape(E, -1))
+        act = np.ascontiguousarray(np.asarray(actuation, dtype=np.float64).reshape(-1))
+        if act.size != robots.n_envs * robots.n_joints:
+            raise _abi.InputError(_abi.FSG_EINPUT, f"actuation has {act.size} entries, expected "
+                                                   f"{robots.n_envs} x {robots.n_joints}")
         gh = None if g_hydro is None else np.ascontiguousarray(np.asarray(g_hydro, dtype=np.float64))
         check(self._L.fsg_batch_step_dynamic(self._h, robots._h, fp, dptr(act), float(rho_fluid),
                                              dptr(gh), float(dt), int(substeps),

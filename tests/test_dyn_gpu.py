@@ -264,3 +264,27 @@ def test_batch_step_dynamic_equals_host_loop():
         assert np.array_equal(A.envs[e].get_f(), Bt.envs[e].get_f())
     A.close()
     Bt.close()
+
+
+def test_batch_step_dynamic_rejects_mismatches():
+    from paper_2206_01683_b200 import EnvBatch, FsgError, InputError, SessionConfig
+    from skin_cases import skin_scene
+    sc = skin_scene()
+    robot = D.koi_robot(sc.bodies[0], sc.articulations()[0])
+    cfg = SessionConfig(dims=sc.dims, dx=sc.dx, dt=sc.dt, rho=sc.rho, nu=sc.nu,
+                        frame_mode=sc.frame_mode, precision="fp32", max_markers=sc.m)
+    b = EnvBatch(cfg, 2)
+    act = np.zeros((2, robot.n_joints))
+    with pytest.raises(InputError, match="robots for"):
+        b.step_dynamic(D.RobotBatch(robot, 3), np.zeros((3, robot.n_joints)))
+    with pytest.raises(FsgError, match="fsg_dyn_set_rest"):
+        b.step_dynamic(D.RobotBatch(robot, 2), act)
+    rb = D.RobotBatch(robot, 2)
+    rb.set_rest(*D.rest_pose(robot))
+    with pytest.raises(FsgError, match="no single skinned body"):
+        b.step_dynamic(rb, act)
+    for s in b.envs:
+        s.set_skin(*sc.skin())
+    st, fl, packed = b.step_dynamic(rb, act)  # now well-formed
+    assert all(x.stable() for x in st) and packed.shape == (2, 43)
+    b.close()
