@@ -639,21 +639,34 @@ __device__ void wk_crba(const DynConst& c, WarpWS& w, int lane) {
       w.X[e] = x;
     }
     __syncwarp();
-    for (int e = lane; e < 36; e += 32) {
-      const int a = e / 6, b = e % 6;
-      double s = 0.0;
+    {  // T = X^T ic: element lane, and lane + 32 on lanes 0-3, as two
+       // interleaved (independent) chains so the second hides behind the first
+      const int e0 = lane, e1 = lane + 32 < 36 ? lane + 32 : lane;
+      const int a0 = e0 / 6, b0 = e0 % 6, a1 = e1 / 6, b1 = e1 % 6;
+      double s0 = 0.0, s1 = 0.0;
 #pragma unroll
-      for (int q = 0; q < 6; ++q) s += w.X[6 * q + a] * w.ic[i][6 * q + b];
-      w.T[e] = s;
+      for (int q = 0; q < 6; ++q) {
+        s0 += w.X[6 * q + a0] * w.ic[i][6 * q + b0];
+        s1 += w.X[6 * q + a1] * w.ic[i][6 * q + b1];
+      }
+      w.T[e0] = s0;
+      if (e1 != e0) w.T[e1] = s1;
     }
     __syncwarp();
     double* P = w.ic[c.parent[i]];
-    for (int e = lane; e < 36; e += 32) {
-      const int a = e / 6, b = e % 6;
-      double s = 0.0;
+    {  // ic[parent] += T X, the same two-chain split
+      const int e0 = lane, e1 = lane + 32 < 36 ? lane + 32 : lane;
+      const int a0 = e0 / 6, b0 = e0 % 6, a1 = e1 / 6, b1 = e1 % 6;
+      double s0 = 0.0, s1 = 0.0;
 #pragma unroll
-      for (int q = 0; q < 6; ++q) s += w.T[6 * a + q] * w.X[6 * q + b];
-      P[e] = P[e] + s;
+      for (int q = 0; q < 6; ++q) {
+        s0 += w.T[6 * a0 + q] * w.X[6 * q + b0];
+        s1 += w.T[6 * a1 + q] * w.X[6 * q + b1];
+      }
+      const double p0 = P[e0] + s0;
+      const double p1 = P[e1] + s1;
+      P[e0] = p0;
+      if (e1 != e0) P[e1] = p1;
     }
     __syncwarp();
   }
