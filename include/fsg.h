@@ -159,8 +159,16 @@ int fsg_last_status(fsg_session* s, fsg_status* st);
 int fsg_get_marker_forces(fsg_session* s, double* force_world, int* valid, double* stats);
 /* Bare macroscopic fields of the last step (CoupledSession::macro(), session.hpp:95-96). */
 int fsg_get_macro(fsg_session* s, double* rho, double* u);
-/* BodyForceField of the last step, IB + virtual force, AoS (session.hpp:148-163). */
+/* BodyForceField of the last step, IB + virtual force, AoS (session.hpp:148-163).
+ * fp64 sessions: the field the collision used.  fp32 sessions: with force
+ * capture on (fsg_set_force_capture) the field the throughput collision
+ * kernel itself consumed, captured cell by cell; otherwise a diagnostic
+ * rebuild from the step's stencil records. */
 int fsg_get_force(fsg_session* s, double* F);
+/* Diagnostic (fp32 coupled steps): have the collision kernel store the body
+ * force it consumes (fixed-point IB band decoded + virtual force, 12 B per
+ * cell per step) for fsg_get_force.  Off by default. */
+int fsg_set_force_capture(fsg_session* s, int on);
 /* Integer stencil sets of the last step, per marker: lo[3], hi[3] (kernel.hpp:36-40). */
 int fsg_get_stencils(fsg_session* s, int* lo_hi);
 

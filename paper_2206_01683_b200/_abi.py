@@ -126,6 +126,7 @@ SIGNATURES = {
     "fsg_get_marker_forces": (C.c_int, [_vp, _vp, _vp, _vp]),
     "fsg_get_macro": (C.c_int, [_vp, _dp, _dp]),
     "fsg_get_force": (C.c_int, [_vp, _dp]),
+    "fsg_set_force_capture": (C.c_int, [_vp, C.c_int]),
     "fsg_get_stencils": (C.c_int, [_vp, _ip]),
     "fsg_set_skin": (C.c_int, [_vp, C.c_int, _i64p, C.POINTER(fsg_skeleton), _dp, _dp, _dp, _dp]),
     "fsg_set_pose": (C.c_int, [_vp, C.POINTER(fsg_body_pose)]),

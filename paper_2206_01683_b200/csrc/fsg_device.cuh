@@ -180,6 +180,8 @@ struct FixBand {
   unsigned* tflag;           // per 4^3 tile: stamp of the last step a stencil touched it
   int tnx, tny, tnz;         // tile grid
   unsigned stamp;            // step stamp (coupled step index + 1; 0 = never)
+  float* fcap;               // diagnostic (fsg_set_force_capture): the body force K4
+                             // consumed this step, IB + virtual, AoS fp32; null = off
 };
 
 __host__ __device__ __forceinline__ unsigned long long ordered_key(double v) {

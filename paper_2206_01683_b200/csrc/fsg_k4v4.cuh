@@ -58,7 +58,7 @@ __device__ __forceinline__ float cell_update(const Grid& g, const DirPtrs& dp,
                                              const float* __restrict__ A, int x, int y, int z,
                                              float Fx, float Fy, float Fz,
                                              const SessionConsts& sc, const StepConsts& st,
-                                             StepScratch* out) {
+                                             StepScratch* out, float* fcap = nullptr) {
   const unsigned m = (unsigned)mem_index(g, x, y, z);
   const int zg = g.z0 + z;
   float s[Q];
@@ -79,7 +79,8 @@ __device__ __forceinline__ float cell_update(const Grid& g, const DirPtrs& dp,
     gather<true>(g, A, x, y, z, s);  // y/z face rows (warp-uniform)
   }
   Band none{nullptr, 0};
-  const float v = collide_cell32<3, VF>(s, x, y, z, g, Fx, Fy, Fz, false, 0, none, sc, st, out);
+  const float v = collide_cell32<3, VF>(s, x, y, z, g, Fx, Fy, Fz, false, 0, none, sc, st, out, fcap,
+                                        (long long)x + (long long)g.nx * ((long long)y + (long long)g.ny * z));
 #pragma unroll
   for (int i = 0; i < Q; ++i) dp.b[i][m] = s[i];
   return v;
@@ -188,7 +189,8 @@ __global__ void __launch_bounds__(128, FSG_K4_MINB)
     // item (stamped: the band phase's)
     if (__ldcg(fb.tflag + (x >> 2) + fb.tnx * ((y >> 2) + fb.tny * (z0 >> 2))) == fb.stamp) continue;
     for (int z = z0; z < z1; ++z)
-      vmin = fminf(vmin, cell_update<PULLED, VF>(g, dp, A, x, y, z, 0.f, 0.f, 0.f, sc, st, out));
+      vmin = fminf(vmin, cell_update<PULLED, VF>(g, dp, A, x, y, z, 0.f, 0.f, 0.f, sc, st, out,
+                                                 fb.fcap));
   }
   // ---- phase B: the stamped tiles, after the marker grid completed.  Block b
   // scans tiles b, b + G, b + 2G ... (G = gridDim.x), one per thread per
@@ -232,7 +234,7 @@ __global__ void __launch_bounds__(128, FSG_K4_MINB)
       const float Fx = (float)((double)f0 * FIX_INV);
       const float Fy = (float)((double)f1 * FIX_INV);
       const float Fz = (float)((double)f2 * FIX_INV);
-      vmin = fminf(vmin, cell_update<PULLED, VF>(g, dp, A, x, y, z, Fx, Fy, Fz, sc, st, out));
+      vmin = fminf(vmin, cell_update<PULLED, VF>(g, dp, A, x, y, z, Fx, Fy, Fz, sc, st, out, fb.fcap));
     }
     __syncthreads();
   }

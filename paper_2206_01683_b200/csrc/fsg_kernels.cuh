@@ -23,6 +23,7 @@
 #pragma once
 
 #include <float.h>
+#include <type_traits>
 #include <math.h>
 
 #include "fsg_device.cuh"
@@ -237,101 +238,187 @@ __device__ __forceinline__ void report_min(StepScratch* out, double v) {
 }
 
 #if FSG_PREC == 32
-/// fp32 BGK + Guo collision of one cell in deviation form (solver.hpp:129-154
+// Arithmetic type of the throughput collision: the populations are STORED as
+// fp32 deviations g_i = f_i - w_i (152 B per cell update) in every variant;
+// FSG_C32_MATH selects the arithmetic between the load and the store:
+//   0  fp32 (the default) with conservation-exact constants (the host picks
+//      fp32 omega*w_i, 1 - omega so that the mass and momentum identities
+//      hold exactly, fsg_session.cu conserving_consts_f32) and the odd part
+//      of the equilibrium built from j = m + F/2 directly.  Independently
+//      rounded constants made rho - 1 and u drift ~1e-7 per step (7e-5 / 2e-4
+//      rel-L2 after 1000 c2 steps); with exact identities c1/c2/c3 stay at
+//      1e-7 .. 3e-6 (tests/test_long_parity_gpu.py)
+//   1  fp64 (the session's fp64 constants, vf_term<double>): ~2e-7 but
+//      spills at 80 registers, 512^3 K4 10-20 % slower
+//   2  fp64 moments (rho - 1, m summed in fp64), the rest fp32
+#ifndef FSG_C32_MATH
+#define FSG_C32_MATH 0
+#endif
+#if FSG_C32_MATH == 1
+using CMath = double;
+#else
+using CMath = float;
+#endif
+constexpr bool kMoments64 = FSG_C32_MATH == 2;
+
+__device__ __forceinline__ float fma_m(float a, float b, float c) { return fmaf(a, b, c); }
+__device__ __forceinline__ double fma_m(double a, double b, double c) { return fma(a, b, c); }
+
+/// BGK + Guo collision of one cell in deviation form (solver.hpp:129-154
 /// restated for g_i = f_i - w_i), with the session force assembled as the
-/// reference does (IB band force, then + virtual force, session.hpp:148-163).
-/// Overwrites s with the post-collision deviations; returns min(post f).
+/// reference does (IB band force, then + virtual force, session.hpp:148-163),
+/// in arithmetic type M on fp32 storage.  Overwrites s with the
+/// post-collision deviations (rounded to fp32); returns min(post f).
+template <class M, int FMODE, bool VF>
+__device__ __forceinline__ float collide_cell_m(float (&s)[Q], int x, int y, int z, const Grid& g,
+                                                float Fx_in, float Fy_in, float Fz_in, bool in_band,
+                                                long long lc, const Band& band,
+                                                const SessionConsts& sc, const StepConsts& st,
+                                                StepScratch* out, float* fcap = nullptr,
+                                                long long cidx = 0) {
+  constexpr bool D = sizeof(M) == 8;
+  // moment arithmetic: fp64 when M is, or when only the moments are
+  using MM = typename std::conditional<D || kMoments64, double, float>::type;
+  M v[Q];
+#pragma unroll
+  for (int i = 0; i < Q; ++i) v[i] = (M)s[i];
+  M drho, mx, my, mz, rho;
+  {
+    MM w[Q];
+#pragma unroll
+    for (int i = 0; i < Q; ++i) w[i] = (MM)s[i];
+    // moments from opposite-pair sums/differences (pairs (1,2),(3,4),...,(17,18))
+    const MM d1 = w[1] - w[2], d3 = w[3] - w[4], d5 = w[5] - w[6], d7 = w[7] - w[8],
+             d9 = w[9] - w[10], d11 = w[11] - w[12], d13 = w[13] - w[14], d15 = w[15] - w[16],
+             d17 = w[17] - w[18];
+    const MM dr = ((w[0] + ((w[1] + w[2]) + (w[3] + w[4]))) + ((w[5] + w[6]) + (w[7] + w[8]))) +
+                  (((w[9] + w[10]) + (w[11] + w[12])) + ((w[13] + w[14]) + ((w[15] + w[16]) + (w[17] + w[18]))));
+    drho = (M)dr;
+    mx = (M)((d1 + d7) + (d9 + (d11 + d13)));
+    my = (M)((d3 + d7) + ((d15 + d17) - d9));
+    mz = (M)((d5 + d11) + ((d15 - d13) - d17));
+    rho = (M)((MM)1 + dr);
+  }
+  M Fx = (M)Fx_in, Fy = (M)Fy_in, Fz = (M)Fz_in;
+  if constexpr (FMODE == 2 || FMODE == 3) {  // 3: IB force already in Fx..Fz (fixed-point band)
+    if constexpr (FMODE == 2) {
+      Fx = in_band ? (M)band.F[3 * lc] : (M)0;
+      Fy = in_band ? (M)band.F[3 * lc + 1] : (M)0;
+      Fz = in_band ? (M)band.F[3 * lc + 2] : (M)0;
+    }
+    if constexpr (VF) {
+      M bx = 0, by = 0, bz = 0;
+      if (rho > (M)0) {
+        const M ir = (M)1 / rho;
+        bx = mx * ir;
+        by = my * ir;
+        bz = mz * ir;
+      }
+#ifndef FSG_VF64
+#define FSG_VF64 (FSG_C32_MATH == 1)
+#endif
+      if constexpr (FSG_VF64) {
+        double vx, vy, vz;
+        vf_term<double>(sc, st, x, y, g.z0 + z, (double)rho, (double)bx, (double)by, (double)bz,
+                        vx, vy, vz);
+        Fx = (M)((double)Fx + vx);
+        Fy = (M)((double)Fy + vy);
+        Fz = (M)((double)Fz + vz);
+      } else {
+        float vx, vy, vz;
+        vf_term32(sc, st, x, y, g.z0 + z, (float)rho, (float)bx, (float)by, (float)bz, vx, vy, vz);
+        Fx += (M)vx;
+        Fy += (M)vy;
+        Fz += (M)vz;
+      }
+    }
+    if (!(rho > (M)0)) {
+      atomicAdd(&out->nonpos, 1);
+      __threadfence();
+    }
+  }
+  if (fcap) {  // diagnostic: the force this collision consumes
+    fcap[3 * cidx] = (float)Fx;
+    fcap[3 * cidx + 1] = (float)Fy;
+    fcap[3 * cidx + 2] = (float)Fz;
+  }
+  const M inv_rho = (M)1 / rho;
+  // equilibrium momentum j = rho u = m + F/2 (solver.hpp:134-137); the odd
+  // (momentum-carrying) part of the equilibrium is built from j itself, not
+  // from rho * (j / rho), so momentum relaxes exactly toward j
+  const M jx = mx + (M)0.5 * Fx, jy = my + (M)0.5 * Fy, jz = mz + (M)0.5 * Fz;
+  const M ux = jx * inv_rho;
+  const M uy = jy * inv_rho;
+  const M uz = jz * inv_rho;
+  const M u2 = ux * ux + uy * uy + uz * uz;
+  if (!isfinite(rho + u2)) {
+    out->nonfinite = 1;
+    __threadfence();
+  }
+  const M uF3 = (M)3 * (ux * Fx + uy * Fy + uz * Fz);
+  const M h15u2 = (M)1.5 * u2;
+  // Pair form of  g'_i = (1-w) g_i + w w_i (drho + rho X_i) + guo w_i S_i  with
+  // X = 3 eu + 4.5 eu^2 - 1.5 u^2 and S = 3(e-u).F + 9 eu e.F: for e_j = -e_i the
+  // even parts (4.5 t^2 - 1.5u^2, 9 t q - 3 u.F) are shared and the odd parts
+  // (3t, 3q) flip sign, t = e.u, q = e.F; rho 3t is taken as 3 e.j.
+  M om1, ow0, ow1, ow2, gw0, gw1, gw2;
+  if constexpr (D) {
+    om1 = 1.0 - sc.omega;
+    ow0 = sc.omega * (1.0 / 3.0);
+    ow1 = sc.omega * (1.0 / 18.0);
+    ow2 = sc.omega * (1.0 / 36.0);
+    gw0 = sc.guo * (1.0 / 3.0);
+    gw1 = sc.guo * (1.0 / 18.0);
+    gw2 = sc.guo * (1.0 / 36.0);
+  } else {
+    om1 = sc.om1_f;
+    ow0 = sc.ow_f[0], ow1 = sc.ow_f[1], ow2 = sc.ow_f[2];
+    gw0 = sc.gw_f[0], gw1 = sc.gw_f[1], gw2 = sc.gw_f[2];
+  }
+  const M owr1 = ow1 * rho, owr2 = ow2 * rho;
+  const M owd1 = fma_m(ow1, drho, -gw1 * uF3);
+  const M owd2 = fma_m(ow2, drho, -gw2 * uF3);
+  const M g9_1 = (M)9 * gw1, g9_2 = (M)9 * gw2;
+  const M g3_1 = (M)3 * gw1, g3_2 = (M)3 * gw2;
+  const float p0 = (float)fma_m(om1, v[0], fma_m(ow0, fma_m(rho, -h15u2, drho), -gw0 * uF3));
+  s[0] = p0;
+  float min1 = FLT_MAX, min2 = FLT_MAX;
+#define FSG_PAIR(I, OWR, OW, OWD, G9, G3, MN)                                            \
+  {                                                                                       \
+    constexpr int a = ex_of(I), b = ey_of(I), c = ez_of(I);                               \
+    const M t = edot<a, b, c, M>(ux, uy, uz);                                             \
+    const M q = edot<a, b, c, M>(Fx, Fy, Fz);                                             \
+    const M S = fma_m(G9, t * q, fma_m(OWR, fma_m((M)4.5 * t, t, -h15u2), OWD));          \
+    const M A = fma_m(OW, (M)3 * edot<a, b, c, M>(jx, jy, jz), G3 * q);                  \
+    const float gi = (float)fma_m(om1, v[I], S + A);                                      \
+    const float gj = (float)fma_m(om1, v[(I) + 1], S - A);                                \
+    s[I] = gi;                                                                            \
+    s[(I) + 1] = gj;                                                                      \
+    MN = fminf(MN, fminf(gi, gj));                                                        \
+  }
+  FSG_PAIR(1, owr1, ow1, owd1, g9_1, g3_1, min1)
+  FSG_PAIR(3, owr1, ow1, owd1, g9_1, g3_1, min1)
+  FSG_PAIR(5, owr1, ow1, owd1, g9_1, g3_1, min1)
+  FSG_PAIR(7, owr2, ow2, owd2, g9_2, g3_2, min2)
+  FSG_PAIR(9, owr2, ow2, owd2, g9_2, g3_2, min2)
+  FSG_PAIR(11, owr2, ow2, owd2, g9_2, g3_2, min2)
+  FSG_PAIR(13, owr2, ow2, owd2, g9_2, g3_2, min2)
+  FSG_PAIR(15, owr2, ow2, owd2, g9_2, g3_2, min2)
+  FSG_PAIR(17, owr2, ow2, owd2, g9_2, g3_2, min2)
+#undef FSG_PAIR
+  // min over post-collision f = g' + w_i, per weight class (monotone in g')
+  return fminf(p0 + (float)(1.0 / 3.0), fminf(min1 + (float)(1.0 / 18.0), min2 + (float)(1.0 / 36.0)));
+}
+
 template <int FMODE, bool VF>
 __device__ __forceinline__ float collide_cell32(float (&s)[Q], int x, int y, int z, const Grid& g,
                                                 float Fx, float Fy, float Fz, bool in_band,
                                                 long long lc, const Band& band,
                                                 const SessionConsts& sc, const StepConsts& st,
-                                                StepScratch* out) {
-  // moments from opposite-pair sums/differences (pairs (1,2),(3,4),...,(17,18))
-  const float d1 = s[1] - s[2], d3 = s[3] - s[4], d5 = s[5] - s[6], d7 = s[7] - s[8],
-              d9 = s[9] - s[10], d11 = s[11] - s[12], d13 = s[13] - s[14], d15 = s[15] - s[16],
-              d17 = s[17] - s[18];
-  const float drho = ((s[0] + ((s[1] + s[2]) + (s[3] + s[4]))) + ((s[5] + s[6]) + (s[7] + s[8]))) +
-                     (((s[9] + s[10]) + (s[11] + s[12])) + ((s[13] + s[14]) + ((s[15] + s[16]) + (s[17] + s[18]))));
-  const float mx = (d1 + d7) + (d9 + (d11 + d13));
-  const float my = (d3 + d7) + ((d15 + d17) - d9);
-  const float mz = (d5 + d11) + ((d15 - d13) - d17);
-  const float rho = 1.0f + drho;
-  if constexpr (FMODE == 2 || FMODE == 3) {  // 3: IB force already in Fx..Fz (fixed-point band)
-    if constexpr (FMODE == 2) {
-      Fx = in_band ? (float)band.F[3 * lc] : 0.0f;
-      Fy = in_band ? (float)band.F[3 * lc + 1] : 0.0f;
-      Fz = in_band ? (float)band.F[3 * lc + 2] : 0.0f;
-    }
-    if constexpr (VF) {
-      float bx = 0.f, by = 0.f, bz = 0.f;
-      if (rho > 0.0f) {
-        const float ir = 1.0f / rho;
-        bx = mx * ir;
-        by = my * ir;
-        bz = mz * ir;
-      }
-      float vx, vy, vz;
-      vf_term32(sc, st, x, y, g.z0 + z, rho, bx, by, bz, vx, vy, vz);
-      Fx += vx;
-      Fy += vy;
-      Fz += vz;
-    }
-    if (!(rho > 0.0f)) {
-      atomicAdd(&out->nonpos, 1);
-      __threadfence();
-    }
-  }
-  const float inv_rho = 1.0f / rho;
-  const float ux = (mx + 0.5f * Fx) * inv_rho;
-  const float uy = (my + 0.5f * Fy) * inv_rho;
-  const float uz = (mz + 0.5f * Fz) * inv_rho;
-  const float u2 = ux * ux + uy * uy + uz * uz;
-  if (!isfinite(rho + u2)) {
-    out->nonfinite = 1;
-    __threadfence();
-  }
-  const float uF3 = 3.0f * (ux * Fx + uy * Fy + uz * Fz);
-  const float h15u2 = 1.5f * u2;
-  // Pair form of  g'_i = (1-w) g_i + w w_i (drho + rho X_i) + guo w_i S_i  with
-  // X = 3 eu + 4.5 eu^2 - 1.5 u^2 and S = 3(e-u).F + 9 eu e.F: for e_j = -e_i the
-  // even parts (4.5 t^2 - 1.5u^2, 9 t q - 3 u.F) are shared and the odd parts
-  // (3t, 3q) flip sign, t = e.u, q = e.F.
-  const float om1 = sc.om1_f;
-  const float owr1 = sc.ow_f[1] * rho, owr2 = sc.ow_f[2] * rho;
-  const float owt1 = 3.0f * owr1, owt2 = 3.0f * owr2;
-  const float owd1 = fmaf(sc.ow_f[1], drho, -sc.gw_f[1] * uF3);
-  const float owd2 = fmaf(sc.ow_f[2], drho, -sc.gw_f[2] * uF3);
-  const float g9_1 = 9.0f * sc.gw_f[1], g9_2 = 9.0f * sc.gw_f[2];
-  const float g3_1 = 3.0f * sc.gw_f[1], g3_2 = 3.0f * sc.gw_f[2];
-  const float p0 = fmaf(om1, s[0], fmaf(sc.ow_f[0], fmaf(rho, -h15u2, drho), -sc.gw_f[0] * uF3));
-  s[0] = p0;
-  float min1 = FLT_MAX, min2 = FLT_MAX;
-#define FSG_PAIR(I, OWR, OWT, OWD, G9, G3, MN)                                            \
-  {                                                                                       \
-    constexpr int a = ex_of(I), b = ey_of(I), c = ez_of(I);                               \
-    const float t = edot<a, b, c, float>(ux, uy, uz);                                     \
-    const float q = edot<a, b, c, float>(Fx, Fy, Fz);                                     \
-    const float S = fmaf(G9, t * q, fmaf(OWR, fmaf(4.5f * t, t, -h15u2), OWD));           \
-    const float A = fmaf(OWT, t, G3 * q);                                                 \
-    const float gi = fmaf(om1, s[I], S + A);                                              \
-    const float gj = fmaf(om1, s[(I) + 1], S - A);                                        \
-    s[I] = gi;                                                                            \
-    s[(I) + 1] = gj;                                                                      \
-    MN = fminf(MN, fminf(gi, gj));                                                        \
-  }
-  FSG_PAIR(1, owr1, owt1, owd1, g9_1, g3_1, min1)
-  FSG_PAIR(3, owr1, owt1, owd1, g9_1, g3_1, min1)
-  FSG_PAIR(5, owr1, owt1, owd1, g9_1, g3_1, min1)
-  FSG_PAIR(7, owr2, owt2, owd2, g9_2, g3_2, min2)
-  FSG_PAIR(9, owr2, owt2, owd2, g9_2, g3_2, min2)
-  FSG_PAIR(11, owr2, owt2, owd2, g9_2, g3_2, min2)
-  FSG_PAIR(13, owr2, owt2, owd2, g9_2, g3_2, min2)
-  FSG_PAIR(15, owr2, owt2, owd2, g9_2, g3_2, min2)
-  FSG_PAIR(17, owr2, owt2, owd2, g9_2, g3_2, min2)
-#undef FSG_PAIR
-  // min over post-collision f = g' + w_i, per weight class (monotone in g')
-  return fminf(p0 + (float)(1.0 / 3.0), fminf(min1 + (float)(1.0 / 18.0), min2 + (float)(1.0 / 36.0)));
+                                                StepScratch* out, float* fcap = nullptr,
+                                                long long cidx = 0) {
+  return collide_cell_m<CMath, FMODE, VF>(s, x, y, z, g, Fx, Fy, Fz, in_band, lc, band, sc, st, out,
+                                          fcap, cidx);
 }
 #endif
 

@@ -158,6 +158,8 @@ struct fsg_session {
   // throughput (fp32) IB: fixed-point tile band
   fsg::FixBand fix{};
   unsigned stamp = 0;          // coupled step stamp (fix.tflag)
+  float* d_fcap = nullptr;     // fsg_set_force_capture: the force K4 consumed (AoS fp32)
+  bool fcap_on = false, last_fcap = false;
   // z-slab halo exchange: session-owned device planes and the event after
   // which this step's boundary planes are packed
   void* d_hsend[2] = {nullptr, nullptr};  // lo, hi
@@ -369,6 +371,51 @@ int launch_step(fsg_session* s, int p, bool copy_mk, bool frame_on) {
 
 }  // namespace
 
+// fp32 collision constants (throughput mode) chosen so that the lattice
+// conservation identities hold EXACTLY in real arithmetic on the rounded
+// constants: with ow1 = omega'/18, ow2 = ow1/2, ow0 = 6 ow1 and
+// om1 = 1 - 18 ow1 all exactly representable,
+//   mass      om1 + ow0 + 6 ow1 + 12 ow2 = 1
+//   momentum  om1 + 3 (2 ow1 + 8 ow2)   = 1
+// (the same for guo * w_i).  Independently rounded constants break both by
+// ~1e-7 per step -- a systematic drift of rho - 1 and u that reached 7e-5 /
+// 2e-4 rel-L2 after 1000 steps of the c2 koi scene; the exact identities leave
+// only data-dependent rounding.  omega' differs from omega by a few ulp of
+// fp32 (a viscosity change < 1e-6 relative).
+static float consistent_w18(double c, bool with_om1) {
+  const float a0 = (float)(c / 18.0);
+  float best = a0;
+  double err = 1e300;
+  float up = a0, dn = a0;
+  for (int k = 0; k < 64; ++k) {
+    for (float a : {up, dn}) {
+      const double ad = (double)a;
+      const bool ok6 = (double)(float)(6.0 * ad) == 6.0 * ad && (double)(a * 0.5f) == 0.5 * ad;
+      const bool ok18 = !with_om1 || (double)(float)(1.0 - 18.0 * ad) == 1.0 - 18.0 * ad;
+      const double e = fabs(ad - c / 18.0);
+      if (ok6 && ok18 && e < err) {
+        err = e;
+        best = a;
+      }
+    }
+    up = nextafterf(up, 1e30f);
+    dn = nextafterf(dn, -1e30f);
+  }
+  return best;
+}
+
+static void conserving_consts_f32(double omega, double guo, float& om1, float ow[3], float gw[3]) {
+  const float o1 = consistent_w18(omega, true);
+  ow[1] = o1;
+  ow[2] = o1 * 0.5f;
+  ow[0] = (float)(6.0 * (double)o1);
+  om1 = (float)(1.0 - 18.0 * (double)o1);
+  const float g1 = consistent_w18(guo, false);
+  gw[1] = g1;
+  gw[2] = g1 * 0.5f;
+  gw[0] = (float)(6.0 * (double)g1);
+}
+
 extern "C" {
 
 const char* fsg_last_error(void) { return g_err; }
@@ -476,12 +523,7 @@ int fsg_create(const fsg_config* cfg_in, fsg_session** out) {
   sc.kernel = cfg.kernel;
   sc.wall = cfg.wall;
   sc.frame_on = cfg.frame_mode != FSG_FRAME_NONE;
-  const double wcls[3] = {1.0 / 3.0, 1.0 / 18.0, 1.0 / 36.0};
-  sc.om1_f = (float)(1.0 - sc.omega);
-  for (int k = 0; k < 3; ++k) {
-    sc.ow_f[k] = (float)(sc.omega * wcls[k]);
-    sc.gw_f[k] = (float)(sc.guo * wcls[k]);
-  }
+  conserving_consts_f32(sc.omega, sc.guo, sc.om1_f, sc.ow_f, sc.gw_f);
   s->frame.q[0] = 1.0;
 
   auto fail = [&](int code) {
@@ -600,6 +642,7 @@ int fsg_destroy(fsg_session* s) {
   cudaFree(s->band.F);
   cudaFree(s->fix.F);
   cudaFree(s->fix.tflag);
+  cudaFree(s->d_fcap);
   for (int k = 0; k < 2; ++k) {
     cudaFree(s->d_hsend[k]);
     cudaFree(s->d_hrecv[k]);
@@ -1071,6 +1114,7 @@ int fsg_step_async(fsg_session* s) {
       // without markers is the plain fluid K4 below.
       fsg::FixBand fb = s->fix;
       fb.stamp = ++s->stamp;
+      fb.fcap = s->fcap_on ? s->d_fcap : nullptr;
       // skinned bodies: up to two are skinned and reduced inside the marker
       // kernel; more take the separate skin kernels around it
       const bool fused = s->skin && s->skp.nb <= 2;
@@ -1133,6 +1177,7 @@ int fsg_step_async(fsg_session* s) {
   if (s->mk_host && s->mk_slot >= 0) s->last_mk_slot = s->mk_slot;
   s->prev_pulled = s->pulled;
   s->last_frame_on = frame_on;
+  s->last_fcap = s->fcap_on && s->m > 0 && s->L->markers_fix != nullptr;
   s->par ^= 1;
   s->pulled = 1;
   s->last_valid = true;
@@ -1296,6 +1341,14 @@ int fsg_get_macro(fsg_session* s, double* rho, double* u) {
   return FSG_OK;
 }
 
+int fsg_set_force_capture(fsg_session* s, int on) {
+  if (!s) return set_err(FSG_EINPUT, "null session");
+  CU(cudaSetDevice(s->cfg.device));
+  if (on && !s->d_fcap) CU(cudaMalloc(&s->d_fcap, sizeof(float) * 3 * (size_t)s->g.n));
+  s->fcap_on = on != 0;
+  return FSG_OK;
+}
+
 int fsg_get_force(fsg_session* s, double* F) {
   if (!s->last_valid) return set_err(FSG_ESTATE, "no coupled step since the last state change");
   CU(cudaSetDevice(s->cfg.device));
@@ -1303,6 +1356,16 @@ int fsg_get_force(fsg_session* s, double* F) {
   int rc = ensure_tmp(s, sizeof(double) * 3 * n);
   if (rc) return rc;
   StepScratch* bscr = s->d_scr[s->last_par];
+  if (s->last_fcap) {
+    // the field the throughput K4 itself consumed (fixed-point IB band
+    // decoded + virtual force), captured as it collided each cell
+    std::vector<float> f(3 * n);
+    CU(cudaMemcpyAsync(f.data(), s->d_fcap, sizeof(float) * 3 * n, cudaMemcpyDeviceToHost,
+                       s->stream));
+    CU(cudaStreamSynchronize(s->stream));
+    for (size_t i = 0; i < 3 * n; ++i) F[i] = (double)f[i];
+    return FSG_OK;
+  }
   if (s->L->markers_fix) {
     // Throughput path: K4 consumed (and re-zeroed) the fixed-point band, so
     // this diagnostic rebuilds the IB field from the stored stencil records

@@ -509,6 +509,11 @@ class CoupledSession:
         check(_abi.lib().fsg_get_macro(self._h, dptr(rho), dptr(u)))
         return rho, u.reshape(-1, 3)
 
+    def set_force_capture(self, on: bool = True) -> None:
+        """fp32 coupled steps: make force() return the body force the collision
+        kernel consumed (captured cell by cell) instead of a rebuild."""
+        check(_abi.lib().fsg_set_force_capture(self._h, 1 if on else 0))
+
     def force(self) -> np.ndarray:
         """BodyForceField of the last step (IB + virtual force), [n,3]."""
         F = np.empty(3 * self.n_cells)
