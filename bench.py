@@ -21,15 +21,17 @@ time.
               workload on this box's cores.
 
 Workloads (BASELINE.json configs): c1 64^3 sphere, c2 128x64x64 koi in an
-accelerating frame (default, configs[1]), c3 256x128x128 two-koi school,
-c4 512^3 pure LBM z-slab-decomposed over the ranks (NCCL halo exchange of the
-boundary planes overlapped with the interior update; weak scaling: 512^3 per
-rank, or --c4-scaling strong), c5 96x48x48 env.  Under torchrun the other
-workloads run one independent replica per rank (weak scaling, no data-path
-collective).
+accelerating frame, c3 256x128x128 two-koi school (default on one GPU: the
+largest single-GPU config, where the HBM fraction is judged), c4 512^3 pure
+LBM z-slab-decomposed over the ranks (default on N > 1 GPUs; weak scaling:
+512^3 per rank, or --c4-scaling strong; the halo exchange runs inside libfsg,
+the boundary-plane kernel storing into the neighbours' halos over NVLink),
+c5 96x48x48 envs.  Under torchrun the other workloads run one independent
+replica per rank (weak scaling, no data-path collective).  --gpus N (N > 1)
+outside torchrun relaunches itself as N ranks.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                  [--workload c2] [--no-cpu-baseline]
+                  [--workload c3] [--halo peer|nccl] [--no-cpu-baseline]
 """
 from __future__ import annotations
 
@@ -55,7 +57,15 @@ def parse_args():
     ap.add_argument("--steps", type=int, default=1000)
     ap.add_argument("--warmup", type=int, default=20)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="c2", choices=["c1", "c2", "c3", "c4", "c5"])
+    ap.add_argument("--workload", default=None, choices=["c1", "c2", "c3", "c4", "c5"],
+                    help="default: c3 (the largest single-GPU config) on one GPU, c4 (the "
+                         "slab-decomposed 512^3 grid, weak scaling) on N > 1")
+    ap.add_argument("--halo", default="peer", choices=["peer", "nccl"],
+                    help="c4 on N > 1: halo exchange inside libfsg over NVLink peer memory "
+                         "(fsg_peer_*), or NCCL point-to-point through torch.distributed")
+    ap.add_argument("--cpu-dry-run", action="store_true",
+                    help="(tests) no GPU: spawn the ranks, rendezvous over gloo, all-gather "
+                         "the slab handles and run the halo routing of c4 on host tensors")
     ap.add_argument("--envs", type=int, default=None,
                     help="c5: envs per GPU (default 8: 64 envs on 8 GPUs)")
     ap.add_argument("--c5-mode", default="batch", choices=["batch", "streams"],
@@ -146,6 +156,51 @@ class ClockSampler:
                 "samples": len(sm)}
 
 
+def share_device() -> bool:
+    """FSG_BENCH_SHARE_DEVICE=1 (testing the multi-rank path on a one-GPU
+    box): every rank on device 0, gloo instead of NCCL for the bench's own
+    barriers and reductions (NCCL refuses two ranks on one device).  The
+    ranks are time-sliced on the device, so its numbers are not throughput."""
+    return os.environ.get("FSG_BENCH_SHARE_DEVICE", "0") == "1"
+
+
+def coll_device(dev):
+    import torch
+    return torch.device("cpu") if share_device() else dev
+
+
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.startswith("model name"):
+                    return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    import platform
+    return platform.processor() or "unknown"
+
+
+def workload_config(scene, args, world):
+    """The `config` object of a bench line -- the workload only, identical in
+    both arms (ours and --impl reference) for the same command line."""
+    m = scene.m
+    skinned = bool(m) and args.markers == "skinned"
+    cfg = {"workload": scene.name, "dims": list(scene.dims), "markers": m,
+           "marker_source": ("skinned on device" if skinned else "host arrays") if m else None,
+           "frame": scene.frame_mode}
+    if args.workload == "c4":
+        nx, ny, nz = scene.dims
+        cfg["dims"] = [nx, ny, nz * world if args.c4_scaling == "weak" else nz]
+        cfg["parallelism"] = (f"z-slabs x{world} ({args.c4_scaling})" if world > 1 else "single GPU")
+    elif args.workload == "c5":
+        cfg["envs_per_gpu"] = args.envs or 8
+        cfg["parallelism"] = f"replicas x{world}" if world > 1 else "single GPU"
+    else:
+        cfg["parallelism"] = f"replicas x{world}" if world > 1 else "single GPU"
+    return cfg
+
+
 # ------------------------------------------------------------ CPU (ref) ----
 def cpu_reference_mlups(scene, seconds: float, max_steps: int = 400):
     """The reference's own CPU code (oracle/_ref: the reference headers compiled
@@ -153,6 +208,10 @@ def cpu_reference_mlups(scene, seconds: float, max_steps: int = 400):
     CoupledSession::step on the same synthetic scene.  Falls back to the C
     restatement (oracle/liboracle.so) when _ref was not built."""
     import numpy as np
+    if "TORCHELASTIC_RUN_ID" in os.environ:
+        # torchrun pins OMP_NUM_THREADS=1 per rank; the CPU reference (rank 0
+        # only) uses every host core.  Set before the oracle's OpenMP runtime loads.
+        os.environ["OMP_NUM_THREADS"] = str(os.cpu_count() or 1)
     from oracle import bind as B
     kind = "reference" if B.have_ref() else "port"
     fm = {"none": 0, "translation": 1, "translation_yaw": 2, "full": 3}[scene.frame_mode]
@@ -204,6 +263,7 @@ def cpu_reference_mlups(scene, seconds: float, max_steps: int = 400):
         O.orc_session_destroy(h)
     cores = int(os.environ.get("OMP_NUM_THREADS", os.cpu_count() or 1))
     return {"value": scene.n_cells * n / dt / 1e6, "unit": "MLUPS", "cores": cores, "kind": kind,
+            "cpu_model": cpu_model(), "steps": n,
             "sample": f"{n} coupled steps of {scene.name} ({dt:.1f} s wall, fp64, OpenMP)"}
 
 
@@ -221,7 +281,8 @@ def run_slab(args, scene, rank, local, world):
     NZ = nz * world if args.c4_scaling == "weak" else nz
     L = SlabLayout(NZ, world, periodic=False)
     run = SlabRunner(dict(dims=(nx, ny, NZ), dx=scene.dx, dt=scene.dt, rho=scene.rho, nu=scene.nu,
-                          frame_mode="none", precision="fp32", device=local, max_markers=1), L, rank)
+                          frame_mode="none", precision="fp32", device=local, max_markers=1), L, rank,
+                     transport=args.halo)
     s = run.session
     stream = torch.cuda.ExternalStream(s.stream, device=dev)
     W, K = args.warmup, args.steps
@@ -235,7 +296,7 @@ def run_slab(args, scene, rank, local, world):
         if world == 1:
             return v
         import torch.distributed as dist
-        t = torch.tensor([v], dtype=torch.float64, device=dev)
+        t = torch.tensor([v], dtype=torch.float64, device=coll_device(dev))
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
@@ -275,10 +336,13 @@ def run_slab(args, scene, rank, local, world):
         "steps": K, "warmup": W, "ms_per_step": round(t_total / K * 1e3, 4), "higher_is_better": True,
         "scaling": args.c4_scaling, "vs_baseline": None, "dtype": "f32 (fp32 storage of f - w_i)",
         "data": "synthetic (fluid at rest, pure LBM; SURVEY.md §8(d) C4)",
-        "config": {"workload": scene.name, "dims": [nx, ny, NZ], "markers": 0, "frame": "none",
-                   "l2": f"state {BYTES_PER_CELL * local_cells / 2 / 1e9:.1f} GB per rank >> L2 (no flush)",
-                   "parallelism": f"z-slabs x{world} ({args.c4_scaling}), NCCL halo {halo_mb:.1f} MB/step/rank"
-                   if world > 1 else "single GPU"},
+        "config": workload_config(scene, args, world),
+        "l2": f"state {BYTES_PER_CELL * local_cells / 2 / 1e9:.1f} GB per rank >> L2 (no flush)",
+        "execution": (f"{world} ranks, one slab each; halo "
+                      + ("inside libfsg: boundary-plane kernel stores into the neighbours' halos "
+                         "over NVLink peer memory (CUDA IPC), stream-ordered delivery counters"
+                         if args.halo == "peer" else "NCCL point-to-point on a comm stream")
+                      + f", {halo_mb:.1f} MB/step/rank") if world > 1 else "single GPU",
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                      "frac": round(achieved / peak, 4),
                      "traffic": k4_traffic("c4") if args.c4_scaling == "weak" and world == 1 else None,
@@ -286,7 +350,9 @@ def run_slab(args, scene, rank, local, world):
                      "peak_source": peak_src},
         "e2e": {"value": round(total_cells * E / e2e_t / 1e6, 1), "unit": "MLUPS",
                 "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 56, "steps": E},
-        "gpu_launches": K * (4 if world > 1 else 1),
+        # peer halo: interior + boundary planes (the exchange is inside the
+        # boundary kernel); nccl: boundary, pack, interior, unpack
+        "gpu_launches": K * ((2 if args.halo == "peer" else 4) if world > 1 else 1),
         "status": {"stable": bool(st.stable()), "min_f": st.min_f},
         "clocks": clk.summary(),
     }
@@ -400,7 +466,7 @@ def run_envs(args, scene, rank, local, world):
     t_total = round_ms * K / 1e3
     if world > 1:
         import torch.distributed as dist
-        t = torch.tensor([t_total], dtype=torch.float64, device=dev)
+        t = torch.tensor([t_total], dtype=torch.float64, device=coll_device(dev))
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         t_total = float(t.item())
     value = E * scene.n_cells * K * world / t_total / 1e6
@@ -441,7 +507,7 @@ def run_envs(args, scene, rank, local, world):
         e2e_t += time.perf_counter() - t0
     if world > 1:
         import torch.distributed as dist
-        t = torch.tensor([e2e_t], dtype=torch.float64, device=dev)
+        t = torch.tensor([e2e_t], dtype=torch.float64, device=coll_device(dev))
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_t = float(t.item())
     e2e_dyn = None
@@ -493,11 +559,10 @@ def run_envs(args, scene, rank, local, world):
         "data": ("synthetic (articulated koi per env skinned on the device from a per-link pose, "
                  "own gait phase; SURVEY.md §8(d) C5)" if skinned else
                  "synthetic (prescribed-kinematics koi per env, own gait phase; SURVEY.md §8(d) C5)"),
-        "config": {"workload": scene.name, "dims": list(scene.dims), "markers": m,
-                   "envs_per_gpu": E, "frame": scene.frame_mode, "l2": "flushed between rounds",
-                   "parallelism": (f"{E} envs per GPU batched: one marker + one collide launch per round"
-                                   if batch else f"{E} env sessions per GPU on {E} streams")
-                                  + (f", replicas x{world}" if world > 1 else "")},
+        "config": workload_config(scene, args, world),
+        "l2": "flushed between rounds",
+        "execution": (f"{E} envs per GPU batched: one marker + one collide launch per round"
+                      if batch else f"{E} env sessions per GPU on {E} streams"),
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                      "frac": round(achieved / peak, 4), "traffic": None,
                      "kernel": ("k_markers_batch + k_collide_band_batch, one round interval" if batch
@@ -623,7 +688,7 @@ def run_ours(args, scene, rank, local, world):
     t_total = step_ms * K / 1e3
     if world > 1:
         import torch.distributed as dist
-        t = torch.tensor([t_total], dtype=torch.float64, device=dev)
+        t = torch.tensor([t_total], dtype=torch.float64, device=coll_device(dev))
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         t_total = float(t.item())
     value = scene.n_cells * K * world / t_total / 1e6
@@ -660,7 +725,7 @@ def run_ours(args, scene, rank, local, world):
     e2e_val = scene.n_cells * E / e2e_t / 1e6
     if world > 1:
         import torch.distributed as dist
-        t = torch.tensor([e2e_t], dtype=torch.float64, device=dev)
+        t = torch.tensor([e2e_t], dtype=torch.float64, device=coll_device(dev))
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_val = scene.n_cells * E * world / float(t.item()) / 1e6
     nb = len(scene.bodies)
@@ -687,10 +752,8 @@ def run_ours(args, scene, rank, local, world):
         "data": ("synthetic (articulated bodies skinned on the device from a prescribed "
                  "per-link pose each step, fluid at rest; SURVEY.md §8(d))" if skinned else
                  "synthetic (prescribed-kinematics bodies, fluid at rest; SURVEY.md §8(d))"),
-        "config": {"workload": scene.name, "dims": list(scene.dims), "markers": m,
-                   "marker_source": "skinned on device" if skinned else ("host arrays" if m else None),
-                   "frame": scene.frame_mode, "l2": "flushed between timed steps",
-                   "parallelism": f"replicas x{world}" if world > 1 else "single GPU"},
+        "config": workload_config(scene, args, world),
+        "l2": "flushed between timed steps",
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                      "frac": round(achieved / peak, 4), "traffic": traffic,
                      "kernel": ("k_collide_band (collide+stream+open BC+VF+IB band) with the "
@@ -715,30 +778,104 @@ def run_ours(args, scene, rank, local, world):
     return out
 
 
+def spawn_ranks(args) -> int:
+    """bench.py --gpus N (N > 1) outside torchrun: relaunch this command as N
+    ranks, one per GPU (torch.distributed.run, rendezvous on 127.0.0.1)."""
+    import socket
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    env = dict(os.environ)
+    if not args.cpu_dry_run:
+        # NCCL's communicator lines (nranks, NVLS/P2P transport) on stderr
+        env.setdefault("NCCL_DEBUG", "INFO")
+        env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+        env.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1", f"--master-port={port}",
+           os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd, env=env)
+
+
+def run_dry(args, rank, world):
+    """--cpu-dry-run (no GPU): the multi-rank launch path of c4 down to the
+    halo exchange -- gloo rendezvous, the slab layout of the weak-scaled
+    512^3-per-rank grid, the all-gather of per-rank handles that
+    fsg_peer_connect consumes, and the halo routing of the NCCL transport on
+    host tensors of one 5-population face (reduced plane) for K steps."""
+    import torch
+    import torch.distributed as dist
+    from paper_2206_01683_b200.slab import SlabLayout, exchange
+    dist.init_process_group("gloo")
+    nx, ny, nz = 512, 512, 512
+    L = SlabLayout(nz * world, world, periodic=False)
+    L.validate()
+    z0, depth = L.planes(rank)
+    handles = [None] * world
+    dist.all_gather_object(handles, {"rank": rank, "z0": z0, "nz": depth})
+    lo, hi = L.neighbours(rank)
+    ok = all(handles[r]["rank"] == r for r in range(world))
+    if lo is not None:
+        ok &= handles[lo]["z0"] + handles[lo]["nz"] == z0
+    if hi is not None:
+        ok &= handles[hi]["z0"] == z0 + depth
+    n = 5 * 64  # 5 populations x a reduced plane
+    for k in range(args.steps):
+        send_lo = torch.full((n,), float(1000 * rank + 2 * k))
+        send_hi = torch.full((n,), float(1000 * rank + 2 * k + 1))
+        recv_lo, recv_hi = torch.full((n,), -1.0), torch.full((n,), -1.0)
+        have_lo, have_hi = exchange(send_lo, send_hi, recv_lo, recv_hi, rank, L)
+        if have_lo:
+            ok &= bool((recv_lo == 1000 * lo + 2 * k + 1).all())
+        if have_hi:
+            ok &= bool((recv_hi == 1000 * hi + 2 * k).all())
+    t = torch.tensor([1 if ok else 0])
+    dist.all_reduce(t, op=dist.ReduceOp.MIN)
+    if rank == 0:
+        print(json.dumps({"dry_run": True, "n_ranks": world, "backend": "gloo",
+                          "workload": "c4", "dims": [nx, ny, nz * world],
+                          "slabs": [[h["z0"], h["nz"]] for h in handles],
+                          "steps": args.steps, "ok": bool(t.item())}))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
 def main():
     args = parse_args()
     rank, local, world = dist_env()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(spawn_ranks(args))
+    if args.cpu_dry_run:
+        run_dry(args, rank, world)
+        return
+    if args.workload is None:
+        args.workload = "c4" if world > 1 else "c3"
     from paper_2206_01683_b200.scenes import make_scene
     scene = make_scene(args.workload)
     if args.impl == "reference":
+        # the reference's own CPU code on the host cores, rank 0 only
         if rank != 0:
             return
         cb = cpu_reference_mlups(cpu_sample_scene(scene), seconds=max(5.0, args.cpu_seconds))
         out = {"metric": METRIC, "value": round(cb["value"], 3), "unit": "MLUPS", "n_gpus": world,
-               "steps": args.steps, "warmup": args.warmup, "higher_is_better": True,
+               "steps": cb["steps"], "warmup": 1, "higher_is_better": True,
                "scaling": "weak", "vs_baseline": None, "dtype": "f64", "impl": "reference",
-               "data": "synthetic", "config": {"workload": scene.name, "dims": list(scene.dims),
-                                               "markers": scene.m},
+               "data": "synthetic", "config": workload_config(scene, args, world),
                "cpu_baseline": cb,
                "e2e": {"value": round(cb["value"], 3), "unit": "MLUPS", "h2d_bytes_per_step": 0,
                        "d2h_bytes_per_step": 0}}
         print(json.dumps(out))
         return
+    if share_device():
+        local = 0
     if world > 1:
         import torch
         import torch.distributed as dist
         torch.cuda.set_device(local)
-        dist.init_process_group("nccl")
+        if share_device():
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     if args.workload == "c4":
         out = run_slab(args, scene, rank, local, world)
     elif args.workload == "c5" and (args.envs or 8) > 1:
@@ -746,7 +883,7 @@ def main():
     else:
         out = run_ours(args, scene, rank, local, world)
     if rank == 0:
-        if not args.no_cpu_baseline:
+        if not args.no_cpu_baseline and world == 1:
             out["cpu_baseline"] = cpu_reference_mlups(cpu_sample_scene(scene), seconds=args.cpu_seconds)
         print(json.dumps(out))
     if world > 1:

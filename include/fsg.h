@@ -428,6 +428,30 @@ int fsg_halo_buffers(fsg_session* s, void** d_send_lo, void** d_send_hi, void** 
 int fsg_halo_begin(fsg_session* s, void* comm_stream);
 int fsg_halo_end(fsg_session* s, void* comm_stream, int have_lo, int have_hi);
 
+/* ---- z-slab peer transport: the halo exchange inside the library ---------
+ * (fp32 slab sessions.)  Each rank exports a handle of its
+ * slab session (CUDA IPC handles of its two distribution buffers and of two
+ * 32-bit delivery counters, plus its geometry), moves the handles between
+ * ranks by any means (MPI, torch.distributed, a file), and connects to its
+ * lower and upper neighbours' handles (NULL at a closed global face).  From
+ * then on fsg_step_async alone runs the sharded step, stream-ordered and
+ * without host involvement: the interior planes; a stream wait until each
+ * neighbour has delivered its previous step's planes; the two boundary
+ * planes, whose collision kernel stores the 5 crossing populations of each
+ * face straight into the neighbour's halo plane (NVLink peer memory); a
+ * stream-ordered counter write into each neighbour.  No pack/unpack, no
+ * NCCL on the data path; the fsg_halo_* calls are not used.
+ * Contract: every rank connects (after all have exported) with its session
+ * idle, all ranks then run the same sequence of steps, and a rank destroys
+ * its session only after all ranks have synchronized (a barrier). */
+#define FSG_PEER_HANDLE_BYTES 512
+typedef struct {
+  unsigned char bytes[FSG_PEER_HANDLE_BYTES];
+} fsg_peer_handle;
+int fsg_peer_export(fsg_session* s, fsg_peer_handle* out);
+int fsg_peer_connect(fsg_session* s, const fsg_peer_handle* lower, const fsg_peer_handle* upper);
+int fsg_peer_disconnect(fsg_session* s);
+
 #ifdef __cplusplus
 }
 #endif

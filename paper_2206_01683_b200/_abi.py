@@ -12,6 +12,8 @@ import os
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
+PEER_HANDLE_BYTES = 512  # FSG_PEER_HANDLE_BYTES (include/fsg.h)
+
 # FSG_LIB: alternative build of the same ABI (dev A/B runs); the default is the in-tree libfsg.so
 LIB_PATH = os.environ.get("FSG_LIB") or os.path.join(HERE, "libfsg.so")
 
@@ -186,6 +188,9 @@ SIGNATURES = {
                                    C.POINTER(_vp)]),
     "fsg_halo_begin": (C.c_int, [_vp, _vp]),
     "fsg_halo_end": (C.c_int, [_vp, _vp, C.c_int, C.c_int]),
+    "fsg_peer_export": (C.c_int, [_vp, C.c_char_p]),
+    "fsg_peer_connect": (C.c_int, [_vp, C.c_char_p, C.c_char_p]),
+    "fsg_peer_disconnect": (C.c_int, [_vp]),
 }
 
 _lib = None

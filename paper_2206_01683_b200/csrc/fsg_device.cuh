@@ -299,6 +299,17 @@ struct BatchHead {
 template <int NB>
 struct SkinParamsN;
 
+// z-slab peer transport (fsg_peer_connect): where the two boundary planes'
+// crossing populations go besides the session's own buffer -- the lower
+// neighbour's top halo plane (ez = -1 populations of local plane 0) and the
+// upper neighbour's bottom halo plane (ez = +1 populations of plane nz-1),
+// each the base of direction 0 of that plane in the neighbour's write buffer
+// (peer memory over NVLink, or the same device).  Null = no neighbour.
+struct PeerOut {
+  float* lo;
+  float* hi;
+};
+
 // Launchers exported by each precision translation unit.
 struct Launchers {
   void (*fill_rest)(const Grid&, void* A, cudaStream_t);
@@ -341,9 +352,11 @@ struct Launchers {
                      cudaStream_t);
   // pure-fluid step (no IB band); planes: 0 all, 1 the two z-boundary planes,
   // 2 the interior planes (z-slab step: boundary first, halo send, interior)
+  // po (planes == 1, peer-connected slabs): the boundary planes' crossing
+  // populations are also stored into the neighbours' halo planes
   void (*collide_fix)(const Grid&, const void* A, int pulled, void* B, const SessionConsts*,
                       const StepConsts& st, int frame_on, StepScratch* scr, StepScratch* scr_next,
-                      int planes, cudaStream_t);
+                      int planes, PeerOut po, cudaStream_t);
   // banded coupled step: one K4 launch, a programmatic dependent (pdl != 0)
   // of the marker kernel launched just before it on the same stream
   void (*collide_band)(const Grid&, const void* A, int pulled, void* B, FixBand,

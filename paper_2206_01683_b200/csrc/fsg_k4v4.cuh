@@ -58,7 +58,8 @@ __device__ __forceinline__ float cell_update(const Grid& g, const DirPtrs& dp,
                                              const float* __restrict__ A, int x, int y, int z,
                                              float Fx, float Fy, float Fz,
                                              const SessionConsts& sc, const StepConsts& st,
-                                             StepScratch* out, float* fcap = nullptr) {
+                                             StepScratch* out, float* fcap = nullptr,
+                                             PeerOut po = PeerOut{nullptr, nullptr}) {
   const unsigned m = (unsigned)mem_index(g, x, y, z);
   const int zg = g.z0 + z;
   float s[Q];
@@ -83,6 +84,25 @@ __device__ __forceinline__ float cell_update(const Grid& g, const DirPtrs& dp,
                                         (long long)x + (long long)g.nx * ((long long)y + (long long)g.ny * z));
 #pragma unroll
   for (int i = 0; i < Q; ++i) dp.b[i][m] = s[i];
+  // peer-connected slab: the crossing populations of the boundary planes go
+  // straight into the neighbours' halo planes (lattice.hpp:25-26: ez = -1
+  // {6,12,13,16,17}, ez = +1 {5,11,14,15,18})
+  if (po.lo && z == 0) {
+    float* d = po.lo + (x + (long long)g.nx * y);
+    d[6 * g.stride] = s[6];
+    d[12 * g.stride] = s[12];
+    d[13 * g.stride] = s[13];
+    d[16 * g.stride] = s[16];
+    d[17 * g.stride] = s[17];
+  }
+  if (po.hi && z == g.nz - 1) {
+    float* d = po.hi + (x + (long long)g.nx * y);
+    d[5 * g.stride] = s[5];
+    d[11 * g.stride] = s[11];
+    d[14 * g.stride] = s[14];
+    d[15 * g.stride] = s[15];
+    d[18 * g.stride] = s[18];
+  }
   return v;
 }
 
@@ -108,7 +128,8 @@ template <bool PULLED, bool VF>
 __global__ void __launch_bounds__(128, FSG_K4_MINB)
     k_collide_fix(Grid g, DirPtrs dp, const float* __restrict__ A,
                   const SessionConsts* __restrict__ scp, const StepConsts st,
-                  StepScratch* __restrict__ out, StepScratch* __restrict__ next, int zc, ZRange zr) {
+                  StepScratch* __restrict__ out, StepScratch* __restrict__ next, int zc, ZRange zr,
+                  PeerOut po) {
   const int tid = threadIdx.x + blockDim.x * threadIdx.y;
   reset_next(next, tid);
   const int tx_n = (g.nx + blockDim.x - 1) / blockDim.x;
@@ -126,7 +147,7 @@ __global__ void __launch_bounds__(128, FSG_K4_MINB)
     if (x >= g.nx || y >= g.ny) continue;
     for (int q = q0; q < q1; ++q)
       vmin = fminf(vmin, cell_update<PULLED, VF>(g, dp, A, x, y, zr.lo + q * zr.step, 0.f, 0.f, 0.f,
-                                                 sc, st, out));
+                                                 sc, st, out, nullptr, po));
   }
   report_min(out, vmin == FLT_MAX ? DBL_MAX : (double)vmin);
 }

@@ -957,7 +957,8 @@ static int L_markers_fix(const Grid& g, const void* A, int pulled, Markers mk,
 }
 static void L_collide_fix(const Grid& g, const void* A, int pulled, void* B,
                           const SessionConsts* sc, const StepConsts& st, int frame_on,
-                          StepScratch* scr, StepScratch* scr_next, int planes, cudaStream_t s) {
+                          StepScratch* scr, StepScratch* scr_next, int planes, PeerOut po,
+                          cudaStream_t s) {
   DirPtrs dp;
   for (int i = 0; i < Q; ++i) {
     dp.a[i] = (const float*)A + (pulled ? g.pull[i] : g.own[i]);
@@ -1017,7 +1018,7 @@ static void L_collide_fix(const Grid& g, const void* A, int pulled, void* B,
   int zc = (int)std::max<long long>(1, nq / std::max<long long>(1, nzc_want));
   zc = std::min(zc, g.plane >= (1 << 17) ? 1 : 2);
 #define FSG_LF(P, V) \
-  k_collide_fix<P, V><<<gr, b, 0, s>>>(g, dp, (const float*)A, sc, st, scr, scr_next, zc, zr)
+  k_collide_fix<P, V><<<gr, b, 0, s>>>(g, dp, (const float*)A, sc, st, scr, scr_next, zc, zr, po)
   if (pulled) {
     if (frame_on) FSG_LF(true, true);
     else FSG_LF(true, false);

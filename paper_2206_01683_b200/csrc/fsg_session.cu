@@ -19,7 +19,9 @@
 // banded K4 as its programmatic dependent (fsg_k4v4.cuh) -- or one K4 when
 // there are no markers.  The host never waits before enqueueing; the status
 // is copied out of the device scratch only when asked for.
+#include <cuda.h>
 #include <cuda_runtime.h>
+#include <unistd.h>
 
 #include <algorithm>
 #include <cfloat>
@@ -159,6 +161,19 @@ struct fsg_session {
   fsg::FixBand fix{};
   unsigned stamp = 0;          // coupled step stamp (fix.tflag)
   float* d_fcap = nullptr;     // fsg_set_force_capture: the force K4 consumed (AoS fp32)
+  // z-slab peer transport (fsg_peer_*): delivery counters written by the
+  // neighbours ([0] from the lower, [1] from the upper), the neighbours'
+  // buffers, and this session's step count since connecting
+  unsigned* d_peer_flags = nullptr;
+  struct PeerLink {
+    bool on = false, ipc = false, owner = false;
+    void* buf[2] = {nullptr, nullptr};
+    unsigned* flags = nullptr;
+    int nz = 0;
+  } nbr[2];
+  int nbr_pid_[2] = {0, 0};
+  bool peer_on = false;
+  unsigned peer_step = 0;
   bool fcap_on = false, last_fcap = false;
   // z-slab halo exchange: session-owned device planes and the event after
   // which this step's boundary planes are packed
@@ -643,6 +658,8 @@ int fsg_destroy(fsg_session* s) {
   cudaFree(s->fix.F);
   cudaFree(s->fix.tflag);
   cudaFree(s->d_fcap);
+  fsg_peer_disconnect(s);
+  cudaFree(s->d_peer_flags);
   for (int k = 0; k < 2; ++k) {
     cudaFree(s->d_hsend[k]);
     cudaFree(s->d_hrecv[k]);
@@ -1082,6 +1099,9 @@ int fsg_get_markers(fsg_session* s, double* pts, double* vel, double* nrm) {
   return FSG_OK;
 }
 
+static int peer_wait(fsg_session* s, unsigned* flag, unsigned v);
+static int peer_signal(fsg_session* s, unsigned* flag, unsigned v);
+
 // ----------------------------------------------------------------- step --
 int fsg_step_async(fsg_session* s) {
   CU(cudaSetDevice(s->cfg.device));
@@ -1143,18 +1163,49 @@ int fsg_step_async(fsg_session* s) {
       if (split)  // beside K4's first phase; fixed tree order; tau + stats into pinned memory
         fsg::skin_tau_launch(s->skp, s->d_fworld, s->d_stencil, s->mk.vel, s->h_wrench[p], 0,
                              s->d_skin_ticket + 1, (unsigned)km_blocks, s->stream);
+    } else if (s->g.zpad && s->peer_on) {
+      // z-slab, peer transport: the interior planes (no halo needed), then a
+      // stream-ordered wait until both neighbours delivered their previous
+      // step's crossing planes into this session's halo (and finished reading
+      // the halo this step overwrites in theirs), then the two boundary planes
+      // with their crossing populations stored straight into the neighbours'
+      // halo planes, then the delivery counter written into each neighbour
+      const unsigned n = ++s->peer_step;
+      s->L->collide_fix(s->g, s->buf[p], s->pulled, s->buf[p ^ 1], s->d_sc, st, frame_on ? 1 : 0,
+                        s->d_scr[p], s->d_scr[p ^ 1], 2, fsg::PeerOut{nullptr, nullptr}, s->stream);
+      for (int k = 0; k < 2; ++k)
+        if (s->nbr[k].on) {
+          int rc = peer_wait(s, s->d_peer_flags + k, n);
+          if (rc) return rc;
+        }
+      fsg::PeerOut po{nullptr, nullptr};
+      if (s->nbr[0].on)  // lower neighbour: its top halo plane (local z = its nz)
+        po.lo = (float*)s->nbr[0].buf[p ^ 1] + s->g.zs * (long long)(s->nbr[0].nz + s->g.zpad);
+      if (s->nbr[1].on)  // upper neighbour: its bottom halo plane (local z = -1)
+        po.hi = (float*)s->nbr[1].buf[p ^ 1];
+      s->L->collide_fix(s->g, s->buf[p], s->pulled, s->buf[p ^ 1], s->d_sc, st, frame_on ? 1 : 0,
+                        s->d_scr[p], s->d_scr[p ^ 1], 1, po, s->stream);
+      CU_LAUNCH();
+      if (s->nbr[0].on) {
+        int rc = peer_signal(s, s->nbr[0].flags + 1, n + 1);
+        if (rc) return rc;
+      }
+      if (s->nbr[1].on) {
+        int rc = peer_signal(s, s->nbr[1].flags + 0, n + 1);
+        if (rc) return rc;
+      }
     } else if (s->g.zpad) {
       // z-slab: the two boundary planes first, packed for the neighbours
       // (fsg_halo_begin lets a comm stream start on them), then the interior
       s->L->collide_fix(s->g, s->buf[p], s->pulled, s->buf[p ^ 1], s->d_sc, st, frame_on ? 1 : 0,
-                        s->d_scr[p], s->d_scr[p ^ 1], 1, s->stream);
+                        s->d_scr[p], s->d_scr[p ^ 1], 1, fsg::PeerOut{nullptr, nullptr}, s->stream);
       s->L->halo_pack(s->g, s->buf[p ^ 1], s->d_hsend[0], s->d_hsend[1], s->stream);
       CU(cudaEventRecord(s->ev_hpack, s->stream));
       s->L->collide_fix(s->g, s->buf[p], s->pulled, s->buf[p ^ 1], s->d_sc, st, frame_on ? 1 : 0,
-                        s->d_scr[p], s->d_scr[p ^ 1], 2, s->stream);
+                        s->d_scr[p], s->d_scr[p ^ 1], 2, fsg::PeerOut{nullptr, nullptr}, s->stream);
     } else {
       s->L->collide_fix(s->g, s->buf[p], s->pulled, s->buf[p ^ 1], s->d_sc, st, frame_on ? 1 : 0,
-                        s->d_scr[p], s->d_scr[p ^ 1], 0, s->stream);
+                        s->d_scr[p], s->d_scr[p ^ 1], 0, fsg::PeerOut{nullptr, nullptr}, s->stream);
     }
     CU_LAUNCH();
     if (prof) {
@@ -1485,6 +1536,222 @@ int fsg_halo_end(fsg_session* s, void* comm_stream, int have_lo, int have_hi) {
   return FSG_OK;
 }
 
+
+// ------------------------------------------------------ peer transport --
+// z-slab halo exchange inside the library: the boundary
+// planes' collision kernel stores the 5 crossing populations of each face
+// straight into the neighbour's halo plane (NVLink peer memory, CUDA IPC
+// across processes), ordered by stream memory operations on 32-bit delivery
+// counters -- no pack/unpack kernels, no host exchange, no NCCL on the data
+// path.  Protocol (every rank runs the same step sequence, so the A/B parity
+// of all slabs agrees): before the boundary planes of step n (n = 1, 2, ...
+// since connecting) a session waits until each neighbour's counter slot is
+// >= n, i.e. that neighbour finished its boundary planes of step n-1 (their
+// crossing populations are in this session's halo, and it has finished
+// reading the halo this step overwrites in its buffer); after them it writes
+// n + 1 into the neighbours' slots (the write is fenced after the kernel's
+// stores).  fsg_peer_connect delivers the current state's boundary planes
+// once (counter 1).
+namespace {
+struct PeerExport {
+  unsigned magic, version;
+  int pid, device;
+  int nx, ny, nz, z0, nzg, zpad, elem, par, periodic, pad_;
+  unsigned long long raw_buf[2], raw_flags;
+  cudaIpcMemHandle_t h_buf[2], h_flags;
+};
+constexpr unsigned kPeerMagic = 0x46534750u;  // "FSGP"
+static_assert(sizeof(PeerExport) <= FSG_PEER_HANDLE_BYTES, "peer handle too small");
+
+using PFN_wait32 = CUresult (*)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+using PFN_write32 = CUresult (*)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+PFN_wait32 g_wait32 = nullptr;
+PFN_write32 g_write32 = nullptr;
+unsigned g_wait_flags = CU_STREAM_WAIT_VALUE_GEQ;
+
+int load_stream_memops(int device) {
+  if (g_wait32 && g_write32) return FSG_OK;
+  cudaDriverEntryPointQueryResult q1, q2;
+  if (cudaGetDriverEntryPoint("cuStreamWaitValue32", (void**)&g_wait32, cudaEnableDefault, &q1) !=
+          cudaSuccess ||
+      cudaGetDriverEntryPoint("cuStreamWriteValue32", (void**)&g_write32, cudaEnableDefault, &q2) !=
+          cudaSuccess ||
+      q1 != cudaDriverEntryPointSuccess || q2 != cudaDriverEntryPointSuccess || !g_wait32 ||
+      !g_write32) {
+    g_wait32 = nullptr;
+    g_write32 = nullptr;
+    return set_err(FSG_ECUDA, "peer transport: stream memory operations unavailable");
+  }
+  int flush = 0;
+  if (cudaDeviceGetAttribute(&flush, (cudaDeviceAttr)CU_DEVICE_ATTRIBUTE_CAN_FLUSH_REMOTE_WRITES,
+                             device) == cudaSuccess &&
+      flush)
+    g_wait_flags |= CU_STREAM_WAIT_VALUE_FLUSH;
+  return FSG_OK;
+}
+}  // namespace
+
+static int peer_wait(fsg_session* s, unsigned* flag, unsigned v) {
+  if (g_wait32((CUstream)s->stream, (CUdeviceptr)flag, v, g_wait_flags) != CUDA_SUCCESS)
+    return set_err(FSG_ECUDA, "cuStreamWaitValue32 failed");
+  return FSG_OK;
+}
+
+static int peer_signal(fsg_session* s, unsigned* flag, unsigned v) {
+  if (g_write32((CUstream)s->stream, (CUdeviceptr)flag, v, CU_STREAM_WRITE_VALUE_DEFAULT) !=
+      CUDA_SUCCESS)
+    return set_err(FSG_ECUDA, "cuStreamWriteValue32 failed");
+  return FSG_OK;
+}
+
+int fsg_peer_export(fsg_session* s, fsg_peer_handle* out) {
+  if (!s || !out) return set_err(FSG_EINPUT, "null argument");
+  if (!s->g.zpad) return set_err(FSG_EINPUT, "fsg_peer_export: not a z-slab session");
+  if (!s->L->markers_fix) return set_err(FSG_EINPUT, "fsg_peer_export: the peer transport runs fp32 (throughput) sessions");
+  if (s->peer_on) return set_err(FSG_ESTATE, "fsg_peer_export: session already connected");
+  CU(cudaSetDevice(s->cfg.device));
+  int rc = load_stream_memops(s->cfg.device);
+  if (rc) return rc;
+  if (!s->d_peer_flags) CU(cudaMalloc(&s->d_peer_flags, 2 * sizeof(unsigned)));
+  CU(cudaStreamSynchronize(s->stream));
+  CU(cudaMemset(s->d_peer_flags, 0, 2 * sizeof(unsigned)));
+  CU(cudaDeviceSynchronize());
+  PeerExport e{};
+  e.magic = kPeerMagic;
+  e.version = 1;
+  e.pid = (int)getpid();
+  e.device = s->cfg.device;
+  e.nx = s->g.nx;
+  e.ny = s->g.ny;
+  e.nz = s->g.nz;
+  e.z0 = s->g.z0;
+  e.nzg = s->g.nzg;
+  e.zpad = s->g.zpad;
+  e.elem = s->L->elem_bytes;
+  e.par = s->par;
+  e.periodic = s->g.periodic;
+  for (int k = 0; k < 2; ++k) {
+    e.raw_buf[k] = (unsigned long long)(uintptr_t)s->buf[k];
+    CU(cudaIpcGetMemHandle(&e.h_buf[k], s->buf[k]));
+  }
+  e.raw_flags = (unsigned long long)(uintptr_t)s->d_peer_flags;
+  CU(cudaIpcGetMemHandle(&e.h_flags, s->d_peer_flags));
+  std::memset(out, 0, sizeof(*out));
+  std::memcpy(out->bytes, &e, sizeof e);
+  return FSG_OK;
+}
+
+static int peer_open(fsg_session* s, const fsg_peer_handle* h, int side) {
+  PeerExport e;
+  std::memcpy(&e, h->bytes, sizeof e);
+  if (e.magic != kPeerMagic || e.version != 1)
+    return set_err(FSG_EINPUT, "fsg_peer_connect: not a peer handle");
+  if (e.nx != s->g.nx || e.ny != s->g.ny || e.nzg != s->g.nzg || e.zpad != s->g.zpad ||
+      e.elem != s->L->elem_bytes || e.periodic != s->g.periodic)
+    return set_err(FSG_EINPUT, "fsg_peer_connect: neighbour slab of another grid");
+  if (e.par != s->par)
+    return set_err(FSG_ESTATE, "fsg_peer_connect: neighbour at another step parity");
+  // geometry: the lower neighbour ends where this slab starts, the upper
+  // starts where it ends (global z, periodic wrap)
+  const int nzg = s->g.nzg;
+  const bool adj = side == 0 ? (e.z0 + e.nz) % nzg == s->g.z0 % nzg
+                             : e.z0 % nzg == (s->g.z0 + s->g.nz) % nzg;
+  if (!adj) return set_err(FSG_EINPUT, "fsg_peer_connect: %s handle is not the adjacent slab",
+                           side == 0 ? "lower" : "upper");
+  auto& L = s->nbr[side];
+  L.nz = e.nz;
+  if (e.pid == (int)getpid()) {  // same process: the pointers themselves
+    if (e.device != s->cfg.device) {
+      const cudaError_t pe = cudaDeviceEnablePeerAccess(e.device, 0);
+      if (pe != cudaSuccess && pe != cudaErrorPeerAccessAlreadyEnabled)
+        return set_err(FSG_ECUDA, "cudaDeviceEnablePeerAccess failed: %s", cudaGetErrorString(pe));
+      cudaGetLastError();
+    }
+    L.buf[0] = (void*)(uintptr_t)e.raw_buf[0];
+    L.buf[1] = (void*)(uintptr_t)e.raw_buf[1];
+    L.flags = (unsigned*)(uintptr_t)e.raw_flags;
+    L.ipc = false;
+  } else {
+    // the same neighbour may be both lower and upper (periodic, 2 slabs):
+    // open its handles once (a process may open a handle only once)
+    const auto& O = s->nbr[side ^ 1];
+    if (O.on && O.ipc && s->nbr_pid_[side ^ 1] == e.pid) {
+      for (int k = 0; k < 2; ++k) L.buf[k] = O.buf[k];
+      L.flags = O.flags;
+      L.owner = false;
+    } else {
+      for (int k = 0; k < 2; ++k)
+        CU(cudaIpcOpenMemHandle(&L.buf[k], e.h_buf[k], cudaIpcMemLazyEnablePeerAccess));
+      void* f = nullptr;
+      CU(cudaIpcOpenMemHandle(&f, e.h_flags, cudaIpcMemLazyEnablePeerAccess));
+      L.flags = (unsigned*)f;
+      L.owner = true;
+    }
+    L.ipc = true;
+  }
+  s->nbr_pid_[side] = e.pid;
+  L.on = true;
+  return FSG_OK;
+}
+
+int fsg_peer_connect(fsg_session* s, const fsg_peer_handle* lower, const fsg_peer_handle* upper) {
+  if (!s) return set_err(FSG_EINPUT, "null session");
+  if (!s->g.zpad) return set_err(FSG_EINPUT, "fsg_peer_connect: not a z-slab session");
+  if (!s->d_peer_flags) return set_err(FSG_ESTATE, "fsg_peer_connect: call fsg_peer_export first");
+  if (s->peer_on) return set_err(FSG_ESTATE, "fsg_peer_connect: already connected");
+  if (!lower && !upper) return set_err(FSG_EINPUT, "fsg_peer_connect: no neighbour");
+  CU(cudaSetDevice(s->cfg.device));
+  int rc = FSG_OK;
+  if (lower && (rc = peer_open(s, lower, 0))) return rc;
+  if (upper && (rc = peer_open(s, upper, 1))) {
+    fsg_peer_disconnect(s);
+    return rc;
+  }
+  // a pulled state needs the neighbours' boundary planes in its halo: deliver
+  // this session's crossing planes of the current state once (counter 1)
+  const size_t eb = (size_t)s->L->elem_bytes, pb = eb * (size_t)s->g.plane;
+  const char* A = (const char*)s->buf[s->par];
+  static const int dn[5] = {6, 12, 13, 16, 17}, up[5] = {5, 11, 14, 15, 18};
+  if (s->pulled) {
+    for (int k = 0; k < 5; ++k) {
+      if (s->nbr[0].on) {  // plane 0 -> lower's top halo plane
+        char* d = (char*)s->nbr[0].buf[s->par] +
+                  eb * (size_t)(s->g.zs * (s->nbr[0].nz + s->g.zpad) + dn[k] * s->g.stride);
+        CU(cudaMemcpyAsync(d, A + eb * (size_t)(s->g.zs * s->g.zpad + dn[k] * s->g.stride), pb,
+                           cudaMemcpyDefault, s->stream));
+      }
+      if (s->nbr[1].on) {  // plane nz-1 -> upper's bottom halo plane
+        char* d = (char*)s->nbr[1].buf[s->par] + eb * (size_t)(up[k] * s->g.stride);
+        CU(cudaMemcpyAsync(
+            d, A + eb * (size_t)(s->g.zs * (s->g.nz - 1 + s->g.zpad) + up[k] * s->g.stride), pb,
+            cudaMemcpyDefault, s->stream));
+      }
+    }
+  }
+  if (s->nbr[0].on && (rc = peer_signal(s, s->nbr[0].flags + 1, 1))) return rc;
+  if (s->nbr[1].on && (rc = peer_signal(s, s->nbr[1].flags + 0, 1))) return rc;
+  s->peer_step = 0;
+  s->peer_on = true;
+  return FSG_OK;
+}
+
+int fsg_peer_disconnect(fsg_session* s) {
+  if (!s) return FSG_OK;
+  if (!s->nbr[0].on && !s->nbr[1].on) return FSG_OK;
+  cudaSetDevice(s->cfg.device);
+  if (s->stream) cudaStreamSynchronize(s->stream);
+  for (int side = 0; side < 2; ++side) {
+    auto& L = s->nbr[side];
+    if (L.on && L.ipc && L.owner) {
+      cudaIpcCloseMemHandle(L.buf[0]);
+      cudaIpcCloseMemHandle(L.buf[1]);
+      cudaIpcCloseMemHandle(L.flags);
+    }
+    L = fsg_session::PeerLink{};
+  }
+  s->peer_on = false;
+  return FSG_OK;
+}
 
 // ---------------------------------------------------------------- batch --
 // E env sessions of one configuration sharing one stream, stepped together

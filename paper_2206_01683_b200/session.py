@@ -562,6 +562,22 @@ class CoupledSession:
         """The session waits for comm_stream, then unpacks the received planes."""
         check(_abi.lib().fsg_halo_end(self._h, comm_stream, int(have_lo), int(have_hi)))
 
+    # -- z-slab peer transport (fsg_peer_*: the halo exchange inside the library)
+    def peer_export(self) -> bytes:
+        """This slab's peer handle (FSG_PEER_HANDLE_BYTES bytes: CUDA IPC handles
+        of its buffers and delivery counters, its geometry)."""
+        buf = C.create_string_buffer(_abi.PEER_HANDLE_BYTES)
+        check(_abi.lib().fsg_peer_export(self._h, buf))
+        return buf.raw
+
+    def peer_connect(self, lower: bytes | None, upper: bytes | None) -> None:
+        """Connect to the neighbours' handles (None at a closed global face);
+        from then on step_async() runs the whole sharded step."""
+        check(_abi.lib().fsg_peer_connect(self._h, lower, upper))
+
+    def peer_disconnect(self) -> None:
+        check(_abi.lib().fsg_peer_disconnect(self._h))
+
 
 class EnvBatch:
     """n_envs independent env sessions of one fp32 configuration stepped

@@ -93,13 +93,25 @@ def device_views(session, dtype_str: str):
 
 
 class SlabRunner:
-    """One rank of a slab-decomposed pure-LBM run: a slab session, a comm
-    stream, and the per-step exchange."""
+    """One rank of a slab-decomposed pure-LBM run: a slab session and its
+    halo transport.
 
-    def __init__(self, cfg_kwargs: dict, layout: SlabLayout, rank: int, group=None):
+    transport="peer" (default): the exchange runs inside libfsg
+    (fsg_peer_*): the handles are all-gathered once over the process group,
+    each session connects to its neighbours, and a step is ONE library call
+    -- the boundary planes' kernel stores the crossing populations straight
+    into the neighbours' halos over NVLink, ordered by stream memory
+    operations.  transport="nccl": the session packs its boundary planes and
+    torch.distributed point-to-point moves them on a comm stream
+    (fsg_halo_begin/end), the pre-peer path, kept for comparison."""
+
+    def __init__(self, cfg_kwargs: dict, layout: SlabLayout, rank: int, group=None,
+                 transport: str = "peer"):
         import torch
         from .session import CoupledSession, SessionConfig
         layout.validate()
+        if transport not in ("peer", "nccl"):
+            raise ValueError(f"unknown transport {transport!r}")
         z0, nz = layout.planes(rank)
         nx, ny, _ = cfg_kwargs["dims"]
         kw = dict(cfg_kwargs)
@@ -111,15 +123,23 @@ class SlabRunner:
         self.z0, self.nz = z0, nz
         # one rank owns the whole grid: a plain session (periodic z wraps in place)
         self.sharded = layout.world > 1
-        self.comm = torch.cuda.Stream(device=self.cfg.device) if self.sharded else None
-        self.bufs = (device_views(self.session, "<f4" if self.cfg.precision == "fp32" else "<f8")
-                     if self.sharded else None)
+        self.transport = transport if self.sharded else None
+        self.comm = None
+        self.bufs = None
+        if self.transport == "nccl":
+            self.comm = torch.cuda.Stream(device=self.cfg.device)
+            self.bufs = device_views(self.session, "<f4" if self.cfg.precision == "fp32" else "<f8")
+        elif self.transport == "peer":
+            import torch.distributed as dist
+            handles = [None] * layout.world
+            dist.all_gather_object(handles, self.session.peer_export(), group=group)
+            connect_peers(self.session, handles, layout, rank)
 
     def step_async(self) -> None:
         import torch
         s = self.session
         s.step_async()
-        if not self.sharded:
+        if self.transport != "nccl":
             return
         s.halo_begin(self.comm.cuda_stream)
         with torch.cuda.stream(self.comm):
@@ -127,7 +147,21 @@ class SlabRunner:
         s.halo_end(self.comm.cuda_stream, have_lo, have_hi)
 
     def close(self) -> None:
+        if self.transport == "peer":
+            # a neighbour may still store into this session's halo until every
+            # rank has drained its stream
+            import torch
+            import torch.distributed as dist
+            torch.cuda.synchronize(self.cfg.device)
+            dist.barrier(group=self.group)
         self.session.close()
+
+
+def connect_peers(session, handles, layout: SlabLayout, rank: int) -> None:
+    """Connect `rank`'s slab session to its neighbours' peer handles."""
+    lo, hi = layout.neighbours(rank)
+    session.peer_connect(handles[lo] if lo is not None else None,
+                         handles[hi] if hi is not None else None)
 
 
 def split_field(arr: np.ndarray, dims, layout: SlabLayout, rank: int, comps: int = 1) -> np.ndarray:
