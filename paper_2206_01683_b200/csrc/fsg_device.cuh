@@ -28,6 +28,7 @@
 #define FSG_KM_MINB 6
 #endif
 
+
 namespace fsg {
 
 // ----------------------------------------------------- dev instrumentation --
@@ -153,6 +154,10 @@ struct StepScratch {
   int bbox_hi_enc[3];
   unsigned work;                     // banded K4: phase-A dynamic work counter
   int _pad;
+  // tile list: tiles stamped this step (the length of FixBand::tlist),
+  // band-phase work counter, marker-kernel block ticket (stamps published)
+  unsigned tcount, bwork, ticket;
+  int _pad2;
 };
 constexpr int LO_BIAS = 0x40000000;
 
@@ -182,7 +187,23 @@ struct FixBand {
   unsigned stamp;            // step stamp (coupled step index + 1; 0 = never)
   float* fcap;               // diagnostic (fsg_set_force_capture): the body force K4
                              // consumed this step, IB + virtual, AoS fp32; null = off
+  // tile list (null: the band phase scans every tile's flag)
+  int* tlist;                // tiles stamped this step, in stamping order (StepScratch::tcount)
+  unsigned* ready;           // set to `stamp` (release) once every tile of the step is stamped
 };
+
+#ifdef __CUDACC__
+// release / acquire at GPU scope (PTX memory model): the marker chain's
+// "every tile stamped" flag (fsg_ib_fix.cuh) and its consumer (fsg_k4v4.cuh)
+__device__ __forceinline__ void st_release_gpu(unsigned* p, unsigned v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ unsigned ld_acquire_gpu(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+#endif
 
 __host__ __device__ __forceinline__ unsigned long long ordered_key(double v) {
 #ifdef __CUDA_ARCH__

@@ -78,6 +78,40 @@ __device__ __forceinline__ void mk_stamp(const Grid& g, const FixBand& fb, const
   }
 }
 
+/// Stamp with the step's tile list (fb.tlist): the first stamp of a tile
+/// this step appends it, so the banded K4's band phase takes the stamped
+/// tiles dynamically from a list instead of scanning every tile's flag.
+__device__ __forceinline__ void mk_stamp_list(const Grid& g, const FixBand& fb, const MkStencil& S,
+                                              int lane, StepScratch* out) {
+  if (S.ok && lane < 8) {
+    const int tx = ((lane & 1) ? S.hi[0] : S.lo[0]) >> 2;
+    const int ty = ((lane & 2) ? S.hi[1] : S.lo[1]) >> 2;
+    const int tz = ((lane & 4) ? S.hi[2] - g.z0 : S.lo[2] - g.z0) >> 2;
+    const int T = tx + fb.tnx * (ty + fb.tny * tz);
+    if (atomicExch(fb.tflag + T, fb.stamp) != fb.stamp)
+      fb.tlist[atomicAdd(&out->tcount, 1u)] = T;  // < 8 m <= list capacity
+  }
+}
+
+/// End of the stamp phase of a marker block, then its dependents' trigger.
+/// Every lane's stamps (and list entries) are ordered before the block
+/// barrier; thread 0's fence + ticket carries them (causality order, PTX
+/// memory model) to the grid's last block, whose release store of
+/// `ready = stamp` the banded K4 acquires before its phase A reads a stamp.
+/// Without a tile list (fb.ready null): barrier + fence only.
+__device__ __forceinline__ void mk_publish_stamps(const FixBand& fb, StepScratch* out) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    if (fb.ready && atomicAdd(&out->ticket, 1u) == gridDim.x - 1) {
+      __threadfence();
+      st_release_gpu(fb.ready, fb.stamp);
+    }
+  }
+  __syncthreads();
+  asm volatile("griddepcontrol.launch_dependents;");
+}
+
 /// The rest of marker t's chain on one warp: phi, gathers + bare moments,
 /// interpolation, forcing, the diagnostic record and the fixed-point spread.
 /// phs: this warp's 15-double scratch in shared memory.
@@ -113,6 +147,7 @@ __device__ __forceinline__ void mk_finish(const Grid& g, const float* __restrict
   const int ncell = S.cnt[0] * S.cnt[1] * S.cnt[2];
   const float r0 = 1.0f / (float)S.cnt[0], r01 = 1.0f / (float)(S.cnt[0] * S.cnt[1]);
   double a0 = 0.0, a1 = 0.0, a2 = 0.0;
+  {
   // this lane's cells c = lane + 32 r: FX_CPL gathered per round trip
   for (int c0 = 0; c0 < ncell; c0 += FX_CPL * FX_LANES) {
     float sv[FX_CPL][Q];
@@ -142,6 +177,7 @@ __device__ __forceinline__ void mk_finish(const Grid& g, const float* __restrict
         a2 += w * (double)(mz * ir);
       }
     }
+  }
   }
 #pragma unroll
   for (int o = FX_LANES / 2; o > 0; o >>= 1) {  // fixed butterfly: every lane gets the total
@@ -250,15 +286,13 @@ __global__ void __launch_bounds__(128, FSG_KM_MINB)
   for (int t = blockIdx.x * FX_PER_BLOCK + slot; t < mk.m; t += stride) {
     MkStencil S;
     mk_stencil(mk, t, sc, st, S);
-    mk_stamp(g, fb, S, lane);
+    if (fb.tlist) mk_stamp_list(g, fb, S, lane, out);
+    else mk_stamp(g, fb, S, lane);
   }
-  // every warp's stamps are visible before this block lets the banded K4
+  // every warp's stamps are published before this block lets the banded K4
   // (programmatic dependent) launch: K4's first phase skips stamped tiles and
   // waits for this grid's completion before updating them
-  __syncthreads();
-  if (threadIdx.x == 0) __threadfence();
-  __syncthreads();
-  asm volatile("griddepcontrol.launch_dependents;");
+  mk_publish_stamps(fb, out);
   for (int t = blockIdx.x * FX_PER_BLOCK + slot; t < mk.m; t += stride) {
     MkStencil S;
     mk_stencil(mk, t, sc, st, S);  // cheap; recomputed rather than kept in registers
@@ -309,12 +343,10 @@ __global__ void __launch_bounds__(128, FSG_KM_MINB)
     }
     MkStencil S;
     mk_stencil_x(xw, sc, st, S);
-    mk_stamp(g, fb, S, lane);
+    if (fb.tlist) mk_stamp_list(g, fb, S, lane, out);
+    else mk_stamp(g, fb, S, lane);
   }
-  __syncthreads();
-  if (threadIdx.x == 0) __threadfence();
-  __syncthreads();
-  asm volatile("griddepcontrol.launch_dependents;");
+  mk_publish_stamps(fb, out);
   double acc[NB];
 #pragma unroll
   for (int b = 0; b < NB; ++b) acc[b] = 0.0;
@@ -352,3 +384,4 @@ __global__ void __launch_bounds__(128, FSG_KM_MINB)
   skin_block_red(acc, fixacc);
 #endif
 }
+

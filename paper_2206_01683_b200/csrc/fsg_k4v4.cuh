@@ -189,10 +189,14 @@ __global__ void __launch_bounds__(128, FSG_K4_MINB)
   const int nitem = ncol * nzc;
   int nxt = 0;
   if (tid == 0) {
+    // phase A may read the stamps once every tile of this step is stamped:
+    // acquire of the marker grid's release (normally set before K4 starts)
+    if (fb.ready)
+      while (ld_acquire_gpu(fb.ready) != fb.stamp) __nanosleep(64);
     nxt = (int)atomicAdd(&out->work, 1u);
     FSG_TL(fb.stamp, 2);  // timeline (dev build): K4 start
   }
-  // ---- phase A: cells outside the stamped tiles (no IB force)
+  // ---- phase A: cells outside the stamped tiles (no IB force), per-block fetch
   float vmin = FLT_MAX;
   for (;;) {
     if (tid == 0) item = nxt;
@@ -234,6 +238,33 @@ __global__ void __launch_bounds__(128, FSG_K4_MINB)
   const int nthr = blockDim.x * blockDim.y;  // 96 or 128 (cell_block)
   const int tpp = nthr >> 6;                 // tiles per pass (64 threads each)
   const int half = tid >> 6, lt = tid & 63;
+  if (fb.tlist) {
+    // tile list: the step's stamped tiles are listed; blocks take them
+    // dynamically, so blocks out of phase A early take more of the band
+    const unsigned nt = __ldcg(&out->tcount);
+    for (;;) {
+      if (tid == 0) item = (int)atomicAdd(&out->bwork, (unsigned)tpp);
+      __syncthreads();
+      const unsigned k = (unsigned)item + (unsigned)half;
+      const bool more = (unsigned)item < nt;
+      __syncthreads();
+      if (!more) break;
+      if (half >= tpp || k >= nt) continue;
+      const int T = __ldcg(fb.tlist + k);
+      const int tx = T % fb.tnx, ty = (T / fb.tnx) % fb.tny, tz = T / (fb.tnx * fb.tny);
+      const int x = 4 * tx + (lt & 3), y = 4 * ty + ((lt >> 2) & 3), z = 4 * tz + (lt >> 4);
+      if (x >= g.nx || y >= g.ny || z >= g.nz) continue;
+      unsigned long long* F = fb.F + 3 * ((long long)x + (long long)g.nx * ((long long)y + (long long)g.ny * z));
+      const long long f0 = (long long)F[0], f1 = (long long)F[1], f2 = (long long)F[2];
+      F[0] = 0ull;
+      F[1] = 0ull;
+      F[2] = 0ull;
+      const float Fx = (float)((double)f0 * FIX_INV);
+      const float Fy = (float)((double)f1 * FIX_INV);
+      const float Fz = (float)((double)f2 * FIX_INV);
+      vmin = fminf(vmin, cell_update<PULLED, VF>(g, dp, A, x, y, z, Fx, Fy, Fz, sc, st, out, fb.fcap));
+    }
+  } else {
   for (int base = 0; (long long)base * gridDim.x < ntile; base += nthr) {
     if (tid == 0) ntl = 0;
     __syncthreads();
@@ -258,6 +289,7 @@ __global__ void __launch_bounds__(128, FSG_K4_MINB)
       vmin = fminf(vmin, cell_update<PULLED, VF>(g, dp, A, x, y, z, Fx, Fy, Fz, sc, st, out, fb.fcap));
     }
     __syncthreads();
+  }
   }
   report_min(out, vmin == FLT_MAX ? DBL_MAX : (double)vmin);
   if (tid == 0) FSG_TL(fb.stamp, 5);  // K4 end

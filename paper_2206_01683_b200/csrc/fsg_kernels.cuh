@@ -1095,7 +1095,13 @@ static void L_collide_band(const Grid& g, const void* A, int pulled, void* B, Fi
   // 2 planes when that still leaves >= 8 items per block, else 1
   const long long ncol = (long long)((g.nx + b.x - 1) / b.x) * ((g.ny + b.y - 1) / b.y);
   const long long full = (long long)nsm * res;
-  const int zc = (g.plane < (1 << 17) && ncol * ((g.nz + 1) / 2) >= 8 * full) ? 2 : 1;
+  static int zc_env = -1;
+  if (zc_env < 0) {
+    const char* e = getenv("FSG_K4_ZC");  // dev A/B: phase-A item depth
+    zc_env = e ? atoi(e) : 0;
+  }
+  const int zc = zc_env > 0 ? zc_env
+                            : ((g.plane < (1 << 17) && ncol * ((g.nz + 1) / 2) >= 8 * full) ? 2 : 1);
   const long long nitem = ncol * ((g.nz + zc - 1) / zc);
   const unsigned grid = (unsigned)std::min<long long>(nitem, full);
   cudaLaunchConfig_t cfg = {};
