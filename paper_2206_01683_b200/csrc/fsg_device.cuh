@@ -13,6 +13,12 @@
 #ifndef FSG_K4_MINB
 #define FSG_K4_MINB 6
 #endif
+// the banded (coupled) K4: 8 blocks (64 registers) -- measured c3 135.5 vs
+// 141.7 us per coupled step at 6; the pure-fluid K4 stays at 6 (512^3: 3.74
+// vs 4.28 ms at 8)
+#ifndef FSG_K4B_MINB
+#define FSG_K4B_MINB 8
+#endif
 #ifndef FSG_KM_PER_SM_DEFAULT
 #define FSG_KM_PER_SM_DEFAULT 0.0
 #endif
@@ -39,6 +45,13 @@ namespace fsg {
 #ifdef FSG_TIMING
 constexpr int TL_SLOTS = 8;
 __device__ unsigned long long g_tl[64 * TL_SLOTS];  // only the fp32 TU is built with FSG_TIMING
+// per banded-K4 block of the latest step: start, phase-A end, items, SM id
+__device__ unsigned long long g_blk[8192 * 4];
+__device__ __forceinline__ unsigned smid_() {
+  unsigned r;
+  asm volatile("mov.u32 %0, %%smid;" : "=r"(r));
+  return r;
+}
 __device__ __forceinline__ unsigned long long tl_now() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));

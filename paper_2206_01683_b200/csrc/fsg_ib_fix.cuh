@@ -27,7 +27,10 @@ constexpr int FX_PER_BLOCK = 128 / FX_LANES;  // markers per 128-thread block
 __device__ __forceinline__ unsigned fx_mask() {
   return FX_LANES == 32 ? 0xFFFFFFFFu : (0xFFFFu << (threadIdx.x & 16));
 }
-constexpr int FX_CPL = 1;        // stencil cells per lane per round trip (register pressure)
+#ifndef FSG_FX_CPL
+#define FSG_FX_CPL 1
+#endif
+constexpr int FX_CPL = FSG_FX_CPL;  // stencil cells per lane per round trip (register pressure)
 
 __device__ __forceinline__ unsigned long long to_fix(double v) {
   return (unsigned long long)__double2ll_rn(v * FIX_SCALE);
@@ -109,7 +112,9 @@ __device__ __forceinline__ void mk_publish_stamps(const FixBand& fb, StepScratch
     }
   }
   __syncthreads();
+#ifndef FSG_KM_LATE_TRIGGER
   asm volatile("griddepcontrol.launch_dependents;");
+#endif
 }
 
 /// The rest of marker t's chain on one warp: phi, gathers + bare moments,
@@ -325,13 +330,25 @@ __global__ void __launch_bounds__(128, FSG_KM_MINB)
                    double* fworld_h, int* valid_h, FixBand fb, StepScratch* out,
                    const __grid_constant__ SkinParamsN<NB> P, unsigned long long* fixacc) {
   __shared__ double phs[FX_PER_BLOCK][3][5];
+  // the bodies' topology and this step's pose, staged once per block: the
+  // chain indexes them by lane-dependent bone / joint, which in the kernel
+  // parameter space (constant bank) serializes per distinct address
+  __shared__ __align__(16) SkinBody sbody[NB];
+  {
+    static_assert(sizeof(SkinBody) % 8 == 0, "SkinBody is copied as doubles");
+    constexpr int NW = (int)(sizeof(SkinBody) / 8) * NB;
+    const double* src = reinterpret_cast<const double*>(&P.body[0]);
+    double* dst = reinterpret_cast<double*>(&sbody[0]);
+    for (int i = threadIdx.x; i < NW; i += blockDim.x) dst[i] = src[i];
+  }
+  __syncthreads();
   const int lane = threadIdx.x & (FX_LANES - 1);
   const int slot = threadIdx.x / FX_LANES;
   const int stride = gridDim.x * FX_PER_BLOCK;
   const SessionConsts& sc = *scp;
   if (threadIdx.x == 0) FSG_TL(fb.stamp, 0);
   for (int t = blockIdx.x * FX_PER_BLOCK + slot; t < mk.m; t += stride) {
-    const SkinBody& B = P.body[skin_body_of(P, t)];
+    const SkinBody& B = sbody[skin_body_of(P, t)];
     const SkinSlot sl = skin_slot(P, t, lane);
     double xw[3];
     skin_point_warp(P, B.pose, t, sl, xw);
@@ -352,11 +369,14 @@ __global__ void __launch_bounds__(128, FSG_KM_MINB)
   for (int b = 0; b < NB; ++b) acc[b] = 0.0;
   for (int t = blockIdx.x * FX_PER_BLOCK + slot; t < mk.m; t += stride) {
     const int bi = skin_body_of(P, t);
-    const SkinBody& B = P.body[bi];
+    const SkinBody& B = sbody[bi];
     const SkinSlot sl = skin_slot(P, t, lane);
     double xw[3], vel[3], nrm[3], fw[3];
-    skin_point_warp(P, B.pose, t, sl, xw);  // recomputed: cheaper than keeping it live
     skin_vel_nrm_warp(P, B.pose, t, sl, vel, nrm);
+    // the position this warp skinned before the stamps (the block barrier
+    // since orders lane 0's store before these loads)
+#pragma unroll
+    for (int c = 0; c < 3; ++c) xw[c] = __ldcg(mk.pts + 3 * t + c);
     if (lane == 0) {
       double* v = const_cast<double*>(mk.vel);
       double* n = const_cast<double*>(mk.nrm);

@@ -169,11 +169,11 @@ __global__ void __launch_bounds__(128, FSG_K4_MINB)
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 
 template <bool PULLED, bool VF>
-__global__ void __launch_bounds__(128, FSG_K4_MINB)
+__global__ void __launch_bounds__(128, FSG_K4B_MINB)
     k_collide_band(Grid g, DirPtrs dp, const float* __restrict__ A, FixBand fb,
                    const SessionConsts* __restrict__ scp, const StepConsts st,
                    StepScratch* __restrict__ out, StepScratch* __restrict__ next, int zc,
-                   SkinOut so) {
+                   int zs1, SkinOut so) {
   __shared__ int item;
   __shared__ int tl[128];
   __shared__ int ntl;
@@ -185,8 +185,13 @@ __global__ void __launch_bounds__(128, FSG_K4_MINB)
   const SessionConsts& sc = *scp;
   const int tx_n = (g.nx + blockDim.x - 1) / blockDim.x;
   const int ty_n = (g.ny + blockDim.y - 1) / blockDim.y;
-  const int ncol = tx_n * ty_n, nzc = (g.nz + zc - 1) / zc;
-  const int nitem = ncol * nzc;
+  // items: zc-plane items over planes [0, zs1), then single-plane items over
+  // [zs1, nz) -- the queue ends with short items, so the blocks' phase-A
+  // finishing times spread by half an item less (an item's cells are one per
+  // thread per plane; under full HBM load a 2-plane item takes ~7 us at c3)
+  const int ncol = tx_n * ty_n;
+  const int nbig = ncol * (zs1 / zc);
+  const int nitem = nbig + ncol * (g.nz - zs1);
   int nxt = 0;
   if (tid == 0) {
     // phase A may read the stamps once every tile of this step is stamped:
@@ -195,7 +200,16 @@ __global__ void __launch_bounds__(128, FSG_K4_MINB)
       while (ld_acquire_gpu(fb.ready) != fb.stamp) __nanosleep(64);
     nxt = (int)atomicAdd(&out->work, 1u);
     FSG_TL(fb.stamp, 2);  // timeline (dev build): K4 start
+#ifdef FSG_TIMING
+    if (blockIdx.x < 8192) {
+      g_blk[4 * blockIdx.x] = tl_now();
+      g_blk[4 * blockIdx.x + 3] = smid_();
+    }
+#endif
   }
+#ifdef FSG_TIMING
+  unsigned n_items = 0;
+#endif
   // ---- phase A: cells outside the stamped tiles (no IB force), per-block fetch
   float vmin = FLT_MAX;
   for (;;) {
@@ -204,14 +218,20 @@ __global__ void __launch_bounds__(128, FSG_K4_MINB)
     const int it = item;
     __syncthreads();
     if (it >= nitem) break;
+#ifdef FSG_TIMING
+    ++n_items;
+#endif
     if (tid == 0) nxt = (int)atomicAdd(&out->work, 1u);  // consumed next iteration
-    const int col = it % ncol, zk = it / ncol;
+    const bool big = it < nbig;
+    const int r = big ? it : it - nbig;
+    const int col = r % ncol;
     const int x = (col % tx_n) * blockDim.x + threadIdx.x;
     const int y = (col / tx_n) * blockDim.y + threadIdx.y;
-    const int z0 = zk * zc, z1 = min(g.nz, z0 + zc);
+    const int z0 = big ? (r / ncol) * zc : zs1 + r / ncol;
+    const int z1 = big ? z0 + zc : z0 + 1;
     if (x >= g.nx || y >= g.ny) continue;
-    // the item's zc (1 or 2) planes share a tile layer: one stamp load per
-    // item (stamped: the band phase's)
+    // the item's planes (1 or 2, zs1 a multiple of 4) share a tile layer:
+    // one stamp load per item (stamped: the band phase's)
     if (__ldcg(fb.tflag + (x >> 2) + fb.tnx * ((y >> 2) + fb.tny * (z0 >> 2))) == fb.stamp) continue;
     for (int z = z0; z < z1; ++z)
       vmin = fminf(vmin, cell_update<PULLED, VF>(g, dp, A, x, y, z, 0.f, 0.f, 0.f, sc, st, out,
@@ -222,6 +242,12 @@ __global__ void __launch_bounds__(128, FSG_K4_MINB)
   // chunk, so a body's clustered tiles spread over all blocks; each 64
   // threads take one stamped tile per pass.
   if (tid == 0) FSG_TL(fb.stamp, 3);  // phase A done (this block)
+#ifdef FSG_TIMING
+  if (tid == 0 && blockIdx.x < 8192) {
+    g_blk[4 * blockIdx.x + 1] = tl_now();
+    g_blk[4 * blockIdx.x + 2] = n_items;
+  }
+#endif
   pdl_wait();
   if (tid == 0) FSG_TL(fb.stamp, 4);  // band phase start
   // skinned bodies: the marker grid's tau_ext / stats sums are complete

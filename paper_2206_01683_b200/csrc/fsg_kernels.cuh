@@ -1102,7 +1102,21 @@ static void L_collide_band(const Grid& g, const void* A, int pulled, void* B, Fi
   }
   const int zc = zc_env > 0 ? zc_env
                             : ((g.plane < (1 << 17) && ncol * ((g.nz + 1) / 2) >= 8 * full) ? 2 : 1);
-  const long long nitem = ncol * ((g.nz + zc - 1) / zc);
+  // 2-plane items end at plane zs1 (a multiple of 4); the last planes are
+  // single-plane items, about 3 per block (FSG_K4_TAIL: that count, 0 = none)
+  static int tail_env = -1;
+  if (tail_env < 0) {
+    const char* e = getenv("FSG_K4_TAIL");
+    tail_env = e ? atoi(e) : 3;
+  }
+  int zs1 = g.nz;
+  if (zc == 2) {
+    const long long want = (tail_env * full + ncol - 1) / ncol;  // single planes
+    zs1 = (int)std::max<long long>(0, ((g.nz - want) / 4) * 4);
+  } else {
+    zs1 = 0;
+  }
+  const long long nitem = ncol * (zs1 / zc) + ncol * (g.nz - zs1);
   const unsigned grid = (unsigned)std::min<long long>(nitem, full);
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
@@ -1116,7 +1130,7 @@ static void L_collide_band(const Grid& g, const void* A, int pulled, void* B, Fi
   cfg.numAttrs = 1;
 #define FSG_PB(P, V)                                                                     \
   cudaLaunchKernelEx(&cfg, k_collide_band<P, V>, g, dp, (const float*)A, fb, sc, st, scr, \
-                     scr_next, zc, so)
+                     scr_next, zc, zs1, so)
   if (pulled) {
     if (frame_on) FSG_PB(true, true);
     else FSG_PB(true, false);

@@ -15,3 +15,10 @@ extern "C" int fsg_debug_timeline(unsigned long long* out) {
   return (int)cudaMemcpyToSymbol(fsg::g_tl, init, sizeof init);
 }
 #endif
+
+#ifdef FSG_TIMING
+extern "C" int fsg_debug_blocks(unsigned long long* out) {
+  cudaDeviceSynchronize();
+  return (int)cudaMemcpyFromSymbol(out, fsg::g_blk, sizeof(unsigned long long) * 8192 * 4);
+}
+#endif

@@ -19,6 +19,9 @@ FLUSH = "--flush" in sys.argv
 SKIN = "--skin" in sys.argv
 if SKIN:
     sys.argv.remove("--skin")
+OOB = "--oob" in sys.argv  # host markers moved out of the box (no band)
+if OOB:
+    sys.argv.remove("--oob")
 if FLUSH:
     sys.argv.remove("--flush")
     fw_buf = torch.empty(64 << 20, dtype=torch.float32, device="cuda")
@@ -35,7 +38,10 @@ for name in sys.argv[1:] or ["c2"]:
         s.set_skin(*sc.skin())
         poses = [sc.poses(k) for k in range(60)]
     else:
-        dm = [torch.tensor(np.ascontiguousarray(a).reshape(-1), device="cuda") for a in sc.markers(0)]
+        mk0 = list(sc.markers(0))
+        if OOB:
+            mk0[0] = mk0[0] + 1e3
+        dm = [torch.tensor(np.ascontiguousarray(a).reshape(-1), device="cuda") for a in mk0]
         s.set_markers_device(sc.offsets, *(t.data_ptr() for t in dm))
     for k in range(30):
         s.set_frame(sc.frame(k))
