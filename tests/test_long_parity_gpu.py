@@ -150,3 +150,27 @@ def test_force_capture_is_the_consumed_field():
     assert np.array_equal(r0, r1) and np.array_equal(u0, u1) and np.array_equal(fw0, fw1)
     assert np.abs(F_cap).max() > 0
     assert K.rel_l2(F_cap, F_rebuild) <= 1e-6
+
+
+def test_skinned_c2_10k_steps_run_to_run_bit_identical():
+    """Race evidence for the banded PDL schedule (stamps published by the
+    marker grid, acquired by K4 before its first stamp load): two 10,000-step
+    runs of the device-skinned c2 step (the bench's coupled path) end in
+    bit-identical distributions, marker forces and tau_ext."""
+    from paper_2206_01683_b200.scenes import make_scene
+    sc = make_scene("c2")
+    outs = []
+    for _ in range(2):
+        s = _session(sc, "fp32")
+        s.set_force_capture(False)
+        s.set_skin(*sc.skin())
+        for k in range(10_000):
+            st, tau, _ = s.step_skinned(sc.frame(k), sc.poses(k))
+        assert st.stable()
+        outs.append((s.get_f(), s.marker_forces()[0], [np.array(t) for t in tau]))
+        s.close()
+    (f0, m0, t0), (f1, m1, t1) = outs
+    assert np.array_equal(f0, f1)
+    assert np.array_equal(m0, m1)
+    for a, b in zip(t0, t1):
+        assert np.array_equal(np.asarray(a), np.asarray(b))
