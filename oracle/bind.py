@@ -272,6 +272,47 @@ def ref() -> C.CDLL:
             "ref_follower_state": (None, [vp, _dp]),
             "ref_quat_exp": (None, [_dp, _dp]),
         }
+        u64 = C.c_uint64
+        # robot/, empirical/, sim/session (ref_robot.cpp)
+        sig.update({
+            "ref_robot_last_error": (C.c_char_p, []),
+            "ref_model_build": (vp, [C.c_char_p]),
+            "ref_model_destroy": (None, [vp]),
+            "ref_model_info": (None, [vp, _ip]),
+            "ref_model_links": (None, [vp, _dp]),
+            "ref_model_bladder": (None, [vp, _dp]),
+            "ref_model_mesh": (None, [vp, _dp, _ip, _dp]),
+            "ref_skeleton_validate": (C.c_int, [C.c_int, _dp]),
+            "ref_samples_create": (vp, [vp, C.c_double, u64]),
+            "ref_samples_destroy": (None, [vp]),
+            "ref_samples_n": (C.c_int64, [vp]),
+            "ref_samples_get": (None, [vp, _dp, _dp, _dp, _dp]),
+            "ref_kinematics": (None, [vp, _dp, _dp]),
+            "ref_mass_matrix": (None, [vp, _dp, _dp]),
+            "ref_bias_forces": (None, [vp, _dp, _dp, _dp]),
+            "ref_robot_step": (C.c_int, [vp, _dp, _dp, _dp, C.c_double, _dp, C.c_double,
+                                         C.c_double, C.c_int]),
+            "ref_update_samples": (None, [vp, vp, _dp, _dp, _dp, _dp]),
+            "ref_skinned_tau": (None, [vp, vp, _dp, _dp, _ip, _dp, _dp]),
+            "ref_emp_create": (vp, [C.c_double, C.c_int, C.c_double, _dp, C.c_double, C.c_double]),
+            "ref_emp_destroy": (None, [vp]),
+            "ref_emp_add_robot": (C.c_int, [vp, vp, _dp, C.c_double, u64]),
+            "ref_be_set_actuation": (None, [vp, C.c_int, C.c_int, _dp]),
+            "ref_be_change_bladder": (None, [vp, C.c_int, C.c_int, C.c_double]),
+            "ref_be_step": (C.c_int, [vp, C.c_int, _ip]),
+            "ref_be_robot": (None, [vp, C.c_int, C.c_int, _dp, _dp, _dp, _dp]),
+            "ref_be_set_state": (None, [vp, C.c_int, C.c_int, _dp]),
+            "ref_be_samples": (None, [vp, C.c_int, C.c_int, _dp, _dp, _dp]),
+            "ref_be_n_samples": (C.c_int64, [vp, C.c_int, C.c_int]),
+            "ref_cs_create": (vp, [C.c_int, C.c_int, C.c_int, C.c_double, C.c_double, C.c_double,
+                                   C.c_double, C.c_int, C.c_int, C.c_int, C.c_double, C.c_double,
+                                   _dp, C.c_int, C.c_double, C.c_int]),
+            "ref_cs_destroy": (None, [vp]),
+            "ref_cs_add_robot": (C.c_int, [vp, vp, _dp, C.c_double, u64]),
+            "ref_cs_frame": (None, [vp, _dp]),
+            "ref_cs_get_f": (None, [vp, _dp]),
+            "ref_cs_macro": (None, [vp, _dp, _dp]),
+        })
         for name, (res, args) in sig.items():
             fn = getattr(lib, name)
             fn.restype = res
