@@ -31,6 +31,61 @@ def _err():
     return B.ref().ref_robot_last_error().decode()
 
 
+# -- conversions from the packed reference layouts (work without _ref: goldens) --
+def robot_from_packed(links, bladder):
+    """dynamics.Robot with the reference's links and bladder, value for value."""
+    from paper_2206_01683_b200 import dynamics as D
+    out = []
+    for o in np.asarray(links, dtype=np.float64):
+        out.append(D.Link(parent=int(o[0]), joint=int(o[1]), joint_origin=o[2:5].copy(),
+                          joint_rotation=o[5:14].reshape(3, 3).copy(), axis=o[14:17].copy(),
+                          mass=float(o[17]), com=o[18:21].copy(),
+                          inertia_com=o[21:30].reshape(3, 3).copy(), stiffness=float(o[30]),
+                          damping=float(o[31]), q_rest=float(o[32]), limit_lo=float(o[33]),
+                          limit_hi=float(o[34]), torque_limit=float(o[35]),
+                          displaced_volume=float(o[36]), volume_centroid=o[37:40].copy()))
+    b = np.asarray(bladder, dtype=np.float64)
+    return D.Robot(out, D.Bladder(volume=float(b[0]), volume_min=float(b[1]),
+                                  volume_max=float(b[2]), rate_bound=float(b[3]),
+                                  centroid=b[4:7].copy()))
+
+
+def skeleton_from_packed(links):
+    """session.Skeleton (the skinning topology, fsg_skeleton) of packed links."""
+    from paper_2206_01683_b200.session import Skeleton
+    r = robot_from_packed(links, np.zeros(8))
+    parent = [l.parent for l in r.links]
+    dofi = [r.dof_index(i) for i in range(r.n_links)]
+    axis = np.array([np.asarray(l.axis) / np.linalg.norm(l.axis) for l in r.links])
+    return Skeleton(parent, dofi, axis, r.floating_base, r.n_dofs)
+
+
+def pose_from_kc(kc) -> np.ndarray:
+    """fsg_body_pose (packed) from ref_kinematics rows [n_links, 30]."""
+    from paper_2206_01683_b200._abi import SKIN_MAX_LINKS
+    k = np.asarray(kc, dtype=np.float64)
+    Lm, n = SKIN_MAX_LINKS, k.shape[0]
+    out = np.zeros(30 * Lm)
+    out[0:9 * n] = k[:, 18:27].reshape(-1)                       # bone_R
+    out[9 * Lm:9 * Lm + 3 * n] = k[:, 27:30].reshape(-1)         # bone_t
+    out[12 * Lm:12 * Lm + 9 * n] = k[:, 0:9].reshape(-1)         # R_world
+    out[21 * Lm:21 * Lm + 3 * n] = k[:, 9:12].reshape(-1)        # p_world
+    out[24 * Lm:24 * Lm + 3 * n] = k[:, 12:15].reshape(-1)       # v_origin_world
+    out[27 * Lm:27 * Lm + 3 * n] = k[:, 15:18].reshape(-1)       # omega_world
+    return out
+
+
+def unpack_state(x, n_joints, n_dofs):
+    from paper_2206_01683_b200.dynamics import JointState
+    x = np.asarray(x, dtype=np.float64)
+    return JointState(x[0:3].copy(), x[3:7].copy(), x[7:7 + n_joints].copy(),
+                      x[7 + n_joints:7 + n_joints + n_dofs].copy(), np.zeros(n_dofs))
+
+
+def pack_state(st) -> np.ndarray:
+    return np.concatenate([st.base_pos, st.base_quat, st.q, st.v]).astype(np.float64)
+
+
 class RefModel:
     def __init__(self, design: str):
         self.L = B.ref()
@@ -53,29 +108,11 @@ class RefModel:
 
     def robot(self):
         """dynamics.Robot with the reference's links and bladder, value for value."""
-        from paper_2206_01683_b200 import dynamics as D
-        links = []
-        for o in self.links:
-            links.append(D.Link(parent=int(o[0]), joint=int(o[1]), joint_origin=o[2:5].copy(),
-                                joint_rotation=o[5:14].reshape(3, 3).copy(), axis=o[14:17].copy(),
-                                mass=float(o[17]), com=o[18:21].copy(),
-                                inertia_com=o[21:30].reshape(3, 3).copy(), stiffness=float(o[30]),
-                                damping=float(o[31]), q_rest=float(o[32]), limit_lo=float(o[33]),
-                                limit_hi=float(o[34]), torque_limit=float(o[35]),
-                                displaced_volume=float(o[36]), volume_centroid=o[37:40].copy()))
-        b = self.bladder
-        return D.Robot(links, D.Bladder(volume=float(b[0]), volume_min=float(b[1]),
-                                        volume_max=float(b[2]), rate_bound=float(b[3]),
-                                        centroid=b[4:7].copy()))
+        return robot_from_packed(self.links, self.bladder)
 
     def skeleton(self):
         """session.Skeleton (the skinning topology, fsg_skeleton) of this model."""
-        from paper_2206_01683_b200.session import Skeleton
-        r = self.robot()
-        parent = [l.parent for l in r.links]
-        dofi = [r.dof_index(i) for i in range(r.n_links)]
-        axis = np.array([np.asarray(l.axis) / np.linalg.norm(l.axis) for l in r.links])
-        return Skeleton(parent, dofi, axis, bool(self.floating), self.n_dofs)
+        return skeleton_from_packed(self.links)
 
     def samples(self, spacing: float, seed: int = 1234):
         """-> (rest_points [m,3], rest_normals [m,3], areas [m], weights [m, n_links])."""
@@ -93,10 +130,7 @@ class RefModel:
         return np.concatenate([st.base_pos, st.base_quat, st.q, st.v]).astype(np.float64)
 
     def unpack(self, x):
-        from paper_2206_01683_b200.dynamics import JointState
-        nj, nd = self.n_joints, self.n_dofs
-        return JointState(x[0:3].copy(), x[3:7].copy(), x[7:7 + nj].copy(),
-                          x[7 + nj:7 + nj + nd].copy(), np.zeros(nd))
+        return unpack_state(x, self.n_joints, self.n_dofs)
 
     def zero_state(self) -> np.ndarray:
         x = np.zeros(7 + self.n_joints + self.n_dofs)
@@ -120,19 +154,8 @@ class RefModel:
         return out
 
     def pose(self, x) -> np.ndarray:
-        """fsg_body_pose (packed, DYN/SKIN_MAX_LINKS slots) at state x."""
-        from paper_2206_01683_b200._abi import SKIN_MAX_LINKS
-        k = self.kinematics(x)
-        Lm = SKIN_MAX_LINKS
-        out = np.zeros(30 * Lm)
-        n = self.n_links
-        out[0:9 * n] = k[:, 18:27].reshape(-1)                       # bone_R
-        out[9 * Lm:9 * Lm + 3 * n] = k[:, 27:30].reshape(-1)         # bone_t
-        out[12 * Lm:12 * Lm + 9 * n] = k[:, 0:9].reshape(-1)         # R_world
-        out[21 * Lm:21 * Lm + 3 * n] = k[:, 9:12].reshape(-1)        # p_world
-        out[24 * Lm:24 * Lm + 3 * n] = k[:, 12:15].reshape(-1)       # v_origin_world
-        out[27 * Lm:27 * Lm + 3 * n] = k[:, 15:18].reshape(-1)       # omega_world
-        return out
+        """fsg_body_pose (packed) at state x."""
+        return pose_from_kc(self.kinematics(x))
 
     def mass_matrix(self, x):
         M = np.zeros(self.n_dofs * self.n_dofs)
