@@ -184,7 +184,7 @@ int fsg_get_stencils(fsg_session* s, int* lo_hi);
  *   CouplingStats (coupling.hpp:88-93, session.hpp:141-143).
  * Forward kinematics and BoneTransforms::of stay with the caller (host, per
  * link); fsg_set_pose takes their results. */
-#define FSG_SKIN_MAX_LINKS 8
+#define FSG_SKIN_MAX_LINKS 12 /* the reference eel: 11 links (model_builder.hpp:234-249) */
 #define FSG_SKIN_MAX_BODIES 4
 #define FSG_SKIN_MAX_WEIGHTS 4 /* nonzero blend weights per marker */
 
@@ -272,7 +272,7 @@ int fsg_drag_step(fsg_drag* d, double* tau_ext, double* stats);
  * a mass matrix that is not positive definite (NumericalError in the
  * reference, dynamics.hpp:208-210) sets FSG_DYN_NOT_SPD in the env's flags
  * and leaves that env's state unchanged. */
-#define FSG_DYN_MAX_LINKS 8
+#define FSG_DYN_MAX_LINKS 12 /* eel: 11 links, 16 dofs */
 #define FSG_DYN_MAX_DOFS (6 + FSG_DYN_MAX_LINKS)
 enum { FSG_JOINT_FREE = 0, FSG_JOINT_REVOLUTE = 1, FSG_JOINT_FIXED = 2 };
 enum { FSG_DYN_CLAMPED = 1, FSG_DYN_NOT_SPD = 2, FSG_DYN_NONFINITE = 4 };

@@ -91,7 +91,7 @@ class OrcSkeleton(C.Structure):
     """orc_skeleton (same layout as fsg_skeleton)."""
 
     _fields_ = [("n_links", C.c_int), ("floating_base", C.c_int), ("n_dofs", C.c_int),
-                ("parent", C.c_int * 8), ("dof_index", C.c_int * 8), ("axis", (C.c_double * 3) * 8)]
+                ("parent", C.c_int * 12), ("dof_index", C.c_int * 12), ("axis", (C.c_double * 3) * 12)]
 
     @classmethod
     def of(cls, sk):
@@ -370,7 +370,7 @@ class Rng:
 # states are the product's host types (paper_2206_01683_b200.dynamics), whose
 # POD structs are the boundary's own layout.
 class DynKC(C.Structure):
-    _L = 8
+    _L = 12
     _fields_ = [("E", (C.c_double * 9) * _L), ("r", (C.c_double * 3) * _L),
                 ("R_world", (C.c_double * 9) * _L), ("p_world", (C.c_double * 3) * _L),
                 ("v_body", (C.c_double * 6) * _L), ("omega_world", (C.c_double * 3) * _L),
@@ -461,7 +461,7 @@ class DynOracle:
         return oracle().orc_mechanical_energy(C.byref(self.rs), C.byref(self._st(st)), dptr(d3(g)))
 
     def pose(self, st, rest_R, rest_p):
-        out = np.zeros(240)
+        out = np.zeros(30 * 12)
         oracle().orc_dyn_pose(C.byref(self.rs), C.byref(self._st(st)), dptr(d3(rest_R)), dptr(d3(rest_p)),
                               out.ctypes.data_as(C.c_void_p))
         return out

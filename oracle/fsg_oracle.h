@@ -105,12 +105,12 @@ void orc_session_recenter(orc_session* s, const int shift[3]);
  * tests/test_skin_oracle.py.  Layouts match fsg_skeleton / fsg_body_pose. */
 typedef struct {
   int n_links, floating_base, n_dofs;
-  int parent[8], dof_index[8];
-  double axis[8][3];
+  int parent[12], dof_index[12];
+  double axis[12][3];
 } orc_skeleton;
 typedef struct {
-  double bone_R[8][9], bone_t[8][3], R_world[8][9], p_world[8][3], v_origin_world[8][3],
-      omega_world[8][3];
+  double bone_R[12][9], bone_t[12][3], R_world[12][9], p_world[12][3], v_origin_world[12][3],
+      omega_world[12][3];
 } orc_body_pose;
 /* update_samples (sampling.hpp:307-322): points, velocities, normals [3m];
  * weights [m][n_links] dense */

@@ -50,7 +50,7 @@ class fsg_frame_state(C.Structure):
                 ("q", C.c_double * 4), ("omega", C.c_double * 3), ("alpha", C.c_double * 3)]
 
 
-SKIN_MAX_LINKS, SKIN_MAX_BODIES, SKIN_MAX_WEIGHTS = 8, 4, 4
+SKIN_MAX_LINKS, SKIN_MAX_BODIES, SKIN_MAX_WEIGHTS = 12, 4, 4
 _L = SKIN_MAX_LINKS
 
 
@@ -66,7 +66,7 @@ class fsg_body_pose(C.Structure):
                 ("v_origin_world", (C.c_double * 3) * _L), ("omega_world", (C.c_double * 3) * _L)]
 
 
-DYN_MAX_LINKS = 8
+DYN_MAX_LINKS = 12
 DYN_MAX_DOFS = 6 + DYN_MAX_LINKS
 FSG_JOINT_FREE, FSG_JOINT_REVOLUTE, FSG_JOINT_FIXED = 0, 1, 2
 FSG_DYN_CLAMPED, FSG_DYN_NOT_SPD, FSG_DYN_NONFINITE = 1, 2, 4

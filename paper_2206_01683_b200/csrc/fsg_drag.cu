@@ -393,6 +393,7 @@ int fsg_drag_set_skin(fsg_drag* d, int env, const fsg_skeleton* k, int m, const 
   B.floating = k->floating_base ? 1 : 0;
   B.n_dofs = k->n_dofs;
   B.tau_off = 0;
+  B.max_level = 0;  // the drag kernels walk the parent chain
   for (int j = 0; j < FSG_SKIN_MAX_LINKS; ++j) {
     B.parent[j] = j < L ? k->parent[j] : -1;
     B.dof[j] = (j > 0 && j < L) ? k->dof_index[j] : -1;

@@ -552,7 +552,7 @@ __global__ void __launch_bounds__(DYN_BLOCK)
 // and the rows of each Cholesky column.  The recursive chains (forward
 // kinematics, RNEA sweeps, triangular solves) stay on lane 0; everything
 // lives in shared memory.
-constexpr int DYN_WARPS = 4;
+constexpr int DYN_WARPS = 3;  // 3 x ~13 KB warp workspaces + DynConst in 48 KB of static smem (12 links)
 
 #ifdef FSG_DYN_TIMING  // dev builds only (scripts/build_variant.sh): per-phase clock64 of warp 0
 __device__ unsigned long long g_dyn_t[8];

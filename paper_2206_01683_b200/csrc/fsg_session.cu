@@ -1005,6 +1005,10 @@ int fsg_set_skin(fsg_session* s, int n_bodies, const int64_t* off, const fsg_ske
       B.dof[j] = (j > 0 && j < k.n_links) ? k.dof_index[j] : -1;
       for (int c = 0; c < 3; ++c) B.axis[j][c] = j < k.n_links ? k.axis[j][c] : 0.0;
     }
+    B.max_level = 0;
+    for (int j = 0; j < FSG_SKIN_MAX_LINKS; ++j)
+      for (int l = 0; l < FSG_SKIN_MAX_LINKS; ++l)
+        if (B.lvl[j][l] > B.max_level) B.max_level = B.lvl[j][l];
     for (int d = 0; d < 6 + FSG_SKIN_MAX_LINKS; ++d) B.dof_link[d] = -1;
     for (int j = 1; j < k.n_links; ++j)
       if (k.dof_index[j] >= 0) B.dof_link[k.dof_index[j]] = (signed char)j;

@@ -25,7 +25,7 @@ struct SkinBody {  // (a multiple of 8 bytes: copied as doubles)
                                     // (anc[b][0] = b), -1 past the base (link 0)
   signed char lvl[SKIN_L][SKIN_L];  // lvl[b][J] = l >= 1 with anc[b][l-1] == J (J > 0), else -1
   signed char dof_link[6 + SKIN_L];  // link whose revolute dof is d (-1: base dof / none)
-  signed char _pad[2];
+  signed char max_level;             // deepest joint chain (levels > 7 take a second lane pass)
   double axis[SKIN_L][3];
   fsg_body_pose pose;
 };

@@ -14,7 +14,8 @@
 // * tau_ext (accumulate_skinned_force -> accumulate_point_force,
 //   skinning.hpp:147-156, dynamics.hpp:216-233): lane k*8 + l evaluates, for
 //   bone slot k, the floating-base wrench (l = 0) or the l-th joint up the
-//   chain; a fixed butterfly sums a marker's terms, lane c keeps dof c's
+//   chain, and on chains deeper than 7 joints (the eel) also the (l+8)-th;
+//   the warp gathers a marker's terms in slot order, lane c keeps dof c's
 //   running sum over the warp's markers; the block sums its warps in order
 //   and adds the total to 64-bit fixed-point accumulators (2^-44) with integer
 //   atomics, which the banded K4 converts once the marker grid is complete:
@@ -165,6 +166,8 @@ __device__ __forceinline__ void skin_tau_warp(const SP& P, const SkinBody& B, in
     if (b >= 0) w = __ldg(P.ww + SKIN_KW * t + k);
   }
   double term[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+  double term2 = 0.0;  // level l + 8 (chains deeper than 7 joints)
+  const bool deep = B.max_level > 7;  // uniform over the warp
   int comp = -1;  // l > 0: the dof this lane's term goes to
   if (b >= 0) {
     const double x[3] = {__ldg(P.rest + 3 * t), __ldg(P.rest + 3 * t + 1), __ldg(P.rest + 3 * t + 2)};
@@ -193,6 +196,17 @@ __device__ __forceinline__ void skin_tau_warp(const SP& P, const SkinBody& B, in
         comp = B.dof[j];
       }
     }
+    if (deep && l + 8 <= SKIN_L) {
+      const int j2 = B.anc[b][l + 7];
+      if (j2 > 0 && B.dof[j2] >= 0) {
+        double aw[3], d[3], cr[3];
+        rn_mv(Q.R_world[j2], B.axis[j2], aw);
+#pragma unroll
+        for (int c = 0; c < 3; ++c) d[c] = rn_sub(p[c], Q.p_world[j2][c]);
+        rn_cross(aw, d, cr);
+        term2 = rn_dot(cr, fv);
+      }
+    }
   }
   // marker total of every dof, lane c keeps dof c.  Base dofs (c < 6): the
   // four level-0 lanes' wrenches through shared memory, in slot order.
@@ -211,7 +225,12 @@ __device__ __forceinline__ void skin_tau_warp(const SP& P, const SkinBody& B, in
   for (int kk = 0; kk < SKIN_KW; ++kk) {
     const int bk = __shfl_sync(0xffffffffu, b, kk * 8);
     const int lv = (J > 0 && bk >= 0) ? B.lvl[bk][J] : -1;
-    const double jt = __shfl_sync(0xffffffffu, term[0], kk * 8 + (lv > 0 ? lv : 0));
+    const int src = kk * 8 + (lv > 0 ? (lv & 7) : 0);
+    double jt = __shfl_sync(0xffffffffu, term[0], src);
+    if (deep) {
+      const double jt2 = __shfl_sync(0xffffffffu, term2, src);
+      if (lv >= 8) jt = jt2;
+    }
     if (lane < 6) v += wr[warp][kk][lane];
     else if (lv > 0) v += jt;
   }

@@ -175,7 +175,8 @@ class JointState:
 
 
 def unpack_states(packed, n_joints: int, n_dofs: int) -> list:
-    """Packed fsg_joint_state rows ([E, 43], EnvBatch.step_dynamic) -> JointStates."""
+    """Packed fsg_joint_state rows ([E, 7 + DYN_MAX_LINKS + 2 DYN_MAX_DOFS], EnvBatch.step_dynamic)
+    -> JointStates."""
     L, Dm = DYN_MAX_LINKS, DYN_MAX_DOFS
     out = []
     for r in np.asarray(packed, dtype=np.float64).reshape(-1, 7 + L + 2 * Dm):
@@ -273,10 +274,10 @@ class RobotBatch:
         return M, c
 
     def poses(self, rest_R, rest_p) -> np.ndarray:
-        """[E, 240] packed fsg_body_pose of every env (FK + BoneTransforms::of)."""
+        """[E, 30 * SKIN_MAX_LINKS] packed fsg_body_pose of every env (FK + BoneTransforms::of)."""
         rR = np.ascontiguousarray(np.asarray(rest_R, dtype=np.float64).reshape(-1))
         rp = np.ascontiguousarray(np.asarray(rest_p, dtype=np.float64).reshape(-1))
-        out = np.zeros((self.n_envs, 240))
+        out = np.zeros((self.n_envs, 30 * _abi.SKIN_MAX_LINKS))
         _abi.check(_abi.lib().fsg_dyn_poses(self._h, _abi.dptr(rR), _abi.dptr(rp),
                                             out.ctypes.data_as(C.c_void_p)), dyn=True)
         return out

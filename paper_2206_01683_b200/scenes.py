@@ -22,6 +22,7 @@ from dataclasses import dataclass, field
 
 import numpy as np
 
+from ._abi import SKIN_MAX_LINKS as SKIN_L
 from .session import FrameState
 
 
@@ -165,16 +166,16 @@ def forward_kinematics(art: Articulation, base_R, base_p, v_gen, q):
 
 
 def pack_pose(R, p, om, vo, rest_R, rest_p) -> np.ndarray:
-    """fsg_body_pose layout (240 doubles): BoneTransforms::of (skinning.hpp:90-99)
+    """fsg_body_pose layout (30 * SKIN_MAX_LINKS doubles): BoneTransforms::of (skinning.hpp:90-99)
     + the KinematicsCache fields."""
     L = R.shape[0]
     bR = np.einsum("lij,lkj->lik", R, rest_R)        # R_world * rest.R^T
     bt = p - np.einsum("lij,lj->li", bR, rest_p)      # p_world - R_b * rest.p
-    out = np.zeros(240)
+    out = np.zeros(30 * SKIN_L)
     o = 0
     for a, w in ((bR, 9), (bt, 3), (R, 9), (p, 3), (vo, 3), (om, 3)):
         out[o:o + L * w] = a.reshape(-1)
-        o += 8 * w
+        o += SKIN_L * w
     return out
 
 
@@ -300,9 +301,9 @@ class Scene:
         return R0, pose.p, v, q
 
     def poses(self, step: int) -> np.ndarray:
-        """[n_bodies, 240] packed fsg_body_pose of every body at `step`."""
+        """[n_bodies, 30 * SKIN_MAX_LINKS] packed fsg_body_pose of every body at `step`."""
         arts = self.articulations()
-        out = np.zeros((len(arts), 240))
+        out = np.zeros((len(arts), 30 * SKIN_L))
         for k, a in enumerate(arts):
             R0, p0, v, q = self.joint_state(k, step)
             R, p, om, vo = forward_kinematics(a, R0, p0, v, q)

@@ -166,7 +166,7 @@ class FrameFollower:
             pass
 
 
-POSE_DOUBLES = 240  # sizeof(fsg_body_pose) / 8
+POSE_DOUBLES = 30 * _abi.SKIN_MAX_LINKS  # sizeof(fsg_body_pose) / 8
 
 
 @dataclass
@@ -405,7 +405,7 @@ class CoupledSession:
 
     def set_pose(self, poses) -> None:
         """This step's pose of every skinned body: a list of BodyPose, or an
-        [n_bodies, 240] array already packed in fsg_body_pose order."""
+        [n_bodies, POSE_DOUBLES] array already packed in fsg_body_pose order."""
         if getattr(self, "_pose", None) is None:  # no skinned bodies: the ABI reports it
             check(self._L.fsg_set_pose(self._h, None))
         if isinstance(poses, np.ndarray):
@@ -428,7 +428,7 @@ class CoupledSession:
     def step_skinned(self, frame, poses):
         """The robot loop's per-step exchange in one ABI call (fsg_step_skinned):
         frame (FrameState, a packed [19] array, or None to keep it), poses
-        ([n_bodies, 240] packed or a list of BodyPose) -> (StepStatus,
+        ([n_bodies, POSE_DOUBLES] packed or a list of BodyPose) -> (StepStatus,
         tau_ext per body, stats[n_bodies, 7])."""
         fp = None
         if frame is not None:
@@ -606,7 +606,7 @@ class EnvBatch:
 
     def step_skinned(self, frames, poses):
         """Every env skinned (set_skin on each): frames ([E, 19] packed, a list
-        of FrameState, or None to keep) and poses ([E, 240] packed) in, one
+        of FrameState, or None to keep) and poses ([E, POSE_DOUBLES] packed) in, one
         batched step -> (statuses, tau_ext per env, stats[E, 7])."""
         E = len(self.envs)
         if not hasattr(self, "_bpose"):
@@ -644,7 +644,7 @@ class EnvBatch:
         (fsg_batch_step_dynamic): ``robots`` is a dynamics.RobotBatch with one
         robot per env (rest pose set), ``actuation`` [E, n_joints] -> (statuses,
         robot flags [E], post-step states as packed fsg_joint_state rows
-        [E, 43]: base_pos 3, base_quat 4, q 8, v 14, qdd 14;
+        [E, 55]: base_pos 3, base_quat 4, q 12, v 18, qdd 18;
         dynamics.unpack_states turns them into JointStates)."""
         E = len(self.envs)
         if not hasattr(self, "_dst"):
@@ -713,13 +713,13 @@ class DragBatch:
         self._ndofs[env] = int(skeleton.n_dofs)
 
     def set_pose(self, env: int, pose) -> None:
-        """pose: a BodyPose or a packed [240] array (fsg_body_pose order)."""
+        """pose: a BodyPose or a packed [POSE_DOUBLES] array (fsg_body_pose order)."""
         self._pose_np[env] = pose if isinstance(pose, np.ndarray) else pose.packed()
         addr = C.addressof(self._poses) + env * C.sizeof(_abi.fsg_body_pose)
         _abi.check(self._L.fsg_drag_set_pose(self._h, int(env), addr), drag=True)
 
     def set_poses(self, poses: np.ndarray) -> None:
-        """Every env's pose: [n_envs, 240] packed fsg_body_pose rows."""
+        """Every env's pose: [n_envs, POSE_DOUBLES] packed fsg_body_pose rows."""
         self._pose_np[...] = np.asarray(poses, dtype=np.float64).reshape(self._pose_np.shape)
         _abi.check(self._L.fsg_drag_set_poses(self._h, C.addressof(self._poses)), drag=True)
 

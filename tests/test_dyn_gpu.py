@@ -12,6 +12,7 @@ import pytest
 
 from oracle import bind as B
 from paper_2206_01683_b200 import dynamics as D
+from paper_2206_01683_b200._abi import DYN_MAX_DOFS, DYN_MAX_LINKS
 from paper_2206_01683_b200.scenes import koi_articulation, koi_body
 from dyn_cases import G, fin_tree, make_chain, skewed_chain
 
@@ -286,5 +287,5 @@ def test_batch_step_dynamic_rejects_mismatches():
     for s in b.envs:
         s.set_skin(*sc.skin())
     st, fl, packed = b.step_dynamic(rb, act)  # now well-formed
-    assert all(x.stable() for x in st) and packed.shape == (2, 43)
+    assert all(x.stable() for x in st) and packed.shape == (2, 7 + DYN_MAX_LINKS + 2 * DYN_MAX_DOFS)
     b.close()

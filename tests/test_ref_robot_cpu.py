@@ -29,7 +29,7 @@ from oracle import bind as B
 
 pytestmark = pytest.mark.skipif(not B.have_ref(), reason="oracle/_ref not built")
 
-DESIGNS = ["koi", "flatfish"]
+DESIGNS = ["koi", "flatfish", "eel"]
 
 
 def _gait(robot, t):
