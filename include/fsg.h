@@ -132,6 +132,11 @@ int fsg_follower_reset(fsg_follower* f, const double p[3], double yaw);         
 int fsg_follower_step(fsg_follower* f, const double target_p[3], const double target_q[4],
                       double dt);                                                     /* :90-119 */
 int fsg_follower_state(const fsg_follower* f, fsg_frame_state* out);
+/* restore a state (e.g. the origin shift of fsg_recenter, a checkpoint) */
+int fsg_follower_set_state(fsg_follower* f, const fsg_frame_state* in);
+/* CoupledSession::center_frame_on_robot (session.hpp:210-221): reset to the
+ * robot base position with its yaw (0 in TRANSLATION mode; origin in NONE) */
+int fsg_follower_center(fsg_follower* f, const double base_p[3], const double base_q[4]);
 
 /* ---- coupled step (session.hpp:87-198, fluid half :94-166) -------------- */
 /* Marker state for this step, world frame SI (what robot::update_samples
@@ -271,7 +276,8 @@ int fsg_drag_step(fsg_drag* d, double* tau_ext, double* stats);
  * Errors: fsg_dyn_last_error() (Skeleton::validate messages, InputError);
  * a mass matrix that is not positive definite (NumericalError in the
  * reference, dynamics.hpp:208-210) sets FSG_DYN_NOT_SPD in the env's flags
- * and leaves that env's state unchanged. */
+ * and stops that env at the failing substep: its state keeps the substeps
+ * completed before it (as the reference's integrate throwing mid-loop). */
 #define FSG_DYN_MAX_LINKS 12 /* eel: 11 links, 16 dofs */
 #define FSG_DYN_MAX_DOFS (6 + FSG_DYN_MAX_LINKS)
 enum { FSG_JOINT_FREE = 0, FSG_JOINT_REVOLUTE = 1, FSG_JOINT_FIXED = 2 };
@@ -397,12 +403,29 @@ int fsg_batch_step_skinned(fsg_batch* b, const fsg_frame_state* frames, const fs
  * runs, and its tau_ext feeds the robot step (buoyancy_gravity_forces +
  * integrate, session.hpp:169-175) in the same stream.  Up: frames (NULL:
  * keep) and actuation [n_envs * n_joints]; down: statuses, robot flags and
- * the post-step robot states (each nullable; states feed the caller's
- * FrameFollower). */
+ * the post-step robot states (each nullable).  tau_ext never leaves the
+ * device between the fluid and the robot step.  dt and rho_fluid must be the
+ * envs' cfg.dt and cfg.rho (the reference integrates with the session's
+ * units, session.hpp:171-174).  With following on (fsg_batch_set_follow)
+ * frames must be NULL: each env's frame is its FrameFollower's state, which
+ * the call advances after the robot step, recentring the env's lattice when
+ * the robot's COM leaves the threshold (session.hpp:177-195) -- the
+ * reference's whole CoupledSession::step with the robot on the device. */
 int fsg_batch_step_dynamic(fsg_batch* b, fsg_dyn* d, const fsg_frame_state* frames,
                            const double* actuation, double rho_fluid, const double* g_hydro,
                            double dt, int substeps, fsg_status* statuses, int* flags,
                            fsg_joint_state* states);
+/* Frame following inside fsg_batch_step_dynamic: one FrameFollower per env in
+ * the envs' cfg.frame_mode (not NONE) with time_constant (frame_time_constant,
+ * session.hpp:17) and recenter_threshold_cells (session.hpp:18).
+ * time_constant <= 0 turns following off (frames are then the caller's). */
+int fsg_batch_set_follow(fsg_batch* b, double time_constant, double recenter_threshold_cells);
+/* center_frame_on_robot for every env (session.hpp:210-221): each follower is
+ * reset to its robot's current base position and yaw; the envs' frames too. */
+int fsg_batch_center_frames(fsg_batch* b, fsg_dyn* d);
+/* the recentre shifts the last fsg_batch_step_dynamic applied, [3 * n_envs]
+ * (0 where the env's robot stayed inside the threshold) */
+int fsg_batch_last_shifts(const fsg_batch* b, int* shifts);
 
 /* ---- z-slab halo exchange ------------------------------
  * A slab session (cfg.z_offset / cfg.nz_global) owns planes [z_offset,

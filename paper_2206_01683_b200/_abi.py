@@ -173,6 +173,11 @@ SIGNATURES = {
     "fsg_follower_reset": (C.c_int, [_vp, _dp, C.c_double]),
     "fsg_follower_step": (C.c_int, [_vp, _dp, _dp, C.c_double]),
     "fsg_follower_state": (C.c_int, [_vp, C.POINTER(fsg_frame_state)]),
+    "fsg_follower_set_state": (C.c_int, [_vp, C.POINTER(fsg_frame_state)]),
+    "fsg_follower_center": (C.c_int, [_vp, _dp, _dp]),
+    "fsg_batch_set_follow": (C.c_int, [_vp, C.c_double, C.c_double]),
+    "fsg_batch_center_frames": (C.c_int, [_vp, _vp]),
+    "fsg_batch_last_shifts": (C.c_int, [_vp, _vp]),
     "fsg_batch_create": (C.c_int, [C.POINTER(fsg_config), C.c_int, C.POINTER(_vp)]),
     "fsg_batch_destroy": (C.c_int, [_vp]),
     "fsg_batch_session": (_vp, [_vp, C.c_int]),

@@ -1000,6 +1000,28 @@ __global__ void __launch_bounds__(DYN_BLOCK)
   }
 }
 
+// RobotInstance::com_world (backend.hpp:24-33) of every env's current state:
+// sum_i mass_i (p_world_i + R_world_i com_i) / sum_i mass_i, ascending links
+// (Eigen's coefficient order), for the recentre trigger of session.hpp:181-193.
+__global__ void __launch_bounds__(DYN_BLOCK)
+    k_dyn_com(const DynConst* __restrict__ gc, const fsg_joint_state* __restrict__ states,
+              double* __restrict__ com, int E) {
+  __shared__ DynConst c;
+  load_const(c, gc);
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= E) return;
+  KC k;
+  dk_fk(c, states[e], k);
+  double w[3] = {0.0, 0.0, 0.0}, m = 0.0;
+  for (int i = 0; i < c.n_links; ++i) {
+    double rc[3];
+    mv3(k.Rw[i], c.com[i], rc);
+    for (int a = 0; a < 3; ++a) w[a] = w[a] + c.mass[i] * (k.pw[i][a] + rc[a]);
+    m = m + c.mass[i];
+  }
+  for (int a = 0; a < 3; ++a) com[3 * e + a] = w[a] / m;
+}
+
 // ---- host ----------------------------------------------------------------
 // Skeleton::validate (skeleton.hpp:95-118); messages follow the reference
 // (links are named by index: fsg_link carries no name)
@@ -1175,6 +1197,13 @@ int dyn_upload_actuation(fsg_dyn* d, const double* act, cudaStream_t s, double**
   return FSG_OK;
 }
 
+int dyn_launch_com(fsg_dyn* d, double* d_com, cudaStream_t s) {
+  DevGuard g(d->dev);
+  k_dyn_com<<<blocks(d->E), DYN_BLOCK, 0, s>>>(d->d_c, d->d_state, d_com, d->E);
+  CK(cudaGetLastError());
+  return FSG_OK;
+}
+
 int dyn_read_states(fsg_dyn* d, fsg_joint_state* out, int* flags, cudaStream_t s) {
   DevGuard g(d->dev);
   if (out)
@@ -1238,7 +1267,7 @@ int fsg_dyn_create(const fsg_robot* robot, int n_envs, int device, fsg_dyn** out
       cudaMalloc(&d->d_bladder, sizeof(double) * n_envs) != cudaSuccess ||
       cudaMalloc(&d->d_act, sizeof(double) * n_envs * (nj > 0 ? nj : 1)) != cudaSuccess ||
       cudaMalloc(&d->d_tau, sizeof(double) * n_envs * nd) != cudaSuccess ||
-      cudaMalloc(&d->d_rest, sizeof(double) * NL * 12) != cudaSuccess ||
+      cudaMalloc(&d->d_rest, sizeof(double) * NL * 24) != cudaSuccess ||  // set_rest | poses scratch
       cudaMalloc(&d->d_flags, sizeof(int) * n_envs) != cudaSuccess ||
       cudaMalloc(&d->d_M, sizeof(double) * n_envs * (nd * nd + nd)) != cudaSuccess ||
       cudaMalloc(&d->d_pose, sizeof(fsg_body_pose) * n_envs) != cudaSuccess)
@@ -1368,9 +1397,11 @@ int fsg_dyn_poses(fsg_dyn* d, const double* rest_R, const double* rest_p, fsg_bo
   if (!d || !rest_R || !rest_p || !poses) return fail(FSG_EINPUT, "NULL argument");
   DevGuard g(d->dev);
   const int nl = d->hc.n_links;
-  CK(cudaMemcpyAsync(d->d_rest, rest_R, sizeof(double) * 9 * nl, cudaMemcpyHostToDevice, d->s));
-  CK(cudaMemcpyAsync(d->d_rest + 9 * NL, rest_p, sizeof(double) * 3 * nl, cudaMemcpyHostToDevice, d->s));
-  k_dyn_pose<<<blocks(d->E), DYN_BLOCK, 0, d->s>>>(d->d_c, d->d_state, d->d_rest, d->d_rest + 9 * NL,
+  // its own scratch: the rest pose fsg_dyn_set_rest gave the batched loop stays
+  double* rs = d->d_rest + 12 * NL;
+  CK(cudaMemcpyAsync(rs, rest_R, sizeof(double) * 9 * nl, cudaMemcpyHostToDevice, d->s));
+  CK(cudaMemcpyAsync(rs + 9 * NL, rest_p, sizeof(double) * 3 * nl, cudaMemcpyHostToDevice, d->s));
+  k_dyn_pose<<<blocks(d->E), DYN_BLOCK, 0, d->s>>>(d->d_c, d->d_state, rs, rs + 9 * NL,
                                                    reinterpret_cast<char*>(d->d_pose),
                                                    sizeof(fsg_body_pose), d->E);
   CK(cudaGetLastError());

@@ -16,6 +16,8 @@ int dyn_launch_step(fsg_dyn* d, const double* d_actuation, const double* d_tau_e
 int dyn_launch_pose(fsg_dyn* d, void* dst, size_t stride, cudaStream_t s);
 int dyn_upload_actuation(fsg_dyn* d, const double* act, cudaStream_t s, double** d_act);
 int dyn_read_states(fsg_dyn* d, fsg_joint_state* out, int* flags, cudaStream_t s);
+// RobotInstance::com_world of every env's current state into d_com [3 * E]
+int dyn_launch_com(fsg_dyn* d, double* d_com, cudaStream_t s);
 int* dyn_flags(fsg_dyn* d);
 int dyn_n_envs(const fsg_dyn* d);
 int dyn_n_links(const fsg_dyn* d);

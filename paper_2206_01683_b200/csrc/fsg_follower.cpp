@@ -170,4 +170,20 @@ int fsg_follower_state(const fsg_follower* f, fsg_frame_state* out) {
   return FSG_OK;
 }
 
+int fsg_follower_set_state(fsg_follower* f, const fsg_frame_state* in) {
+  if (!f || !in) return FSG_EINPUT;
+  f->f = *in;
+  return FSG_OK;
+}
+
+int fsg_follower_center(fsg_follower* f, const double base_p[3], const double base_q[4]) {
+  if (!f || !base_p || !base_q) return FSG_EINPUT;
+  // CoupledSession::center_frame_on_robot (session.hpp:210-221)
+  if (f->mode == FSG_FRAME_NONE) {
+    const double z[3] = {0.0, 0.0, 0.0};
+    return fsg_follower_reset(f, z, 0.0);
+  }
+  return fsg_follower_reset(f, base_p, f->mode == FSG_FRAME_TRANSLATION ? 0.0 : yaw_of(base_q));
+}
+
 }  // extern "C"

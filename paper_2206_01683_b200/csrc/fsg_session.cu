@@ -871,12 +871,11 @@ int fsg_get_frame(fsg_session* s, fsg_frame_state* fs) {
   return FSG_OK;
 }
 
-int fsg_recenter(fsg_session* s, const int shift[3]) {
-  if (s->g.zpad) return set_err(FSG_EINPUT, "recenter is not defined for z-slab sessions");
-  CU(cudaSetDevice(s->cfg.device));
+// frame::recenter (frame.hpp:132-154) enqueued on the session stream: the
+// shifted, clamped gather of the post-stream state, and the frame origin.
+static int recenter_async(fsg_session* s, const int shift[3]) {
   s->L->recenter(s->g, s->A(), s->pulled, s->B(), shift[0], shift[1], shift[2], s->stream);
   CU_LAUNCH();
-  CU(cudaStreamSynchronize(s->stream));
   s->par ^= 1;
   s->pulled = 0;
   state_changed(s);
@@ -887,6 +886,15 @@ int fsg_recenter(fsg_session* s, const int shift[3]) {
   double r[3];
   mat_vec(R, off, r);
   for (int k = 0; k < 3; ++k) s->frame.p[k] = s->frame.p[k] + r[k];
+  return FSG_OK;
+}
+
+int fsg_recenter(fsg_session* s, const int shift[3]) {
+  if (s->g.zpad) return set_err(FSG_EINPUT, "recenter is not defined for z-slab sessions");
+  CU(cudaSetDevice(s->cfg.device));
+  const int rc = recenter_async(s, shift);
+  if (rc) return rc;
+  CU(cudaStreamSynchronize(s->stream));
   return FSG_OK;
 }
 
@@ -1795,8 +1803,21 @@ struct fsg_batch {
   int par = 0;
   dim3 block;
   fsg_dyn* dyn = nullptr;                          // set during fsg_batch_step_dynamic
-  const double** h_tauptr = nullptr;               // pinned: every env's tau_ext (mapped)
-  const double** d_tauptr = nullptr;
+  // the robot loop on the device (fsg_batch_step_dynamic): tau_ext + stats of
+  // every env stay in device memory for the robot step; one copy comes back
+  static constexpr int WSTRIDE = 6 + FSG_SKIN_MAX_LINKS + fsg::SKIN_NSTAT;
+  double* d_wrench = nullptr;                      // [E][WSTRIDE]
+  double* h_wbatch = nullptr;                      // pinned copy
+  const double** d_tauptr = nullptr;               // [E] -> d_wrench rows
+  fsg_joint_state* h_states = nullptr;             // pinned: post-step robot states
+  int* h_flags = nullptr;
+  // frame following + recentring inside the loop (session.hpp:177-195)
+  int follow = 0;
+  double follow_thresh = 2.0;
+  std::vector<fsg_follower*> fol;
+  double* d_com = nullptr;                         // [3E] com_world of the post-step states
+  double* h_com = nullptr;
+  std::vector<int> shifts;                         // [3E] last call's recentre shifts
 };
 
 int fsg_batch_destroy(fsg_batch* b) {
@@ -1810,8 +1831,14 @@ int fsg_batch_destroy(fsg_batch* b) {
     cudaFree(b->d_skb[k]);
     if (b->ev[k]) cudaEventDestroy(b->ev[k]);
   }
-  if (b->h_tauptr) cudaFreeHost(b->h_tauptr);
   cudaFree(b->d_tauptr);
+  cudaFree(b->d_wrench);
+  cudaFree(b->d_com);
+  if (b->h_wbatch) cudaFreeHost(b->h_wbatch);
+  if (b->h_states) cudaFreeHost(b->h_states);
+  if (b->h_flags) cudaFreeHost(b->h_flags);
+  if (b->h_com) cudaFreeHost(b->h_com);
+  for (auto* f : b->fol) fsg_follower_destroy(f);
   cudaFree(b->d_work);
   if (b->h_stat) cudaFreeHost(b->h_stat);
   if (b->stream) cudaStreamDestroy(b->stream);
@@ -1923,7 +1950,8 @@ int fsg_batch_step_async(fsg_batch* b) {
       P.sk_wb = s->skp.wb;
       P.sk_ww = s->skp.ww;
       P.sk_acc = s->d_skin_fix;
-      P.sk_out = s->h_wrench[p];
+      // robot loop on the device: tau_ext stays in HBM for the robot step
+      P.sk_out = (b->dyn && b->d_wrench) ? b->d_wrench + (size_t)e * fsg_batch::WSTRIDE : s->h_wrench[p];
       P.sk_ndof = s->skp.body[0].n_dofs;
       ++nskin;
     }
@@ -2017,6 +2045,68 @@ int fsg_batch_step_skinned(fsg_batch* b, const fsg_frame_state* frames, const fs
   return FSG_OK;
 }
 
+// the device-resident robot loop's buffers (allocated at the first call)
+static int batch_dyn_buffers(fsg_batch* b) {
+  if (b->d_wrench) return FSG_OK;
+  CU(cudaMalloc(&b->d_wrench, sizeof(double) * fsg_batch::WSTRIDE * b->E));
+  CU(cudaMemsetAsync(b->d_wrench, 0, sizeof(double) * fsg_batch::WSTRIDE * b->E, b->stream));
+  CU(cudaMallocHost(&b->h_wbatch, sizeof(double) * fsg_batch::WSTRIDE * b->E));
+  CU(cudaMalloc(&b->d_tauptr, sizeof(double*) * b->E));
+  std::vector<const double*> tp(b->E);
+  for (int e = 0; e < b->E; ++e) tp[e] = b->d_wrench + (size_t)e * fsg_batch::WSTRIDE;
+  CU(cudaMemcpyAsync(b->d_tauptr, tp.data(), sizeof(double*) * b->E, cudaMemcpyHostToDevice,
+                     b->stream));
+  CU(cudaMallocHost(&b->h_states, sizeof(fsg_joint_state) * b->E));
+  CU(cudaMallocHost(&b->h_flags, sizeof(int) * b->E));
+  CU(cudaMalloc(&b->d_com, sizeof(double) * 3 * b->E));
+  CU(cudaMallocHost(&b->h_com, sizeof(double) * 3 * b->E));
+  CU(stream_wait(b->stream));
+  b->shifts.assign(3 * (size_t)b->E, 0);
+  return FSG_OK;
+}
+
+int fsg_batch_set_follow(fsg_batch* b, double time_constant, double recenter_threshold_cells) {
+  if (!b) return set_err(FSG_EINPUT, "fsg_batch_set_follow: NULL handle");
+  for (auto* f : b->fol) fsg_follower_destroy(f);
+  b->fol.clear();
+  b->follow = 0;
+  if (!(time_constant > 0.0)) return FSG_OK;
+  const int mode = b->envs[0]->cfg.frame_mode;
+  if (mode == FSG_FRAME_NONE)
+    return set_err(FSG_EINPUT, "fsg_batch_set_follow: frame_mode NONE is the static domain (nothing to follow)");
+  if (!(recenter_threshold_cells >= 0.0))
+    return set_err(FSG_EINPUT, "fsg_batch_set_follow: negative recenter threshold");
+  for (int e = 0; e < b->E; ++e) {
+    fsg_follower* f = nullptr;
+    if (fsg_follower_create(mode, time_constant, &f)) return set_err(FSG_EINPUT, "bad follow mode");
+    b->fol.push_back(f);
+    fsg_follower_state(f, &b->envs[e]->frame);
+  }
+  b->follow = 1;
+  b->follow_thresh = recenter_threshold_cells;
+  return FSG_OK;
+}
+
+int fsg_batch_center_frames(fsg_batch* b, fsg_dyn* d) {
+  if (!b || !d) return set_err(FSG_EINPUT, "fsg_batch_center_frames: NULL handle");
+  if (!b->follow) return set_err(FSG_ESTATE, "fsg_batch_center_frames: following is off");
+  if (fsg::dyn_n_envs(d) != b->E)
+    return set_err(FSG_EINPUT, "fsg_batch_center_frames: %d robots for %d envs", fsg::dyn_n_envs(d), b->E);
+  std::vector<fsg_joint_state> st(b->E);
+  if (fsg_dyn_get_state(d, st.data())) return set_err(FSG_ECUDA, "%s", fsg_dyn_last_error());
+  for (int e = 0; e < b->E; ++e) {
+    fsg_follower_center(b->fol[e], st[e].base_pos, st[e].base_quat);
+    fsg_follower_state(b->fol[e], &b->envs[e]->frame);
+  }
+  return FSG_OK;
+}
+
+int fsg_batch_last_shifts(const fsg_batch* b, int* shifts) {
+  if (!b || !shifts) return set_err(FSG_EINPUT, "fsg_batch_last_shifts: NULL argument");
+  for (int k = 0; k < 3 * b->E; ++k) shifts[k] = b->shifts.empty() ? 0 : b->shifts[k];
+  return FSG_OK;
+}
+
 int fsg_batch_step_dynamic(fsg_batch* b, fsg_dyn* d, const fsg_frame_state* frames,
                            const double* actuation, double rho_fluid, const double* g_hydro,
                            double dt, int substeps, fsg_status* statuses, int* flags,
@@ -2028,40 +2118,60 @@ int fsg_batch_step_dynamic(fsg_batch* b, fsg_dyn* d, const fsg_frame_state* fram
     return set_err(FSG_EINPUT, "fsg_batch_step_dynamic: robots and envs on different devices");
   if (!fsg::dyn_rest_set(d))
     return set_err(FSG_ESTATE, "fsg_batch_step_dynamic: fsg_dyn_set_rest has not been called");
-  CU(cudaSetDevice(b->envs[0]->cfg.device));
+  const fsg_config& c0 = b->envs[0]->cfg;
+  if (dt != c0.dt || rho_fluid != c0.rho)
+    return set_err(FSG_EINPUT, "fsg_batch_step_dynamic: dt %g / rho %g differ from the envs' %g / %g "
+                               "(the robots integrate with the session's units, session.hpp:171-174)",
+                   dt, rho_fluid, c0.dt, c0.rho);
+  if (b->follow && frames)
+    return set_err(FSG_EINPUT, "fsg_batch_step_dynamic: frames come from the followers (pass NULL)");
+  // every check before any env is touched
   for (int e = 0; e < b->E; ++e) {
     fsg_session* s = b->envs[e];
     if (!s->skin || s->skp.nb != 1)
       return set_err(FSG_ESTATE, "fsg_batch_step_dynamic: env %d has no single skinned body", e);
     if (s->skp.body[0].n_dofs != fsg_dyn_n_dofs(d) || s->skp.body[0].n_links != fsg::dyn_n_links(d))
       return set_err(FSG_EINPUT, "fsg_batch_step_dynamic: env %d's skeleton is not the robot's", e);
-    if (frames) s->frame = frames[e];
-    s->pose_set = true;  // the pose is produced on the device
   }
+  CU(cudaSetDevice(c0.device));
+  int rc = batch_dyn_buffers(b);
+  if (rc) return rc;
+  std::vector<char> had_pose(b->E);
+  for (int e = 0; e < b->E; ++e) {
+    fsg_session* s = b->envs[e];
+    if (b->follow) fsg_follower_state(b->fol[e], &s->frame);
+    else if (frames) s->frame = frames[e];
+    had_pose[e] = s->pose_set;
+    s->pose_set = true;  // this step's pose is produced on the device
+  }
+  auto restore_pose = [&] {  // the host pose was not updated: plain steps need fsg_set_pose again
+    for (int e = 0; e < b->E; ++e) b->envs[e]->pose_set = false;
+  };
   double* d_act = nullptr;
-  int rc = fsg::dyn_upload_actuation(d, actuation, b->stream, &d_act);
-  if (rc) return set_err(rc, "%s", fsg_dyn_last_error());
+  rc = fsg::dyn_upload_actuation(d, actuation, b->stream, &d_act);
+  if (rc) return restore_pose(), set_err(rc, "%s", fsg_dyn_last_error());
   const int q = b->par;
   b->dyn = d;
   rc = fsg_batch_step_async(b);
   b->dyn = nullptr;
+  restore_pose();
   if (rc) return rc;
-  if (!b->h_tauptr) {
-    CU(cudaMallocHost(&b->h_tauptr, sizeof(double*) * b->E));
-    CU(cudaMalloc(&b->d_tauptr, sizeof(double*) * b->E));
-  }
-  for (int e = 0; e < b->E; ++e) b->h_tauptr[e] = b->envs[e]->h_wrench[b->envs[e]->last_par];
-  CU(cudaMemcpyAsync(b->d_tauptr, b->h_tauptr, sizeof(double*) * b->E, cudaMemcpyHostToDevice,
-                     b->stream));
   // session.hpp:169-175: buoyancy on the pre-step kinematics + integrate
-  // (gravity enters through the hydrostatics only)
+  // (gravity enters through the hydrostatics only); tau_ext from HBM
   rc = fsg::dyn_launch_step(d, d_act, nullptr, b->d_tauptr, rho_fluid, g_hydro, dt, substeps, nullptr,
                             fsg::dyn_flags(d), b->stream);
   if (rc) return set_err(rc, "%s", fsg_dyn_last_error());
   if (!b->h_stat) CU(cudaMallocHost(&b->h_stat, sizeof(StepScratch) * b->E));
   k_batch_status<<<1, 256, 0, b->stream>>>(b->d_packs[q], b->E, b->h_stat);
   CU_LAUNCH();
-  rc = fsg::dyn_read_states(d, states, flags, b->stream);
+  if (b->follow) {
+    rc = fsg::dyn_launch_com(d, b->d_com, b->stream);
+    if (rc) return set_err(rc, "%s", fsg_dyn_last_error());
+    CU(cudaMemcpyAsync(b->h_com, b->d_com, sizeof(double) * 3 * b->E, cudaMemcpyDeviceToHost, b->stream));
+  }
+  CU(cudaMemcpyAsync(b->h_wbatch, b->d_wrench, sizeof(double) * fsg_batch::WSTRIDE * b->E,
+                     cudaMemcpyDeviceToHost, b->stream));
+  rc = fsg::dyn_read_states(d, b->h_states, b->h_flags, b->stream);
   if (rc) return set_err(rc, "%s", fsg_dyn_last_error());
   CU(stream_wait(b->stream));
   for (int e = 0; e < b->E; ++e) {
@@ -2069,6 +2179,41 @@ int fsg_batch_step_dynamic(fsg_batch* b, fsg_dyn* d, const fsg_frame_state* fram
     if (b->h_stat[e].band_overflow) return set_err(FSG_ESTATE, "env %d: IB band overflow", e);
     decode_status(b->h_stat[e], &s->last, true);
     if (statuses) statuses[e] = s->last;
+    // tau_ext + stats of the step for fsg_get_body_wrench
+    std::memcpy(s->h_wrench[s->last_par], b->h_wbatch + (size_t)e * fsg_batch::WSTRIDE,
+                sizeof(double) * fsg_batch::WSTRIDE);
+  }
+  if (states) std::memcpy(states, b->h_states, sizeof(fsg_joint_state) * b->E);
+  if (flags) std::memcpy(flags, b->h_flags, sizeof(int) * b->E);
+  if (b->follow) {
+    // session.hpp:177-195: follower toward the new base pose, then the
+    // integer-cell recentre when the robot's COM (frame coordinates) is more
+    // than threshold cells from the centre on any axis
+    for (int e = 0; e < b->E; ++e) {
+      fsg_session* s = b->envs[e];
+      const fsg_joint_state& st = b->h_states[e];
+      fsg_follower_step(b->fol[e], st.base_pos, st.base_quat, dt);
+      fsg_follower_state(b->fol[e], &s->frame);
+      double R[9], d3[3], cf[3];
+      quat_to_R(s->frame.q, R);
+      for (int a = 0; a < 3; ++a) d3[a] = b->h_com[3 * e + a] - s->frame.p[a];
+      mat_t_vec(R, d3, cf);  // world_to_frame_point (frame.hpp:24-26)
+      int shift[3] = {0, 0, 0};
+      bool need = false;
+      for (int a = 0; a < 3; ++a) {
+        const double cells = cf[a] / c0.dx;
+        if (std::abs(cells) > b->follow_thresh) {
+          shift[a] = (int)std::round(cells);
+          need = true;
+        }
+      }
+      for (int a = 0; a < 3; ++a) b->shifts[3 * e + a] = shift[a];
+      if (need) {
+        rc = recenter_async(s, shift);
+        if (rc) return rc;
+        fsg_follower_set_state(b->fol[e], &s->frame);  // the origin advanced by R shift dx
+      }
+    }
   }
   return FSG_OK;
 }

@@ -591,6 +591,7 @@ class EnvBatch:
         h = C.c_void_p()
         check(L.fsg_batch_create(C.byref(cfg.to_c()), int(n_envs), C.byref(h)))
         self._h, self._L = h, L
+        self.cfg = cfg
         self.envs = [CoupledSession(cfg, _borrowed=L.fsg_batch_session(h, e)) for e in range(n_envs)]
 
     def step_async(self) -> None:
@@ -638,11 +639,28 @@ class EnvBatch:
             k += n
         return [StepStatus.of(x) for x in self._bst], taus, out[nt:].reshape(E, 7)
 
-    def step_dynamic(self, robots, actuation, frames=None, rho_fluid: float = 1000.0,
-                     g_hydro=(0.0, 0.0, -9.81), dt: float = 0.004, substeps: int = 4):
+    def set_follow(self, time_constant: float = 0.2, recenter_threshold_cells: float = 2.0) -> None:
+        """FrameFollower + recentring inside step_dynamic (session.hpp:177-195),
+        in the config's frame mode; time_constant <= 0 turns it off."""
+        check(self._L.fsg_batch_set_follow(self._h, float(time_constant),
+                                           float(recenter_threshold_cells)))
+
+    def center_frames(self, robots) -> None:
+        """center_frame_on_robot of every env (session.hpp:210-221)."""
+        check(self._L.fsg_batch_center_frames(self._h, robots._h))
+
+    def last_shifts(self) -> np.ndarray:
+        """[E, 3] recentre shifts the last step_dynamic applied."""
+        out = np.zeros(3 * len(self.envs), dtype=np.int32)
+        check(self._L.fsg_batch_last_shifts(self._h, out.ctypes.data))
+        return out.reshape(-1, 3)
+
+    def step_dynamic(self, robots, actuation, frames=None, rho_fluid: float | None = None,
+                     g_hydro=(0.0, 0.0, -9.81), dt: float | None = None, substeps: int = 4):
         """The whole coupled step with the robots on the device
         (fsg_batch_step_dynamic): ``robots`` is a dynamics.RobotBatch with one
-        robot per env (rest pose set), ``actuation`` [E, n_joints] -> (statuses,
+        robot per env (rest pose set), ``actuation`` [E, n_joints]; dt and
+        rho_fluid default to (and must equal) the config's -> (statuses,
         robot flags [E], post-step states as packed fsg_joint_state rows
         [E, 55]: base_pos 3, base_quat 4, q 12, v 18, qdd 18;
         dynamics.unpack_states turns them into JointStates)."""
@@ -667,6 +685,8 @@ class EnvBatch:
             raise _abi.InputError(_abi.FSG_EINPUT, f"actuation has {act.size} entries, expected "
                                                    f"{robots.n_envs} x {robots.n_joints}")
         gh = None if g_hydro is None else np.ascontiguousarray(np.asarray(g_hydro, dtype=np.float64))
+        rho_fluid = self.cfg.rho if rho_fluid is None else rho_fluid
+        dt = self.cfg.dt if dt is None else dt
         check(self._L.fsg_batch_step_dynamic(self._h, robots._h, fp, dptr(act), float(rho_fluid),
                                              dptr(gh), float(dt), int(substeps),
                                              C.addressof(self._dst_s), self._dfl.ctypes.data,
