@@ -513,13 +513,18 @@ def run_envs(args, scene, rank, local, world):
     e2e_dyn = None
     if skinned and batch and not args.no_robot_leg:
         # the rollout loop with the robots on the device too:
-        # one call per round uploads the actuation, steps fluid + robots, and
-        # returns statuses and the post-step robot states
+        # one call per round uploads the actuation, steps fluid + robots,
+        # advances every env's FrameFollower (and recentres its lattice when
+        # the robot drifts), and returns statuses and the post-step robot
+        # states -- no prescribed frames
         from paper_2206_01683_b200 import dynamics as D
         robot = D.koi_robot(scene.bodies[0], scene.articulations()[0])
         rb = D.RobotBatch(robot, E, device=local)
         rb.set_rest(*D.rest_pose(robot))
         nj = robot.n_joints
+        batch.set_follow(0.2, 2.0)
+        batch.center_frames(rb)
+        n_shift = 0
         dyn_t, dyn_ok, per_call = 0.0, True, []
         for k in range(-3, Ee):  # 3 untimed warm-up rounds (lazy module load, first-call allocations)
             fw_buf.fill_(1.0)
@@ -528,23 +533,27 @@ def run_envs(args, scene, rank, local, world):
             t_ = (kk + Ee + k) * scene.dt
             act = np.array([[0.2 * math.sin(2 * math.pi * 2.0 * t_ - 0.8 * j + e) for j in range(nj)]
                             for e in range(E)])
-            fr = np.stack([frames[e][(kk + k) % nsteps].packed() for e in range(E)])
             t0 = time.perf_counter()
-            sts_d, fl_d, _ = batch.step_dynamic(rb, act, fr, scene.rho, (0.0, 0.0, -9.81), scene.dt, 4)
+            sts_d, fl_d, _ = batch.step_dynamic(rb, act, None, scene.rho, (0.0, 0.0, -9.81), scene.dt, 4)
             if k < 0:
                 continue
+            n_shift += int((batch.last_shifts() != 0).any(axis=1).sum())
             per_call.append(time.perf_counter() - t0)
             dyn_t += per_call[-1]
             dyn_ok &= all(x.stable() for x in sts_d) and not (fl_d & D.FSG_DYN_NONFINITE).any()
         rb.close()
         e2e_dyn = {"value": round(E * scene.n_cells * Ee * world / dyn_t / 1e6, 1), "unit": "MLUPS",
-                   "h2d_bytes_per_step": E * (8 * nj + 152),
-                   "d2h_bytes_per_step": E * (64 + 344 + 4), "steps": Ee, "stable": bool(dyn_ok),
+                   # up: actuation + the env pack (frame constants, state pointers);
+                   # down: status, tau_ext + stats, post-step state, flags, COM
+                   "h2d_bytes_per_step": E * (8 * nj + 440),
+                   "d2h_bytes_per_step": E * (32 + 200 + 440 + 4 + 24), "steps": Ee,
+                   "stable": bool(dyn_ok), "recentres": n_shift,
                    "call_us": {q: round(float(np.percentile(per_call, p)) * 1e6, 1)
                                for q, p in (("p50", 50), ("p90", 90), ("max", 100))},
                    "what": "fsg_batch_step_dynamic: actuation up; device poses, coupled step, "
-                           "buoyancy + integrate (4 substeps) of every robot; statuses + robot "
-                           "states down (the reference's full CoupledSession::step)"}
+                           "buoyancy + integrate (4 substeps) of every robot, FrameFollower + "
+                           "recentre trigger per env; statuses + robot states down (the "
+                           "reference's full CoupledSession::step)"}
     if batch:
         batch.close()
     else:

@@ -1799,6 +1799,7 @@ struct fsg_batch {
   StepScratch* h_stat = nullptr;                   // pinned: every env's status (one-call step)
   fsg::SkinBody* h_skb[2] = {nullptr, nullptr};    // pinned: skinned envs' topology + pose
   fsg::SkinBody* d_skb[2] = {nullptr, nullptr};
+  bool skb_up[2] = {false, false};                 // d_skb[q] topology current (device-pose steps)
   cudaEvent_t ev[2] = {nullptr, nullptr};
   int par = 0;
   dim3 block;
@@ -1908,6 +1909,7 @@ int fsg_batch_step_async(fsg_batch* b) {
   fsg::BatchHead h{b->E, 0, 0, 0, fb0.tnx, fb0.tny, fb0.tnz, 1,
                    b->envs[0]->cfg.frame_mode != FSG_FRAME_NONE ? 1 : 0, 0, 0};
   int npulled = 0, nskin = 0;
+  bool skb_dirty = !b->dyn;  // robot loop: the pose is made on the device, the topology rarely changes
   const int tx_n = (g0.nx + (int)b->block.x - 1) / (int)b->block.x;
   const int ty_n = (g0.ny + (int)b->block.y - 1) / (int)b->block.y;
   // phase-A items: 2 planes when that still leaves >= 8 per resident block
@@ -1943,6 +1945,9 @@ int fsg_batch_step_async(fsg_batch* b) {
       if (s->skp.nb != 1)
         return set_err(FSG_EINPUT, "batched envs: one skinned body per env (env %d has %d)", e, s->skp.nb);
       if (!s->pose_set) return set_err(FSG_ESTATE, "env %d: fsg_set_pose has not been called", e);
+      if (b->dyn && !skb_dirty &&
+          std::memcmp(&b->h_skb[q][e], &s->skp.body[0], offsetof(fsg::SkinBody, pose)) != 0)
+        skb_dirty = true;
       b->h_skb[q][e] = s->skp.body[0];
       P.skb = b->d_skb[q] + e;
       P.sk_rest = s->skp.rest;
@@ -1967,9 +1972,11 @@ int fsg_batch_step_async(fsg_batch* b) {
   h.skin = nskin > 0 ? 1 : 0;
   CU(cudaMemcpyAsync(b->d_packs[q], packs, sizeof(fsg::EnvPack) * b->E, cudaMemcpyHostToDevice,
                      b->stream));
-  if (nskin)
+  if (nskin && (skb_dirty || !b->skb_up[q])) {
     CU(cudaMemcpyAsync(b->d_skb[q], b->h_skb[q], sizeof(fsg::SkinBody) * b->E, cudaMemcpyHostToDevice,
                        b->stream));
+    b->skb_up[q] = b->dyn != nullptr;  // valid topology for the next device-pose step of parity q
+  }
   if (b->dyn) {  // this step's poses from the robot states, written over the uploaded ones
     const int rc = fsg::dyn_launch_pose(b->dyn,
                                         reinterpret_cast<char*>(b->d_skb[q]) + offsetof(fsg::SkinBody, pose),
