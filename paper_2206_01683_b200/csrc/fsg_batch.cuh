@@ -149,7 +149,7 @@ __global__ void __launch_bounds__(128, FSG_KMB_MINB)
       if (S.ok) {
         double acc = 0.0;
         skin_tau_warp(V, B, t, lane, fw, vel, acc);
-        skin_red_marker(acc, lane, P.sk_acc);
+        skin_red_marker(acc, lane, P.sk_acc, t);
       }
       continue;
     }
@@ -232,8 +232,14 @@ __global__ void __launch_bounds__(128, FSG_K4_MINB)
       const EnvPack& Q0 = packs[k >> 5];
       const int c = k & 31;
       if (!Q0.skb) continue;
-      const double d = (double)(long long)__ldcg(Q0.sk_acc + c) * SKIN_FIX_INV;
-      Q0.sk_acc[c] = 0ull;
+      long long v = 0, bad = 0;  // the replicas summed as integers; slot 31 the flag
+      for (int r = 0; r < SKIN_FIX_REP; ++r) {
+        v += (long long)__ldcg(Q0.sk_acc + 64 * r + c);
+        bad |= (long long)__ldcg(Q0.sk_acc + 64 * r + 31);
+      }
+      __syncwarp();  // (env, c) pairs are warp-aligned: every read before the re-zeroing
+      for (int r = 0; r < SKIN_FIX_REP; ++r) Q0.sk_acc[64 * r + c] = 0ull;
+      const double d = bad ? __longlong_as_double(0x7ff8000000000000ll) : (double)v * SKIN_FIX_INV;
       if (c < Q0.sk_ndof) Q0.sk_out[c] = d;
       if (c >= SKIN_TAU_MAX && c < SKIN_TAU_MAX + SKIN_NSTAT) Q0.sk_out[Q0.sk_ndof + (c - SKIN_TAU_MAX)] = d;
     }

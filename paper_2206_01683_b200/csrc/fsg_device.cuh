@@ -186,6 +186,8 @@ constexpr double FIX_INV = 1.0 / 1099511627776.0;   // 2^-40
 // re-zeroes them.  acc = nullptr: no skinned bodies.
 constexpr double SKIN_FIX_SCALE = 17592186044416.0;      // 2^44
 constexpr double SKIN_FIX_INV = 1.0 / 17592186044416.0;  // 2^-44
+constexpr double SKIN_FIX_RANGE = 524288.0;               // 2^19: |sum| * 2^44 < 2^63
+constexpr int SKIN_FIX_REP = 16;  // copies of the fused path's [2][32] accumulators
 struct SkinOut {
   unsigned long long* acc;  // [nb][32]: dof c (< 14) and stat 14 + k
   double* out;              // tau (concatenated) then 7 stats per body

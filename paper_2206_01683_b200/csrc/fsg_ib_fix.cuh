@@ -166,7 +166,11 @@ __device__ __forceinline__ void mk_finish(const Grid& g, const float* __restrict
       cio[r] = rem - jo * S.cnt[0];
       cjo[r] = jo;
       cko[r] = ko;
+#ifndef FSG_KM_NO_GATHER  // dev attribution only (wrong results)
       if (c < ncell) gather_cell<PULLED>(g, A, S.lo[0] + cio[r], S.lo[1] + jo, S.lo[2] + ko - g.z0, sv[r]);
+#else
+      for (int i = 0; i < Q; ++i) sv[r][i] = 0.f;
+#endif
     }
 #pragma unroll
     for (int r = 0; r < FX_CPL; ++r) {
@@ -261,9 +265,13 @@ __device__ __forceinline__ void mk_finish(const Grid& g, const float* __restrict
     const long long cell = (long long)(S.lo[0] + io) +
                            (long long)g.nx * ((long long)(S.lo[1] + jo) + (long long)g.ny * (S.lo[2] + ko - g.z0));
     unsigned long long* F = fb.F + 3 * cell;
+#ifndef FSG_KM_NO_SPREAD  // dev attribution only (wrong results)
     atomicAdd(F, to_fix(w * fx));
     atomicAdd(F + 1, to_fix(w * fy));
     atomicAdd(F + 2, to_fix(w * fz));
+#else
+    if (w * fx == 12345.0) atomicAdd(F, 1ull);
+#endif
   }
 }
 
@@ -339,13 +347,33 @@ __global__ void __launch_bounds__(128, FSG_KM_MINB)
     constexpr int NW = (int)(sizeof(SkinBody) / 8) * NB;
     const double* src = reinterpret_cast<const double*>(&P.body[0]);
     double* dst = reinterpret_cast<double*>(&sbody[0]);
+#if FSG_SKIN_STAGE == 1
+    // warp-uniform parameter loads (one constant-bank access each, broadcast);
+    // lane j keeps the j-th of every 32 and stores it
+    const int ln = threadIdx.x & 31;
+    for (int base = (threadIdx.x >> 5) * 32; base < NW; base += 128) {
+      double mine = 0.0;
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {
+        const double v = base + j < NW ? src[base + j] : 0.0;
+        if (ln == j) mine = v;
+      }
+      if (base + ln < NW) dst[base + ln] = mine;
+    }
+#else
     for (int i = threadIdx.x; i < NW; i += blockDim.x) dst[i] = src[i];
+#endif
   }
   __syncthreads();
   const int lane = threadIdx.x & (FX_LANES - 1);
   const int slot = threadIdx.x / FX_LANES;
   const int stride = gridDim.x * FX_PER_BLOCK;
   const SessionConsts& sc = *scp;
+  // the stencil of the group's last stamped marker, reused after the trigger
+  // (one marker per group in the default single-wave grid)
+  __shared__ MkStencil s_st[FX_PER_BLOCK];
+  __shared__ int s_t[FX_PER_BLOCK];
+  if (lane == 0) s_t[slot] = -1;
   if (threadIdx.x == 0) FSG_TL(fb.stamp, 0);
   for (int t = blockIdx.x * FX_PER_BLOCK + slot; t < mk.m; t += stride) {
     const SkinBody& B = sbody[skin_body_of(P, t)];
@@ -362,6 +390,10 @@ __global__ void __launch_bounds__(128, FSG_KM_MINB)
     mk_stencil_x(xw, sc, st, S);
     if (fb.tlist) mk_stamp_list(g, fb, S, lane, out);
     else mk_stamp(g, fb, S, lane);
+    if (lane == 0) {
+      s_st[slot] = S;
+      s_t[slot] = t;
+    }
   }
   mk_publish_stamps(fb, out);
   double acc[NB];
@@ -371,12 +403,19 @@ __global__ void __launch_bounds__(128, FSG_KM_MINB)
     const int bi = skin_body_of(P, t);
     const SkinBody& B = sbody[bi];
     const SkinSlot sl = skin_slot(P, t, lane);
-    double xw[3], vel[3], nrm[3], fw[3];
+    double vel[3], nrm[3], fw[3];
     skin_vel_nrm_warp(P, B.pose, t, sl, vel, nrm);
-    // the position this warp skinned before the stamps (the block barrier
-    // since orders lane 0's store before these loads)
+    MkStencil S;
+    if (s_t[slot] == t) {
+      S = s_st[slot];  // lane 0's copy from the stamp phase (the block barrier since orders it)
+    } else {
+      // the position this warp skinned before the stamps (the block barrier
+      // since orders lane 0's store before these loads)
+      double xw[3];
 #pragma unroll
-    for (int c = 0; c < 3; ++c) xw[c] = __ldcg(mk.pts + 3 * t + c);
+      for (int c = 0; c < 3; ++c) xw[c] = __ldcg(mk.pts + 3 * t + c);
+      mk_stencil_x(xw, sc, st, S);
+    }
     if (lane == 0) {
       double* v = const_cast<double*>(mk.vel);
       double* n = const_cast<double*>(mk.nrm);
@@ -386,8 +425,6 @@ __global__ void __launch_bounds__(128, FSG_KM_MINB)
         n[3 * t + c] = nrm[c];
       }
     }
-    MkStencil S;
-    mk_stencil_x(xw, sc, st, S);
     mk_finish<PULLED>(g, A, mk, t, lane, sc, st, S, phs[slot], rec_out, fworld, fworld_h, valid_h, fb,
                       out, vel, nrm, fw);
     __syncwarp(fx_mask());

@@ -253,9 +253,13 @@ __global__ void __launch_bounds__(128, FSG_K4B_MINB)
   // skinned bodies: the marker grid's tau_ext / stats sums are complete
   if (so.acc && blockIdx.x == gridDim.x - 1 && tid < so.nb * 32) {
     const int b = tid >> 5, c = tid & 31;
-    const long long v = (long long)__ldcg(so.acc + tid);
-    so.acc[tid] = 0ull;
-    const double d = (double)v * SKIN_FIX_INV;
+    long long v = 0;  // the SKIN_FIX_REP copies, summed as integers (wraps alike)
+#pragma unroll 4
+    for (int r = 0; r < SKIN_FIX_REP; ++r) v += (long long)__ldcg(so.acc + 64 * r + tid);
+    const bool bad = __shfl_sync(0xffffffffu, v, 31) != 0;  // slot 31: non-finite flag
+#pragma unroll 4
+    for (int r = 0; r < SKIN_FIX_REP; ++r) so.acc[64 * r + tid] = 0ull;
+    const double d = bad ? __longlong_as_double(0x7ff8000000000000ll) : (double)v * SKIN_FIX_INV;
     if (c < so.ndof[b]) so.out[so.off[b] + c] = d;
     if (c >= SKIN_TAU_MAX && c < SKIN_TAU_MAX + SKIN_NSTAT)
       so.out[so.nt + SKIN_NSTAT * b + (c - SKIN_TAU_MAX)] = d;

@@ -1005,6 +1005,8 @@ static void L_collide_fix(const Grid& g, const void* A, int pulled, void* B,
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&resident, k_collide_fix<true, true>, 128, 0);
+    const char* e = getenv("FSG_K4_PER_SM");  // dev A/B: resident fluid-K4 blocks per SM
+    if (e && atoi(e) > 0) resident = std::min(resident, atoi(e));
     if (resident < 1) resident = 1;
   }
   const long long grid = std::min<long long>(ntile, (long long)nsm * resident);
@@ -1088,6 +1090,8 @@ static void L_collide_band(const Grid& g, const void* A, int pulled, void* B, Fi
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&res, k_collide_band<true, true>, 128, 0);
+    const char* e = getenv("FSG_K4B_PER_SM");  // dev A/B: resident banded-K4 blocks per SM
+    if (e && atoi(e) > 0) res = std::min(res, atoi(e));
     res = std::max(res, 1);
   }
   const dim3 b = cell_block(g);

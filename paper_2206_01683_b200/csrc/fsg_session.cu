@@ -512,8 +512,13 @@ int fsg_create(const fsg_config* cfg_in, fsg_session** out) {
   g.periodic = cfg.boundary == FSG_BOUNDARY_PERIODIC ? 1 : 0;
   g.plane = (long long)g.nx * g.ny;
   g.n = g.plane * g.nz;
-  g.stride = g.plane;
-  g.zs = 19 * g.plane;
+  {
+    // dev A/B: elements of padding between direction planes (DRAM channel /
+    // L2 slice spread of the 19 per-warp streams on power-of-two planes)
+    const char* e = getenv("FSG_PLANE_PAD");
+    g.stride = g.plane + (e ? atoll(e) : 0);
+  }
+  g.zs = 19 * g.stride;
   fsg::grid_offsets(g);
 
   // session constants, host fp64 in the reference's order
@@ -1064,8 +1069,8 @@ int fsg_set_skin(fsg_session* s, int n_bodies, const int64_t* off, const fsg_ske
     }
   }
   if (!s->d_skin_fix) {
-    CU(cudaMalloc(&s->d_skin_fix, sizeof(unsigned long long) * 64));
-    CU(cudaMemset(s->d_skin_fix, 0, sizeof(unsigned long long) * 64));
+    CU(cudaMalloc(&s->d_skin_fix, sizeof(unsigned long long) * 64 * fsg::SKIN_FIX_REP));
+    CU(cudaMemset(s->d_skin_fix, 0, sizeof(unsigned long long) * 64 * fsg::SKIN_FIX_REP));
   }
   P.part = s->d_skin_part;
   P.ticket = s->d_skin_ticket;

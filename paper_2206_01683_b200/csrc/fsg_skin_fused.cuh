@@ -245,7 +245,12 @@ __device__ __forceinline__ void skin_tau_warp(const SP& P, const SkinBody& B, in
 
 /// Block tail: sum the warps' running sums in warp order and add the block's
 /// total to the fixed-point accumulators (integer atomics: the accumulated
-/// value does not depend on the order the blocks land in).
+/// value does not depend on the order the blocks land in).  The blocks spread
+/// over SKIN_FIX_REP copies of the accumulators (summed, as integers, by the
+/// banded K4's conversion) so ~700 blocks do not queue on the same 50 words.
+/// A non-finite or out-of-range (|v| >= 2^19) block sum sets the body's flag
+/// word (slot 31), which the conversion turns into NaN (the reference
+/// propagates a blown-up fluid's NaN into tau_ext).
 template <int NB>
 __device__ __forceinline__ void skin_block_red(const double (&acc)[NB], unsigned long long* fixacc) {
   __shared__ double wsum[FX_PER_BLOCK][NB * 32];
@@ -257,12 +262,19 @@ __device__ __forceinline__ void skin_block_red(const double (&acc)[NB], unsigned
     double v = wsum[0][threadIdx.x];
 #pragma unroll
     for (int w = 1; w < FX_PER_BLOCK; ++w) v = v + wsum[w][threadIdx.x];
-    if (v != 0.0) atomicAdd(fixacc + threadIdx.x, (unsigned long long)__double2ll_rn(v * SKIN_FIX_SCALE));
+    unsigned long long* a = fixacc + 64 * (blockIdx.x % SKIN_FIX_REP);
+    if (!(fabs(v) < SKIN_FIX_RANGE)) atomicOr(a + (threadIdx.x | 31), 1ull);
+    else if (v != 0.0) atomicAdd(a + threadIdx.x, (unsigned long long)__double2ll_rn(v * SKIN_FIX_SCALE));
   }
 }
 
-/// Batched envs: one marker's terms straight into its env's fixed-point sums.
-__device__ __forceinline__ void skin_red_marker(double v, int lane, unsigned long long* fixacc) {
-  if (lane < SKIN_TAU_MAX + SKIN_NSTAT && v != 0.0)
-    atomicAdd(fixacc + lane, (unsigned long long)__double2ll_rn(v * SKIN_FIX_SCALE));
+/// Batched envs: one marker's terms straight into its env's fixed-point sums
+/// (copy `rep` of the SKIN_FIX_REP replicas; non-finite / out-of-range terms
+/// set the flag word, slot 31, as skin_block_red).
+__device__ __forceinline__ void skin_red_marker(double v, int lane, unsigned long long* fixacc, int rep) {
+  unsigned long long* a = fixacc + 64 * (rep % SKIN_FIX_REP);
+  if (lane < SKIN_TAU_MAX + SKIN_NSTAT) {
+    if (!(fabs(v) < SKIN_FIX_RANGE)) atomicOr(a + 31, 1ull);
+    else if (v != 0.0) atomicAdd(a + lane, (unsigned long long)__double2ll_rn(v * SKIN_FIX_SCALE));
+  }
 }
