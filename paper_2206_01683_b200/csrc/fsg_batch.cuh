@@ -43,6 +43,11 @@ __device__ __forceinline__ float cell_update_ab(const Grid& g, const float* __re
       const int cx = ex_of(i) > 0 ? cxp : (ex_of(i) < 0 ? cxm : 0);
       s[i] = __ldg(A + (m + (int)g.pull[i] + cx));
     }
+  } else if (!g.periodic) {  // open y/z face rows: constant offsets (FaceFlags)
+    const FaceFlags f = face_flags(g, x, y, zg);
+#pragma unroll
+    for (int i = 0; i < Q; ++i)
+      s[i] = __ldg(A + (m + (int)g.pull[i] + (face_unknown(ex_of(i), ey_of(i), ez_of(i), f) ? f.D : 0)));
   } else {
     gather<true>(g, A, x, y, z, s);
   }
@@ -167,7 +172,7 @@ __global__ void __launch_bounds__(128, FSG_KMB_MINB)
 /// Banded K4 over every env (see k_collide_band); a programmatic dependent
 /// of k_markers_batch.  The status minimum is reported per env.
 template <int PMODE, bool VF>
-__global__ void __launch_bounds__(128, FSG_K4_MINB)
+__global__ void __launch_bounds__(128, FSG_K4BB_MINB)
     k_collide_band_batch(Grid g, const SessionConsts* __restrict__ scp,
                          const EnvPack* __restrict__ packs, BatchHead h, unsigned* work) {
   __shared__ int item;

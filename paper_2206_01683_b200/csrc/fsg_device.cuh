@@ -24,6 +24,9 @@
 #endif
 // batched marker kernel: register budget (min resident blocks) and grid cap
 // per SM (it is persistent over every env's markers)
+#ifndef FSG_K4BB_MINB  // batched banded K4: resident 128-thread blocks per SM
+#define FSG_K4BB_MINB 6
+#endif
 #ifndef FSG_KMB_MINB
 #define FSG_KMB_MINB 6
 #endif
@@ -274,9 +277,40 @@ struct Band {
 
 // Cell-kernel block shape: up to 128 threads along x, the rest along y.
 inline dim3 cell_block_dims(const Grid& g) {
-  int bx = g.nx >= 128 ? 128 : ((g.nx + 31) / 32) * 32;
-  if (bx > 128) bx = 128;
+  // always 128 threads (the kernels' launch bounds and residency assume it):
+  // whole 128-cell rows when they tile nx, else 32 x 4 (e.g. nx = 96: a
+  // 96 x 1 block left a quarter of every SM's warp slots empty)
+  int bx;
+  if (g.nx >= 128 && g.nx % 128 == 0) bx = 128;
+  else if (g.nx == 64) bx = 64;
+  else bx = 32;
   return dim3(bx, 128 / bx, 1);
+}
+
+// Open-boundary pull of a face cell (solver.hpp:59-97 as a pull): an unknown
+// population (standard source c - e_i outside the domain) comes from
+// clamp(c, 1, n-2) - e_i, i.e. the standard source shifted by the cell's
+// clamp displacement D = clamp(c) - c (memory units) -- one offset for every
+// unknown direction of the cell, so face cells stay on the constant-offset
+// fast path (bit-identical to the general gather).
+struct FaceFlags {
+  bool x0, x1, y0, y1, z0, z1;
+  int D;
+};
+__device__ __forceinline__ FaceFlags face_flags(const Grid& g, int x, int y, int zg) {
+  FaceFlags f;
+  f.x0 = x == 0;
+  f.x1 = x == g.nx - 1;
+  f.y0 = y == 0;
+  f.y1 = y == g.ny - 1;
+  f.z0 = zg == 0;
+  f.z1 = zg == g.nzg - 1;
+  f.D = ((int)f.x0 - (int)f.x1) + g.nx * ((int)f.y0 - (int)f.y1) + (int)g.zs * ((int)f.z0 - (int)f.z1);
+  return f;
+}
+__device__ __forceinline__ bool face_unknown(int ex, int ey, int ez, const FaceFlags& f) {
+  return (ex > 0 && f.x0) || (ex < 0 && f.x1) || (ey > 0 && f.y0) || (ey < 0 && f.y1) ||
+         (ez > 0 && f.z0) || (ez < 0 && f.z1);
 }
 
 // Throughput kernels address the 19 pull sources / destinations through

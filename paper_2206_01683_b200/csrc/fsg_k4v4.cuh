@@ -52,8 +52,11 @@ __global__ void __launch_bounds__(128)
   report_min(out, vmin == FLT_MAX ? DBL_MAX : (double)vmin);
 }
 
-/// One cell: pull gather (x faces on the fast path), collide, store.
-template <bool PULLED, bool VF>
+/// One cell: pull gather (x faces on the fast path; FACE: open y/z face rows
+/// too), collide, store.  The banded K4 keeps FACE off: at 64 registers the
+/// extra path spills and the coupled step measured slower (c3 143 vs 141 us),
+/// while the fluid K4 gains (c1 15.9 -> 13.8 us, c2 22.5 -> 20.5 us).
+template <bool PULLED, bool VF, bool FACE = false>
 __device__ __forceinline__ float cell_update(const Grid& g, const DirPtrs& dp,
                                              const float* __restrict__ A, int x, int y, int z,
                                              float Fx, float Fy, float Fz,
@@ -76,6 +79,13 @@ __device__ __forceinline__ float cell_update(const Grid& g, const DirPtrs& dp,
       const int cx = ex_of(i) > 0 ? cxp : (ex_of(i) < 0 ? cxm : 0);
       s[i] = __ldg(dp.a[i] + (m + cx));
     }
+  } else if (FACE && !g.periodic) {
+    // open y/z face rows (warp-uniform): unknown populations shifted by the
+    // cell's clamp displacement, still constant offsets (FaceFlags)
+    const FaceFlags f = face_flags(g, x, y, zg);
+#pragma unroll
+    for (int i = 0; i < Q; ++i)
+      s[i] = __ldg(dp.a[i] + (m + (face_unknown(ex_of(i), ey_of(i), ez_of(i), f) ? f.D : 0)));
   } else {
     gather<true>(g, A, x, y, z, s);  // y/z face rows (warp-uniform)
   }
@@ -146,8 +156,8 @@ __global__ void __launch_bounds__(128, FSG_K4_MINB)
     const int q0 = zk * zc, q1 = min(nq, q0 + zc);
     if (x >= g.nx || y >= g.ny) continue;
     for (int q = q0; q < q1; ++q)
-      vmin = fminf(vmin, cell_update<PULLED, VF>(g, dp, A, x, y, zr.lo + q * zr.step, 0.f, 0.f, 0.f,
-                                                 sc, st, out, nullptr, po));
+      vmin = fminf(vmin, cell_update<PULLED, VF, true>(g, dp, A, x, y, zr.lo + q * zr.step, 0.f, 0.f,
+                                                       0.f, sc, st, out, nullptr, po));
   }
   report_min(out, vmin == FLT_MAX ? DBL_MAX : (double)vmin);
 }
