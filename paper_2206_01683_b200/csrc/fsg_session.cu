@@ -1917,9 +1917,19 @@ int fsg_batch_step_async(fsg_batch* b) {
   bool skb_dirty = !b->dyn;  // robot loop: the pose is made on the device, the topology rarely changes
   const int tx_n = (g0.nx + (int)b->block.x - 1) / (int)b->block.x;
   const int ty_n = (g0.ny + (int)b->block.y - 1) / (int)b->block.y;
-  // phase-A items: 2 planes when that still leaves >= 8 per resident block
+  // phase-A items: the deepest of 4 / 2 / 1 planes (one tile layer, so one
+  // stamp load per item) that still leaves >= 3 items per resident block
+  // (c5, 8 envs of 96x48x48: 4 planes, round 165 -> 157 us; the per-item
+  // fetch, barrier pair and status reduction were a third of phase A)
+  const long long per_env4 = (long long)tx_n * ty_n * ((g0.nz + 3) / 4);
   const long long per_env2 = (long long)tx_n * ty_n * ((g0.nz + 1) / 2);
-  const int zc = (g0.plane < (1 << 17) && per_env2 * b->E >= 8ll * 148 * 6) ? 2 : 1;
+  static const int zc_env = [] {  // dev A/B: phase-A item depth of the batch
+    const char* e = getenv("FSG_BATCH_ZC");
+    return e ? atoi(e) : 0;
+  }();
+  const int zc = zc_env > 0 ? zc_env
+                            : (per_env4 * b->E >= 3ll * 148 * 6 ? 4
+                                                                 : (per_env2 * b->E >= 3ll * 148 * 6 ? 2 : 1));
   h.zc = zc;
   for (int e = 0; e < b->E; ++e) {
     fsg_session* s = b->envs[e];
