@@ -24,7 +24,7 @@
 namespace fsg {
 namespace {
 
-constexpr int DRAG_ACC = 32;  // per env: dofs 0..13, stats 14..20
+constexpr int DRAG_ACC = 32;  // per env: dofs 0..17, stats 18..24, non-finite flag 25
 
 struct DragDev {
   int E, m;
@@ -159,8 +159,10 @@ __global__ void __launch_bounds__(128) k_drag(DragDev D) {
   drag_contrib(D, B, i, f, vel, acc);
   unsigned long long* dst = D.acc + (size_t)e * DRAG_ACC;
 #pragma unroll
-  for (int q = 0; q < SKIN_ACC_N; ++q)
-    if (acc[q] != 0.0) atomicAdd(dst + q, (unsigned long long)__double2ll_rn(acc[q] * SKIN_FIX_SCALE));
+  for (int q = 0; q < SKIN_ACC_N; ++q) {
+    if (!(fabs(acc[q]) < SKIN_FIX_RANGE)) atomicOr(dst + SKIN_ACC_N, 1ull);  // non-finite flag
+    else if (acc[q] != 0.0) atomicAdd(dst + q, (unsigned long long)__double2ll_rn(acc[q] * SKIN_FIX_SCALE));
+  }
 }
 
 /// Converts (and re-zeroes) every env's sums: tau at tau_off[e], then 7 stats
@@ -169,7 +171,11 @@ __global__ void k_drag_finish(DragDev D, const int* tau_off, const int* ndof, in
   for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < D.E * DRAG_ACC; t += gridDim.x * blockDim.x) {
     const int e = t / DRAG_ACC, q = t % DRAG_ACC;
     if (q >= SKIN_ACC_N) continue;
-    const double v = (double)(long long)D.acc[t] * SKIN_FIX_INV;
+    // a non-finite or out-of-range term anywhere in the env (flag word after
+    // its sums) makes every sum NaN, as the reference's would be
+    const bool bad = D.acc[(size_t)e * DRAG_ACC + SKIN_ACC_N] != 0ull;
+    const double v = bad ? __longlong_as_double(0x7ff8000000000000ll)
+                         : (double)(long long)D.acc[t] * SKIN_FIX_INV;
     D.acc[t] = 0ull;
     if (q < ndof[e]) out[tau_off[e] + q] = v;
     if (q >= SKIN_TAU_MAX) out[nt + SKIN_NSTAT * e + (q - SKIN_TAU_MAX)] = v;
@@ -437,6 +443,9 @@ int fsg_drag_step(fsg_drag* d, double* tau_ext, double* stats) {
     if (d->m > 0) fsg::k_drag<<<(d->m + 127) / 128, 128, 0, d->stream>>>(d->D);
     fsg::k_drag_finish<<<(d->E * fsg::DRAG_ACC + 255) / 256, 256, 0, d->stream>>>(
         d->D, d->d_tau_off, d->d_ndof, d->nt, d->h_out);
+    // every env's non-finite flag word back to zero after the conversion read it
+    DCU(cudaMemset2DAsync(d->d_acc + fsg::SKIN_ACC_N, sizeof(unsigned long long) * fsg::DRAG_ACC, 0,
+                          sizeof(unsigned long long), d->E, d->stream));
   }
   DCU(cudaGetLastError());
   DCU(cudaStreamSynchronize(d->stream));

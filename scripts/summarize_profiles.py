@@ -50,16 +50,18 @@ def main(tag):
             "note": "Launch times are cold-cache and serialised by ncu: live, the marker kernel "
                     "and the banded K4 overlap (K4 is its programmatic dependent).  c2's 80 MB "
                     "state fits the 126 MB L2; c3 (640 MB) and c4 (20 GB) show full traffic."}
-    lst = os.path.join(OUT, f"{tag}_c2_launches.csv")
-    if os.path.exists(lst):
+    for w in ("c3", "c2"):  # c3: the headline workload (bench.py's default)
+        lst = os.path.join(OUT, f"{tag}_{w}_launches.csv")
+        if not os.path.exists(lst):
+            continue
         rows = [r for r in csv.reader(open(lst)) if len(r) > 10]
         h = rows[0]
         agg = defaultdict(list)
         for r in rows[1:]:
             name = r[h.index("Kernel Name")].split("(")[0] + " grid" + r[h.index("Grid Size")]
             agg[name].append(float(r[h.index("Metric Value")].replace(",", "")) / 1e3)
-        summ["c2_launch_list"] = {k: {"n": len(v), "mean_us": round(sum(v) / len(v), 2)}
-                                  for k, v in agg.items()}
+        summ[f"{w}_launch_list"] = {k: {"n": len(v), "mean_us": round(sum(v) / len(v), 2)}
+                                    for k, v in agg.items()}
     traffic = {}
     for w in ("c2", "c3", "c4", "c5"):
         rep = os.path.join(OUT, f"{tag}_{w}_full.ncu-rep")
