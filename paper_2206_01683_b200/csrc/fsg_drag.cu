@@ -98,7 +98,9 @@ __device__ __forceinline__ bool drag_force(const DragDev& D, const SkinBody& B, 
   const double s = ((-D.k) * vn) * D.area[i];
 #pragma unroll
   for (int c = 0; c < 3; ++c) f[c] = s * nn[c];
-  return fabs(f[0]) > 1e-12 || fabs(f[1]) > 1e-12 || fabs(f[2]) > 1e-12;  // !f.isZero()
+  // !f.isZero(): Eigen's isZero is |f_k| <= 1e-12 for every k, so a NaN force
+  // is NOT zero and is accumulated (the reference propagates it)
+  return !(fabs(f[0]) <= 1e-12 && fabs(f[1]) <= 1e-12 && fabs(f[2]) <= 1e-12);
 }
 
 /// accumulate_skinned_force(..., f, tau) and the stats into acc (reference order).

@@ -911,17 +911,24 @@ static int L_markers_fix(const Grid& g, const void* A, int pulled, Markers mk,
                          StepScratch* out, unsigned* km_done, int pdl, const SkinParams* skin,
                          unsigned long long* skin_acc, cudaStream_t s) {
   if (mk.m == 0) return 0;
-  // marker blocks per SM (FSG_KM_PER_SM, default below; 0 = one marker per
-  // warp, a single wave of up to m/4 blocks)
-  static int cap = -1;
-  if (cap < 0) {
-    int dev = 0, nsm = 0;
+  // marker blocks per SM (FSG_KM_PER_SM overrides; 0 = one marker per warp,
+  // a single wave of up to m/4 blocks).  Default: a persistent grid of
+  // FSG_KM_PER_SM_DEFAULT blocks per SM when the state exceeds L2 (K4's phase
+  // A is long enough to hide the longer marker chain and keeps more of every
+  // SM: c3 141.4 -> 139.8 us), one wave otherwise (the marker chain is the
+  // step's critical path: c1 40.5 vs 48.0 us at 3 per SM)
+  static int nsm = 0, l2 = 0, env_cap = -2;
+  if (!nsm) {
+    int dev = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, dev);
     const char* e = getenv("FSG_KM_PER_SM");
-    const double per = e ? atof(e) : FSG_KM_PER_SM_DEFAULT;
-    cap = per > 0 ? std::max(1, (int)(per * nsm)) : 0;
+    env_cap = e ? (atof(e) > 0 ? std::max(1, (int)(atof(e) * nsm)) : 0) : -1;
   }
+  const bool big = (double)g.n * 152.0 > (double)l2;
+  const int cap = env_cap >= 0 ? env_cap
+                               : (big ? std::max(1, (int)(FSG_KM_PER_SM_DEFAULT * nsm)) : 0);
   unsigned nb = (unsigned)((mk.m + FX_PER_BLOCK - 1) / FX_PER_BLOCK);
   if (cap > 0) nb = std::min(nb, (unsigned)cap);
   cudaLaunchConfig_t cfg = {};

@@ -615,11 +615,17 @@ int fsg_create(const fsg_config* cfg_in, fsg_session** out) {
       CUF(cudaMalloc(&fb.ready, sizeof(unsigned)));
       CUF(cudaMemsetAsync(fb.ready, 0, sizeof(unsigned), s->stream));
     }
-    // stamped-tile list (FSG_TILE_LIST=1): the band phase takes the listed
-    // tiles dynamically instead of scanning every tile's flag (measured:
-    // c3 -1 %, c2 +7 %: off by default)
+    // stamped-tile list: the band phase takes the listed tiles dynamically
+    // instead of scanning every tile's flag, so blocks leaving phase A early
+    // take the band while the late ones finish.  On by default when the state
+    // exceeds L2 (the phase-A tail is then several us wide: c3 141.4 ->
+    // 137.6 us with 3 marker blocks per SM); off for L2-resident grids (c2
+    // 43.1 -> 44.8 us).  FSG_TILE_LIST=0/1 overrides.
     const char* tl = getenv("FSG_TILE_LIST");
-    if (tl && tl[0] == '1') {
+    int l2 = 0;
+    cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, cfg.device);
+    const bool big = (double)g.n * 152.0 > (double)l2;
+    if (tl ? tl[0] == '1' : big) {
       const size_t tcap = std::min<size_t>(ntile, 8 * (size_t)std::max(1, cfg.max_markers));
       CUF(cudaMalloc(&fb.tlist, sizeof(int) * tcap));
     }
