@@ -17,7 +17,10 @@
 // 141.7 us per coupled step at 6; the pure-fluid K4 stays at 6 (512^3: 3.74
 // vs 4.28 ms at 8)
 #ifndef FSG_K4B_MINB
-#define FSG_K4B_MINB 8
+#define FSG_K4B_MINB 8  // 64 registers (L2-resident grids)
+#endif
+#ifndef FSG_K4B_MINB_PAIR
+#define FSG_K4B_MINB_PAIR 6  // 80 registers: room for the paired phase-A loads
 #endif
 #ifndef FSG_KM_PER_SM_DEFAULT
 #define FSG_KM_PER_SM_DEFAULT 3.0  // persistent marker grid: c3 141.4 -> 139.8 us vs one wave

@@ -116,6 +116,39 @@ __device__ __forceinline__ float cell_update(const Grid& g, const DirPtrs& dp,
   return v;
 }
 
+/// Two cells of one column, planes z and z + 1, both with y and z interior
+/// (pulled state, no IB force): all 38 pull loads are issued before either
+/// cell collides, so a warp keeps twice the bytes in flight (c3 coupled step
+/// 138.2 -> 134.9 us at 80 registers / 6 blocks per SM; at 64 registers the
+/// pair spills and is slower).
+/// Same per-cell arithmetic as cell_update (bit-identical).
+template <bool VF>
+__device__ __forceinline__ float cell_update_pair(const Grid& g, const DirPtrs& dp, int x, int y, int z,
+                                                  const SessionConsts& sc, const StepConsts& st,
+                                                  StepScratch* out, float* fcap) {
+  const unsigned m0 = (unsigned)mem_index(g, x, y, z);
+  const unsigned m1 = m0 + (unsigned)g.zs;
+  const int cxp = x == 0 ? (g.periodic ? g.nx : 1) : 0;
+  const int cxm = x == g.nx - 1 ? (g.periodic ? -g.nx : -1) : 0;
+  float s0[Q], s1[Q];
+#pragma unroll
+  for (int i = 0; i < Q; ++i) {
+    const int cx = ex_of(i) > 0 ? cxp : (ex_of(i) < 0 ? cxm : 0);
+    s0[i] = __ldg(dp.a[i] + (m0 + cx));
+    s1[i] = __ldg(dp.a[i] + (m1 + cx));
+  }
+  Band none{nullptr, 0};
+  const long long c0 = (long long)x + (long long)g.nx * ((long long)y + (long long)g.ny * z);
+  const float v0 = collide_cell32<3, VF>(s0, x, y, z, g, 0.f, 0.f, 0.f, false, 0, none, sc, st, out, fcap, c0);
+#pragma unroll
+  for (int i = 0; i < Q; ++i) dp.b[i][m0] = s0[i];
+  const float v1 = collide_cell32<3, VF>(s1, x, y, z + 1, g, 0.f, 0.f, 0.f, false, 0, none, sc, st, out, fcap,
+                                        c0 + g.plane);
+#pragma unroll
+  for (int i = 0; i < Q; ++i) dp.b[i][m1] = s1[i];
+  return fminf(v0, v1);
+}
+
 /// Block 0 zeroes the next step's scratch (status + work counters).  Nothing
 /// is published from the kernel: the host copies the status out of the
 /// device scratch when it asks for it, after a stream sync, so the kernel
@@ -155,6 +188,16 @@ __global__ void __launch_bounds__(128, FSG_K4_MINB)
     const int y = (col / tx_n) * blockDim.y + threadIdx.y;
     const int q0 = zk * zc, q1 = min(nq, q0 + zc);
     if (x >= g.nx || y >= g.ny) continue;
+#ifdef FSG_K4F_PAIR  // dev A/B: 512^3 3.77 -> 3.70 ms at 2-plane items, but c3 104 -> 111 us, and
+                     // a runtime switch alone (path compiled in) slowed every grid 2-10 %
+    if (PULLED && q1 - q0 == 2 && zr.step == 1 && !po.lo && !po.hi && y > 0 && y < g.ny - 1) {
+      const int z = zr.lo + q0;
+      if (g.z0 + z > 0 && g.z0 + z + 1 < g.nzg - 1) {
+        vmin = fminf(vmin, cell_update_pair<VF>(g, dp, x, y, z, sc, st, out, nullptr));
+        continue;
+      }
+    }
+#endif
     for (int q = q0; q < q1; ++q)
       vmin = fminf(vmin, cell_update<PULLED, VF, true>(g, dp, A, x, y, zr.lo + q * zr.step, 0.f, 0.f,
                                                        0.f, sc, st, out, nullptr, po));
@@ -178,8 +221,11 @@ __global__ void __launch_bounds__(128, FSG_K4_MINB)
 
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 
-template <bool PULLED, bool VF>
-__global__ void __launch_bounds__(128, FSG_K4B_MINB)
+// PAIR (grids larger than L2): 80 registers / 6 blocks per SM and paired
+// phase-A loads; else 64 registers / 8 blocks, one cell at a time (the pair
+// variant measured slower on the L2-resident c2: 45.7 vs 42.9 us)
+template <bool PULLED, bool VF, bool PAIR>
+__global__ void __launch_bounds__(128, PAIR ? FSG_K4B_MINB_PAIR : FSG_K4B_MINB)
     k_collide_band(Grid g, DirPtrs dp, const float* __restrict__ A, FixBand fb,
                    const SessionConsts* __restrict__ scp, const StepConsts st,
                    StepScratch* __restrict__ out, StepScratch* __restrict__ next, int zc,
@@ -243,6 +289,12 @@ __global__ void __launch_bounds__(128, FSG_K4B_MINB)
     // the item's planes (1 or 2, zs1 a multiple of 4) share a tile layer:
     // one stamp load per item (stamped: the band phase's)
     if (__ldcg(fb.tflag + (x >> 2) + fb.tnx * ((y >> 2) + fb.tny * (z0 >> 2))) == fb.stamp) continue;
+#ifndef FSG_K4_NO_PAIR
+    if (PAIR && PULLED && z1 - z0 == 2 && y > 0 && y < g.ny - 1 && g.z0 + z0 > 0 && g.z0 + z0 + 1 < g.nzg - 1) {
+      vmin = fminf(vmin, cell_update_pair<VF>(g, dp, x, y, z0, sc, st, out, fb.fcap));
+      continue;
+    }
+#endif
     for (int z = z0; z < z1; ++z)
       vmin = fminf(vmin, cell_update<PULLED, VF>(g, dp, A, x, y, z, 0.f, 0.f, 0.f, sc, st, out,
                                                  fb.fcap));

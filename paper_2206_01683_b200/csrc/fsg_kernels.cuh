@@ -1026,6 +1026,11 @@ static void L_collide_fix(const Grid& g, const void* A, int pulled, void* B,
   const long long nzc_want = (8 * grid + ncol - 1) / ncol;
   int zc = (int)std::max<long long>(1, nq / std::max<long long>(1, nzc_want));
   zc = std::min(zc, g.plane >= (1 << 17) ? 1 : 2);
+  static const int zc_env = [] {  // dev A/B: fluid-K4 item depth
+    const char* e = getenv("FSG_K4F_ZC");
+    return e ? atoi(e) : 0;
+  }();
+  if (zc_env > 0) zc = zc_env;
 #define FSG_LF(P, V) \
   k_collide_fix<P, V><<<gr, b, 0, s>>>(g, dp, (const float*)A, sc, st, scr, scr_next, zc, zr, po)
   if (pulled) {
@@ -1091,16 +1096,25 @@ static void L_collide_band(const Grid& g, const void* A, int pulled, void* B, Fi
     dp.a[i] = (const float*)A + (pulled ? g.pull[i] : g.own[i]);
     dp.b[i] = (float*)B + g.own[i];
   }
-  static int nsm = 0, res = 0;
+  static int nsm = 0, res1 = 0, res2 = 0, l2 = 0;
   if (!nsm) {
     int dev = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&res, k_collide_band<true, true>, 128, 0);
+    cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&res1, k_collide_band<true, true, false>, 128, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&res2, k_collide_band<true, true, true>, 128, 0);
     const char* e = getenv("FSG_K4B_PER_SM");  // dev A/B: resident banded-K4 blocks per SM
-    if (e && atoi(e) > 0) res = std::min(res, atoi(e));
-    res = std::max(res, 1);
+    if (e && atoi(e) > 0) res1 = std::min(res1, atoi(e)), res2 = std::min(res2, atoi(e));
+    res1 = std::max(res1, 1);
+    res2 = std::max(res2, 1);
   }
+  static const int pair_env = [] {  // dev A/B: FSG_K4_PAIR=0/1 forces the variant
+    const char* e = getenv("FSG_K4_PAIR");
+    return e ? atoi(e) : -1;
+  }();
+  const bool pair = pair_env >= 0 ? pair_env > 0 : (double)g.n * 152.0 > (double)l2;
+  const int res = pair ? res2 : res1;
   const dim3 b = cell_block(g);
   // phase-A item: one block row x zc planes inside one tile layer (zc | 4);
   // 2 planes when that still leaves >= 8 items per block, else 1
@@ -1139,15 +1153,25 @@ static void L_collide_band(const Grid& g, const void* A, int pulled, void* B, Fi
   attr[0].val.programmaticStreamSerializationAllowed = pdl ? 1 : 0;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-#define FSG_PB(P, V)                                                                     \
-  cudaLaunchKernelEx(&cfg, k_collide_band<P, V>, g, dp, (const float*)A, fb, sc, st, scr, \
+#define FSG_PB(P, V, PR)                                                                     \
+  cudaLaunchKernelEx(&cfg, k_collide_band<P, V, PR>, g, dp, (const float*)A, fb, sc, st, scr, \
                      scr_next, zc, zs1, so)
-  if (pulled) {
-    if (frame_on) FSG_PB(true, true);
-    else FSG_PB(true, false);
+  if (pair) {
+    if (pulled) {
+      if (frame_on) FSG_PB(true, true, true);
+      else FSG_PB(true, false, true);
+    } else {
+      if (frame_on) FSG_PB(false, true, true);
+      else FSG_PB(false, false, true);
+    }
   } else {
-    if (frame_on) FSG_PB(false, true);
-    else FSG_PB(false, false);
+    if (pulled) {
+      if (frame_on) FSG_PB(true, true, false);
+      else FSG_PB(true, false, false);
+    } else {
+      if (frame_on) FSG_PB(false, true, false);
+      else FSG_PB(false, false, false);
+    }
   }
 #undef FSG_PB
 }
