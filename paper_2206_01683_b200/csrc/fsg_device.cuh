@@ -63,11 +63,21 @@ __device__ __forceinline__ unsigned long long tl_now() {
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
   return t;
 }
+// per marker warp (first marker of the warp): phase timestamps, 16 slots
+__device__ unsigned long long g_mkt[4096 * 16];
+#define FSG_MKT(first, slot)                                                               \
+  do {                                                                                     \
+    if ((first) && (threadIdx.x & 31) == 0) {                                              \
+      const unsigned w_ = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);             \
+      if (w_ < 4096) fsg::g_mkt[w_ * 16 + (slot)] = fsg::tl_now();                         \
+    }                                                                                      \
+  } while (0)
 #define FSG_TL(stamp, slot) \
   ((slot) & 1 ? atomicMax(&fsg::g_tl[((stamp) & 63) * fsg::TL_SLOTS + (slot)], fsg::tl_now()) \
               : atomicMin(&fsg::g_tl[((stamp) & 63) * fsg::TL_SLOTS + (slot)], fsg::tl_now()))
 #else
 #define FSG_TL(stamp, slot) ((void)0)
+#define FSG_MKT(first, slot) ((void)0)
 #endif
 
 // ----------------------------------------------------------------- D3Q19 --

@@ -129,6 +129,9 @@ __device__ __forceinline__ void mk_finish(const Grid& g, const float* __restrict
                                           StepScratch* out, const double* vel_in = nullptr,
                                           const double* nrm_in = nullptr, double* fw_out = nullptr) {
   const unsigned full = fx_mask();
+  const bool mkt_first = t == (int)(blockIdx.x * FX_PER_BLOCK + threadIdx.x / FX_LANES);
+  (void)mkt_first;
+  FSG_MKT(mkt_first, 5);
   if (!S.ok) {
     if (lane == 0) {
       rec_out[t].valid = 0;
@@ -149,6 +152,7 @@ __device__ __forceinline__ void mk_finish(const Grid& g, const float* __restrict
     phs[a][q] = q < ca ? ib_phi(sc.kernel, (la + q) - xa) : 0.0;
   }
   __syncwarp(full);
+  FSG_MKT(mkt_first, 6);
   const int ncell = S.cnt[0] * S.cnt[1] * S.cnt[2];
   const float r0 = 1.0f / (float)S.cnt[0], r01 = 1.0f / (float)(S.cnt[0] * S.cnt[1]);
   double a0 = 0.0, a1 = 0.0, a2 = 0.0;
@@ -188,12 +192,14 @@ __device__ __forceinline__ void mk_finish(const Grid& g, const float* __restrict
     }
   }
   }
+  FSG_MKT(mkt_first, 7);
 #pragma unroll
   for (int o = FX_LANES / 2; o > 0; o >>= 1) {  // fixed butterfly: every lane gets the total
     a0 += __shfl_xor_sync(full, a0, o);
     a1 += __shfl_xor_sync(full, a1, o);
     a2 += __shfl_xor_sync(full, a2, o);
   }
+  FSG_MKT(mkt_first, 8);
   // body velocity, direct forcing, world force (identical on every lane);
   // the rest of the marker state is loaded only now (register pressure)
   const double uf[3] = {a0 * sc.v2p, a1 * sc.v2p, a2 * sc.v2p};
@@ -255,6 +261,7 @@ __device__ __forceinline__ void mk_finish(const Grid& g, const float* __restrict
     r._pad = 0;
     rec_out[t] = r;
   }
+  FSG_MKT(mkt_first, 9);
   // spread: this lane's own cells, fixed-point integer atomics
   for (int c = lane; c < ncell; c += FX_LANES) {
     const int ko = (int)(((float)c + 0.5f) * r01);
@@ -338,33 +345,16 @@ __global__ void __launch_bounds__(128, FSG_KM_MINB)
                    double* fworld_h, int* valid_h, FixBand fb, StepScratch* out,
                    const __grid_constant__ SkinParamsN<NB> P, unsigned long long* fixacc) {
   __shared__ double phs[FX_PER_BLOCK][3][5];
-  // the bodies' topology and this step's pose, staged once per block: the
-  // chain indexes them by lane-dependent bone / joint, which in the kernel
-  // parameter space (constant bank) serializes per distinct address
+  // the bodies' topology and this step's pose, staged once per block after
+  // the trigger: the heavy phase indexes them by lane-dependent bone / joint,
+  // which in the kernel parameter space (constant bank) serializes per
+  // distinct address.  The stamp phase reads its (<= 4 distinct) bone
+  // transforms straight from the parameters, so the staging (~3-4 us per
+  // block) is off the path to K4's launch.
   __shared__ __align__(16) SkinBody sbody[NB];
-  {
-    static_assert(sizeof(SkinBody) % 8 == 0, "SkinBody is copied as doubles");
-    constexpr int NW = (int)(sizeof(SkinBody) / 8) * NB;
-    const double* src = reinterpret_cast<const double*>(&P.body[0]);
-    double* dst = reinterpret_cast<double*>(&sbody[0]);
-#if FSG_SKIN_STAGE == 1
-    // warp-uniform parameter loads (one constant-bank access each, broadcast);
-    // lane j keeps the j-th of every 32 and stores it
-    const int ln = threadIdx.x & 31;
-    for (int base = (threadIdx.x >> 5) * 32; base < NW; base += 128) {
-      double mine = 0.0;
-#pragma unroll
-      for (int j = 0; j < 32; ++j) {
-        const double v = base + j < NW ? src[base + j] : 0.0;
-        if (ln == j) mine = v;
-      }
-      if (base + ln < NW) dst[base + ln] = mine;
-    }
-#else
-    for (int i = threadIdx.x; i < NW; i += blockDim.x) dst[i] = src[i];
-#endif
-  }
+  FSG_MKT(true, 0);
   __syncthreads();
+  FSG_MKT(true, 1);
   const int lane = threadIdx.x & (FX_LANES - 1);
   const int slot = threadIdx.x / FX_LANES;
   const int stride = gridDim.x * FX_PER_BLOCK;
@@ -376,10 +366,9 @@ __global__ void __launch_bounds__(128, FSG_KM_MINB)
   if (lane == 0) s_t[slot] = -1;
   if (threadIdx.x == 0) FSG_TL(fb.stamp, 0);
   for (int t = blockIdx.x * FX_PER_BLOCK + slot; t < mk.m; t += stride) {
-    const SkinBody& B = sbody[skin_body_of(P, t)];
     const SkinSlot sl = skin_slot(P, t, lane);
     double xw[3];
-    skin_point_warp(P, B.pose, t, sl, xw);
+    skin_point_warp(P, P.body[skin_body_of(P, t)].pose, t, sl, xw);
     if (lane == 0) {
       double* pts = const_cast<double*>(mk.pts);
       pts[3 * t] = xw[0];
@@ -395,16 +384,24 @@ __global__ void __launch_bounds__(128, FSG_KM_MINB)
       s_t[slot] = t;
     }
   }
+  FSG_MKT(true, 2);
   mk_publish_stamps(fb, out);
+  FSG_MKT(true, 3);
+  skin_stage_bodies(P, sbody);
   double acc[NB];
 #pragma unroll
   for (int b = 0; b < NB; ++b) acc[b] = 0.0;
-  for (int t = blockIdx.x * FX_PER_BLOCK + slot; t < mk.m; t += stride) {
+  // the heavy loop runs the group's markers last-stamped first, so the first
+  // one reuses the stencil cached by the stamp phase
+  const int t_first = blockIdx.x * FX_PER_BLOCK + slot;
+  const int t_last = t_first < mk.m ? t_first + stride * ((mk.m - 1 - t_first) / stride) : -1;
+  for (int t = t_last; t >= t_first; t -= stride) {
     const int bi = skin_body_of(P, t);
     const SkinBody& B = sbody[bi];
     const SkinSlot sl = skin_slot(P, t, lane);
     double vel[3], nrm[3], fw[3];
     skin_vel_nrm_warp(P, B.pose, t, sl, vel, nrm);
+    FSG_MKT(t == t_last, 4);
     MkStencil S;
     if (s_t[slot] == t) {
       S = s_st[slot];  // lane 0's copy from the stamp phase (the block barrier since orders it)
@@ -428,6 +425,7 @@ __global__ void __launch_bounds__(128, FSG_KM_MINB)
     mk_finish<PULLED>(g, A, mk, t, lane, sc, st, S, phs[slot], rec_out, fworld, fworld_h, valid_h, fb,
                       out, vel, nrm, fw);
     __syncwarp(fx_mask());
+    FSG_MKT(t == t_last, 10);
 #ifndef FSG_SKIN_NO_TAU
     if (S.ok) {
 #pragma unroll
@@ -435,10 +433,13 @@ __global__ void __launch_bounds__(128, FSG_KM_MINB)
         if (b == bi) skin_tau_warp(P, B, t, lane, fw, vel, acc[b]);
     }
 #endif
+    FSG_MKT(t == t_last, 11);
   }
+  FSG_MKT(true, 12);
   if (lane == 0) FSG_TL(fb.stamp, 1);
 #ifndef FSG_SKIN_NO_TAIL
   skin_block_red(acc, fixacc);
 #endif
+  FSG_MKT(true, 13);
 }
 

@@ -149,6 +149,35 @@ __device__ __forceinline__ float cell_update_pair(const Grid& g, const DirPtrs& 
   return fminf(v0, v1);
 }
 
+/// NP cells of one column (planes z .. z + NP - 1, all y/z-interior), every
+/// pull load issued before any cell collides (generalises cell_update_pair).
+template <bool VF, int NP>
+__device__ __forceinline__ float cell_update_multi(const Grid& g, const DirPtrs& dp, int x, int y, int z,
+                                                   const SessionConsts& sc, const StepConsts& st,
+                                                   StepScratch* out, float* fcap) {
+  const unsigned m0 = (unsigned)mem_index(g, x, y, z);
+  const int cxp = x == 0 ? (g.periodic ? g.nx : 1) : 0;
+  const int cxm = x == g.nx - 1 ? (g.periodic ? -g.nx : -1) : 0;
+  float s[NP][Q];
+#pragma unroll
+  for (int i = 0; i < Q; ++i) {
+    const int cx = ex_of(i) > 0 ? cxp : (ex_of(i) < 0 ? cxm : 0);
+#pragma unroll
+    for (int k = 0; k < NP; ++k) s[k][i] = __ldg(dp.a[i] + (m0 + (unsigned)(k * g.zs) + cx));
+  }
+  Band none{nullptr, 0};
+  const long long c0 = (long long)x + (long long)g.nx * ((long long)y + (long long)g.ny * z);
+  float v = FLT_MAX;
+#pragma unroll
+  for (int k = 0; k < NP; ++k) {
+    v = fminf(v, collide_cell32<3, VF>(s[k], x, y, z + k, g, 0.f, 0.f, 0.f, false, 0, none, sc, st, out,
+                                       fcap, c0 + k * g.plane));
+#pragma unroll
+    for (int i = 0; i < Q; ++i) dp.b[i][m0 + (unsigned)(k * g.zs)] = s[k][i];
+  }
+  return v;
+}
+
 /// Block 0 zeroes the next step's scratch (status + work counters).  Nothing
 /// is published from the kernel: the host copies the status out of the
 /// device scratch when it asks for it, after a stream sync, so the kernel
@@ -290,8 +319,15 @@ __global__ void __launch_bounds__(128, PAIR ? FSG_K4B_MINB_PAIR : FSG_K4B_MINB)
     // one stamp load per item (stamped: the band phase's)
     if (__ldcg(fb.tflag + (x >> 2) + fb.tnx * ((y >> 2) + fb.tny * (z0 >> 2))) == fb.stamp) continue;
 #ifndef FSG_K4_NO_PAIR
-    if (PAIR && PULLED && z1 - z0 == 2 && y > 0 && y < g.ny - 1 && g.z0 + z0 > 0 && g.z0 + z0 + 1 < g.nzg - 1) {
-      vmin = fminf(vmin, cell_update_pair<VF>(g, dp, x, y, z0, sc, st, out, fb.fcap));
+#ifndef FSG_K4_NP
+#define FSG_K4_NP 2
+#endif
+    if (PAIR && PULLED && z1 - z0 == FSG_K4_NP && y > 0 && y < g.ny - 1 && g.z0 + z0 > 0 &&
+        g.z0 + z1 < g.nzg) {
+      if (FSG_K4_NP == 2)
+        vmin = fminf(vmin, cell_update_pair<VF>(g, dp, x, y, z0, sc, st, out, fb.fcap));
+      else
+        vmin = fminf(vmin, cell_update_multi<VF, FSG_K4_NP>(g, dp, x, y, z0, sc, st, out, fb.fcap));
       continue;
     }
 #endif

@@ -1135,7 +1135,7 @@ static void L_collide_band(const Grid& g, const void* A, int pulled, void* B, Fi
     tail_env = e ? atoi(e) : 3;
   }
   int zs1 = g.nz;
-  if (zc == 2) {
+  if (zc > 1) {
     const long long want = (tail_env * full + ncol - 1) / ncol;  // single planes
     zs1 = (int)std::max<long long>(0, ((g.nz - want) / 4) * 4);
   } else {

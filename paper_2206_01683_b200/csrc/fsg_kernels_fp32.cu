@@ -22,3 +22,10 @@ extern "C" int fsg_debug_blocks(unsigned long long* out) {
   return (int)cudaMemcpyFromSymbol(out, fsg::g_blk, sizeof(unsigned long long) * 8192 * 4);
 }
 #endif
+
+#ifdef FSG_TIMING
+extern "C" int fsg_debug_mkt(unsigned long long* out) {
+  cudaDeviceSynchronize();
+  return (int)cudaMemcpyFromSymbol(out, fsg::g_mkt, sizeof(unsigned long long) * 4096 * 16);
+}
+#endif

@@ -59,6 +59,44 @@ struct SkinView {
   const double* ww;     // [m][SKIN_KW]
 };
 
+/// Stage the bodies (topology + pose) of the launch parameters in shared
+/// memory, compacted to the links in use: the topology part whole, each pose
+/// array only its first n_links rows (the koi uses 6 of the 12 slots).  Ends
+/// with a block barrier.
+template <int NB>
+__device__ __forceinline__ void skin_stage_bodies(const SkinParamsN<NB>& P, SkinBody* dst) {
+  static_assert(sizeof(SkinBody) % 8 == 0 && offsetof(SkinBody, pose) % 8 == 0, "copied as doubles");
+  constexpr int TOPO = (int)(offsetof(SkinBody, pose) / 8);
+  constexpr int POSE0 = TOPO;
+  constexpr int L = SKIN_L;
+  // pose arrays (doubles per link): bone_R 9, bone_t 3, R_world 9, p_world 3, v_origin 3, omega 3
+  for (int b = 0; b < NB; ++b) {
+    if (b >= P.nb) break;
+    const double* src = reinterpret_cast<const double*>(&P.body[b]);
+    double* d = reinterpret_cast<double*>(&dst[b]);
+    const int nl = P.body[b].n_links;
+    const int n = TOPO + 30 * nl;
+    for (int k = threadIdx.x; k < n; k += blockDim.x) {
+      int off;
+      if (k < TOPO) {
+        off = k;
+      } else {
+        int r = k - TOPO, base = POSE0;
+        const int w[6] = {9, 3, 9, 3, 3, 3};
+#pragma unroll
+        for (int a = 0; a < 6; ++a) {
+          if (r < w[a] * nl) break;
+          r -= w[a] * nl;
+          base += w[a] * L;
+        }
+        off = base + r;
+      }
+      d[off] = src[off];
+    }
+  }
+  __syncthreads();
+}
+
 /// This lane's bone slot of marker t (lanes >= SKIN_KW: none).
 struct SkinSlot {
   int b;     // bone (-1: none)
