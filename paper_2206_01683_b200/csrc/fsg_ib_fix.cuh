@@ -399,8 +399,8 @@ __global__ void __launch_bounds__(128, FSG_KM_MINB)
     const int bi = skin_body_of(P, t);
     const SkinBody& B = sbody[bi];
     const SkinSlot sl = skin_slot(P, t, lane);
-    double vel[3], nrm[3], fw[3];
-    skin_vel_nrm_warp(P, B.pose, t, sl, vel, nrm);
+    double vel[3], nrm[3], fw[3], xb[3] = {0.0, 0.0, 0.0};
+    skin_vel_nrm_warp(P, B.pose, t, sl, vel, nrm, xb);
     FSG_MKT(t == t_last, 4);
     MkStencil S;
     if (s_t[slot] == t) {
@@ -430,7 +430,7 @@ __global__ void __launch_bounds__(128, FSG_KM_MINB)
     if (S.ok) {
 #pragma unroll
       for (int b = 0; b < NB; ++b)
-        if (b == bi) skin_tau_warp(P, B, t, lane, fw, vel, acc[b]);
+        if (b == bi) skin_tau_pre(B, lane, sl, xb, fw, vel, acc[b]);
     }
 #endif
     FSG_MKT(t == t_last, 11);

@@ -161,15 +161,22 @@ __device__ __forceinline__ void skin_point_warp(const SP& P, const fsg_body_pose
 }
 
 /// skin_point_velocity and the blended normal, normalized() (all lanes).
+/// xb_out (nullable): this slot lane's bone-transformed point (the p of the
+/// tau terms, skin_tau_pre).
 template <class SP>
 __device__ __forceinline__ void skin_vel_nrm_warp(const SP& P, const fsg_body_pose& Q, int t,
-                                                  const SkinSlot& s, double* vel, double* nrm) {
+                                                  const SkinSlot& s, double* vel, double* nrm,
+                                                  double* xb_out = nullptr) {
   double tv[3] = {0.0, 0.0, 0.0}, tn[3] = {0.0, 0.0, 0.0};
   if (s.b >= 0) {
     const double x[3] = {__ldg(P.rest + 3 * t), __ldg(P.rest + 3 * t + 1), __ldg(P.rest + 3 * t + 2)};
     const double n0[3] = {__ldg(P.nrest + 3 * t), __ldg(P.nrest + 3 * t + 1), __ldg(P.nrest + 3 * t + 2)};
     double xb[3], d[3], cr[3], rn[3];
     rn_apply(Q, s.b, x, xb);
+    if (xb_out) {
+#pragma unroll
+      for (int c = 0; c < 3; ++c) xb_out[c] = xb[c];
+    }
 #pragma unroll
     for (int c = 0; c < 3; ++c) d[c] = rn_sub(xb[c], Q.p_world[s.b][c]);
     rn_cross(Q.omega_world[s.b], d, cr);
@@ -190,27 +197,68 @@ __device__ __forceinline__ void skin_vel_nrm_warp(const SP& P, const fsg_body_po
   }
 }
 
+template <class SP>
+__device__ __forceinline__ void skin_tau_warp(const SP& P, const SkinBody& B, int t, int lane,
+                                              const double* fw, const double* vel, double& acc);
+
+/// skin_tau_warp with the slot data the velocity phase already has: lane k
+/// (< SKIN_KW) holds slot k's bone, weight and bone-transformed point; the
+/// lanes of slot k take them by shuffle instead of reloading the marker and
+/// re-applying the bone transform (same values: bit-identical).
+__device__ __forceinline__ void skin_tau_pre(const SkinBody& B, int lane, const SkinSlot& sl,
+                                             const double* xb, const double* fw, const double* vel,
+                                             double& acc);
+
 /// Add marker t's J^T(-f) terms and CouplingStats to the warp's running sums:
 /// lane c (< SKIN_TAU_MAX) holds dof c, lane SKIN_TAU_MAX + k stat k.
+template <bool PRE>
+__device__ __forceinline__ void skin_tau_core(const SkinBody& B, int lane, int b, double w,
+                                              const double* p_in, const double* fw, const double* vel,
+                                              double& acc);
+
 template <class SP>
 __device__ __forceinline__ void skin_tau_warp(const SP& P, const SkinBody& B, int t, int lane,
                                               const double* fw, const double* vel, double& acc) {
-  const fsg_body_pose& Q = B.pose;
-  const int k = lane >> 3, l = lane & 7;  // bone slot, level (0: base wrench, l: l-th joint up)
+  const int k = lane >> 3;
   int b = -1;
   double w = 0.0;
   if (k < SKIN_KW) {
     b = __ldg(P.wb + SKIN_KW * t + k);
     if (b >= 0) w = __ldg(P.ww + SKIN_KW * t + k);
   }
+  double p[3] = {0.0, 0.0, 0.0};
+  if (b >= 0) {
+    const double x[3] = {__ldg(P.rest + 3 * t), __ldg(P.rest + 3 * t + 1), __ldg(P.rest + 3 * t + 2)};
+    rn_apply(B.pose, b, x, p);
+  }
+  skin_tau_core<false>(B, lane, b, w, p, fw, vel, acc);
+}
+
+__device__ __forceinline__ void skin_tau_pre(const SkinBody& B, int lane, const SkinSlot& sl,
+                                             const double* xb, const double* fw, const double* vel,
+                                             double& acc) {
+  const int k = lane >> 3;  // SKIN_KW == 4: every lane's slot is a real lane
+  static_assert(SKIN_KW == 4, "slot k lives on lane k");
+  const int b = __shfl_sync(0xffffffffu, sl.b, k);
+  const double w = __shfl_sync(0xffffffffu, sl.w, k);
+  const double p[3] = {__shfl_sync(0xffffffffu, xb[0], k), __shfl_sync(0xffffffffu, xb[1], k),
+                       __shfl_sync(0xffffffffu, xb[2], k)};
+  skin_tau_core<true>(B, lane, b, w, p, fw, vel, acc);
+}
+
+template <bool PRE>
+__device__ __forceinline__ void skin_tau_core(const SkinBody& B, int lane, int b, double w,
+                                              const double* p_in, const double* fw, const double* vel,
+                                              double& acc) {
+  const fsg_body_pose& Q = B.pose;
+  const int k = lane >> 3, l = lane & 7;  // bone slot, level (0: base wrench, l: l-th joint up)
   double term[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
   double term2 = 0.0;  // level l + 8 (chains deeper than 7 joints)
   const bool deep = B.max_level > 7;  // uniform over the warp
   int comp = -1;  // l > 0: the dof this lane's term goes to
   if (b >= 0) {
-    const double x[3] = {__ldg(P.rest + 3 * t), __ldg(P.rest + 3 * t + 1), __ldg(P.rest + 3 * t + 2)};
-    double p[3], fv[3];
-    rn_apply(Q, b, x, p);
+    const double p[3] = {p_in[0], p_in[1], p_in[2]};
+    double fv[3];
 #pragma unroll
     for (int c = 0; c < 3; ++c) fv[c] = rn_mul(w, -fw[c]);
     if (l == 0) {
