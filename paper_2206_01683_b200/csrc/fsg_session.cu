@@ -2239,6 +2239,7 @@ int fsg_batch_step_dynamic(fsg_batch* b, fsg_dyn* d, const fsg_frame_state* fram
       if (need) {
         rc = recenter_async(s, shift);
         if (rc) return rc;
+        s->stepped = true;  // the step's outputs (tau_ext, marker forces) stay readable
         fsg_follower_set_state(b->fol[e], &s->frame);  // the origin advanced by R shift dx
       }
     }

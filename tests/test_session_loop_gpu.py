@@ -2,7 +2,8 @@
 
 sim::CoupledSession (session.hpp:29-241) is compiled unmodified into
 oracle/_ref (oracle/ref_robot.cpp) and run live on the box's CPU with the
-reference's own koi (build_fish_model(koi_design())), its own surface samples
+reference's own koi and eel (build_fish_model(koi_design() / eel_design());
+the eel's 11 links / 16 dofs exercise the raised caps), its own surface samples
 (sample_surface at the lattice spacing) and a SineGait (gait.hpp:12-40).  The
 product runs the same session through fsg_batch_step_dynamic (EnvBatch.
 step_dynamic): device skinning of the samples, IB coupling + the banded
@@ -51,14 +52,18 @@ def _rel(a, b):
     return float(np.linalg.norm(np.asarray(a) - np.asarray(b)) / max(np.linalg.norm(b), 1e-300))
 
 
-@pytest.mark.parametrize("frame_mode,steps", [("translation_yaw", 300), ("none", 120)])
-def test_coupled_session_loop_vs_reference(frame_mode, steps):
+@pytest.mark.parametrize("design,frame_mode,steps", [("koi", "translation_yaw", 300),
+                                                     ("koi", "none", 120),
+                                                     ("eel", "translation_yaw", 200)])
+def test_coupled_session_loop_vs_reference(design, frame_mode, steps):
     import ref_models as RM
     from paper_2206_01683_b200 import EnvBatch, SessionConfig
     from paper_2206_01683_b200.dynamics import RobotBatch, rest_pose
-    dims, dx, dt, rho, nu = (64, 32, 32), 0.01, 0.004, 1000.0, 0.00089
+    # the eel (0.6 m, 11 links, 16 dofs) in a longer box
+    dims = (64, 32, 32) if design == "koi" else (96, 32, 32)
+    dx, dt, rho, nu = 0.01, 0.004, 1000.0, 0.00089
     fm = {"none": 0, "translation_yaw": 2}[frame_mode]
-    model = RM.RefModel("koi")
+    model = RM.RefModel(design)
     ref = RM.SessionRef(dims, dx, dt, rho, nu, kernel=0, wall=0, frame_mode=fm, frame_tc=0.2,
                         recenter_cells=0.5, gravity=(0.0, 0.0, -9.81), substeps=4,
                         marker_spacing=0.0)
@@ -105,5 +110,7 @@ def test_coupled_session_loop_vs_reference(frame_mode, steps):
     fr = ref.get_f().reshape(19, n) - W[:, None]
     fgd = b.envs[0].get_f().reshape(19, n) - W[:, None]
     assert _rel(fgd, fr) <= 1e-4, _rel(fgd, fr)
+    print(f"{design} {frame_mode} {steps} steps: state rel {_rel(xg, xr):.2e}, tau_ext rel "
+          f"{_rel(tau_g[0], tr):.2e}, f - w rel-L2 {_rel(fgd, fr):.2e}, recentres {n_shift}")
     b.close()
     rb.close()
