@@ -96,7 +96,9 @@ __global__ void __launch_bounds__(128, FSG_KMB_MINB)
   const int slot = threadIdx.x / FX_LANES;
   const int stride = gridDim.x * FX_PER_BLOCK;
   const SessionConsts& sc = *scp;
-  for (int tg = blockIdx.x * FX_PER_BLOCK + slot; tg < h.m_total; tg += stride) {
+  // the stencils of a group's first 4 markers, reused by the heavy loop
+  __shared__ MkStencil s_st[FX_PER_BLOCK][4];
+  for (int tg = blockIdx.x * FX_PER_BLOCK + slot, k = 0; tg < h.m_total; tg += stride, ++k) {
     const EnvPack& P = packs[env_of(mkb, h.E, tg)];
     const FixBand fb{P.F, P.tflag, h.tnx, h.tny, h.tnz, P.stamp};
     const int t = tg - P.mk_begin;
@@ -117,12 +119,13 @@ __global__ void __launch_bounds__(128, FSG_KMB_MINB)
       mk_stencil(P.mk, t, sc, P.st, S);
     }
     mk_stamp(g, fb, S, lane);
+    if (k < 4 && lane == 0) s_st[slot][k] = S;
   }
   __syncthreads();  // all stamps of the block before the K4 trigger (k_markers_fix)
   if (threadIdx.x == 0) __threadfence();
   __syncthreads();
   asm volatile("griddepcontrol.launch_dependents;");
-  for (int tg = blockIdx.x * FX_PER_BLOCK + slot; tg < h.m_total; tg += stride) {
+  for (int tg = blockIdx.x * FX_PER_BLOCK + slot, k = 0; tg < h.m_total; tg += stride, ++k) {
     const EnvPack& P = packs[env_of(mkb, h.E, tg)];
     const FixBand fb{P.F, P.tflag, h.tnx, h.tny, h.tnz, P.stamp};
     const int t = tg - P.mk_begin;
@@ -131,9 +134,8 @@ __global__ void __launch_bounds__(128, FSG_KMB_MINB)
       const SkinView V{P.sk_rest, P.sk_nrest, P.sk_wb, P.sk_ww};
       const SkinBody& B = *P.skb;
       const SkinSlot sl = skin_slot(V, t, lane);
-      double xw[3], vel[3], nrm[3], fw[3];
-      skin_point_warp(V, B.pose, t, sl, xw);
-      skin_vel_nrm_warp(V, B.pose, t, sl, vel, nrm);
+      double vel[3], nrm[3], fw[3], xb[3] = {0.0, 0.0, 0.0};
+      skin_vel_nrm_warp(V, B.pose, t, sl, vel, nrm, xb);
       if (lane == 0) {
         double* v = const_cast<double*>(P.mk.vel);
         double* n = const_cast<double*>(P.mk.nrm);
@@ -143,7 +145,14 @@ __global__ void __launch_bounds__(128, FSG_KMB_MINB)
           n[3 * t + c] = nrm[c];
         }
       }
-      mk_stencil_x(xw, sc, P.st, S);
+      if (k < 4) {
+        S = s_st[slot][k];  // from the stamp phase (the block barrier since orders it)
+      } else {  // the position the stamp phase skinned (same warp)
+        double xw[3];
+#pragma unroll
+        for (int c = 0; c < 3; ++c) xw[c] = __ldcg(P.mk.pts + 3 * t + c);
+        mk_stencil_x(xw, sc, P.st, S);
+      }
       if (P.pulled)
         mk_finish<true>(g, P.A, P.mk, t, lane, sc, P.st, S, phs[slot], P.rec, P.fworld, P.fworld_h,
                         P.valid_h, fb, P.out, vel, nrm, fw);
@@ -153,12 +162,13 @@ __global__ void __launch_bounds__(128, FSG_KMB_MINB)
       __syncwarp(fx_mask());
       if (S.ok) {
         double acc = 0.0;
-        skin_tau_warp(V, B, t, lane, fw, vel, acc);
+        skin_tau_pre(B, lane, sl, xb, fw, vel, acc);
         skin_red_marker(acc, lane, P.sk_acc, t);
       }
       continue;
     }
-    mk_stencil(P.mk, t, sc, P.st, S);
+    if (k < 4) S = s_st[slot][k];
+    else mk_stencil(P.mk, t, sc, P.st, S);
     if (P.pulled)
       mk_finish<true>(g, P.A, P.mk, t, lane, sc, P.st, S, phs[slot], P.rec, P.fworld, P.fworld_h,
                       P.valid_h, fb, P.out);
