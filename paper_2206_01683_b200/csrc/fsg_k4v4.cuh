@@ -8,6 +8,16 @@
 
 // DirPtrs (fsg_device.cuh): per-direction base pointers A + pull[i] / B + own[i]
 
+// load / store flavour of the fast-path populations (dev A/B: FSG_K4_CS=1
+// streaming .cs hints, evict-first in L2)
+#if FSG_K4_CS
+#define K4_LD(p) __ldcs(p)
+#define K4_ST(p, v) __stcs((p), (v))
+#else
+#define K4_LD(p) __ldg(p)
+#define K4_ST(p, v) (*(p) = (v))
+#endif
+
 template <int FMODE, bool VF>
 __global__ void __launch_bounds__(128)
     k_collide_fast(Grid g, DirPtrs dp, const float* __restrict__ A, const float* __restrict__ Fext,
@@ -77,7 +87,7 @@ __device__ __forceinline__ float cell_update(const Grid& g, const DirPtrs& dp,
 #pragma unroll
     for (int i = 0; i < Q; ++i) {
       const int cx = ex_of(i) > 0 ? cxp : (ex_of(i) < 0 ? cxm : 0);
-      s[i] = __ldg(dp.a[i] + (m + cx));
+      s[i] = K4_LD(dp.a[i] + (m + cx));
     }
   } else if (FACE && !g.periodic) {
     // open y/z face rows (warp-uniform): unknown populations shifted by the
@@ -93,7 +103,7 @@ __device__ __forceinline__ float cell_update(const Grid& g, const DirPtrs& dp,
   const float v = collide_cell32<3, VF>(s, x, y, z, g, Fx, Fy, Fz, false, 0, none, sc, st, out, fcap,
                                         (long long)x + (long long)g.nx * ((long long)y + (long long)g.ny * z));
 #pragma unroll
-  for (int i = 0; i < Q; ++i) dp.b[i][m] = s[i];
+  for (int i = 0; i < Q; ++i) K4_ST(dp.b[i] + m, s[i]);
   // peer-connected slab: the crossing populations of the boundary planes go
   // straight into the neighbours' halo planes (lattice.hpp:25-26: ez = -1
   // {6,12,13,16,17}, ez = +1 {5,11,14,15,18})

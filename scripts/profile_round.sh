@@ -18,8 +18,9 @@ ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv \
 $C2 > $out/${tag}_c2_plain.log 2>&1 &&
 ncu --metrics gpu__time_duration.sum --clock-control none -c 800 --csv \
     --log-file $out/${tag}_c2_launches.csv $C2 > $out/${tag}_c2_ncu_list.log 2>&1
-# full sections: the coupled pair at c2
-ncu --set full --clock-control none --import-source on -k regex:"k_collide_band|k_markers_fix|k_markers_skin" \
+# full sections: the coupled pair at c2 (PROFILE_SKIP_C2_FULL=1: skip, keeps
+# gpurun_out under the 64 MiB copy-back limit)
+[ "${PROFILE_SKIP_C2_FULL:-0}" = 1 ] || ncu --set full --clock-control none --import-source on -k regex:"k_collide_band|k_markers_fix|k_markers_skin" \
     -s 20 -c 4 -o $out/${tag}_c2_full $C2 > $out/${tag}_c2_ncu_full.log 2>&1
 # c3: the coupled pair on a grid larger than L2
 ncu --set full --clock-control none --import-source on -k regex:"k_collide_band|k_markers_fix|k_markers_skin" \
