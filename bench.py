@@ -739,13 +739,15 @@ def run_ours(args, scene, rank, local, world):
         e2e_val = scene.n_cells * E * world / float(t.item()) / 1e6
     nb = len(scene.bodies)
     if skinned:
+        from paper_2206_01683_b200.session import POSE_DOUBLES
         ndof = sum(sk.n_dofs for sk in scene.skin()[1])
-        h2d = 1920 * nb + 232   # fsg_body_pose per body (240 doubles) + frame consts
+        h2d = 8 * POSE_DOUBLES * nb + 232  # fsg_body_pose per body + frame consts
         d2h = 8 * (ndof + 7 * nb) + 64  # tau_ext + CouplingStats + step status
     else:
         h2d = 80 * m + 232      # marker state (pts, vel, nrm 3x8 B, area 8 B) + frame consts
         d2h = 28 * m + 64       # marker forces (3x8 B) + validity (4 B) + step status
     s.close()
+    cpp = host_e2e(scene, cfg, frames, poses) if (skinned and world == 1) else None
 
     peak, peak_src = measured_peaks()
     # the coupled step's kernels overlap (the banded K4 is a programmatic
@@ -776,8 +778,15 @@ def run_ours(args, scene, rank, local, world):
                          "ms": round(fluid_ms, 4),
                          "achieved": round(BYTES_PER_CELL * scene.n_cells / (fluid_ms / 1e3) / 1e9, 1),
                          "frac": round(BYTES_PER_CELL * scene.n_cells / (fluid_ms / 1e3) / 1e9 / peak, 4)}},
-        "e2e": {"value": round(e2e_val, 1), "unit": "MLUPS", "h2d_bytes_per_step": h2d,
-                "d2h_bytes_per_step": d2h, "steps": E},
+        # e2e: the C++ host through the C ABI (scripts/host_e2e.cpp) when it
+        # builds here, else the Python host; both are kept
+        "e2e": ({"value": cpp["mlups"], "unit": "MLUPS", "h2d_bytes_per_step": h2d,
+                 "d2h_bytes_per_step": d2h, "steps": cpp["steps"],
+                 "host": "C++ through include/fsg.h (fsg_step_skinned, synchronous)",
+                 "us_per_step": cpp["us_per_step"]} if cpp else
+                {"value": round(e2e_val, 1), "unit": "MLUPS", "h2d_bytes_per_step": h2d,
+                 "d2h_bytes_per_step": d2h, "steps": E, "host": "Python (ctypes)"}),
+        "e2e_python": {"value": round(e2e_val, 1), "unit": "MLUPS", "steps": E},
         # skinned bodies ride in the marker kernel (<= 2 bodies; more use the
         # split skin kernels beside K4): K_m + K4 per step
         "gpu_launches": K * ((2 if len(scene.bodies) <= 2 else 4) if skinned else (2 if m else 1)),
@@ -785,6 +794,49 @@ def run_ours(args, scene, rank, local, world):
         "clocks": clk.summary(),
     }
     return out
+
+
+def host_e2e(scene, cfg, frames, poses, n_steps: int = 100):
+    """End to end from a C++ host through the C ABI (scripts/host_e2e.cpp):
+    per step the frame + per-link poses go up from host memory, the coupled
+    step runs synchronously and tau_ext + CouplingStats come back
+    (fsg_step_skinned) -- the FishGym binding of INTEGRATION.md, no Python on
+    the timed path.  Returns its JSON result, or None when it cannot be built
+    or run here (the Python e2e is reported either way)."""
+    import tempfile
+    import numpy as np
+    from paper_2206_01683_b200.session import POSE_DOUBLES
+    off, sks, rest, nrest, W, areas = scene.skin()
+    n = min(n_steps, len(frames))
+    c = cfg.to_c()
+    tmp = tempfile.mkdtemp(prefix="fsg_host_e2e_")
+    case = os.path.join(tmp, "case.bin")
+    with open(case, "wb") as f:
+        f.write(np.array([c.dims[0], c.dims[1], c.dims[2], c.frame_mode, len(sks), n,
+                          int(off[-1])], dtype=np.int32).tobytes())
+        f.write(np.array([c.dx, c.dt, c.rho, c.nu], dtype=np.float64).tobytes())
+        f.write(np.asarray(off, dtype=np.int64).tobytes())
+        for sk in sks:
+            f.write(bytes(sk.to_c()))
+        for a in (rest, nrest, areas):
+            f.write(np.ascontiguousarray(a, dtype=np.float64).tobytes())
+        f.write(np.concatenate([np.asarray(w, dtype=np.float64).reshape(-1) for w in W]).tobytes())
+        for k in range(n):
+            fr = frames[k]
+            f.write(np.asarray(fr if isinstance(fr, np.ndarray) else fr.packed(), dtype=np.float64).tobytes())
+        for k in range(n):
+            f.write(np.asarray(poses[k], dtype=np.float64).reshape(-1, POSE_DOUBLES).tobytes())
+    exe = os.path.join(tmp, "host_e2e")
+    lib = os.path.join(ROOT, "paper_2206_01683_b200")
+    try:
+        subprocess.run(["g++", "-O2", "-std=c++17", "-I", os.path.join(ROOT, "include"),
+                        os.path.join(ROOT, "scripts", "host_e2e.cpp"), "-L", lib, "-lfsg",
+                        f"-Wl,-rpath,{lib}", "-o", exe], check=True, capture_output=True, timeout=120)
+        r = subprocess.run([exe, case, "5"], check=True, capture_output=True, text=True, timeout=300)
+        return json.loads(r.stdout.strip().splitlines()[-1])
+    except Exception as e:  # noqa: BLE001 -- reported, the Python e2e stands
+        print(f"host_e2e unavailable: {e}", file=sys.stderr)
+        return None
 
 
 def spawn_ranks(args) -> int:

@@ -44,3 +44,12 @@ def test_cpp_robot_wrapper_pendulum_kat(tmp_path):
     r = subprocess.run([exe], capture_output=True, text=True, timeout=300)
     assert r.returncode == 0, r.stdout + r.stderr
     assert "pendulum_period_rel_err" in r.stdout and "joint limits inverted" in r.stdout
+
+
+HOST_E2E = os.path.join(ROOT, "scripts", "host_e2e.cpp")
+
+
+def test_host_e2e_driver_compiles_and_links(tmp_path):
+    """bench.py's C++-host e2e driver (the FishGym binding's per-step exchange
+    through include/fsg.h) builds against the C ABI."""
+    assert os.path.exists(build(tmp_path, HOST_E2E))
