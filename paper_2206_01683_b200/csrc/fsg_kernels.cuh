@@ -1128,15 +1128,18 @@ static void L_collide_band(const Grid& g, const void* A, int pulled, void* B, Fi
   const int zc = zc_env > 0 ? zc_env
                             : ((g.plane < (1 << 17) && ncol * ((g.nz + 1) / 2) >= 8 * full) ? 2 : 1);
   // 2-plane items end at plane zs1 (a multiple of 4); the last planes are
-  // single-plane items, about 3 per block (FSG_K4_TAIL: that count, 0 = none)
-  static int tail_env = -1;
-  if (tail_env < 0) {
+  // single-plane items, about 3 per block (FSG_K4_TAIL: that count, 0 = none).
+  // The paired-load variant takes none: its single-plane items are unpaired
+  // and the dynamic band phase already evens out the tail (c3 132.8 -> 130.0 us)
+  static int tail_env = -2;
+  if (tail_env == -2) {
     const char* e = getenv("FSG_K4_TAIL");
-    tail_env = e ? atoi(e) : 3;
+    tail_env = e ? atoi(e) : -1;
   }
+  const int tail_n = tail_env >= 0 ? tail_env : (pair ? 0 : 3);
   int zs1 = g.nz;
   if (zc > 1) {
-    const long long want = (tail_env * full + ncol - 1) / ncol;  // single planes
+    const long long want = (tail_n * full + ncol - 1) / ncol;  // single planes
     zs1 = (int)std::max<long long>(0, ((g.nz - want) / 4) * 4);
   } else {
     zs1 = 0;
