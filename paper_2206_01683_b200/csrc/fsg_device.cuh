@@ -34,7 +34,7 @@
 #define FSG_KMB_MINB 6
 #endif
 #ifndef FSG_KMB_PER_SM
-#define FSG_KMB_PER_SM 4
+#define FSG_KMB_PER_SM 5
 #endif
 #ifndef FSG_KM_MINB
 #define FSG_KM_MINB 6
