@@ -379,6 +379,54 @@ def cpu_sample_scene(scene):
 
 
 # ------------------------------------------------------ ours: envs (c5) ---
+def robot_leg(batch, scene, E, Ee, kk, local, dev, world, flush_bufs):
+    """The rollout loop with the robots on the device too:
+    one fsg_batch_step_dynamic call per round uploads the actuation, steps
+    fluid + robots, advances every env's FrameFollower (recentring its
+    lattice when the robot drifts) and returns statuses and the post-step
+    robot states -- no prescribed frames, no host marker or robot work."""
+    import numpy as np
+    import torch
+    from paper_2206_01683_b200 import dynamics as D
+    fw_buf, fr_buf, sink = flush_bufs
+    robot = D.koi_robot(scene.bodies[0], scene.articulations()[0])
+    rb = D.RobotBatch(robot, E, device=local)
+    rb.set_rest(*D.rest_pose(robot))
+    nj = robot.n_joints
+    batch.set_follow(0.2, 2.0)
+    batch.center_frames(rb)
+    n_shift = 0
+    dyn_t, dyn_ok, per_call = 0.0, True, []
+    for k in range(-3, Ee):  # 3 untimed warm-up rounds (lazy module load, first-call allocations)
+        fw_buf.fill_(1.0)
+        torch.sum(fr_buf, dim=0, out=sink[0])
+        torch.cuda.synchronize(dev)
+        t_ = (kk + Ee + k) * scene.dt
+        act = np.array([[0.2 * math.sin(2 * math.pi * 2.0 * t_ - 0.8 * j + e) for j in range(nj)]
+                        for e in range(E)])
+        t0 = time.perf_counter()
+        sts_d, fl_d, _ = batch.step_dynamic(rb, act, None, scene.rho, (0.0, 0.0, -9.81), scene.dt, 4)
+        if k < 0:
+            continue
+        n_shift += int((batch.last_shifts() != 0).any(axis=1).sum())
+        per_call.append(time.perf_counter() - t0)
+        dyn_t += per_call[-1]
+        dyn_ok &= all(x.stable() for x in sts_d) and not (fl_d & D.FSG_DYN_NONFINITE).any()
+    rb.close()
+    return {"value": round(E * scene.n_cells * Ee * world / dyn_t / 1e6, 1), "unit": "MLUPS",
+            # up: actuation + the env pack (frame constants, state pointers);
+            # down: status, tau_ext + stats, post-step state, flags, COM
+            "h2d_bytes_per_step": E * (8 * nj + 440),
+            "d2h_bytes_per_step": E * (32 + 200 + 440 + 4 + 24), "steps": Ee,
+            "stable": bool(dyn_ok), "recentres": n_shift,
+            "call_us": {q: round(float(np.percentile(per_call, p)) * 1e6, 1)
+                        for q, p in (("p50", 50), ("p90", 90), ("max", 100))},
+            "what": "fsg_batch_step_dynamic: actuation up; device poses, coupled step, "
+                    "buoyancy + integrate (4 substeps) of every robot, FrameFollower + "
+                    "recentre trigger per env; statuses + robot states down (the "
+                    "reference's full CoupledSession::step)"}
+
+
 def run_envs(args, scene, rank, local, world):
     """c5: E independent envs per GPU (BASELINE: 64 envs on 8 GPUs).  batch
     mode: an EnvBatch steps every env with one marker launch and one
@@ -512,48 +560,7 @@ def run_envs(args, scene, rank, local, world):
         e2e_t = float(t.item())
     e2e_dyn = None
     if skinned and batch and not args.no_robot_leg:
-        # the rollout loop with the robots on the device too:
-        # one call per round uploads the actuation, steps fluid + robots,
-        # advances every env's FrameFollower (and recentres its lattice when
-        # the robot drifts), and returns statuses and the post-step robot
-        # states -- no prescribed frames
-        from paper_2206_01683_b200 import dynamics as D
-        robot = D.koi_robot(scene.bodies[0], scene.articulations()[0])
-        rb = D.RobotBatch(robot, E, device=local)
-        rb.set_rest(*D.rest_pose(robot))
-        nj = robot.n_joints
-        batch.set_follow(0.2, 2.0)
-        batch.center_frames(rb)
-        n_shift = 0
-        dyn_t, dyn_ok, per_call = 0.0, True, []
-        for k in range(-3, Ee):  # 3 untimed warm-up rounds (lazy module load, first-call allocations)
-            fw_buf.fill_(1.0)
-            torch.sum(fr_buf, dim=0, out=sink[0])
-            torch.cuda.synchronize(dev)
-            t_ = (kk + Ee + k) * scene.dt
-            act = np.array([[0.2 * math.sin(2 * math.pi * 2.0 * t_ - 0.8 * j + e) for j in range(nj)]
-                            for e in range(E)])
-            t0 = time.perf_counter()
-            sts_d, fl_d, _ = batch.step_dynamic(rb, act, None, scene.rho, (0.0, 0.0, -9.81), scene.dt, 4)
-            if k < 0:
-                continue
-            n_shift += int((batch.last_shifts() != 0).any(axis=1).sum())
-            per_call.append(time.perf_counter() - t0)
-            dyn_t += per_call[-1]
-            dyn_ok &= all(x.stable() for x in sts_d) and not (fl_d & D.FSG_DYN_NONFINITE).any()
-        rb.close()
-        e2e_dyn = {"value": round(E * scene.n_cells * Ee * world / dyn_t / 1e6, 1), "unit": "MLUPS",
-                   # up: actuation + the env pack (frame constants, state pointers);
-                   # down: status, tau_ext + stats, post-step state, flags, COM
-                   "h2d_bytes_per_step": E * (8 * nj + 440),
-                   "d2h_bytes_per_step": E * (32 + 200 + 440 + 4 + 24), "steps": Ee,
-                   "stable": bool(dyn_ok), "recentres": n_shift,
-                   "call_us": {q: round(float(np.percentile(per_call, p)) * 1e6, 1)
-                               for q, p in (("p50", 50), ("p90", 90), ("max", 100))},
-                   "what": "fsg_batch_step_dynamic: actuation up; device poses, coupled step, "
-                           "buoyancy + integrate (4 substeps) of every robot, FrameFollower + "
-                           "recentre trigger per env; statuses + robot states down (the "
-                           "reference's full CoupledSession::step)"}
+        e2e_dyn = robot_leg(batch, scene, E, Ee, kk, local, dev, world, flush_bufs=(fw_buf, fr_buf, sink))
     if batch:
         batch.close()
     else:
@@ -748,6 +755,18 @@ def run_ours(args, scene, rank, local, world):
         d2h = 28 * m + 64       # marker forces (3x8 B) + validity (4 B) + step status
     s.close()
     cpp = host_e2e(scene, cfg, frames, poses) if (skinned and world == 1) else None
+    # one robot in the followed frame (c2): the whole CoupledSession::step with
+    # the robot on the device too (SURVEY.md §8(d) asks for e2e with the robot
+    # work included for C2)
+    e2e_dyn = None
+    if skinned and len(scene.bodies) == 1 and scene.frame_mode != "none" and world == 1 \
+            and not args.no_robot_leg:
+        from paper_2206_01683_b200 import EnvBatch
+        b1 = EnvBatch(cfg, 1)
+        b1.envs[0].set_skin(*scene.skin())
+        e2e_dyn = robot_leg(b1, scene, 1, min(args.e2e_steps, K), W + K, local, dev, world,
+                            flush_bufs=(fw_buf, fr_buf, sink))
+        b1.close()
 
     peak, peak_src = measured_peaks()
     # the coupled step's kernels overlap (the banded K4 is a programmatic
@@ -787,6 +806,7 @@ def run_ours(args, scene, rank, local, world):
                 {"value": round(e2e_val, 1), "unit": "MLUPS", "h2d_bytes_per_step": h2d,
                  "d2h_bytes_per_step": d2h, "steps": E, "host": "Python (ctypes)"}),
         "e2e_python": {"value": round(e2e_val, 1), "unit": "MLUPS", "steps": E},
+        **({"e2e_robots_on_device": e2e_dyn} if e2e_dyn else {}),
         # skinned bodies ride in the marker kernel (<= 2 bodies; more use the
         # split skin kernels beside K4): K_m + K4 per step
         "gpu_launches": K * ((2 if len(scene.bodies) <= 2 else 4) if skinned else (2 if m else 1)),
