@@ -225,7 +225,7 @@ struct FixBand {
 
 #ifdef __CUDACC__
 // release / acquire at GPU scope (PTX memory model): the marker chain's
-// "every tile stamped" flag (fsg_ib_fix.cuh) and its consumer (fsg_k4v4.cuh)
+// "every tile stamped" flag (fsg_ib_fix.cuh) and its consumer (fsg_k4.cuh)
 __device__ __forceinline__ void st_release_gpu(unsigned* p, unsigned v) {
   asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }

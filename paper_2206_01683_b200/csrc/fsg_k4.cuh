@@ -1,4 +1,4 @@
-// fsg_k4v4.cuh -- throughput K4 (fp32 deviations), included inside namespace
+// fsg_k4.cuh -- throughput K4 (fp32 deviations), included inside namespace
 // fsg::p32.  One cell per thread; the 19 pull sources and 19 destinations are
 // addressed through per-direction base pointers passed as kernel parameters
 // (constant bank), so each access costs one LDC + one IMAD.WIDE instead of a

@@ -1,5 +1,5 @@
 // fsg_k4_tma.cuh -- pure-fluid K4 with bulk-async (TMA 1D) staging of the
-// pull sources, included inside namespace fsg::p32 after fsg_k4v4.cuh.
+// pull sources, included inside namespace fsg::p32 after fsg_k4.cuh.
 //
 // A tile is TW = 128 consecutive cells of one z-plane in the flattened
 // (x + nx*y) order.  The pull source of direction i for cell c is element

@@ -520,7 +520,7 @@ __global__ void __launch_bounds__(128) k_collide(Grid g, const Store* __restrict
 }
 
 #if FSG_PREC == 32
-#include "fsg_k4v4.cuh"
+#include "fsg_k4.cuh"
 #include "fsg_k4_tma.cuh"
 #endif
 

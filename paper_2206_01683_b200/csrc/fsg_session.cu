@@ -16,7 +16,7 @@
 // buffers.
 // Throughput mode (fp32): two direct launches per coupled step, frame
 // constants by value -- the marker kernel (fixed-point spread) and the
-// banded K4 as its programmatic dependent (fsg_k4v4.cuh) -- or one K4 when
+// banded K4 as its programmatic dependent (fsg_k4.cuh) -- or one K4 when
 // there are no markers.  The host never waits before enqueueing; the status
 // is copied out of the device scratch only when asked for.
 #include <cuda.h>
