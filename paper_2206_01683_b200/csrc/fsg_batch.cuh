@@ -21,6 +21,13 @@ __device__ __forceinline__ int env_of(const int* pref, int E, int v) {
   return e;
 }
 
+/// env_of for a non-decreasing sequence of v: advances the previous answer e
+/// (a thread's markers, a block's fetched items), amortised O(1) per call.
+__device__ __forceinline__ int env_adv(const int* pref, int E, int v, int e) {
+  while (e + 1 < E && pref[e + 1] <= v) ++e;
+  return e;
+}
+
 /// cell_update addressed from the env's state base pointers: the 19 source
 /// and destination offsets are the common grid's (constant bank).
 template <bool PULLED, bool VF>
@@ -31,30 +38,34 @@ __device__ __forceinline__ float cell_update_ab(const Grid& g, const float* __re
                                                 StepScratch* out) {
   const unsigned m = (unsigned)mem_index(g, x, y, z);
   const int zg = g.z0 + z;
+  // cell base pointers + 32-bit direction offsets: one IMAD.WIDE per access
+  // (m + offset in unsigned arithmetic cost ~8 instructions per access)
+  const float* __restrict__ Am = A + m;
+  float* __restrict__ Bm = B + m;
   float s[Q];
   if (!PULLED) {
 #pragma unroll
-    for (int i = 0; i < Q; ++i) s[i] = __ldg(A + (m + (int)g.own[i]));
+    for (int i = 0; i < Q; ++i) s[i] = __ldg(Am + (int)g.own[i]);
   } else if (y > 0 && y < g.ny - 1 && zg > 0 && zg < g.nzg - 1) {
     const int cxp = x == 0 ? (g.periodic ? g.nx : 1) : 0;
     const int cxm = x == g.nx - 1 ? (g.periodic ? -g.nx : -1) : 0;
 #pragma unroll
     for (int i = 0; i < Q; ++i) {
       const int cx = ex_of(i) > 0 ? cxp : (ex_of(i) < 0 ? cxm : 0);
-      s[i] = __ldg(A + (m + (int)g.pull[i] + cx));
+      s[i] = __ldg(Am + ((int)g.pull[i] + cx));
     }
   } else if (!g.periodic) {  // open y/z face rows: constant offsets (FaceFlags)
     const FaceFlags f = face_flags(g, x, y, zg);
 #pragma unroll
     for (int i = 0; i < Q; ++i)
-      s[i] = __ldg(A + (m + (int)g.pull[i] + (face_unknown(ex_of(i), ey_of(i), ez_of(i), f) ? f.D : 0)));
+      s[i] = __ldg(Am + ((int)g.pull[i] + (face_unknown(ex_of(i), ey_of(i), ez_of(i), f) ? f.D : 0)));
   } else {
     gather<true>(g, A, x, y, z, s);
   }
   Band none{nullptr, 0};
   const float v = collide_cell32<3, VF>(s, x, y, z, g, Fx, Fy, Fz, false, 0, none, sc, st, out);
 #pragma unroll
-  for (int i = 0; i < Q; ++i) B[m + (int)g.own[i]] = s[i];
+  for (int i = 0; i < Q; ++i) Bm[(int)g.own[i]] = s[i];
   return v;
 }
 
@@ -98,8 +109,10 @@ __global__ void __launch_bounds__(128, FSG_KMB_MINB)
   const SessionConsts& sc = *scp;
   // the stencils of a group's first 4 markers, reused by the heavy loop
   __shared__ MkStencil s_st[FX_PER_BLOCK][4];
+  int ev = 0;  // the group's markers run in increasing order: env by advancing
   for (int tg = blockIdx.x * FX_PER_BLOCK + slot, k = 0; tg < h.m_total; tg += stride, ++k) {
-    const EnvPack& P = packs[env_of(mkb, h.E, tg)];
+    ev = env_adv(mkb, h.E, tg, ev);
+    const EnvPack& P = packs[ev];
     const FixBand fb{P.F, P.tflag, h.tnx, h.tny, h.tnz, P.stamp};
     const int t = tg - P.mk_begin;
     MkStencil S;
@@ -125,8 +138,10 @@ __global__ void __launch_bounds__(128, FSG_KMB_MINB)
   if (threadIdx.x == 0) __threadfence();
   __syncthreads();
   asm volatile("griddepcontrol.launch_dependents;");
+  ev = 0;
   for (int tg = blockIdx.x * FX_PER_BLOCK + slot, k = 0; tg < h.m_total; tg += stride, ++k) {
-    const EnvPack& P = packs[env_of(mkb, h.E, tg)];
+    ev = env_adv(mkb, h.E, tg, ev);
+    const EnvPack& P = packs[ev];
     const FixBand fb{P.F, P.tflag, h.tnx, h.tny, h.tnz, P.stamp};
     const int t = tg - P.mk_begin;
     MkStencil S;
@@ -210,7 +225,7 @@ __global__ void __launch_bounds__(128, FSG_K4BB_MINB)
   constexpr int CH = 1;
   int nxt = 0;
   if (tid == 0) nxt = (int)atomicAdd(work, 1u) * CH;
-  int itg = h.item_total, iend = 0;
+  int itg = h.item_total, iend = 0, ev = 0;
   for (;;) {
     if (itg >= iend) {  // block-uniform: next chunk
       if (tid == 0) item = nxt;
@@ -224,7 +239,8 @@ __global__ void __launch_bounds__(128, FSG_K4BB_MINB)
     // pack array: restaging a pack in shared memory on nearly every item (a
     // block's successive items usually belong to different envs) costs an
     // L2 round trip and two barriers
-    const EnvPack& P = packs[env_of(ib, h.E, itg)];
+    ev = env_adv(ib, h.E, itg, ev);  // a block's items are fetched in increasing order
+    const EnvPack& P = packs[ev];
     const int it = itg - P.item_begin;
     const int col = it % ncol, zk = it / ncol;
     const int x = (col % tx_n) * blockDim.x + threadIdx.x;

@@ -61,13 +61,15 @@ __device__ __forceinline__ void gather_slow(const Grid& g, const Store* __restri
 template <bool PULLED>
 __device__ __forceinline__ void gather_cell(const Grid& g, const Store* __restrict__ A, int x, int y,
                                             int z, Store (&s)[Q]) {
+  // 32-bit direction offsets (|pull| < 38 planes < 2^31 under the host's
+  // 19 x cells < 2^32 bound): one IMAD.WIDE per load
   const Store* __restrict__ base = A + (unsigned)mem_index(g, x, y, z);
   if (!PULLED) {
 #pragma unroll
-    for (int i = 0; i < Q; ++i) s[i] = base[g.own[i]];
+    for (int i = 0; i < Q; ++i) s[i] = base[(int)g.own[i]];
   } else if (is_interior(g, x, y, z)) {
 #pragma unroll
-    for (int i = 0; i < Q; ++i) s[i] = base[g.pull[i]];
+    for (int i = 0; i < Q; ++i) s[i] = base[(int)g.pull[i]];
   } else {
     gather_slow<PULLED>(g, A, x, y, z, s);
   }
