@@ -26,15 +26,19 @@
 #define FSG_KM_PER_SM_DEFAULT 3.0  // persistent marker grid: c3 141.4 -> 139.8 us vs one wave
 #endif
 // batched marker kernel: register budget (min resident blocks) and grid cap
-// per SM (it is persistent over every env's markers)
+// per SM (it is persistent over every env's markers).  Both batched kernels
+// at 64 registers: the 4 marker blocks per SM leave room for 4 K4 blocks, so
+// phase A runs beside the markers instead of behind them (c5 round 148.1 ->
+// 143.6 us; 80/80 registers with 5 marker blocks: 148.1; 64/64 with 3, 5, 6
+// marker blocks: 154.8, 148.4, 150.9; K4 at 80: 145.0)
 #ifndef FSG_K4BB_MINB  // batched banded K4: resident 128-thread blocks per SM
-#define FSG_K4BB_MINB 6
+#define FSG_K4BB_MINB 8
 #endif
 #ifndef FSG_KMB_MINB
-#define FSG_KMB_MINB 6
+#define FSG_KMB_MINB 8
 #endif
 #ifndef FSG_KMB_PER_SM
-#define FSG_KMB_PER_SM 5
+#define FSG_KMB_PER_SM 4
 #endif
 #ifndef FSG_KM_MINB
 #define FSG_KM_MINB 6
