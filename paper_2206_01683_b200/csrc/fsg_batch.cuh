@@ -94,7 +94,11 @@ __device__ __forceinline__ void report_min_red(StepScratch* out, float v) {
 /// the dependent K4 launches only once every marker block has triggered).
 /// Each group first stamps the tiles of ALL its markers, the block fences
 /// and triggers K4, then the groups do the heavy per-marker work (the cheap
-/// stencil is recomputed rather than kept).
+/// stencil is recomputed rather than kept).  Skinned envs: the group's
+/// markers are skinned SKC at a time into a shared-memory cache (one lane per
+/// marker and bone slot) before their stamps; the heavy loop takes position,
+/// velocity, normal and the tau slot data from it (c5 round 145.1 -> 141.8
+/// us against one marker per warp pass).
 template <bool SKIN>  // SKIN: some env has a skinned body (P.skb)
 __global__ void __launch_bounds__(128, FSG_KMB_MINB)
     k_markers_batch(Grid g, const SessionConsts* __restrict__ scp, const EnvPack* __restrict__ packs,
@@ -109,24 +113,34 @@ __global__ void __launch_bounds__(128, FSG_KMB_MINB)
   const SessionConsts& sc = *scp;
   // the stencils of a group's first 4 markers, reused by the heavy loop
   __shared__ MkStencil s_st[FX_PER_BLOCK][4];
+  // skinned envs: the group's markers skinned SKC at a time (fsg_skin_fused.cuh)
+  __shared__ SkinCache s_sk[SKIN ? FX_PER_BLOCK : 1];
+  const int tg0 = blockIdx.x * FX_PER_BLOCK + slot;
+  auto fill = [&](int k) {  // warp-uniform: the cache for markers k .. k + SKC - 1
+    skin_cache_fill(s_sk[slot], tg0 + k * stride, stride, h.m_total,
+                    [&](int tg, SkinView& V, const fsg_body_pose*& Q, int& t, double** outp) {
+                      const EnvPack& P = packs[env_of(mkb, h.E, tg)];
+                      if (!P.skb) return false;
+                      V = SkinView{P.sk_rest, P.sk_nrest, P.sk_wb, P.sk_ww};
+                      Q = &P.skb->pose;
+                      t = tg - P.mk_begin;
+                      outp[0] = const_cast<double*>(P.mk.pts);
+                      outp[1] = const_cast<double*>(P.mk.vel);
+                      outp[2] = const_cast<double*>(P.mk.nrm);
+                      return true;
+                    });
+  };
   int ev = 0;  // the group's markers run in increasing order: env by advancing
-  for (int tg = blockIdx.x * FX_PER_BLOCK + slot, k = 0; tg < h.m_total; tg += stride, ++k) {
+  for (int tg = tg0, k = 0; tg < h.m_total; tg += stride, ++k) {
+    if (SKIN && k % SKC == 0) fill(k);
     ev = env_adv(mkb, h.E, tg, ev);
     const EnvPack& P = packs[ev];
     const FixBand fb{P.F, P.tflag, h.tnx, h.tny, h.tnz, P.stamp};
     const int t = tg - P.mk_begin;
     MkStencil S;
-    if (SKIN && P.skb) {  // skinned env (fsg_skin_fused.cuh): LBS of the marker first
-      const SkinView V{P.sk_rest, P.sk_nrest, P.sk_wb, P.sk_ww};
-      const SkinSlot sl = skin_slot(V, t, lane);
-      double xw[3];
-      skin_point_warp(V, P.skb->pose, t, sl, xw);
-      if (lane == 0) {
-        double* pts = const_cast<double*>(P.mk.pts);
-        pts[3 * t] = xw[0];
-        pts[3 * t + 1] = xw[1];
-        pts[3 * t + 2] = xw[2];
-      }
+    if (SKIN && P.skb) {
+      const double* xc = s_sk[slot].x[k % SKC];
+      const double xw[3] = {xc[0], xc[1], xc[2]};
       mk_stencil_x(xw, sc, P.st, S);
     } else {
       mk_stencil(P.mk, t, sc, P.st, S);
@@ -138,36 +152,31 @@ __global__ void __launch_bounds__(128, FSG_KMB_MINB)
   if (threadIdx.x == 0) __threadfence();
   __syncthreads();
   asm volatile("griddepcontrol.launch_dependents;");
+  // a group with more than SKC markers refills the cache chunk by chunk again
+  const bool refill = tg0 + SKC * stride < h.m_total;
   ev = 0;
-  for (int tg = blockIdx.x * FX_PER_BLOCK + slot, k = 0; tg < h.m_total; tg += stride, ++k) {
+  for (int tg = tg0, k = 0; tg < h.m_total; tg += stride, ++k) {
+    if (SKIN && refill && k % SKC == 0) fill(k);
     ev = env_adv(mkb, h.E, tg, ev);
     const EnvPack& P = packs[ev];
     const FixBand fb{P.F, P.tflag, h.tnx, h.tny, h.tnz, P.stamp};
     const int t = tg - P.mk_begin;
     MkStencil S;
+    if (k < 4) {
+      S = s_st[slot][k];  // from the stamp phase (the block barrier since orders it)
+    } else if (SKIN && P.skb) {
+      const double* xc = s_sk[slot].x[k % SKC];
+      const double xw[3] = {xc[0], xc[1], xc[2]};
+      mk_stencil_x(xw, sc, P.st, S);
+    } else {
+      mk_stencil(P.mk, t, sc, P.st, S);
+    }
     if (SKIN && P.skb) {
-      const SkinView V{P.sk_rest, P.sk_nrest, P.sk_wb, P.sk_ww};
-      const SkinBody& B = *P.skb;
-      const SkinSlot sl = skin_slot(V, t, lane);
-      double vel[3], nrm[3], fw[3], xb[3] = {0.0, 0.0, 0.0};
-      skin_vel_nrm_warp(V, B.pose, t, sl, vel, nrm, xb);
-      if (lane == 0) {
-        double* v = const_cast<double*>(P.mk.vel);
-        double* n = const_cast<double*>(P.mk.nrm);
-#pragma unroll
-        for (int c = 0; c < 3; ++c) {
-          v[3 * t + c] = vel[c];
-          n[3 * t + c] = nrm[c];
-        }
-      }
-      if (k < 4) {
-        S = s_st[slot][k];  // from the stamp phase (the block barrier since orders it)
-      } else {  // the position the stamp phase skinned (same warp)
-        double xw[3];
-#pragma unroll
-        for (int c = 0; c < 3; ++c) xw[c] = __ldcg(P.mk.pts + 3 * t + c);
-        mk_stencil_x(xw, sc, P.st, S);
-      }
+      const SkinCache& C = s_sk[slot];
+      const int kc = k % SKC;
+      const double vel[3] = {C.v[kc][0], C.v[kc][1], C.v[kc][2]};
+      const double nrm[3] = {C.n[kc][0], C.n[kc][1], C.n[kc][2]};
+      double fw[3];
       if (P.pulled)
         mk_finish<true>(g, P.A, P.mk, t, lane, sc, P.st, S, phs[slot], P.rec, P.fworld, P.fworld_h,
                         P.valid_h, fb, P.out, vel, nrm, fw);
@@ -177,13 +186,14 @@ __global__ void __launch_bounds__(128, FSG_KMB_MINB)
       __syncwarp(fx_mask());
       if (S.ok) {
         double acc = 0.0;
-        skin_tau_pre(B, lane, sl, xb, fw, vel, acc);
+        const int q = lane >> 3;  // the bone slot this lane's tau terms belong to
+        const double p[3] = {C.xb[kc][q][0], C.xb[kc][q][1], C.xb[kc][q][2]};
+        skin_tau_core<true>(*P.skb, lane, C.b[kc][q], C.w[kc][q], p, fw, vel, acc);
         skin_red_marker(acc, lane, P.sk_acc, t);
       }
+      __syncwarp();  // the cache may be refilled for the next chunk
       continue;
     }
-    if (k < 4) S = s_st[slot][k];
-    else mk_stencil(P.mk, t, sc, P.st, S);
     if (P.pulled)
       mk_finish<true>(g, P.A, P.mk, t, lane, sc, P.st, S, phs[slot], P.rec, P.fworld, P.fworld_h,
                       P.valid_h, fb, P.out);

@@ -197,6 +197,112 @@ __device__ __forceinline__ void skin_vel_nrm_warp(const SP& P, const fsg_body_po
   }
 }
 
+/// Skinning of up to SKC of a warp's markers at once: lane 4j + s evaluates
+/// bone slot s of the warp's j-th marker (SKIN_KW == 4 slots), the four lanes
+/// of a group add their slot terms in ascending slot order by shuffles.  Per
+/// slot the arithmetic, and per marker the order of the sums, are
+/// skin_point_warp's and skin_vel_nrm_warp's (bit-identical), at an eighth of
+/// their warp instructions (those evaluate one marker per warp, 4 lanes busy).
+constexpr int SKC = 8;
+struct SkinCache {
+  double x[SKC][3], v[SKC][3], n[SKC][3];  // position, velocity, unit normal
+  double xb[SKC][SKIN_KW][3];              // slot s's bone-transformed point (tau terms)
+  double w[SKC][SKIN_KW];
+  int b[SKC][SKIN_KW];
+};
+
+/// Sum over the 4 lanes of this lane's group in slot order from 0, stopping at
+/// the first empty slot (slot_sum's rule); every lane of the group gets it.
+__device__ __forceinline__ void grp_slot_sum(bool has, const double* term, double* out) {
+  static_assert(SKIN_KW == 4, "4 lanes per marker");
+  const int g0 = (threadIdx.x & 31) & ~3;
+  bool live = true;
+#pragma unroll
+  for (int c = 0; c < 3; ++c) out[c] = 0.0;
+#pragma unroll
+  for (int l = 0; l < SKIN_KW; ++l) {
+    const int h = __shfl_sync(0xffffffffu, has ? 1 : 0, g0 + l);
+    double t[3];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) t[c] = __shfl_sync(0xffffffffu, term[c], g0 + l);
+    live = live && h;
+    if (live) {
+#pragma unroll
+      for (int c = 0; c < 3; ++c) out[c] = rn_add(out[c], t[c]);
+    }
+  }
+}
+
+/// Fill C (all 32 lanes): marker j (< SKC) of the warp is global index
+/// tg0 + j * stride if below m_total; `locate(tg, V, Q, t)` gives its skin
+/// view, pose and local index (false: not a skinned marker).  Writes the
+/// markers' pts / vel / nrm (lanes s = 0, 1, 2 of the group).  Ends with
+/// __syncwarp.
+template <class Locate>
+__device__ __forceinline__ void skin_cache_fill(SkinCache& C, int tg0, int stride, int m_total,
+                                                Locate locate) {
+  static_assert(FX_LANES == 32, "a warp per marker group");
+  const int lane = threadIdx.x & 31, j = lane >> 2, s = lane & 3;
+  const int tg = tg0 + j * stride;
+  int b = -1;
+  double w = 0.0, tx[3] = {0.0, 0.0, 0.0}, tv[3] = {0.0, 0.0, 0.0}, tn[3] = {0.0, 0.0, 0.0};
+  double xb[3] = {0.0, 0.0, 0.0};
+  double* outp[3] = {nullptr, nullptr, nullptr};
+  int t = 0;
+  SkinView V;
+  const fsg_body_pose* Q = nullptr;
+  if (tg < m_total && locate(tg, V, Q, t, outp)) {
+    b = __ldg(V.wb + SKIN_KW * t + s);
+    if (b >= 0) {
+      w = __ldg(V.ww + SKIN_KW * t + s);
+      const double x[3] = {__ldg(V.rest + 3 * t), __ldg(V.rest + 3 * t + 1), __ldg(V.rest + 3 * t + 2)};
+      const double n0[3] = {__ldg(V.nrest + 3 * t), __ldg(V.nrest + 3 * t + 1), __ldg(V.nrest + 3 * t + 2)};
+      double d[3], cr[3], rn[3];
+      rn_apply(*Q, b, x, xb);
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        tx[c] = rn_mul(w, xb[c]);
+        d[c] = rn_sub(xb[c], Q->p_world[b][c]);
+      }
+      rn_cross(Q->omega_world[b], d, cr);
+      rn_mv(Q->bone_R[b], n0, rn);
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        tv[c] = rn_mul(w, rn_add(Q->v_origin_world[b][c], cr[c]));
+        tn[c] = rn_mul(w, rn[c]);
+      }
+    }
+  }
+  double X[3], Vv[3], N[3];
+  grp_slot_sum(b >= 0, tx, X);
+  grp_slot_sum(b >= 0, tv, Vv);
+  grp_slot_sum(b >= 0, tn, N);
+  const double z = rn_dot(N, N);
+  if (z > 0.0) {
+    const double sz = __dsqrt_rn(z);
+#pragma unroll
+    for (int c = 0; c < 3; ++c) N[c] = __ddiv_rn(N[c], sz);
+  }
+  if (s == 0) {
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      C.x[j][c] = X[c];
+      C.v[j][c] = Vv[c];
+      C.n[j][c] = N[c];
+    }
+  }
+#pragma unroll
+  for (int c = 0; c < 3; ++c) C.xb[j][s][c] = xb[c];
+  C.b[j][s] = b;
+  C.w[j][s] = w;
+  if (s < 3 && outp[s]) {
+    const double* src = s == 0 ? X : (s == 1 ? Vv : N);
+#pragma unroll
+    for (int c = 0; c < 3; ++c) outp[s][3 * t + c] = src[c];
+  }
+  __syncwarp();
+}
+
 template <class SP>
 __device__ __forceinline__ void skin_tau_warp(const SP& P, const SkinBody& B, int t, int lane,
                                               const double* fw, const double* vel, double& acc);

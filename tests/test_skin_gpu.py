@@ -128,15 +128,16 @@ def test_skin_api_contract():
     s.close()
 
 
-def test_batched_skinned_envs_match_single_sessions():
+@pytest.mark.parametrize("E", [4, 32])
+def test_batched_skinned_envs_match_single_sessions(E):
     """EnvBatch with skinned envs (one fish per env, each its own gait phase)
     plus one env with host markers: distributions, skinned markers and marker
     forces bit-identical to the envs stepped one by one; tau_ext / stats within
     1e-9 (the batch sums each marker's fixed-point terms, a session its warps'
-    sums)."""
+    sums).  E = 32 (20480 markers): more than SKC = 8 markers per warp of the batched
+    marker grid, so the warps refill their skin cache chunk by chunk."""
     from paper_2206_01683_b200 import CoupledSession, EnvBatch, SessionConfig
     sc = skin_scene()
-    E = 4
     cfg = SessionConfig(dims=sc.dims, dx=sc.dx, dt=sc.dt, rho=sc.rho, nu=sc.nu,
                         frame_mode=sc.frame_mode, precision="fp32", max_markers=sc.m)
     rho, u = init_fluid(sc)
