@@ -76,9 +76,12 @@ def main(tag):
                           "source": f"profiles/{tag}_ncu_summary.json"}
     with open(os.path.join(ROOT, "profiles", f"{tag}_ncu_summary.json"), "w") as f:
         json.dump(summ, f, indent=1)
-    if traffic:
-        with open(os.path.join(ROOT, "profiles", "k4_traffic.json"), "w") as f:
-            json.dump(traffic, f, indent=1)
+    if traffic:  # merged: a partial round updates only the workloads it captured
+        tp = os.path.join(ROOT, "profiles", "k4_traffic.json")
+        merged = json.load(open(tp)) if os.path.exists(tp) else {}
+        merged.update(traffic)
+        with open(tp, "w") as f:
+            json.dump(merged, f, indent=1)
     print(json.dumps(traffic, indent=1))
 
 
