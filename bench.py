@@ -853,6 +853,8 @@ def host_e2e(scene, cfg, frames, poses, n_steps: int = 100):
                         os.path.join(ROOT, "scripts", "host_e2e.cpp"), "-L", lib, "-lfsg",
                         f"-Wl,-rpath,{lib}", "-o", exe], check=True, capture_output=True, timeout=120)
         r = subprocess.run([exe, case, "5"], check=True, capture_output=True, text=True, timeout=300)
+        if r.stderr:  # (dev: HOST_E2E_SPLIT=1 prints the enqueue / wait split)
+            print(r.stderr.strip(), file=sys.stderr)
         return json.loads(r.stdout.strip().splitlines()[-1])
     except Exception as e:  # noqa: BLE001 -- reported, the Python e2e stands
         print(f"host_e2e unavailable: {e}", file=sys.stderr)

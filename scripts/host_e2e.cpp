@@ -106,6 +106,27 @@ int main(int argc, char** argv) {
   }
   std::sort(us.begin(), us.end());
   const double cells = (double)hdr[0] * hdr[1] * hdr[2];
+  if (std::getenv("HOST_E2E_SPLIT")) {  // dev: host time to enqueue vs to wait, per step
+    std::vector<double> ta, tl, tw;
+    for (int k = 0; k < ns; ++k) {
+      const auto t0 = std::chrono::steady_clock::now();
+      fsg_set_frame(s, &frames[k]);
+      fsg_set_pose(s, &poses[(size_t)k * nb]);
+      const auto ta0 = std::chrono::steady_clock::now();
+      fsg_step_async(s);
+      const auto t1 = std::chrono::steady_clock::now();
+      fsg_last_status(s, &st);
+      const auto t2 = std::chrono::steady_clock::now();
+      ta.push_back(std::chrono::duration<double, std::micro>(ta0 - t0).count());
+      tl.push_back(std::chrono::duration<double, std::micro>(t1 - ta0).count());
+      tw.push_back(std::chrono::duration<double, std::micro>(t2 - t1).count());
+    }
+    std::sort(ta.begin(), ta.end());
+    std::sort(tl.begin(), tl.end());
+    std::sort(tw.begin(), tw.end());
+    std::fprintf(stderr, "set frame+pose %.2f us, enqueue %.2f us, wait %.2f us (medians)\n", ta[ns / 2],
+                 tl[ns / 2], tw[ns / 2]);
+  }
   std::printf("{\"steps\": %d, \"us_per_step\": %.2f, \"mlups\": %.1f, \"stable\": %d, \"min_f\": %.6g}\n",
               ns, us[1], cells / us[1], st.finite && st.n_nonpositive_rho == 0 ? 1 : 0, st.min_f);
   fsg_destroy(s);
