@@ -217,6 +217,8 @@ __global__ void __launch_bounds__(128, FSG_K4BB_MINB)
   const int tid = threadIdx.x + blockDim.x * threadIdx.y;
   const int nthr = blockDim.x * blockDim.y;
   const SessionConsts& sc = *scp;
+  // a programmatic dependent (the one-call step's status copy) may start now
+  asm volatile("griddepcontrol.launch_dependents;");
   for (int e = tid; e < h.E; e += nthr) {
     ib[e] = packs[e].item_begin;
     tb[e] = packs[e].tile_begin;

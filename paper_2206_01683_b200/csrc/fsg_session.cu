@@ -2063,7 +2063,12 @@ int fsg_batch_step_async(fsg_batch* b) {
 namespace {
 // every env's step status into pinned host memory in one launch (the batched
 // K4 left each in its env's device scratch, packs[e].out)
+// Launched as a programmatic dependent of the batched K4 (which triggers at
+// its start) where it directly follows it: resident before K4 ends, it copies
+// as soon as K4's writes are visible.  griddepcontrol.wait is a no-op in a
+// normal launch.
 __global__ void k_batch_status(const fsg::EnvPack* __restrict__ packs, int E, StepScratch* dst) {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   constexpr int NS = (int)(sizeof(StepScratch) / 4);
   for (int k = threadIdx.x; k < E * NS; k += blockDim.x)
     reinterpret_cast<volatile int*>(dst)[k] = reinterpret_cast<const int*>(packs[k / NS].out)[k % NS];
@@ -2085,7 +2090,18 @@ int fsg_batch_step_skinned(fsg_batch* b, const fsg_frame_state* frames, const fs
   int rc = fsg_batch_step_async(b);
   if (rc) return rc;
   if (!b->h_stat) CU(cudaMallocHost(&b->h_stat, sizeof(StepScratch) * b->E));
-  k_batch_status<<<1, 256, 0, b->stream>>>(b->d_packs[q], b->E, b->h_stat);
+  {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(1);
+    cfg.blockDim = dim3(256);
+    cfg.stream = b->stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    CU(cudaLaunchKernelEx(&cfg, k_batch_status, (const fsg::EnvPack*)b->d_packs[q], b->E, b->h_stat));
+  }
   CU_LAUNCH();
   CU(stream_wait(b->stream));
   int off = 0;
