@@ -1221,6 +1221,7 @@ int dyn_read_states(fsg_dyn* d, fsg_joint_state* out, int* flags, cudaStream_t s
 }
 
 int* dyn_flags(fsg_dyn* d) { return d->d_flags; }
+const fsg_joint_state* dyn_states_dev(const fsg_dyn* d) { return d->d_state; }
 int dyn_n_envs(const fsg_dyn* d) { return d->E; }
 int dyn_n_links(const fsg_dyn* d) { return d->hc.n_links; }
 bool dyn_rest_set(const fsg_dyn* d) { return d->rest_set; }

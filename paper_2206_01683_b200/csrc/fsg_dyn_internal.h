@@ -19,6 +19,8 @@ int dyn_read_states(fsg_dyn* d, fsg_joint_state* out, int* flags, cudaStream_t s
 // RobotInstance::com_world of every env's current state into d_com [3 * E]
 int dyn_launch_com(fsg_dyn* d, double* d_com, cudaStream_t s);
 int* dyn_flags(fsg_dyn* d);
+// the robot states in device memory [E] (read back by the batched step)
+const fsg_joint_state* dyn_states_dev(const fsg_dyn* d);
 int dyn_n_envs(const fsg_dyn* d);
 int dyn_n_links(const fsg_dyn* d);
 int dyn_device(const fsg_dyn* d);

@@ -2073,6 +2073,26 @@ __global__ void k_batch_status(const fsg::EnvPack* __restrict__ packs, int E, St
   for (int k = threadIdx.x; k < E * NS; k += blockDim.x)
     reinterpret_cast<volatile int*>(dst)[k] = reinterpret_cast<const int*>(packs[k / NS].out)[k % NS];
 }
+// The robots-on-device step's whole readback into pinned host memory in one
+// launch: every env's status, tau_ext + stats, robot state and flag, and the
+// robots' COM (null: no follower) -- instead of a status kernel and four
+// device-to-host copies queued behind the robot step (each ~5-9 us of
+// latency on a synchronous call).
+__global__ void k_batch_readback(const fsg::EnvPack* __restrict__ packs, int E, StepScratch* hst,
+                                 const double* __restrict__ wr, double* hwr, int nwr,
+                                 const int* __restrict__ st, int* hst_state, int nst,
+                                 const int* __restrict__ fl, int* hfl,
+                                 const double* __restrict__ com, double* hcom) {
+  constexpr int NS = (int)(sizeof(StepScratch) / 4);
+  const int t = threadIdx.x;
+  for (int k = t; k < E * NS; k += blockDim.x)
+    reinterpret_cast<volatile int*>(hst)[k] = reinterpret_cast<const int*>(packs[k / NS].out)[k % NS];
+  for (int k = t; k < nwr; k += blockDim.x) reinterpret_cast<volatile double*>(hwr)[k] = wr[k];
+  for (int k = t; k < nst; k += blockDim.x) reinterpret_cast<volatile int*>(hst_state)[k] = st[k];
+  for (int k = t; k < E; k += blockDim.x) reinterpret_cast<volatile int*>(hfl)[k] = fl[k];
+  if (com)
+    for (int k = t; k < 3 * E; k += blockDim.x) reinterpret_cast<volatile double*>(hcom)[k] = com[k];
+}
 }  // namespace
 
 int fsg_batch_step_skinned(fsg_batch* b, const fsg_frame_state* frames, const fsg_body_pose* poses,
@@ -2236,17 +2256,17 @@ int fsg_batch_step_dynamic(fsg_batch* b, fsg_dyn* d, const fsg_frame_state* fram
                             fsg::dyn_flags(d), b->stream);
   if (rc) return set_err(rc, "%s", fsg_dyn_last_error());
   if (!b->h_stat) CU(cudaMallocHost(&b->h_stat, sizeof(StepScratch) * b->E));
-  k_batch_status<<<1, 256, 0, b->stream>>>(b->d_packs[q], b->E, b->h_stat);
-  CU_LAUNCH();
   if (b->follow) {
     rc = fsg::dyn_launch_com(d, b->d_com, b->stream);
     if (rc) return set_err(rc, "%s", fsg_dyn_last_error());
-    CU(cudaMemcpyAsync(b->h_com, b->d_com, sizeof(double) * 3 * b->E, cudaMemcpyDeviceToHost, b->stream));
   }
-  CU(cudaMemcpyAsync(b->h_wbatch, b->d_wrench, sizeof(double) * fsg_batch::WSTRIDE * b->E,
-                     cudaMemcpyDeviceToHost, b->stream));
-  rc = fsg::dyn_read_states(d, b->h_states, b->h_flags, b->stream);
-  if (rc) return set_err(rc, "%s", fsg_dyn_last_error());
+  static_assert(sizeof(fsg_joint_state) % sizeof(int) == 0, "copied as ints");
+  k_batch_readback<<<1, 256, 0, b->stream>>>(
+      b->d_packs[q], b->E, b->h_stat, b->d_wrench, b->h_wbatch, fsg_batch::WSTRIDE * b->E,
+      reinterpret_cast<const int*>(fsg::dyn_states_dev(d)), reinterpret_cast<int*>(b->h_states),
+      (int)(sizeof(fsg_joint_state) / sizeof(int)) * b->E, fsg::dyn_flags(d), b->h_flags,
+      b->follow ? b->d_com : nullptr, b->h_com);
+  CU_LAUNCH();
   CU(stream_wait(b->stream));
   for (int e = 0; e < b->E; ++e) {
     fsg_session* s = b->envs[e];
