@@ -43,6 +43,59 @@ __global__ void __launch_bounds__(128, 6) k_pull(P p, int nx, int ny, int nz, lo
   }
 }
 
+// y-tiled: f[((z*nyt + y/TY)*19 + i)*(nx*TY) + x + nx*(y%TY)] -- the 19
+// direction sub-arrays of a (z, y-tile) group lie within 19*nx*TY*4 bytes
+// (TY = 8 at nx = 512: 304 KB) instead of 19 planes (19 MB) apart.
+template <int LT>
+__global__ void __launch_bounds__(128, 6) k_pull_tiled(const float* __restrict__ A, float* __restrict__ B,
+                                                        int nx, int lnx, int ny, int nz) {
+  constexpr int TY = 1 << LT;
+  const int tx_n = nx / 128, ty_n = ny;
+  const int ncol = tx_n * ty_n, nyt = ny >> LT;
+  const long long tileN = (long long)nx << LT;
+  const int nitem = ncol * (nz - 2);
+  for (int it = blockIdx.x; it < nitem; it += gridDim.x) {
+    const int col = it % ncol, z = 1 + it / ncol;
+    const int x = (col % tx_n) * 128 + threadIdx.x;
+    const int y = col / tx_n;
+    if (y == 0 || y == ny - 1 || x == 0 || x == nx - 1) continue;
+    float s[19];
+#pragma unroll
+    for (int i = 0; i < 19; ++i) {
+      const int xs = x - cex[i], ys = y - cey[i], zs = z - cez[i];
+      const long long a = (((long long)zs * nyt + (ys >> LT)) * 19 + i) * tileN + xs + ((ys & (TY - 1)) << lnx);
+      s[i] = __ldg(A + a);
+    }
+    float t = 0.f;
+#pragma unroll
+    for (int i = 0; i < 19; ++i) t += s[i];
+    t *= 1.0f / 19.0f;
+    const long long o = (((long long)z * nyt + (y >> LT)) * 19) * tileN + x + ((y & (TY - 1)) << lnx);
+#pragma unroll
+    for (int i = 0; i < 19; ++i) B[o + i * tileN] = 0.9f * s[i] + 0.1f * t;
+  }
+}
+
+template <int LT>
+void run_tiled(float* A, float* B, int nx, int ny, int nz, int nsm) {
+  const int grid = nsm * 6;
+  for (int w = 0; w < 3; ++w) k_pull_tiled<LT><<<grid, 128>>>(w & 1 ? B : A, w & 1 ? A : B, nx, 9, ny, nz);
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  const int reps = nz >= 256 ? 10 : 40;
+  cudaEventRecord(e0);
+  for (int r = 0; r < reps; ++r) k_pull_tiled<LT><<<grid, 128>>>(r & 1 ? B : A, r & 1 ? A : B, nx, 9, ny, nz);
+  cudaEventRecord(e1);
+  cudaEventSynchronize(e1);
+  float ms = 0;
+  cudaEventElapsedTime(&ms, e0, e1);
+  const double cells = (double)(nx - 2) * (ny - 2) * (nz - 2);
+  const double sec = ms / 1e3 / reps;
+  printf("nz=%4d            y-tiled TY=%-3d %.3f ms  %.1f GLUPS  %.0f GB/s\n", nz, 1 << LT, sec * 1e3,
+         cells / sec / 1e9, cells * 152 / sec / 1e9);
+}
+
 int main() {
   const int nx = 512, ny = 512;
   int nsm = 0;
@@ -87,6 +140,11 @@ int main() {
       const double s = ms / 1e3 / reps;
       printf("nz=%4d state %.1f GB  %-11s  %.3f ms  %.1f GLUPS  %.0f GB/s\n", nz, 2.0 * 19 * n * 4 / 1e9,
              layout == 0 ? "dir-major" : "plane-inter", s * 1e3, cells / s / 1e9, cells * 152 / s / 1e9);
+    }
+    if (nx == 512) {  // (lnx = 9 hard-wired)
+      run_tiled<2>(A, B, nx, ny, nz, nsm);
+      run_tiled<3>(A, B, nx, ny, nz, nsm);
+      run_tiled<4>(A, B, nx, ny, nz, nsm);
     }
     cudaFree(A);
     cudaFree(B);
