@@ -552,6 +552,7 @@ __global__ void __launch_bounds__(DYN_BLOCK)
 // and the rows of each Cholesky column.  The recursive chains (forward
 // kinematics, RNEA sweeps, triangular solves) stay on lane 0; everything
 // lives in shared memory.
+constexpr int DYN_TWO_MAX = 256;  // envs up to which the warp kernel runs two warps per env
 constexpr int DYN_WARPS = 3;  // 3 x ~13 KB warp workspaces + DynConst in 48 KB of static smem (12 links)
 
 #ifdef FSG_DYN_TIMING  // dev builds only (scripts/build_variant.sh): per-phase clock64 of warp 0
@@ -816,7 +817,23 @@ __device__ bool wk_llt_solve(WarpWS& w, int lane, int n) {
   return true;
 }
 
-__global__ void __launch_bounds__(32 * DYN_WARPS)
+/// Named barrier of an env's two warps (ids 1..DYN_WARPS; 0 is __syncthreads).
+__device__ __forceinline__ void pair_sync(int wi) {
+  // literal ids: a register id makes ptxas reserve all 16 barriers (one block per SM)
+  static_assert(DYN_WARPS == 3, "one named barrier per env slot");
+  if (wi == 0) asm volatile("bar.sync 1, 64;" ::: "memory");
+  else if (wi == 1) asm volatile("bar.sync 2, 64;" ::: "memory");
+  else asm volatile("bar.sync 3, 64;" ::: "memory");
+}
+
+/// TWO (latency-bound batches): two warps per env -- the main warp runs the
+/// step, the helper warp runs RNEA (bias forces) while the main warp runs CRBA
+/// (mass matrix): independent given the kinematics, disjoint workspace fields
+/// (ic/X/T/H vs a/f/cb), the same arithmetic bit for bit (8 koi: 102.8 ->
+/// 96.3 us per step).  Large batches keep one warp per env (the idle helper
+/// warps cost throughput: 4096 envs 397 vs 582 us).
+template <bool TWO>
+__global__ void __launch_bounds__(64 * DYN_WARPS)
     k_dyn_step_warp(const DynConst* __restrict__ gc, fsg_joint_state* __restrict__ states,
                     const double* __restrict__ bladder, const double* __restrict__ act,
                     const double* __restrict__ tau_ext, double rho, int hydro, double3 gh,
@@ -825,11 +842,22 @@ __global__ void __launch_bounds__(32 * DYN_WARPS)
   __shared__ DynConst c;
   __shared__ WarpWS ws[DYN_WARPS];
   load_const(c, gc);
-  const int lane = threadIdx.x & 31, wi = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31, wi = TWO ? threadIdx.x >> 6 : threadIdx.x >> 5;
+  const bool helper = TWO && ((threadIdx.x >> 5) & 1);
   const int e = blockIdx.x * DYN_WARPS + wi;
-  if (e >= E) return;
+  if (e >= E) return;  // (both warps of the env)
   WarpWS& w = ws[wi];
   const int nd = c.nd, nj = c.nj;
+  if (helper) {  // RNEA of every substep, between the main warp's kinematics and its solve
+    const double g[3] = {gv.x, gv.y, gv.z};
+    for (int s = 0; s < substeps; ++s) {
+      pair_sync(wi);  // kinematics of substep s ready (or the main warp stopped)
+      if (w.ok < 0) break;
+      wk_rnea(c, w, lane, g);
+      pair_sync(wi);  // bias forces ready
+    }
+    return;
+  }
 #ifdef FSG_DYN_TIMING
   long long t_last = clock64();
 #endif
@@ -843,7 +871,7 @@ __global__ void __launch_bounds__(32 * DYN_WARPS)
     for (int q = lane; q < nd; q += 32) w.te[q] = te ? te[q] : 0.0;
   }
   for (int q = lane; q < nj; q += 32) w.sig[q] = act[(size_t)e * nj + q];
-  if (lane == 0) w.fl = 0;
+  if (lane == 0) w.fl = 0, w.ok = 0;  // (ok < 0: stop signal to the helper warp)
   __syncwarp();
   if (hydro) {
     wk_fk(c, w, lane);
@@ -881,15 +909,22 @@ __global__ void __launch_bounds__(32 * DYN_WARPS)
     if (__any_sync(0xffffffffu, clamped) && lane == 0) w.fl |= FSG_DYN_CLAMPED;
     DYN_T(1);
     wk_fk(c, w, lane);
+    if (TWO) pair_sync(wi);  // the helper warp starts RNEA
     DYN_T(2);
     wk_crba(c, w, lane);
     DYN_T(3);
-    wk_rnea(c, w, lane, g);
+    if (TWO) pair_sync(wi);  // RNEA done
+    else wk_rnea(c, w, lane, g);
     for (int q = lane; q < nd; q += 32) w.rhs[q] = (w.tsum[q] + w.te[q]) - w.cb[q];
     __syncwarp();
     DYN_T(4);
     if (!wk_llt_solve(w, lane, nd)) {
-      if (lane == 0) w.fl |= FSG_DYN_NOT_SPD;
+      if (lane == 0) {
+        w.fl |= FSG_DYN_NOT_SPD;
+        w.ok = -1;  // the helper warp leaves at its next barrier
+      }
+      __syncwarp();
+      if (TWO && s + 1 < substeps) pair_sync(wi);
       break;
     }
     DYN_T(5);
@@ -1175,8 +1210,13 @@ int dyn_launch_step(fsg_dyn* d, const double* d_actuation, const double* d_tau_e
   const double3 gh = g_hydro ? make_double3(g_hydro[0], g_hydro[1], g_hydro[2]) : make_double3(0, 0, 0);
   const double3 gv = gravity ? make_double3(gravity[0], gravity[1], gravity[2]) : make_double3(0, 0, 0);
   const double* act = d_actuation ? d_actuation : d->d_act;
-  if (d->warp_kernel)
-    k_dyn_step_warp<<<(unsigned)((d->E + DYN_WARPS - 1) / DYN_WARPS), 32 * DYN_WARPS, 0, s>>>(
+  const unsigned nblk = (unsigned)((d->E + DYN_WARPS - 1) / DYN_WARPS);
+  if (d->warp_kernel && d->E <= DYN_TWO_MAX)
+    k_dyn_step_warp<true><<<nblk, 64 * DYN_WARPS, 0, s>>>(
+        d->d_c, d->d_state, d->d_bladder, act, d_tau_ext, rho_fluid, g_hydro ? 1 : 0, gh, dt,
+        substeps, gv, d_flags, d->E, d_tau_ptrs);
+  else if (d->warp_kernel)
+    k_dyn_step_warp<false><<<nblk, 32 * DYN_WARPS, 0, s>>>(
         d->d_c, d->d_state, d->d_bladder, act, d_tau_ext, rho_fluid, g_hydro ? 1 : 0, gh, dt,
         substeps, gv, d_flags, d->E, d_tau_ptrs);
   else
