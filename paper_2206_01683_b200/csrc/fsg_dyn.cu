@@ -908,7 +908,9 @@ __global__ void __launch_bounds__(64 * DYN_WARPS)
     }
     if (__any_sync(0xffffffffu, clamped) && lane == 0) w.fl |= FSG_DYN_CLAMPED;
     DYN_T(1);
-    wk_fk(c, w, lane);
+    // substep 0 after the hydrostatics: the kinematics of the unchanged
+    // pre-step state are already in w (wk_fk writes w.k / w.rr from w.st only)
+    if (s > 0 || !hydro) wk_fk(c, w, lane);
     if (TWO) pair_sync(wi);  // the helper warp starts RNEA
     DYN_T(2);
     wk_crba(c, w, lane);
