@@ -196,12 +196,14 @@ def test_bladder_change_matches_host_mirror():
             assert vol[e] == b[e].volume
 
 
+@pytest.mark.parametrize("E", [24, 300])
 @pytest.mark.parametrize("name", ["koi", "fins"])
-def test_warp_and_thread_kernels_are_bit_identical(name, monkeypatch):
+def test_warp_and_thread_kernels_are_bit_identical(name, E, monkeypatch):
     """The warp-per-env kernel (small batches) and the thread-per-env kernel
-    (large batches) run the same arithmetic: identical states and flags."""
+    (large batches) run the same arithmetic: identical states and flags.
+    E = 24: the warp kernel's two-warp form (RNEA on a helper warp, batches
+    up to 256 envs); E = 300: its one-warp form."""
     robot = _robots()[name]
-    E = 24
     rng = np.random.default_rng(13)
     sts = _random_states(robot, E, 14)
     act = rng.uniform(-0.5, 0.5, (E, robot.n_joints))
