@@ -291,3 +291,35 @@ def test_batch_step_dynamic_rejects_mismatches():
     st, fl, packed = b.step_dynamic(rb, act)  # now well-formed
     assert all(x.stable() for x in st) and packed.shape == (2, 7 + DYN_MAX_LINKS + 2 * DYN_MAX_DOFS)
     b.close()
+
+
+@pytest.mark.parametrize("E,wmax", [(4, "4096"), (300, "4096"), (4, "0")])
+def test_not_spd_env_stops_alone(E, wmax, monkeypatch):
+    """A NaN joint angle makes that env's mass matrix NaN: the Cholesky stops
+    it with FSG_DYN_NOT_SPD (the reference's NumericalError) at the first
+    substep -- in the warp kernel's two-warp form (the helper warp must leave
+    its barrier loop), its one-warp form and the thread kernel -- while the
+    other envs step on, identical to a batch without the bad env."""
+    monkeypatch.setenv("FSG_DYN_WARP_MAX", wmax)
+    robot = _koi()
+    sts = _random_states(robot, E, 21)
+    act = np.zeros((E, robot.n_joints))
+    tau = np.zeros((E, robot.n_dofs))
+    good = D.RobotBatch(robot, E)
+    good.set_states(sts)
+    fl_good = good.step(act, tau, 1000.0, G, 0.004, 4)
+    bad_sts = list(sts)
+    bad = D.JointState.zero(robot)
+    bad.q[0] = np.nan
+    bad_sts[1] = bad
+    rb = D.RobotBatch(robot, E)
+    rb.set_states(bad_sts)
+    fl = rb.step(act, tau, 1000.0, G, 0.004, 4)
+    assert fl[1] & D.FSG_DYN_NOT_SPD
+    keep = [e for e in range(E) if e != 1]
+    assert np.array_equal(fl[keep], fl_good[keep])
+    a = np.stack([_state_vec(s) for s in rb.states()])[keep]
+    b = np.stack([_state_vec(s) for s in good.states()])[keep]
+    assert np.array_equal(a, b)
+    rb.close()
+    good.close()
